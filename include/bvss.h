@@ -1,0 +1,197 @@
+/*
+ * bvss.h — C ABI of the B200-native BioVSS hot path (arXiv 2412.03301).
+ *
+ * The library (paper_2412_03301_b200/libbvss.so) implements top-k vector-set
+ * search under the Hausdorff distance (Def 4), filtered by
+ * FlyHash codes (Def 7; Alg 1) folded into per-set Bloom
+ * or count-Bloom sketches (Def 10 P:729-732 / Alg 5; Def 8 P:657 / Alg 3), with
+ * the cascade of Alg 6 run with stage 1 open (reading R6):
+ * sketch scan -> top-T candidates -> exact Hausdorff rerank -> top-k.
+ *
+ * Every step runs in hand-written sm_100a kernels.  There is no CPU fallback:
+ * on a machine without an sm_100 device every compute entry point returns
+ * BVSS_EUNSUPPORTED (or BVSS_ECUDA) and sets bvss_last_error().
+ *
+ * Conventions (all entry points):
+ *  - Return 0 (BVSS_OK) on success or a negative bvss_status; never throw,
+ *    never abort.  A thread-local message describes the last failure.
+ *  - Ownership: inputs are caller-owned; the library copies what it keeps
+ *    before returning and never retains caller pointers.  Outputs are
+ *    caller-allocated.  An index owns all of its device memory until
+ *    bvss_free_index().
+ *  - Pointers are HOST pointers unless BVSS_DEVICE_PTRS is passed in the call's
+ *    flags, in which case every array argument of that call is a device
+ *    pointer on the index's device.  Host inputs may be pageable or pinned.
+ *  - Set ids are positions 0..n-1 in set_offsets (int64).  Vectors are fp32,
+ *    row-major [rows][d].  set_offsets[0] == 0, strictly increasing (Def 2:
+ *    every set has m >= 1 vectors), set_offsets[n] == number of rows.
+ *  - Bits: code/sketch Bloom position j lives in uint32 word j>>5, bit j&31.
+ *  - Results are sorted by (distance ascending, id ascending); missing
+ *    results (k > n) are padded with id -1 and distance +inf.
+ *  - An index is not thread-safe; distinct indexes are independent.
+ *  - All work of a call is issued on the index's stream (bvss_set_stream);
+ *    calls with host outputs synchronise that stream before returning; calls
+ *    with BVSS_DEVICE_PTRS are asynchronous with respect to the host.
+ */
+#ifndef BVSS_H
+#define BVSS_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define BVSS_API __attribute__((visibility("default")))
+#else
+#define BVSS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  BVSS_OK = 0,
+  BVSS_EINVAL = -1,       /* bad argument (null, sizes, offsets, L>m, s>d, m%32, k<1, T<k, ...) */
+  BVSS_ENONFINITE = -2,   /* NaN/Inf found while BVSS_VALIDATE_FINITE was set */
+  BVSS_ENOMEM = -3,       /* device or host allocation failed */
+  BVSS_ECUDA = -4,        /* a CUDA runtime error (message has the CUDA error string) */
+  BVSS_EUNSUPPORTED = -5, /* no sm_100 device, or a size beyond this build's limits */
+  BVSS_ESTATE = -6        /* call out of order (e.g. distributed phases) */
+} bvss_status;
+
+typedef enum { BVSS_SKETCH_BINARY = 0, BVSS_SKETCH_COUNT_U8 = 1 } bvss_sketch_kind;
+
+/* call flags */
+#define BVSS_DEVICE_PTRS 0x1u      /* array arguments are device pointers */
+#define BVSS_VALIDATE_FINITE 0x2u  /* reject NaN/Inf inputs (one extra pass) */
+#define BVSS_KEEP_CODES 0x4u       /* build: keep per-vector codes for bvss_export_codes */
+
+typedef struct {
+  uint32_t m;            /* code length b = Bloom length (reading R21); m % 32 == 0, 32 <= m <= 2048 */
+  uint32_t s;            /* ones per projection row, 1 <= s <= min(d, 32) */
+  uint32_t L;            /* WTA winners L_wta, 1 <= L <= m */
+  uint32_t sketch;       /* bvss_sketch_kind */
+  uint64_t seed;         /* projection seed (reading R7) */
+  const uint16_t* projection; /* optional host [m][s] sorted row indices; NULL = generate from seed */
+  int32_t device;        /* CUDA device ordinal of this index (shard) */
+  uint32_t flags;        /* build flags (BVSS_DEVICE_PTRS | BVSS_VALIDATE_FINITE | BVSS_KEEP_CODES) */
+  uint32_t query_batch;  /* queries per internal sub-batch; 0 = auto */
+  uint32_t refine_terms; /* bf16 split terms for the tensor-core Gram: 3 (default) or 1 */
+} bvss_params;
+
+typedef struct bvss_index bvss_index;
+
+typedef struct {
+  int64_t n, nvec;       /* sets and vectors in the index */
+  int32_t d, dpad;       /* dimension, and its padding to a multiple of 64 for the bf16 copies */
+  uint32_t m, s, L, sketch;
+  int32_t device;
+  uint64_t device_bytes; /* device memory owned by the index (excluding search workspace) */
+  uint64_t workspace_bytes;
+} bvss_info;
+
+typedef struct {
+  /* per-stage device time of the most recent bvss_search / bvss_filter / bvss_refine, ms */
+  float ms_h2d, ms_encode, ms_scan, ms_select, ms_refine, ms_topk, ms_d2h, ms_total;
+  uint64_t scan_bytes;    /* sketch bytes streamed by the scan kernel (algorithmic) */
+  uint64_t gather_bytes;  /* candidate-vector bytes gathered by the refine kernel (algorithmic) */
+  uint64_t cand_rows;     /* candidate vectors refined */
+  uint64_t fixup_sets;    /* candidates recomputed by the exact fp32 fix-up */
+  int32_t kernel_launches;/* kernels launched by the call */
+  int32_t query_batch;
+} bvss_stats;
+
+/* ---------------------------------------------------------------- core -- */
+
+/* Build an index over n sets (Alg 1 + Alg 3 / Alg 5, P:323-343, P:665-682,
+ * P:738-757): copies vectors to the device, generates W (or takes p->projection),
+ * encodes every vector (FlyHash + WTA), folds per-set sketches, and prepares the
+ * refine operands (bf16 hi/lo split, fp32 squared norms).
+ *   vectors     [set_offsets[n]][d] fp32
+ *   set_offsets [n+1] int64
+ * Errors: BVSS_EINVAL for bad sizes/offsets/params, BVSS_ENONFINITE (with
+ * BVSS_VALIDATE_FINITE), BVSS_ENOMEM, BVSS_ECUDA, BVSS_EUNSUPPORTED. */
+BVSS_API int bvss_build_index(const float* vectors, const int64_t* set_offsets, int64_t n, int32_t d,
+                     const bvss_params* p, bvss_index** out);
+
+/* Approximate top-k vector-set search (Def 5 P:162-169 via Alg 6):
+ * for each query set, scan all n sketches, keep the T smallest filter scores
+ * (ties -> lower id), rerank them by exact Hausdorff distance, return the k
+ * nearest.  T >= n gives exact brute force.  T is clamped to n.
+ *   queries       [query_offsets[nq]][d] fp32
+ *   query_offsets [nq+1] int64
+ *   out_ids  [nq][k] int64, out_dist [nq][k] fp32 (Hausdorff distance, not squared)
+ * Errors: BVSS_EINVAL (k < 1, T < k, bad offsets), plus the build errors. */
+BVSS_API int bvss_search(bvss_index* idx, const float* queries, const int64_t* query_offsets, int64_t nq,
+                int32_t k, int32_t T, int64_t* out_ids, float* out_dist, uint32_t flags);
+
+BVSS_API void bvss_free_index(bvss_index* idx);
+BVSS_API const char* bvss_last_error(void);
+BVSS_API int bvss_get_info(const bvss_index* idx, bvss_info* out);
+BVSS_API int bvss_get_stats(const bvss_index* idx, bvss_stats* out);
+/* Issue all work of this index on `stream` (a cudaStream_t; NULL = the index's own stream). */
+BVSS_API int bvss_set_stream(bvss_index* idx, void* stream);
+/* Number of sm_100-class devices visible (0 if none); never fails. */
+BVSS_API int bvss_device_count(void);
+
+/* ---------------------------------------------------- stage entry points -- */
+
+/* W as built, host [m][s] uint16 (a-1). */
+BVSS_API int bvss_export_projection(const bvss_index* idx, uint16_t* out);
+/* Codes of vectors [first, first+count), host [count][m/32] uint32 (a-2).
+ * Needs BVSS_KEEP_CODES at build. */
+BVSS_API int bvss_export_codes(const bvss_index* idx, int64_t first, int64_t count, uint32_t* out);
+/* Sketches of sets [first, first+count) in row-major host layout (a-3):
+ * binary: uint32 [count][m/32]; count-Bloom: uint8 [count][m]. */
+BVSS_API int bvss_export_sketches(const bvss_index* idx, int64_t first, int64_t count, void* out);
+/* Query sketches (a-4: Alg 6 lines 1-2), same layout as above,
+ * host [nq][m/32] uint32 or [nq][m] uint8; codes optional ([rows][m/32], may be NULL). */
+BVSS_API int bvss_query_sketch(bvss_index* idx, const float* queries, const int64_t* query_offsets, int64_t nq,
+                      void* out_sketch, uint32_t* out_codes, uint32_t flags);
+/* Filter (a-5 + a-6: Alg 6 lines 10-18): per query the min(T, n) candidates in
+ * ASCENDING id order and their filter scores (binary: Hamming; count: squared
+ * L2 between counters, reading R2).  out_cand [nq][T] int32 (padded with -1),
+ * out_score [nq][T] int32 (may be NULL). */
+BVSS_API int bvss_filter(bvss_index* idx, const float* queries, const int64_t* query_offsets, int64_t nq,
+                int32_t T, int32_t* out_cand, int32_t* out_score, uint32_t flags);
+/* Refine (a-7 + a-8: Alg 6 lines 19-23): given candidate lists (as from
+ * bvss_filter, -1 padded), compute the tensor-core Hausdorff of every candidate
+ * and the exact top-k.  out_approx [nq][T] fp32 receives the tensor-core
+ * squared Hausdorff per candidate (NaN where cand == -1; may be NULL). */
+BVSS_API int bvss_refine(bvss_index* idx, const float* queries, const int64_t* query_offsets, int64_t nq,
+                const int32_t* cand, int32_t T, int32_t k, int64_t* out_ids, float* out_dist,
+                float* out_approx, uint32_t flags);
+/* Squared-distance error bound E used by the fix-up window for a query whose
+ * largest vector norm is qnorm_max. */
+BVSS_API double bvss_refine_error_bound(const bvss_index* idx, double qnorm_max);
+
+/* ------------------------------------------- sharded (multi-GPU) search -- */
+/* Exact global-T protocol over P shards: each rank holds an
+ * index over a contiguous id range [id_base, id_base + n).  The caller runs
+ * the collectives (NCCL via torch.distributed) between phases; all buffers
+ * named *_dev are device pointers on the index's device.                     */
+typedef struct bvss_search_ctx bvss_search_ctx;
+
+/* Encode + sketch + scan one query batch; returns the number of radix rounds. */
+BVSS_API int bvss_dist_begin(bvss_index* idx, const float* queries, const int64_t* query_offsets, int64_t nq,
+                    int32_t k, int32_t T, int64_t id_base, uint32_t flags, bvss_search_ctx** out,
+                    int32_t* rounds);
+/* Local histogram of radix round r: hist_dev int32 [nq][2048]. */
+BVSS_API int bvss_dist_hist(bvss_search_ctx* ctx, int32_t round, int32_t* hist_dev);
+/* Apply the GLOBAL (all-reduced) histogram of round r. */
+BVSS_API int bvss_dist_resolve(bvss_search_ctx* ctx, int32_t round, const int32_t* global_hist_dev);
+/* Local count of candidates tied at the global threshold: eq_dev int64 [nq]. */
+BVSS_API int bvss_dist_tie_counts(bvss_search_ctx* ctx, int64_t* eq_dev);
+/* Given the all-gathered tie counts [P][nq] int64 of every rank, take this
+ * rank's share of the global top-T, refine it and write the local top-k
+ * (global ids) to topk_ids_dev [nq][k] int64 and topk_dist_dev [nq][k] fp32. */
+BVSS_API int bvss_dist_finish(bvss_search_ctx* ctx, const int64_t* all_eq_dev, int32_t world, int32_t rank,
+                     int64_t* topk_ids_dev, float* topk_dist_dev);
+/* Merge P local top-k lists [P][nq][k] into the global top-k [nq][k] (K7). */
+BVSS_API int bvss_merge_topk(bvss_index* idx, const int64_t* ids_dev, const float* dist_dev, int32_t world,
+                    int64_t nq, int32_t k, int64_t* out_ids_dev, float* out_dist_dev);
+BVSS_API void bvss_dist_end(bvss_search_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BVSS_H */

@@ -1,0 +1,289 @@
+"""Thin ctypes binding of libbvss (include/bvss.h): argument marshalling only.
+
+Every step of the hot path runs in the library's sm_100a kernels.  Host inputs
+(numpy arrays) are passed as host pointers; torch CUDA tensors are passed as
+device pointers with BVSS_DEVICE_PTRS, and the index is bound to torch's
+current stream for the call so that ordering with surrounding torch work is
+preserved.  There is no CPU fallback: if libbvss.so is missing the import of
+this module raises, and if no sm_100 device is present the library returns
+BVSS_EUNSUPPORTED, raised here as ``BvssError``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbvss.so")
+
+OK, EINVAL, ENONFINITE, ENOMEM, ECUDA, EUNSUPPORTED, ESTATE = 0, -1, -2, -3, -4, -5, -6
+SKETCH_BINARY, SKETCH_COUNT_U8 = 0, 1
+DEVICE_PTRS, VALIDATE_FINITE, KEEP_CODES = 0x1, 0x2, 0x4
+
+# every symbol include/bvss.h declares (checked by tests/test_abi.py)
+EXPORTS = (
+    "bvss_build_index", "bvss_search", "bvss_free_index", "bvss_last_error", "bvss_get_info", "bvss_get_stats",
+    "bvss_set_stream", "bvss_device_count", "bvss_export_projection", "bvss_export_codes", "bvss_export_sketches",
+    "bvss_query_sketch", "bvss_filter", "bvss_refine", "bvss_refine_error_bound", "bvss_dist_begin",
+    "bvss_dist_hist", "bvss_dist_resolve", "bvss_dist_tie_counts", "bvss_dist_finish", "bvss_merge_topk",
+    "bvss_dist_end",
+)
+
+
+class BvssError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"bvss error {code}: {msg}")
+        self.code = code
+
+
+class Params(C.Structure):
+    _fields_ = [("m", C.c_uint32), ("s", C.c_uint32), ("L", C.c_uint32), ("sketch", C.c_uint32),
+                ("seed", C.c_uint64), ("projection", C.c_void_p), ("device", C.c_int32), ("flags", C.c_uint32),
+                ("query_batch", C.c_uint32), ("refine_terms", C.c_uint32)]
+
+
+class Info(C.Structure):
+    _fields_ = [("n", C.c_int64), ("nvec", C.c_int64), ("d", C.c_int32), ("dpad", C.c_int32), ("m", C.c_uint32),
+                ("s", C.c_uint32), ("L", C.c_uint32), ("sketch", C.c_uint32), ("device", C.c_int32),
+                ("device_bytes", C.c_uint64), ("workspace_bytes", C.c_uint64)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("ms_h2d", C.c_float), ("ms_encode", C.c_float), ("ms_scan", C.c_float), ("ms_select", C.c_float),
+                ("ms_refine", C.c_float), ("ms_topk", C.c_float), ("ms_d2h", C.c_float), ("ms_total", C.c_float),
+                ("scan_bytes", C.c_uint64), ("gather_bytes", C.c_uint64), ("cand_rows", C.c_uint64),
+                ("fixup_sets", C.c_uint64), ("kernel_launches", C.c_int32), ("query_batch", C.c_int32)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2412_03301_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    P, I64, I32, U32, VP = C.c_void_p, C.c_int64, C.c_int32, C.c_uint32, C.c_void_p
+    sig = {
+        "bvss_build_index": (C.c_int, [P, P, I64, I32, C.POINTER(Params), C.POINTER(VP)]),
+        "bvss_search": (C.c_int, [VP, P, P, I64, I32, I32, P, P, U32]),
+        "bvss_free_index": (None, [VP]),
+        "bvss_last_error": (C.c_char_p, []),
+        "bvss_get_info": (C.c_int, [VP, C.POINTER(Info)]),
+        "bvss_get_stats": (C.c_int, [VP, C.POINTER(Stats)]),
+        "bvss_set_stream": (C.c_int, [VP, VP]),
+        "bvss_device_count": (C.c_int, []),
+        "bvss_export_projection": (C.c_int, [VP, P]),
+        "bvss_export_codes": (C.c_int, [VP, I64, I64, P]),
+        "bvss_export_sketches": (C.c_int, [VP, I64, I64, P]),
+        "bvss_query_sketch": (C.c_int, [VP, P, P, I64, P, P, U32]),
+        "bvss_filter": (C.c_int, [VP, P, P, I64, I32, P, P, U32]),
+        "bvss_refine": (C.c_int, [VP, P, P, I64, P, I32, I32, P, P, P, U32]),
+        "bvss_refine_error_bound": (C.c_double, [VP, C.c_double]),
+        "bvss_dist_begin": (C.c_int, [VP, P, P, I64, I32, I32, I64, U32, C.POINTER(VP), C.POINTER(I32)]),
+        "bvss_dist_hist": (C.c_int, [VP, I32, P]),
+        "bvss_dist_resolve": (C.c_int, [VP, I32, P]),
+        "bvss_dist_tie_counts": (C.c_int, [VP, P]),
+        "bvss_dist_finish": (C.c_int, [VP, P, I32, I32, P, P]),
+        "bvss_merge_topk": (C.c_int, [VP, P, P, I32, I64, I32, P, P]),
+        "bvss_dist_end": (None, [VP]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+lib = _load()
+
+
+def _check(code):
+    if code != OK:
+        raise BvssError(code, lib.bvss_last_error().decode(errors="replace"))
+
+
+def device_count() -> int:
+    return lib.bvss_device_count()
+
+
+def _is_cuda(x) -> bool:
+    return hasattr(x, "is_cuda") and bool(x.is_cuda)
+
+
+def _ptr(x):
+    """(pointer, keepalive) for a numpy array or torch tensor (contiguous)."""
+    if x is None:
+        return None, None
+    if hasattr(x, "data_ptr"):
+        x = x.contiguous()
+        return C.c_void_p(x.data_ptr()), x
+    a = np.ascontiguousarray(x)
+    return C.c_void_p(a.ctypes.data), a
+
+
+class Index:
+    """A device-resident BioVSS index over one database shard (one GPU)."""
+
+    def __init__(self, vectors, offsets, *, m, s, L, sketch="binary", seed=0, device=0, keep_codes=False,
+                 validate=False, projection=None, refine_terms=3, query_batch=0):
+        dev = _is_cuda(vectors)
+        if dev != _is_cuda(offsets):
+            raise ValueError("vectors and offsets must both be host arrays or both CUDA tensors")
+        if dev:
+            import torch
+            vectors = vectors.to(torch.float32).contiguous()
+            offsets = offsets.to(torch.int64).contiguous()
+            device = vectors.device.index
+        else:
+            vectors = np.ascontiguousarray(vectors, dtype=np.float32)
+            offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+        n = int(offsets.shape[0]) - 1
+        d = int(vectors.shape[1])
+        self.sketch_kind = sketch
+        proj = None if projection is None else np.ascontiguousarray(projection, dtype=np.uint16)
+        p = Params(m=m, s=s, L=L, sketch=SKETCH_BINARY if sketch == "binary" else SKETCH_COUNT_U8, seed=seed,
+                   projection=(proj.ctypes.data if proj is not None else None), device=device,
+                   flags=(DEVICE_PTRS if dev else 0) | (KEEP_CODES if keep_codes else 0) |
+                   (VALIDATE_FINITE if validate else 0), query_batch=query_batch, refine_terms=refine_terms)
+        self._h = C.c_void_p()
+        vp, _k1 = _ptr(vectors)
+        op, _k2 = _ptr(offsets)
+        if dev:
+            import torch
+            torch.cuda.current_stream(device).synchronize()
+        _check(lib.bvss_build_index(vp, op, n, d, C.byref(p), C.byref(self._h)))
+        self.n, self.d, self.m, self.s, self.L, self.device = n, d, m, s, L, device
+
+    # ------------------------------------------------------------- helpers
+    def _bind_stream(self, tensors):
+        if any(_is_cuda(t) for t in tensors if t is not None):
+            import torch
+            st = torch.cuda.current_stream(self.device).cuda_stream
+            _check(lib.bvss_set_stream(self._h, C.c_void_p(st)))
+            return DEVICE_PTRS
+        _check(lib.bvss_set_stream(self._h, None))
+        return 0
+
+    def _alloc(self, like_dev, shape, dtype):
+        if like_dev:
+            import torch
+            tdt = {np.int64: torch.int64, np.float32: torch.float32, np.int32: torch.int32,
+                   np.uint32: torch.int32, np.uint8: torch.uint8}[dtype]
+            return torch.empty(shape, dtype=tdt, device=f"cuda:{self.device}")
+        return np.empty(shape, dtype=dtype)
+
+    def _queries(self, queries, q_offsets):
+        dev = _is_cuda(queries)
+        if dev != _is_cuda(q_offsets):
+            raise ValueError("queries and q_offsets must both be host arrays or both CUDA tensors")
+        if not dev:
+            queries = np.ascontiguousarray(queries, dtype=np.float32)
+            q_offsets = np.ascontiguousarray(q_offsets, dtype=np.int64)
+        return queries, q_offsets, dev, int(q_offsets.shape[0]) - 1
+
+    # ---------------------------------------------------------------- API
+    def search(self, queries, q_offsets, k, T, validate=False):
+        """bvss_search: returns (ids int64 [nq][k], dist fp32 [nq][k])."""
+        queries, q_offsets, dev, nq = self._queries(queries, q_offsets)
+        fl = self._bind_stream([queries]) | (VALIDATE_FINITE if validate else 0)
+        ids = self._alloc(dev, (nq, k), np.int64)
+        dist = self._alloc(dev, (nq, k), np.float32)
+        qp, _a = _ptr(queries)
+        op, _b = _ptr(q_offsets)
+        _check(lib.bvss_search(self._h, qp, op, nq, k, T, _ptr(ids)[0], _ptr(dist)[0], fl))
+        return ids, dist
+
+    def filter(self, queries, q_offsets, T):
+        """bvss_filter: candidates (ascending id, -1 padded) and their filter scores."""
+        queries, q_offsets, dev, nq = self._queries(queries, q_offsets)
+        fl = self._bind_stream([queries])
+        cand = self._alloc(dev, (nq, T), np.int32)
+        score = self._alloc(dev, (nq, T), np.int32)
+        qp, _a = _ptr(queries)
+        op, _b = _ptr(q_offsets)
+        _check(lib.bvss_filter(self._h, qp, op, nq, T, _ptr(cand)[0], _ptr(score)[0], fl))
+        return cand, score
+
+    def refine(self, queries, q_offsets, cand, k, with_approx=True):
+        """bvss_refine: top-k from given candidate lists; optionally the per-candidate tensor-core H^2."""
+        queries, q_offsets, dev, nq = self._queries(queries, q_offsets)
+        if not dev:
+            cand = np.ascontiguousarray(cand, dtype=np.int32)
+        T = int(cand.shape[1])
+        fl = self._bind_stream([queries])
+        ids = self._alloc(dev, (nq, k), np.int64)
+        dist = self._alloc(dev, (nq, k), np.float32)
+        approx = self._alloc(dev, (nq, T), np.float32) if with_approx else None
+        qp, _a = _ptr(queries)
+        op, _b = _ptr(q_offsets)
+        cp, _c = _ptr(cand)
+        _check(lib.bvss_refine(self._h, qp, op, nq, cp, T, k, _ptr(ids)[0], _ptr(dist)[0],
+                               _ptr(approx)[0] if approx is not None else None, fl))
+        return ids, dist, approx
+
+    def query_sketch(self, queries, q_offsets, with_codes=False):
+        queries, q_offsets, dev, nq = self._queries(queries, q_offsets)
+        fl = self._bind_stream([queries])
+        if self.sketch_kind == "binary":
+            sk = self._alloc(dev, (nq, self.m // 32), np.uint32)
+        else:
+            sk = self._alloc(dev, (nq, self.m), np.uint8)
+        nrows = int(q_offsets[-1])
+        codes = self._alloc(dev, (nrows, self.m // 32), np.uint32) if with_codes else None
+        qp, _a = _ptr(queries)
+        op, _b = _ptr(q_offsets)
+        _check(lib.bvss_query_sketch(self._h, qp, op, nq, _ptr(sk)[0], _ptr(codes)[0] if codes is not None else None,
+                                     fl))
+        return (sk, codes) if with_codes else sk
+
+    def export_projection(self):
+        out = np.empty((self.m, self.s), dtype=np.uint16)
+        _check(lib.bvss_export_projection(self._h, C.c_void_p(out.ctypes.data)))
+        return out
+
+    def export_codes(self, first=0, count=None):
+        info = self.info()
+        count = info["nvec"] - first if count is None else count
+        out = np.empty((count, self.m // 32), dtype=np.uint32)
+        _check(lib.bvss_export_codes(self._h, first, count, C.c_void_p(out.ctypes.data)))
+        return out
+
+    def export_sketches(self, first=0, count=None):
+        count = self.n - first if count is None else count
+        if self.sketch_kind == "binary":
+            out = np.empty((count, self.m // 32), dtype=np.uint32)
+        else:
+            out = np.empty((count, self.m), dtype=np.uint8)
+        _check(lib.bvss_export_sketches(self._h, first, count, C.c_void_p(out.ctypes.data)))
+        return out
+
+    def error_bound(self, qnorm_max):
+        return lib.bvss_refine_error_bound(self._h, float(qnorm_max))
+
+    def info(self):
+        i = Info()
+        _check(lib.bvss_get_info(self._h, C.byref(i)))
+        return {f: getattr(i, f) for f, _ in i._fields_}
+
+    def stats(self):
+        s = Stats()
+        _check(lib.bvss_get_stats(self._h, C.byref(s)))
+        return s.as_dict()
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.bvss_free_index(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h

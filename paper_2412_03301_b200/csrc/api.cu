@@ -1,0 +1,911 @@
+// api.cu — host runtime and C ABI of libbvss (include/bvss.h).
+//
+// Owns the index (device buffers, stream, workspace), validates arguments,
+// generates the projection W (H2, reading R7), plans query sub-batches and
+// launches the kernels of the hot path:
+//   build : K1 encode (+K9 norms, bf16 split)  ->  K2 sketches
+//   search: K1/K2 on the queries -> K3 scan -> K4 select -> K5 refine -> K6 top-k
+#include <algorithm>
+#include <cstdarg>
+#include <cstdlib>
+#include <cstdio>
+#include <cstring>
+#include <cmath>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace bvss {
+
+// ---------------------------------------------------------------- errors --
+static thread_local char g_err[1024] = "";
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int post_launch(const char* what, cudaStream_t st) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("%s: launch failed: %s", what, cudaGetErrorString(e));
+    return BVSS_ECUDA;
+  }
+  static const bool dbg = [] {
+    const char* v = getenv("BVSS_DEBUG_SYNC");
+    return v && v[0] == '1';
+  }();
+  if (dbg) {
+    e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      set_error("%s: kernel failed: %s", what, cudaGetErrorString(e));
+      return BVSS_ECUDA;
+    }
+  }
+  return BVSS_OK;
+}
+
+// kernels (other translation units)
+int launch_encode(const float* V, int64_t nvec, int d, const uint16_t* Wt, int m, int s, int L, uint32_t* codes,
+                  float* norms, __nv_bfloat16* hi, __nv_bfloat16* lo, int dpad, int num_sms, cudaStream_t st);
+int launch_finite_check(const float* x, int64_t count, int* bad_dev, int num_sms, cudaStream_t st);
+int launch_sketch(const uint32_t* codes, int m, const int64_t* off, int64_t n, int kind, void* S, int32_t* mass,
+                  int64_t cstride, int64_t sstride, int num_sms, cudaStream_t st);
+int launch_unchunk(const void* S, int64_t n_stride, int64_t first, int64_t count, int words, uint32_t* out,
+                   cudaStream_t st);
+int launch_scan(int kind, const void* S, const int32_t* mass, int64_t n, int64_t n_stride, int m, const void* SQ,
+                const int32_t* massQ, int nq, void* keys, int64_t key_stride, int num_sms, cudaStream_t st);
+struct SelectState {
+  uint32_t* prefix;
+  int64_t* below;
+  int64_t* teff;
+  int64_t* eq;
+  int64_t* quota;
+  int32_t* digit;
+};
+int key_bits_for(int kind, int m);
+int rounds_for(int key_bits);
+int launch_select_init(SelectState st, int nq, int64_t teff, cudaStream_t s);
+int launch_select_hist(int key_size, const void* keys, int64_t key_stride, int64_t n, int nq, SelectState st,
+                       int key_bits, int r, int32_t* hist, cudaStream_t s);
+int launch_select_resolve(const int32_t* hist, SelectState st, int nq, int key_bits, int r, cudaStream_t s);
+int launch_select_quota(SelectState st, const int64_t* all_eq, int nq, int world, int rank, cudaStream_t s);
+int launch_select_tiecount(const int32_t* local_hist, SelectState st, int nq, int64_t* eq_out, cudaStream_t s);
+int launch_select_emit(int key_size, const void* keys, int64_t key_stride, int64_t n, int nq, SelectState st, int T,
+                       int64_t id_base, int32_t* cand, int32_t* score, int32_t* count, cudaStream_t s);
+int launch_refine_tc(const __nv_bfloat16* hi, const __nv_bfloat16* lo, const float* vnorm, const int64_t* off,
+                     int dpad, const __nv_bfloat16* qhi, const __nv_bfloat16* qlo, const float* qnorm,
+                     const int64_t* qoff, int max_mq, const int32_t* cand, const int32_t* count, int T, int nq,
+                     int64_t id_base, float* out_h2, int terms, int* work_counter,
+                     unsigned long long* rows_counter, int num_sms, cudaStream_t st);
+int launch_topk_fixup(const float* approx, const int32_t* cand, const int32_t* count, int T, int k, const float* V,
+                      const int64_t* off, int64_t id_base, int d, const float* Qv, const int64_t* qoff,
+                      const float* qnorm, float vmax2, float c1, float c2, int exact_all, int64_t* out_ids,
+                      float* out_dist, int nq, int64_t* fixup_counter, cudaStream_t st);
+int launch_merge_topk(const int64_t* ids, const float* dist, int P, int64_t nq, int k, int64_t* out_ids,
+                      float* out_dist, cudaStream_t st);
+
+// ------------------------------------------------------- small kernels --
+__global__ void max_float_kernel(const float* __restrict__ x, int64_t n, unsigned int* __restrict__ out) {
+  float m = 0.0f;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    m = fmaxf(m, x[i]);
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));  // values >= 0
+}
+__global__ void count_valid_kernel(const int32_t* __restrict__ cand, int T, int nq, int32_t* __restrict__ count) {
+  const int q = blockIdx.x;
+  int c = 0;
+  for (int i = threadIdx.x; i < T; i += blockDim.x) c += cand[static_cast<int64_t>(q) * T + i] >= 0 ? 1 : 0;
+  c = __reduce_add_sync(0xffffffffu, c);
+  __shared__ int s[8];
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < (blockDim.x >> 5); ++w) t += s[w];
+    count[q] = t;
+  }
+}
+
+// ------------------------------------------------------------ workspace --
+struct Workspace {
+  std::map<std::string, std::pair<void*, size_t>> bufs;
+  size_t total = 0;
+  int get(const char* name, size_t bytes, void** out) {
+    auto it = bufs.find(name);
+    if (it != bufs.end() && it->second.second >= bytes) {
+      *out = it->second.first;
+      return BVSS_OK;
+    }
+    if (it != bufs.end()) {
+      cudaFree(it->second.first);
+      total -= it->second.second;
+      bufs.erase(it);
+    }
+    void* p = nullptr;
+    const size_t b = bytes < 256 ? 256 : bytes;
+    BVSS_CUDA(cudaMalloc(&p, b));
+    bufs[name] = {p, b};
+    total += b;
+    *out = p;
+    return BVSS_OK;
+  }
+  void release() {
+    for (auto& kv : bufs) cudaFree(kv.second.first);
+    bufs.clear();
+    total = 0;
+  }
+};
+
+// ------------------------------------------------------------ projection --
+// H2: W from the seed, reading R7 (SplitMix64 per row, rejection of the
+// modulo-biased tail, distinct dims, sorted).  Independent of the oracle.
+static uint64_t splitmix_next(uint64_t& x) {
+  x += 0x9E3779B97F4A7C15ull;
+  uint64_t z = x;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+static void make_projection(uint64_t seed, int m, int s, int d, std::vector<uint16_t>& W) {
+  W.assign(static_cast<size_t>(m) * s, 0);
+  const uint64_t r = (0ull - static_cast<uint64_t>(d)) % static_cast<uint64_t>(d);  // 2^64 mod d
+  for (int j = 0; j < m; ++j) {
+    uint64_t x = seed ^ (static_cast<uint64_t>(j) * 0xD1B54A32D192ED03ull);
+    std::vector<int> chosen;
+    while (static_cast<int>(chosen.size()) < s) {
+      const uint64_t u = splitmix_next(x);
+      if (r != 0 && u >= 0ull - r) continue;  // u >= 2^64 - r
+      const int i = static_cast<int>(u % static_cast<uint64_t>(d));
+      bool dup = false;
+      for (int c : chosen) dup |= (c == i);
+      if (!dup) chosen.push_back(i);
+    }
+    std::sort(chosen.begin(), chosen.end());
+    for (int t = 0; t < s; ++t) W[static_cast<size_t>(j) * s + t] = static_cast<uint16_t>(chosen[t]);
+  }
+}
+
+}  // namespace bvss
+
+using namespace bvss;
+
+struct bvss_index {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
+  int num_sms = 148;
+  int64_t n = 0, nvec = 0;
+  int d = 0, dpad = 0;
+  uint32_t m = 0, s = 0, L = 0, sketch = 0;
+  uint64_t seed = 0;
+  int terms = 3;
+  uint32_t query_batch = 0;
+  std::vector<uint16_t> W;    // [m][s]
+  uint16_t* Wt = nullptr;     // device [s][m]
+  float* V = nullptr;         // [nvec][d]
+  int64_t* off = nullptr;     // [n+1]
+  __nv_bfloat16* hi = nullptr;
+  __nv_bfloat16* lo = nullptr;
+  float* vnorm = nullptr;
+  float vmax2 = 0.0f;
+  uint32_t* codes = nullptr;  // optional [nvec][m/32]
+  void* sk = nullptr;         // chunk-major sketches
+  int32_t* mass = nullptr;
+  size_t owned_bytes = 0;
+  Workspace ws;
+  bvss_stats stats{};
+  cudaEvent_t ev[8] = {};
+};
+
+struct bvss_search_ctx {
+  bvss_index* idx = nullptr;
+  int64_t nq = 0;
+  int k = 0, T = 0;
+  int64_t teff = 0;
+  int64_t id_base = 0;
+  int key_bits = 0, rounds = 0, next_round = 0;
+  int max_mq = 0;
+  int64_t nqvec = 0;
+  std::vector<int64_t> qoff_host;
+  // device
+  float* qv = nullptr;
+  int64_t* qoff = nullptr;
+  float* qnorm = nullptr;
+  __nv_bfloat16* qhi = nullptr;
+  __nv_bfloat16* qlo = nullptr;
+  void* keys = nullptr;
+  int64_t key_stride = 0;
+  SelectState sel{};
+  int32_t* local_hist = nullptr;
+  int32_t* cand = nullptr;
+  int32_t* count = nullptr;
+  float* approx = nullptr;
+  void* qsk = nullptr;        // query sketches, row-major padded to whole chunks
+  int32_t* qmass = nullptr;   // query sketch masses
+  uint32_t* qcodes = nullptr; // query codes
+  int nalloc = 0;
+  // buffers come from the index workspace (grow-only, reused across calls in the same order)
+  int alloc(size_t bytes, void** p);
+};
+
+int bvss_search_ctx::alloc(size_t bytes, void** p) {
+  const std::string name = "ctx" + std::to_string(nalloc++);
+  return idx->ws.get(name.c_str(), bytes, p);
+}
+
+namespace {
+
+int check_device(int dev, int* num_sms) {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) BVSS_FAIL(BVSS_EUNSUPPORTED, "no CUDA device available (no CPU fallback)");
+  if (dev < 0 || dev >= count) BVSS_FAIL(BVSS_EINVAL, "device %d out of range (%d visible)", dev, count);
+  cudaDeviceProp p;
+  BVSS_CUDA(cudaGetDeviceProperties(&p, dev));
+  if (p.major != 10) BVSS_FAIL(BVSS_EUNSUPPORTED, "device %d is sm_%d%d; this build targets sm_100a", dev, p.major, p.minor);
+  *num_sms = p.multiProcessorCount;
+  return BVSS_OK;
+}
+
+int check_offsets(const int64_t* o, int64_t n, const char* what) {
+  if (o[0] != 0) BVSS_FAIL(BVSS_EINVAL, "%s offsets must start at 0", what);
+  for (int64_t i = 0; i < n; ++i)
+    if (o[i + 1] <= o[i]) BVSS_FAIL(BVSS_EINVAL, "%s set %lld is empty or offsets decrease (Def 2: m >= 1)", what,
+                                    static_cast<long long>(i));
+  return BVSS_OK;
+}
+
+int to_device(bvss_index* idx, void* dst, const void* src, size_t bytes, bool dev_ptrs) {
+  if (bytes == 0) return BVSS_OK;
+  BVSS_CUDA(cudaMemcpyAsync(dst, src, bytes, dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, idx->stream));
+  return BVSS_OK;
+}
+int from_device(bvss_index* idx, void* dst, const void* src, size_t bytes, bool dev_ptrs) {
+  if (bytes == 0) return BVSS_OK;
+  BVSS_CUDA(cudaMemcpyAsync(dst, src, bytes, dev_ptrs ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, idx->stream));
+  return BVSS_OK;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+int chunks_per_set(const bvss_index* idx) {
+  return idx->sketch == BVSS_SKETCH_BINARY ? static_cast<int>(((idx->m / 32) + 3) / 4) : static_cast<int>(idx->m / 16);
+}
+
+// error-bound constants of the refine arithmetic
+void error_consts(const bvss_index* idx, float* c1, float* c2) {
+  const double u23 = std::ldexp(1.0, -23);
+  const double dd = static_cast<double>(idx->dpad);
+  const double prod = idx->terms == 3 ? 3.01 * std::ldexp(1.0, -18) : (2.0 * std::ldexp(1.0, -9) + std::ldexp(1.0, -18));
+  const double accum = (3.0 * dd + 64.0) * u23 * 1.01;
+  *c1 = static_cast<float>(2.0 * (prod + accum));
+  *c2 = static_cast<float>((dd + 4.0) * u23);
+}
+
+// host copy of an offsets array (device or host input), validated
+int host_offsets(bvss_index* idx, const int64_t* qoff_in, int64_t nq, bool dev_ptrs, std::vector<int64_t>& out) {
+  out.resize(nq + 1);
+  if (dev_ptrs) {
+    BVSS_CUDA(cudaMemcpyAsync(out.data(), qoff_in, (nq + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, idx->stream));
+    BVSS_CUDA(cudaStreamSynchronize(idx->stream));
+  } else {
+    std::memcpy(out.data(), qoff_in, (nq + 1) * sizeof(int64_t));
+  }
+  return check_offsets(out.data(), nq, "query");
+}
+
+// ---- query preparation (a-4, Alg 6 lines 1-2): copy, encode (+norms, bf16 split), sketch.
+// `queries` points at row qoff_host[0] == 0 of this batch; qoff_host is validated.
+int prepare_queries(bvss_index* idx, bvss_search_ctx* c, const float* queries, const std::vector<int64_t>& qoff_host,
+                    bool vec_dev, bool validate) {
+  const int64_t nq = static_cast<int64_t>(qoff_host.size()) - 1;
+  c->nq = nq;
+  c->qoff_host = qoff_host;
+  c->nqvec = qoff_host[nq];
+  int max_mq = 0;
+  for (int64_t i = 0; i < nq; ++i) {
+    const int64_t sz = qoff_host[i + 1] - qoff_host[i];
+    if (sz > max_mq) max_mq = static_cast<int>(sz > (1 << 30) ? (1 << 30) : sz);
+  }
+  c->max_mq = max_mq;
+  const int d = idx->d, dpad = idx->dpad, R = idx->m / 32;
+  cudaEventRecord(idx->ev[0], idx->stream);
+  BVSS_TRY(c->alloc(c->nqvec * d * sizeof(float), reinterpret_cast<void**>(&c->qv)));
+  BVSS_TRY(c->alloc((nq + 1) * sizeof(int64_t), reinterpret_cast<void**>(&c->qoff)));
+  BVSS_TRY(c->alloc(c->nqvec * sizeof(float), reinterpret_cast<void**>(&c->qnorm)));
+  BVSS_TRY(c->alloc(c->nqvec * dpad * sizeof(__nv_bfloat16), reinterpret_cast<void**>(&c->qhi)));
+  BVSS_TRY(c->alloc(c->nqvec * dpad * sizeof(__nv_bfloat16), reinterpret_cast<void**>(&c->qlo)));
+  BVSS_TRY(to_device(idx, c->qv, queries, c->nqvec * d * sizeof(float), vec_dev));
+  BVSS_CUDA(cudaMemcpyAsync(c->qoff, c->qoff_host.data(), (nq + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, idx->stream));
+  if (validate) {
+    int* bad;
+    BVSS_TRY(c->alloc(sizeof(int), reinterpret_cast<void**>(&bad)));
+    BVSS_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), idx->stream));
+    BVSS_TRY(launch_finite_check(c->qv, c->nqvec * d, bad, idx->num_sms, idx->stream));
+    int hbad = 0;
+    BVSS_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, idx->stream));
+    BVSS_CUDA(cudaStreamSynchronize(idx->stream));
+    if (hbad) BVSS_FAIL(BVSS_ENONFINITE, "queries contain NaN or Inf");
+  }
+  BVSS_TRY(c->alloc(c->nqvec * R * sizeof(uint32_t), reinterpret_cast<void**>(&c->qcodes)));
+  cudaEventRecord(idx->ev[1], idx->stream);
+  BVSS_TRY(launch_encode(c->qv, c->nqvec, d, idx->Wt, idx->m, idx->s, idx->L, c->qcodes, c->qnorm, c->qhi, c->qlo, dpad,
+                         idx->num_sms, idx->stream));
+  const int cps = chunks_per_set(idx);
+  BVSS_TRY(c->alloc(nq * cps * 16, &c->qsk));
+  BVSS_TRY(c->alloc(nq * sizeof(int32_t), reinterpret_cast<void**>(&c->qmass)));
+  BVSS_TRY(launch_sketch(c->qcodes, idx->m, c->qoff, nq, idx->sketch, c->qsk, c->qmass, 1, cps, idx->num_sms,
+                         idx->stream));
+  cudaEventRecord(idx->ev[2], idx->stream);
+  idx->stats.kernel_launches += 2;
+  return BVSS_OK;
+}
+
+// scan + select (local phases) for a prepared batch; when `global` the caller drives resolve
+int scan_batch(bvss_index* idx, bvss_search_ctx* c) {
+  const int64_t n = idx->n;
+  const int key_size = idx->sketch == BVSS_SKETCH_BINARY ? 2 : 4;
+  c->key_stride = (n + 7) & ~int64_t(7);
+  BVSS_TRY(c->alloc(static_cast<size_t>(c->nq) * c->key_stride * key_size, &c->keys));
+  BVSS_TRY(launch_scan(idx->sketch, idx->sk, idx->mass, n, n, idx->m, c->qsk, c->qmass, static_cast<int>(c->nq), c->keys,
+                       c->key_stride, idx->num_sms, idx->stream));
+  cudaEventRecord(idx->ev[3], idx->stream);
+  idx->stats.kernel_launches += 1;
+  idx->stats.scan_bytes += static_cast<uint64_t>(ceil_div<int64_t>(c->nq, 8)) * n * chunks_per_set(idx) * 16;
+  const int nq = static_cast<int>(c->nq);
+  BVSS_TRY(c->alloc(nq * sizeof(uint32_t), reinterpret_cast<void**>(&c->sel.prefix)));
+  BVSS_TRY(c->alloc(nq * sizeof(int64_t), reinterpret_cast<void**>(&c->sel.below)));
+  BVSS_TRY(c->alloc(nq * sizeof(int64_t), reinterpret_cast<void**>(&c->sel.teff)));
+  BVSS_TRY(c->alloc(nq * sizeof(int64_t), reinterpret_cast<void**>(&c->sel.eq)));
+  BVSS_TRY(c->alloc(nq * sizeof(int64_t), reinterpret_cast<void**>(&c->sel.quota)));
+  BVSS_TRY(c->alloc(nq * sizeof(int32_t), reinterpret_cast<void**>(&c->sel.digit)));
+  BVSS_TRY(c->alloc(static_cast<size_t>(nq) * kHistBins * sizeof(int32_t), reinterpret_cast<void**>(&c->local_hist)));
+  BVSS_TRY(launch_select_init(c->sel, nq, c->teff, idx->stream));
+  c->key_bits = key_bits_for(idx->sketch, idx->m);
+  c->rounds = rounds_for(c->key_bits);
+  c->next_round = 0;
+  return BVSS_OK;
+}
+
+int emit_refine_topk(bvss_index* idx, bvss_search_ctx* c, int64_t* out_ids_dev, float* out_dist_dev, bool refine) {
+  const int nq = static_cast<int>(c->nq);
+  const int key_size = idx->sketch == BVSS_SKETCH_BINARY ? 2 : 4;
+  BVSS_TRY(c->alloc(static_cast<size_t>(nq) * c->T * sizeof(int32_t), reinterpret_cast<void**>(&c->cand)));
+  BVSS_TRY(c->alloc(nq * sizeof(int32_t), reinterpret_cast<void**>(&c->count)));
+  BVSS_TRY(launch_select_emit(key_size, c->keys, c->key_stride, idx->n, nq, c->sel, c->T, c->id_base, c->cand, nullptr,
+                              c->count, idx->stream));
+  cudaEventRecord(idx->ev[4], idx->stream);
+  idx->stats.kernel_launches += 1;
+  if (!refine) return BVSS_OK;
+  int exact_all = 0;
+  if (idx->terms != 0) {
+    BVSS_TRY(c->alloc(static_cast<size_t>(nq) * c->T * sizeof(float), reinterpret_cast<void**>(&c->approx)));
+    int* counter;
+    BVSS_TRY(idx->ws.get("work_counter", sizeof(int), reinterpret_cast<void**>(&counter)));
+    unsigned long long* rows;
+    BVSS_TRY(idx->ws.get("rows_counter", sizeof(unsigned long long), reinterpret_cast<void**>(&rows)));
+    BVSS_TRY(launch_refine_tc(idx->hi, idx->lo, idx->vnorm, idx->off, idx->dpad, c->qhi, c->qlo, c->qnorm, c->qoff,
+                              c->max_mq, c->cand, c->count, c->T, nq, c->id_base, c->approx, idx->terms, counter,
+                              rows, idx->num_sms, idx->stream));
+    idx->stats.kernel_launches += 1;
+  } else {
+    exact_all = 1;
+  }
+  cudaEventRecord(idx->ev[5], idx->stream);
+  float c1, c2;
+  error_consts(idx, &c1, &c2);
+  int64_t* fix;
+  BVSS_TRY(idx->ws.get("fixup_counter", sizeof(int64_t), reinterpret_cast<void**>(&fix)));
+  BVSS_CUDA(cudaMemsetAsync(fix, 0, sizeof(int64_t), idx->stream));
+  BVSS_TRY(launch_topk_fixup(c->approx, c->cand, c->count, c->T, c->k, idx->V, idx->off, c->id_base, idx->d, c->qv,
+                             c->qoff, c->qnorm, idx->vmax2, c1, c2, exact_all, out_ids_dev, out_dist_dev, nq, fix,
+                             idx->stream));
+  cudaEventRecord(idx->ev[6], idx->stream);
+  idx->stats.kernel_launches += 1;
+  return BVSS_OK;
+}
+
+float ev_ms(bvss_index* idx, int a, int b) {
+  float ms = 0.0f;
+  if (cudaEventElapsedTime(&ms, idx->ev[a], idx->ev[b]) != cudaSuccess) return 0.0f;
+  return ms;
+}
+
+int run_select_single(bvss_index* idx, bvss_search_ctx* c) {
+  const int nq = static_cast<int>(c->nq);
+  const int key_size = idx->sketch == BVSS_SKETCH_BINARY ? 2 : 4;
+  for (int r = 0; r < c->rounds; ++r) {
+    BVSS_TRY(launch_select_hist(key_size, c->keys, c->key_stride, idx->n, nq, c->sel, c->key_bits, r, c->local_hist,
+                                idx->stream));
+    BVSS_TRY(launch_select_resolve(c->local_hist, c->sel, nq, c->key_bits, r, idx->stream));
+    idx->stats.kernel_launches += 2;
+  }
+  return BVSS_OK;
+}
+
+int make_ctx(bvss_index* idx, const float* queries, const std::vector<int64_t>& qoff_host, int k, int T,
+             int64_t n_total, uint32_t flags, std::unique_ptr<bvss_search_ctx>& c) {
+  c.reset(new bvss_search_ctx());
+  c->idx = idx;
+  c->k = k;
+  c->T = T;
+  c->teff = T < n_total ? T : n_total;
+  BVSS_TRY(prepare_queries(idx, c.get(), queries, qoff_host, (flags & BVSS_DEVICE_PTRS) != 0,
+                           (flags & BVSS_VALIDATE_FINITE) != 0));
+  BVSS_TRY(scan_batch(idx, c.get()));
+  return BVSS_OK;
+}
+
+int validate_search(bvss_index* idx, const float* q, const int64_t* qo, int64_t nq, int k, int T) {
+  if (!idx) BVSS_FAIL(BVSS_EINVAL, "null index");
+  if (!q || !qo) BVSS_FAIL(BVSS_EINVAL, "null query pointer");
+  if (nq < 1) BVSS_FAIL(BVSS_EINVAL, "nq must be >= 1");
+  if (k < 1) BVSS_FAIL(BVSS_EINVAL, "k must be >= 1");
+  if (T < k) BVSS_FAIL(BVSS_EINVAL, "T (%d) < k (%d) (reading R16)", T, k);
+  return BVSS_OK;
+}
+
+int64_t batch_size(const bvss_index* idx, int64_t nq) {
+  if (idx->query_batch) return idx->query_batch < nq ? idx->query_batch : nq;
+  const int key_size = idx->sketch == BVSS_SKETCH_BINARY ? 2 : 4;
+  const double per_q = static_cast<double>((idx->n + 7) & ~int64_t(7)) * key_size;
+  int64_t b = static_cast<int64_t>((4.0 * (1ull << 30)) / per_q);
+  if (b > 4096) b = 4096;
+  if (b < 1) b = 1;
+  return b < nq ? b : nq;
+}
+
+}  // namespace
+
+// =================================================================== ABI ==
+extern "C" {
+
+const char* bvss_last_error(void) { return g_err; }
+
+int bvss_device_count(void) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess) return 0;
+  int ok = 0;
+  for (int i = 0; i < count; ++i) {
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, i) == cudaSuccess && p.major == 10) ++ok;
+  }
+  return ok;
+}
+
+int bvss_build_index(const float* vectors, const int64_t* set_offsets, int64_t n, int32_t d, const bvss_params* p,
+                     bvss_index** out) {
+  if (!out) BVSS_FAIL(BVSS_EINVAL, "null out");
+  *out = nullptr;
+  if (!vectors || !set_offsets || !p) BVSS_FAIL(BVSS_EINVAL, "null argument");
+  if (n < 1) BVSS_FAIL(BVSS_EINVAL, "n must be >= 1");
+  if (d < 1 || d > 65535) BVSS_FAIL(BVSS_EINVAL, "d must be in [1, 65535]");
+  if (p->m < 32 || p->m % 32 || p->m > 2048) BVSS_FAIL(BVSS_EINVAL, "m must be a multiple of 32 in [32, 2048]");
+  if (p->L < 1 || p->L > p->m) BVSS_FAIL(BVSS_EINVAL, "L must be in [1, m]");
+  if (p->s < 1 || static_cast<int>(p->s) > d || p->s > 32) BVSS_FAIL(BVSS_EINVAL, "s must be in [1, min(d, 32)]");
+  if (p->sketch > 1) BVSS_FAIL(BVSS_EINVAL, "unknown sketch kind");
+  if (p->refine_terms != 0 && p->refine_terms != 1 && p->refine_terms != 3 && p->refine_terms != 0xFFFFFFFFu)
+    BVSS_FAIL(BVSS_EINVAL, "refine_terms must be 3, 1 or 0");
+  int num_sms = 0;
+  BVSS_TRY(check_device(p->device, &num_sms));
+  DeviceGuard g(p->device);
+  const bool dev_ptrs = (p->flags & BVSS_DEVICE_PTRS) != 0;
+  std::vector<int64_t> off_h(n + 1);
+  if (dev_ptrs) {
+    BVSS_CUDA(cudaMemcpy(off_h.data(), set_offsets, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));  // before any work
+  } else {
+    std::memcpy(off_h.data(), set_offsets, (n + 1) * sizeof(int64_t));
+  }
+  BVSS_TRY(check_offsets(off_h.data(), n, "database"));
+  std::unique_ptr<bvss_index> idx(new bvss_index());
+  idx->device = p->device;
+  idx->num_sms = num_sms;
+  idx->n = n;
+  idx->nvec = off_h[n];
+  idx->d = d;
+  idx->dpad = (d + 63) / 64 * 64;
+  idx->m = p->m;
+  idx->s = p->s;
+  idx->L = p->L;
+  idx->sketch = p->sketch;
+  idx->seed = p->seed;
+  idx->terms = (p->refine_terms == 1 || p->refine_terms == 0) ? static_cast<int>(p->refine_terms) : 3;
+  idx->query_batch = p->query_batch;
+  BVSS_CUDA(cudaStreamCreateWithFlags(&idx->own_stream, cudaStreamNonBlocking));
+  idx->stream = idx->own_stream;
+  for (auto& e : idx->ev) BVSS_CUDA(cudaEventCreate(&e));
+  cudaStream_t st = idx->stream;
+  const int64_t nvec = idx->nvec;
+  const int R = p->m / 32;
+  auto dalloc = [&](size_t bytes, void** ptr) -> int {
+    BVSS_CUDA(cudaMalloc(ptr, bytes < 256 ? 256 : bytes));
+    idx->owned_bytes += bytes;
+    return BVSS_OK;
+  };
+  // projection
+  if (p->projection) {
+    idx->W.assign(p->projection, p->projection + static_cast<size_t>(p->m) * p->s);
+    for (uint32_t j = 0; j < p->m; ++j)
+      for (uint32_t t = 0; t < p->s; ++t) {
+        const uint16_t v = idx->W[j * p->s + t];
+        if (v >= d || (t > 0 && v <= idx->W[j * p->s + t - 1]))
+          BVSS_FAIL(BVSS_EINVAL, "projection row %u must hold s sorted distinct dims < d", j);
+      }
+  } else {
+    make_projection(p->seed, p->m, p->s, d, idx->W);
+  }
+  std::vector<uint16_t> Wt(static_cast<size_t>(p->m) * p->s);
+  for (uint32_t j = 0; j < p->m; ++j)
+    for (uint32_t t = 0; t < p->s; ++t) Wt[static_cast<size_t>(t) * p->m + j] = idx->W[static_cast<size_t>(j) * p->s + t];
+  BVSS_TRY(dalloc(Wt.size() * 2, reinterpret_cast<void**>(&idx->Wt)));
+  BVSS_CUDA(cudaMemcpyAsync(idx->Wt, Wt.data(), Wt.size() * 2, cudaMemcpyHostToDevice, idx->stream));
+  BVSS_CUDA(cudaStreamSynchronize(idx->stream));
+  // data
+  BVSS_TRY(dalloc(static_cast<size_t>(nvec) * d * 4, reinterpret_cast<void**>(&idx->V)));
+  BVSS_TRY(dalloc((n + 1) * 8, reinterpret_cast<void**>(&idx->off)));
+  BVSS_TRY(to_device(idx.get(), idx->V, vectors, static_cast<size_t>(nvec) * d * 4, dev_ptrs));
+  BVSS_CUDA(cudaMemcpyAsync(idx->off, off_h.data(), (n + 1) * 8, cudaMemcpyHostToDevice, st));
+  if (p->flags & BVSS_VALIDATE_FINITE) {
+    int* bad;
+    BVSS_TRY(idx->ws.get("bad", sizeof(int), reinterpret_cast<void**>(&bad)));
+    BVSS_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), st));
+    BVSS_TRY(launch_finite_check(idx->V, nvec * d, bad, num_sms, st));
+    int hbad = 0;
+    BVSS_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    BVSS_CUDA(cudaStreamSynchronize(st));
+    if (hbad) BVSS_FAIL(BVSS_ENONFINITE, "database vectors contain NaN or Inf");
+  }
+  BVSS_TRY(dalloc(static_cast<size_t>(nvec) * idx->dpad * 2, reinterpret_cast<void**>(&idx->hi)));
+  BVSS_TRY(dalloc(static_cast<size_t>(nvec) * idx->dpad * 2, reinterpret_cast<void**>(&idx->lo)));
+  BVSS_TRY(dalloc(static_cast<size_t>(nvec) * 4, reinterpret_cast<void**>(&idx->vnorm)));
+  uint32_t* codes = nullptr;
+  const bool keep = (p->flags & BVSS_KEEP_CODES) != 0;
+  if (keep) {
+    BVSS_TRY(dalloc(static_cast<size_t>(nvec) * R * 4, reinterpret_cast<void**>(&idx->codes)));
+    codes = idx->codes;
+  } else {
+    BVSS_TRY(idx->ws.get("codes", static_cast<size_t>(nvec) * R * 4, reinterpret_cast<void**>(&codes)));
+  }
+  BVSS_TRY(launch_encode(idx->V, nvec, d, idx->Wt, p->m, p->s, p->L, codes, idx->vnorm, idx->hi, idx->lo, idx->dpad,
+                         num_sms, st));
+  const int cps = chunks_per_set(idx.get());
+  BVSS_TRY(dalloc(static_cast<size_t>(n) * cps * 16, &idx->sk));
+  BVSS_TRY(dalloc(static_cast<size_t>(n) * 4, reinterpret_cast<void**>(&idx->mass)));
+  BVSS_TRY(launch_sketch(codes, p->m, idx->off, n, p->sketch, idx->sk, idx->mass, n, 1, num_sms, st));
+  unsigned int* vmax;
+  BVSS_TRY(idx->ws.get("vmax", sizeof(unsigned int), reinterpret_cast<void**>(&vmax)));
+  BVSS_CUDA(cudaMemsetAsync(vmax, 0, sizeof(unsigned int), st));
+  max_float_kernel<<<num_sms * 2, 256, 0, st>>>(idx->vnorm, nvec, vmax);
+  BVSS_TRY(post_launch("max_float_kernel", st));
+  unsigned int hv = 0;
+  BVSS_CUDA(cudaMemcpyAsync(&hv, vmax, sizeof(hv), cudaMemcpyDeviceToHost, st));
+  BVSS_CUDA(cudaStreamSynchronize(st));
+  std::memcpy(&idx->vmax2, &hv, 4);
+  if (!keep) {
+    idx->ws.release();
+  }
+  *out = idx.release();
+  return BVSS_OK;
+}
+
+void bvss_free_index(bvss_index* idx) {
+  if (!idx) return;
+  DeviceGuard g(idx->device);
+  if (idx->stream) cudaStreamSynchronize(idx->stream);
+  void* ptrs[] = {idx->Wt, idx->V, idx->off, idx->hi, idx->lo, idx->vnorm, idx->codes, idx->sk, idx->mass};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  idx->ws.release();
+  for (auto& e : idx->ev)
+    if (e) cudaEventDestroy(e);
+  if (idx->own_stream) cudaStreamDestroy(idx->own_stream);
+  delete idx;
+}
+
+int bvss_set_stream(bvss_index* idx, void* stream) {
+  if (!idx) BVSS_FAIL(BVSS_EINVAL, "null index");
+  idx->stream = stream ? static_cast<cudaStream_t>(stream) : idx->own_stream;
+  return BVSS_OK;
+}
+
+int bvss_get_info(const bvss_index* idx, bvss_info* out) {
+  if (!idx || !out) BVSS_FAIL(BVSS_EINVAL, "null argument");
+  out->n = idx->n;
+  out->nvec = idx->nvec;
+  out->d = idx->d;
+  out->dpad = idx->dpad;
+  out->m = idx->m;
+  out->s = idx->s;
+  out->L = idx->L;
+  out->sketch = idx->sketch;
+  out->device = idx->device;
+  out->device_bytes = idx->owned_bytes;
+  out->workspace_bytes = idx->ws.total;
+  return BVSS_OK;
+}
+
+int bvss_get_stats(const bvss_index* idx, bvss_stats* out) {
+  if (!idx || !out) BVSS_FAIL(BVSS_EINVAL, "null argument");
+  *out = idx->stats;
+  return BVSS_OK;
+}
+
+double bvss_refine_error_bound(const bvss_index* idx, double qnorm_max) {
+  if (!idx) return -1.0;
+  float c1, c2;
+  error_consts(idx, &c1, &c2);
+  const double mv = std::sqrt(static_cast<double>(idx->vmax2));
+  return c1 * qnorm_max * mv + c2 * (qnorm_max * qnorm_max + idx->vmax2);
+}
+
+int bvss_export_projection(const bvss_index* idx, uint16_t* out) {
+  if (!idx || !out) BVSS_FAIL(BVSS_EINVAL, "null argument");
+  std::memcpy(out, idx->W.data(), idx->W.size() * 2);
+  return BVSS_OK;
+}
+
+int bvss_export_codes(const bvss_index* idx, int64_t first, int64_t count, uint32_t* out) {
+  if (!idx || !out) BVSS_FAIL(BVSS_EINVAL, "null argument");
+  if (!idx->codes) BVSS_FAIL(BVSS_ESTATE, "index was built without BVSS_KEEP_CODES");
+  if (first < 0 || count < 0 || first + count > idx->nvec) BVSS_FAIL(BVSS_EINVAL, "vector range out of bounds");
+  DeviceGuard g(idx->device);
+  const size_t R = idx->m / 32;
+  BVSS_CUDA(cudaMemcpyAsync(out, idx->codes + first * R, count * R * 4, cudaMemcpyDeviceToHost, idx->stream));
+  BVSS_CUDA(cudaStreamSynchronize(idx->stream));
+  return BVSS_OK;
+}
+
+int bvss_export_sketches(const bvss_index* idx_c, int64_t first, int64_t count, void* out) {
+  bvss_index* idx = const_cast<bvss_index*>(idx_c);
+  if (!idx || !out) BVSS_FAIL(BVSS_EINVAL, "null argument");
+  if (first < 0 || count < 0 || first + count > idx->n) BVSS_FAIL(BVSS_EINVAL, "set range out of bounds");
+  DeviceGuard g(idx->device);
+  const int words = idx->sketch == BVSS_SKETCH_BINARY ? static_cast<int>(idx->m / 32) : static_cast<int>(idx->m / 4);
+  uint32_t* tmp;
+  BVSS_TRY(idx->ws.get("export", static_cast<size_t>(count) * words * 4, reinterpret_cast<void**>(&tmp)));
+  BVSS_TRY(launch_unchunk(idx->sk, idx->n, first, count, words, tmp, idx->stream));
+  BVSS_CUDA(cudaMemcpyAsync(out, tmp, static_cast<size_t>(count) * words * 4, cudaMemcpyDeviceToHost, idx->stream));
+  BVSS_CUDA(cudaStreamSynchronize(idx->stream));
+  return BVSS_OK;
+}
+
+int bvss_query_sketch(bvss_index* idx, const float* queries, const int64_t* query_offsets, int64_t nq, void* out_sketch,
+                      uint32_t* out_codes, uint32_t flags) {
+  if (!idx || !queries || !query_offsets || !out_sketch) BVSS_FAIL(BVSS_EINVAL, "null argument");
+  if (nq < 1) BVSS_FAIL(BVSS_EINVAL, "nq must be >= 1");
+  DeviceGuard g(idx->device);
+  const bool dev = (flags & BVSS_DEVICE_PTRS) != 0;
+  std::vector<int64_t> qo;
+  BVSS_TRY(host_offsets(idx, query_offsets, nq, dev, qo));
+  std::unique_ptr<bvss_search_ctx> c(new bvss_search_ctx());
+  c->idx = idx;
+  BVSS_TRY(prepare_queries(idx, c.get(), queries, qo, dev, (flags & BVSS_VALIDATE_FINITE) != 0));
+  const int cps = chunks_per_set(idx);
+  const size_t row_bytes = idx->sketch == BVSS_SKETCH_BINARY ? idx->m / 8 : idx->m;
+  BVSS_CUDA(cudaMemcpy2DAsync(out_sketch, row_bytes, c->qsk, static_cast<size_t>(cps) * 16, row_bytes, nq,
+                              dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, idx->stream));
+  if (out_codes)
+    BVSS_TRY(from_device(idx, out_codes, c->qcodes, static_cast<size_t>(c->nqvec) * (idx->m / 32) * 4, dev));
+  BVSS_CUDA(cudaStreamSynchronize(idx->stream));
+  return BVSS_OK;
+}
+
+int bvss_filter(bvss_index* idx, const float* queries, const int64_t* query_offsets, int64_t nq, int32_t T,
+                int32_t* out_cand, int32_t* out_score, uint32_t flags) {
+  BVSS_TRY(validate_search(idx, queries, query_offsets, nq, 1, T));
+  if (!out_cand) BVSS_FAIL(BVSS_EINVAL, "null out_cand");
+  DeviceGuard g(idx->device);
+  const bool dev = (flags & BVSS_DEVICE_PTRS) != 0;
+  std::vector<int64_t> qo;
+  BVSS_TRY(host_offsets(idx, query_offsets, nq, dev, qo));
+  std::unique_ptr<bvss_search_ctx> c;
+  BVSS_TRY(make_ctx(idx, queries, qo, 1, T, idx->n, flags, c));
+  BVSS_TRY(run_select_single(idx, c.get()));
+  const int key_size = idx->sketch == BVSS_SKETCH_BINARY ? 2 : 4;
+  int32_t *cand, *score;
+  BVSS_TRY(c->alloc(static_cast<size_t>(nq) * T * 4, reinterpret_cast<void**>(&cand)));
+  BVSS_TRY(c->alloc(static_cast<size_t>(nq) * T * 4, reinterpret_cast<void**>(&score)));
+  BVSS_TRY(launch_select_emit(key_size, c->keys, c->key_stride, idx->n, static_cast<int>(nq), c->sel, T, 0, cand, score,
+                              nullptr, idx->stream));
+  BVSS_TRY(from_device(idx, out_cand, cand, static_cast<size_t>(nq) * T * 4, dev));
+  if (out_score) BVSS_TRY(from_device(idx, out_score, score, static_cast<size_t>(nq) * T * 4, dev));
+  BVSS_CUDA(cudaStreamSynchronize(idx->stream));
+  return BVSS_OK;
+}
+
+int bvss_refine(bvss_index* idx, const float* queries, const int64_t* query_offsets, int64_t nq, const int32_t* cand,
+                int32_t T, int32_t k, int64_t* out_ids, float* out_dist, float* out_approx, uint32_t flags) {
+  BVSS_TRY(validate_search(idx, queries, query_offsets, nq, k, T < k ? k : T));
+  if (!cand || !out_ids || !out_dist) BVSS_FAIL(BVSS_EINVAL, "null argument");
+  DeviceGuard g(idx->device);
+  const bool dev = (flags & BVSS_DEVICE_PTRS) != 0;
+  std::vector<int64_t> qo;
+  BVSS_TRY(host_offsets(idx, query_offsets, nq, dev, qo));
+  std::unique_ptr<bvss_search_ctx> c(new bvss_search_ctx());
+  c->idx = idx;
+  c->k = k;
+  c->T = T;
+  BVSS_TRY(prepare_queries(idx, c.get(), queries, qo, dev, (flags & BVSS_VALIDATE_FINITE) != 0));
+  BVSS_TRY(c->alloc(static_cast<size_t>(nq) * T * 4, reinterpret_cast<void**>(&c->cand)));
+  BVSS_TRY(c->alloc(nq * 4, reinterpret_cast<void**>(&c->count)));
+  BVSS_TRY(to_device(idx, c->cand, cand, static_cast<size_t>(nq) * T * 4, dev));
+  count_valid_kernel<<<static_cast<int>(nq), 256, 0, idx->stream>>>(c->cand, T, static_cast<int>(nq), c->count);
+  BVSS_TRY(post_launch("count_valid_kernel", idx->stream));
+  int64_t* oid;
+  float* odist;
+  BVSS_TRY(c->alloc(static_cast<size_t>(nq) * k * 8, reinterpret_cast<void**>(&oid)));
+  BVSS_TRY(c->alloc(static_cast<size_t>(nq) * k * 4, reinterpret_cast<void**>(&odist)));
+  int exact_all = 0;
+  if (idx->terms != 0) {
+    BVSS_TRY(c->alloc(static_cast<size_t>(nq) * T * 4, reinterpret_cast<void**>(&c->approx)));
+    BVSS_CUDA(cudaMemsetAsync(c->approx, 0xFF, static_cast<size_t>(nq) * T * 4, idx->stream));  // NaN where unused
+    int* counter;
+    BVSS_TRY(idx->ws.get("work_counter", sizeof(int), reinterpret_cast<void**>(&counter)));
+    BVSS_TRY(launch_refine_tc(idx->hi, idx->lo, idx->vnorm, idx->off, idx->dpad, c->qhi, c->qlo, c->qnorm, c->qoff,
+                              c->max_mq, c->cand, c->count, T, static_cast<int>(nq), 0, c->approx, idx->terms, counter,
+                              nullptr, idx->num_sms, idx->stream));
+  } else {
+    exact_all = 1;
+  }
+  float c1, c2;
+  error_consts(idx, &c1, &c2);
+  BVSS_TRY(launch_topk_fixup(c->approx, c->cand, c->count, T, k, idx->V, idx->off, 0, idx->d, c->qv, c->qoff, c->qnorm,
+                             idx->vmax2, c1, c2, exact_all, oid, odist, static_cast<int>(nq), nullptr, idx->stream));
+  BVSS_TRY(from_device(idx, out_ids, oid, static_cast<size_t>(nq) * k * 8, dev));
+  BVSS_TRY(from_device(idx, out_dist, odist, static_cast<size_t>(nq) * k * 4, dev));
+  if (out_approx && c->approx) BVSS_TRY(from_device(idx, out_approx, c->approx, static_cast<size_t>(nq) * T * 4, dev));
+  BVSS_CUDA(cudaStreamSynchronize(idx->stream));
+  return BVSS_OK;
+}
+
+int bvss_search(bvss_index* idx, const float* queries, const int64_t* query_offsets, int64_t nq, int32_t k, int32_t T,
+                int64_t* out_ids, float* out_dist, uint32_t flags) {
+  BVSS_TRY(validate_search(idx, queries, query_offsets, nq, k, T));
+  if (!out_ids || !out_dist) BVSS_FAIL(BVSS_EINVAL, "null output");
+  DeviceGuard g(idx->device);
+  const bool dev = (flags & BVSS_DEVICE_PTRS) != 0;
+  std::vector<int64_t> qo;
+  BVSS_TRY(host_offsets(idx, query_offsets, nq, dev, qo));
+  idx->stats = bvss_stats{};
+  const int64_t B = batch_size(idx, nq);
+  idx->stats.query_batch = static_cast<int32_t>(B);
+  int64_t* oid;
+  float* odist;
+  BVSS_TRY(idx->ws.get("out_ids", static_cast<size_t>(B) * k * 8, reinterpret_cast<void**>(&oid)));
+  BVSS_TRY(idx->ws.get("out_dist", static_cast<size_t>(B) * k * 4, reinterpret_cast<void**>(&odist)));
+  int64_t* fix;
+  unsigned long long* rows;
+  BVSS_TRY(idx->ws.get("rows_counter", sizeof(unsigned long long), reinterpret_cast<void**>(&rows)));
+  BVSS_CUDA(cudaMemsetAsync(rows, 0, sizeof(unsigned long long), idx->stream));
+  float ms[6] = {0, 0, 0, 0, 0, 0};
+  float tot = 0.0f;
+  uint64_t fixups = 0;
+  for (int64_t b0 = 0; b0 < nq; b0 += B) {
+    const int64_t nb = (b0 + B <= nq) ? B : nq - b0;
+    std::vector<int64_t> sub(nb + 1);
+    for (int64_t i = 0; i <= nb; ++i) sub[i] = qo[b0 + i] - qo[b0];
+    std::unique_ptr<bvss_search_ctx> c;
+    BVSS_TRY(make_ctx(idx, queries + qo[b0] * idx->d, sub, k, T, idx->n, flags, c));
+    BVSS_TRY(run_select_single(idx, c.get()));
+    BVSS_TRY(emit_refine_topk(idx, c.get(), oid, odist, true));
+    BVSS_TRY(from_device(idx, out_ids + b0 * k, oid, static_cast<size_t>(nb) * k * 8, dev));
+    BVSS_TRY(from_device(idx, out_dist + b0 * k, odist, static_cast<size_t>(nb) * k * 4, dev));
+    BVSS_CUDA(cudaEventRecord(idx->ev[7], idx->stream));
+    BVSS_CUDA(cudaStreamSynchronize(idx->stream));
+    for (int i = 0; i < 6; ++i) ms[i] += ev_ms(idx, i, i + 1);
+    tot += ev_ms(idx, 0, 7);
+    BVSS_TRY(idx->ws.get("fixup_counter", sizeof(int64_t), reinterpret_cast<void**>(&fix)));
+    int64_t hf = 0;
+    BVSS_CUDA(cudaMemcpyAsync(&hf, fix, sizeof(hf), cudaMemcpyDeviceToHost, idx->stream));
+    BVSS_CUDA(cudaStreamSynchronize(idx->stream));
+    fixups += static_cast<uint64_t>(hf);
+  }
+  idx->stats.ms_h2d = ms[0];
+  idx->stats.ms_encode = ms[1];
+  idx->stats.ms_scan = ms[2];
+  idx->stats.ms_select = ms[3];
+  idx->stats.ms_refine = ms[4];
+  idx->stats.ms_topk = ms[5];
+  idx->stats.ms_total = tot;
+  idx->stats.fixup_sets = fixups;
+  unsigned long long hr = 0;
+  BVSS_CUDA(cudaMemcpyAsync(&hr, rows, sizeof(hr), cudaMemcpyDeviceToHost, idx->stream));
+  BVSS_CUDA(cudaStreamSynchronize(idx->stream));
+  idx->stats.cand_rows = hr;
+  idx->stats.gather_bytes = hr * static_cast<uint64_t>(idx->dpad) * 2u * (idx->terms == 3 ? 2u : 1u);
+  return BVSS_OK;
+}
+
+// ------------------------------------------------------------- sharded --
+int bvss_dist_begin(bvss_index* idx, const float* queries, const int64_t* query_offsets, int64_t nq, int32_t k,
+                    int32_t T, int64_t id_base, uint32_t flags, bvss_search_ctx** out, int32_t* rounds) {
+  if (!out || !rounds) BVSS_FAIL(BVSS_EINVAL, "null out");
+  *out = nullptr;
+  BVSS_TRY(validate_search(idx, queries, query_offsets, nq, k, T));
+  DeviceGuard g(idx->device);
+  std::vector<int64_t> qo;
+  BVSS_TRY(host_offsets(idx, query_offsets, nq, (flags & BVSS_DEVICE_PTRS) != 0, qo));
+  std::unique_ptr<bvss_search_ctx> c;
+  // T is the GLOBAL budget, already clamped by the caller to the total number of sets
+  BVSS_TRY(make_ctx(idx, queries, qo, k, T, int64_t(1) << 62, flags, c));
+  c->id_base = id_base;
+  *rounds = c->rounds;
+  *out = c.release();
+  return BVSS_OK;
+}
+
+int bvss_dist_hist(bvss_search_ctx* c, int32_t round, int32_t* hist_dev) {
+  if (!c || !hist_dev) BVSS_FAIL(BVSS_EINVAL, "null argument");
+  if (round != c->next_round || round >= c->rounds) BVSS_FAIL(BVSS_ESTATE, "rounds must run in order");
+  bvss_index* idx = c->idx;
+  DeviceGuard g(idx->device);
+  const int key_size = idx->sketch == BVSS_SKETCH_BINARY ? 2 : 4;
+  BVSS_TRY(launch_select_hist(key_size, c->keys, c->key_stride, idx->n, static_cast<int>(c->nq), c->sel, c->key_bits,
+                              round, c->local_hist, idx->stream));
+  BVSS_CUDA(cudaMemcpyAsync(hist_dev, c->local_hist, static_cast<size_t>(c->nq) * kHistBins * 4,
+                            cudaMemcpyDeviceToDevice, idx->stream));
+  return BVSS_OK;
+}
+
+int bvss_dist_resolve(bvss_search_ctx* c, int32_t round, const int32_t* global_hist_dev) {
+  if (!c || !global_hist_dev) BVSS_FAIL(BVSS_EINVAL, "null argument");
+  if (round != c->next_round) BVSS_FAIL(BVSS_ESTATE, "rounds must run in order");
+  bvss_index* idx = c->idx;
+  DeviceGuard g(idx->device);
+  BVSS_TRY(launch_select_resolve(global_hist_dev, c->sel, static_cast<int>(c->nq), c->key_bits, round, idx->stream));
+  c->next_round++;
+  return BVSS_OK;
+}
+
+int bvss_dist_tie_counts(bvss_search_ctx* c, int64_t* eq_dev) {
+  if (!c || !eq_dev) BVSS_FAIL(BVSS_EINVAL, "null argument");
+  if (c->next_round != c->rounds) BVSS_FAIL(BVSS_ESTATE, "resolve every round first");
+  DeviceGuard g(c->idx->device);
+  BVSS_TRY(launch_select_tiecount(c->local_hist, c->sel, static_cast<int>(c->nq), eq_dev, c->idx->stream));
+  return BVSS_OK;
+}
+
+int bvss_dist_finish(bvss_search_ctx* c, const int64_t* all_eq_dev, int32_t world, int32_t rank, int64_t* topk_ids_dev,
+                     float* topk_dist_dev) {
+  if (!c || !all_eq_dev || !topk_ids_dev || !topk_dist_dev) BVSS_FAIL(BVSS_EINVAL, "null argument");
+  if (c->next_round != c->rounds) BVSS_FAIL(BVSS_ESTATE, "resolve every round first");
+  if (world < 1 || rank < 0 || rank >= world) BVSS_FAIL(BVSS_EINVAL, "bad rank/world");
+  bvss_index* idx = c->idx;
+  DeviceGuard g(idx->device);
+  BVSS_TRY(launch_select_quota(c->sel, all_eq_dev, static_cast<int>(c->nq), world, rank, idx->stream));
+  BVSS_TRY(emit_refine_topk(idx, c, topk_ids_dev, topk_dist_dev, true));
+  return BVSS_OK;
+}
+
+int bvss_merge_topk(bvss_index* idx, const int64_t* ids_dev, const float* dist_dev, int32_t world, int64_t nq, int32_t k,
+                    int64_t* out_ids_dev, float* out_dist_dev) {
+  if (!idx || !ids_dev || !dist_dev || !out_ids_dev || !out_dist_dev) BVSS_FAIL(BVSS_EINVAL, "null argument");
+  DeviceGuard g(idx->device);
+  BVSS_TRY(launch_merge_topk(ids_dev, dist_dev, world, nq, k, out_ids_dev, out_dist_dev, idx->stream));
+  return BVSS_OK;
+}
+
+void bvss_dist_end(bvss_search_ctx* c) {
+  if (!c) return;
+  DeviceGuard g(c->idx->device);
+  cudaStreamSynchronize(c->idx->stream);
+  delete c;
+}
+
+}  // extern "C"

@@ -1,0 +1,327 @@
+// select.cu — K4: exact top-T candidate selection (Alg 6 lines 10-18).
+//
+// The paper keeps a T-capacity max-heap over the filter scores.  Here the T
+// smallest (score, id) pairs per query are found exactly by an MSB-first radix
+// select over the score keys (11-bit digits, one histogram round per digit),
+// then emitted in ascending id order by an order-preserving block compaction
+// that takes every key below the threshold tau and the lowest-id keys equal to
+// tau up to the quota (readings R3/R4: one budget T, ties -> lower id).
+//
+// Each round is split into hist (local) and resolve (global) kernels so that the
+// sharded protocol can all-reduce the histograms in between; on
+// one GPU the local histogram is the global one.  One CTA per query streams that
+// query's key row with 16-byte loads.
+#include "common.cuh"
+
+namespace bvss {
+
+struct SelectState {  // device arrays, one entry per query
+  uint32_t* prefix;   // resolved high bits of tau
+  int64_t* below;     // # keys (global) strictly below the current range
+  int64_t* teff;      // min(T, n_total)
+  int64_t* eq;        // # keys (global) equal to tau, after the last round
+  int64_t* quota;     // # keys equal to tau this rank emits
+  int32_t* digit;     // chosen digit of the last resolved round
+};
+
+template <typename K>
+struct KeyVec;
+template <>
+struct KeyVec<uint16_t> {
+  static constexpr int kPer = 8;
+};
+template <>
+struct KeyVec<uint32_t> {
+  static constexpr int kPer = 4;
+};
+
+template <typename K>
+__device__ __forceinline__ void load_keys(const K* row, int64_t base, int64_t n, K (&k)[8]) {
+  // 8 consecutive keys starting at base (16B aligned); out-of-range -> max
+  if (base + 8 <= n) {
+    if (sizeof(K) == 2) {
+      const uint4 v = *reinterpret_cast<const uint4*>(row + base);
+      const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        k[2 * i] = static_cast<K>(w[i] & 0xFFFFu);
+        k[2 * i + 1] = static_cast<K>(w[i] >> 16);
+      }
+    } else {
+      const uint4 v0 = *reinterpret_cast<const uint4*>(row + base);
+      const uint4 v1 = *reinterpret_cast<const uint4*>(row + base + 4);
+      k[0] = v0.x; k[1] = v0.y; k[2] = v0.z; k[3] = v0.w;
+      k[4] = v1.x; k[5] = v1.y; k[6] = v1.z; k[7] = v1.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) k[i] = (base + i < n) ? row[base + i] : static_cast<K>(~static_cast<K>(0));
+  }
+}
+
+// ------------------------------------------------------------- histogram --
+template <typename K>
+__global__ void __launch_bounds__(256) select_hist_kernel(const K* __restrict__ keys, int64_t key_stride, int64_t n,
+                                                          SelectState st, int hi, int shift, int width,
+                                                          int32_t* __restrict__ hist_out /*[nq][2048]*/) {
+  extern __shared__ uint32_t wh[];  // [8 warps][nbins]
+  const int q = blockIdx.x;
+  const int warp = threadIdx.x >> 5;
+  const int nbins = 1 << width;
+  for (int i = threadIdx.x; i < 8 * nbins; i += blockDim.x) wh[i] = 0u;
+  __syncthreads();
+  const uint32_t prefix = st.prefix[q];
+  const K* row = keys + static_cast<int64_t>(q) * key_stride;
+  uint32_t* myh = wh + warp * nbins;
+  const uint32_t mask = static_cast<uint32_t>(nbins) - 1u;
+  for (int64_t base = static_cast<int64_t>(threadIdx.x) * 8; base < n; base += static_cast<int64_t>(blockDim.x) * 8) {
+    K k[8];
+    load_keys<K>(row, base, n, k);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t kk = static_cast<uint32_t>(k[i]);
+      const bool in = (base + i < n) && ((hi >= 32) ? true : ((kk >> hi) == prefix));
+      if (in) atomicAdd(&myh[(kk >> shift) & mask], 1u);
+    }
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < kHistBins; b += blockDim.x) {
+    uint32_t s = 0;
+    if (b < nbins) {
+#pragma unroll
+      for (int w = 0; w < 8; ++w) s += wh[w * nbins + b];
+    }
+    hist_out[static_cast<int64_t>(q) * kHistBins + b] = static_cast<int32_t>(s);
+  }
+}
+
+// --------------------------------------------------------------- resolve --
+// One warp per query: find the digit where the cumulative (global) count
+// reaches need = teff - below.
+__global__ void select_resolve_kernel(const int32_t* __restrict__ hist, SelectState st, int nq, int width, int last) {
+  const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (q >= nq) return;
+  const int64_t need = st.teff[q] - st.below[q];
+  const int32_t* h = hist + static_cast<int64_t>(q) * kHistBins;
+  const int nbins = 1 << width;
+  int64_t run = 0;
+  int chosen = -1;
+  int64_t before = 0;
+  for (int b0 = 0; b0 < nbins && chosen < 0; b0 += 32) {
+    const int b = b0 + lane;
+    int64_t v = (b < nbins) ? h[b] : 0;
+    int64_t inc = v;  // inclusive warp scan
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    const unsigned hit = __ballot_sync(0xffffffffu, (b < nbins) && (run + inc >= need));
+    if (hit) {
+      const int src = __ffs(hit) - 1;
+      chosen = b0 + src;
+      before = run + __shfl_sync(0xffffffffu, inc - v, src);
+    }
+    run += __shfl_sync(0xffffffffu, inc, 31);
+  }
+  if (lane == 0) {
+    if (chosen < 0) chosen = nbins - 1;  // unreachable when need <= keys in range
+    st.prefix[q] = (st.prefix[q] << width) | static_cast<uint32_t>(chosen);
+    st.below[q] += before;
+    st.digit[q] = chosen;
+    if (last) {
+      st.eq[q] = h[chosen];
+      st.quota[q] = need - before;  // single shard: all remaining slots go to the ties
+    }
+  }
+}
+
+// Sharded: this rank's quota of ties from the all-gathered local tie counts.
+__global__ void select_quota_kernel(SelectState st, const int64_t* __restrict__ all_eq /*[P][nq]*/, int nq, int world,
+                                    int rank) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  int64_t left = st.teff[q] - st.below[q];
+  for (int r = 0; r < rank; ++r) left -= all_eq[static_cast<int64_t>(r) * nq + q];
+  const int64_t mine = all_eq[static_cast<int64_t>(rank) * nq + q];
+  st.quota[q] = left < 0 ? 0 : (left > mine ? mine : left);
+}
+
+// local count of keys equal to tau (from the rank's last-round local histogram)
+__global__ void select_tiecount_kernel(const int32_t* __restrict__ local_hist, SelectState st, int nq,
+                                       int64_t* __restrict__ eq_out) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  eq_out[q] = local_hist[static_cast<int64_t>(q) * kHistBins + st.digit[q]];
+}
+
+// ------------------------------------------------------------------ emit --
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* smem_warp /*[8]*/, uint32_t& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) smem_warp[warp] = inc;
+  __syncthreads();
+  uint32_t wpre = 0, tot = 0;
+  const int nw = blockDim.x >> 5;
+  for (int w = 0; w < nw; ++w) {
+    const uint32_t x = smem_warp[w];
+    if (w < warp) wpre += x;
+    tot += x;
+  }
+  __syncthreads();
+  total = tot;
+  return wpre + inc - v;
+}
+
+template <typename K>
+__global__ void __launch_bounds__(256) select_emit_kernel(const K* __restrict__ keys, int64_t key_stride, int64_t n,
+                                                          SelectState st, int T, int64_t id_base,
+                                                          int32_t* __restrict__ cand, int32_t* __restrict__ score,
+                                                          int32_t* __restrict__ count) {
+  __shared__ uint32_t sw[8];
+  const int q = blockIdx.x;
+  const uint32_t tau = st.prefix[q];
+  const int64_t quota = st.quota[q];
+  const K* row = keys + static_cast<int64_t>(q) * key_stride;
+  int32_t* crow = cand + static_cast<int64_t>(q) * T;
+  int32_t* srow = score ? score + static_cast<int64_t>(q) * T : nullptr;
+  int64_t taken = 0, eq_seen = 0;
+  for (int64_t tile = 0; tile < n && taken < T; tile += static_cast<int64_t>(blockDim.x) * 8) {
+    const int64_t base = tile + static_cast<int64_t>(threadIdx.x) * 8;
+    K k[8];
+    uint32_t nlt = 0, neq = 0;
+    if (base < n) {
+      load_keys<K>(row, base, n, k);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t kk = static_cast<uint32_t>(k[i]);
+        const bool valid = base + i < n;
+        nlt += (valid && kk < tau) ? 1u : 0u;
+        neq += (valid && kk == tau) ? 1u : 0u;
+      }
+    }
+    uint32_t total;
+    const uint32_t ex = block_exclusive_scan(nlt | (neq << 16), sw, total);
+    const int64_t lt_pre = ex & 0xFFFFu, eq_pre = ex >> 16;
+    int64_t eq_room = quota - eq_seen;  // ties still to take, in id order
+    if (eq_room < 0) eq_room = 0;
+    int64_t pos = taken + lt_pre + (eq_pre < eq_room ? eq_pre : eq_room);
+    int64_t my_eq = eq_seen + eq_pre;
+    if (base < n) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t kk = static_cast<uint32_t>(k[i]);
+        if (base + i >= n) break;
+        bool take = false;
+        if (kk < tau) take = true;
+        else if (kk == tau) { take = my_eq < quota; ++my_eq; }
+        if (take && pos < T) {
+          crow[pos] = static_cast<int32_t>(id_base + base + i);
+          if (srow) srow[pos] = static_cast<int32_t>(kk);
+          ++pos;
+        }
+      }
+    }
+    const int64_t tlt = total & 0xFFFFu, teq = total >> 16;
+    taken += tlt + (teq < eq_room ? teq : eq_room);
+    eq_seen += teq;
+  }
+  if (taken > T) taken = T;
+  for (int64_t i = taken + threadIdx.x; i < T; i += blockDim.x) {
+    crow[i] = -1;
+    if (srow) srow[i] = -1;
+  }
+  if (threadIdx.x == 0 && count) count[q] = static_cast<int32_t>(taken);
+}
+
+// --------------------------------------------------------------- drivers --
+__global__ void select_init_kernel(SelectState st, int nq, int64_t teff) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  st.prefix[q] = 0u;
+  st.below[q] = 0;
+  st.teff[q] = teff;
+  st.eq[q] = 0;
+  st.quota[q] = 0;
+  st.digit[q] = 0;
+}
+
+int key_bits_for(int kind, int m) {
+  uint64_t maxkey = kind == BVSS_SKETCH_BINARY ? static_cast<uint64_t>(m) : static_cast<uint64_t>(m) * 255u * 255u;
+  int b = 1;
+  while ((maxkey >> b) != 0) ++b;
+  return b;
+}
+int rounds_for(int key_bits) { return ceil_div(key_bits, kHistBits); }
+
+void round_params(int key_bits, int r, int& hi, int& shift, int& width) {
+  hi = key_bits - kHistBits * r;
+  shift = hi - kHistBits > 0 ? hi - kHistBits : 0;
+  width = hi - shift;
+}
+
+int launch_select_init(SelectState st, int nq, int64_t teff, cudaStream_t s) {
+  select_init_kernel<<<ceil_div(nq, 256), 256, 0, s>>>(st, nq, teff);
+  BVSS_TRY(post_launch(__func__, s));
+  return BVSS_OK;
+}
+
+int launch_select_hist(int key_size, const void* keys, int64_t key_stride, int64_t n, int nq, SelectState st,
+                       int key_bits, int r, int32_t* hist, cudaStream_t s) {
+  int hi, shift, width;
+  round_params(key_bits, r, hi, shift, width);
+  const int hi_eff = (r == 0) ? 32 : hi;  // round 0: every key is in range
+  const size_t smem = static_cast<size_t>(8) * (1u << width) * 4;
+  if (key_size == 2) {
+    auto kfn = select_hist_kernel<uint16_t>;
+    BVSS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    kfn<<<nq, 256, smem, s>>>(static_cast<const uint16_t*>(keys), key_stride, n, st, hi_eff, shift, width, hist);
+  } else {
+    auto kfn = select_hist_kernel<uint32_t>;
+    BVSS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    kfn<<<nq, 256, smem, s>>>(static_cast<const uint32_t*>(keys), key_stride, n, st, hi_eff, shift, width, hist);
+  }
+  BVSS_TRY(post_launch(__func__, s));
+  return BVSS_OK;
+}
+
+int launch_select_resolve(const int32_t* hist, SelectState st, int nq, int key_bits, int r, cudaStream_t s) {
+  int hi, shift, width;
+  round_params(key_bits, r, hi, shift, width);
+  const int last = (shift == 0) ? 1 : 0;
+  select_resolve_kernel<<<ceil_div(nq, 8), 256, 0, s>>>(hist, st, nq, width, last);
+  BVSS_TRY(post_launch(__func__, s));
+  return BVSS_OK;
+}
+
+int launch_select_quota(SelectState st, const int64_t* all_eq, int nq, int world, int rank, cudaStream_t s) {
+  select_quota_kernel<<<ceil_div(nq, 256), 256, 0, s>>>(st, all_eq, nq, world, rank);
+  BVSS_TRY(post_launch(__func__, s));
+  return BVSS_OK;
+}
+
+int launch_select_tiecount(const int32_t* local_hist, SelectState st, int nq, int64_t* eq_out, cudaStream_t s) {
+  select_tiecount_kernel<<<ceil_div(nq, 256), 256, 0, s>>>(local_hist, st, nq, eq_out);
+  BVSS_TRY(post_launch(__func__, s));
+  return BVSS_OK;
+}
+
+int launch_select_emit(int key_size, const void* keys, int64_t key_stride, int64_t n, int nq, SelectState st, int T,
+                       int64_t id_base, int32_t* cand, int32_t* score, int32_t* count, cudaStream_t s) {
+  if (key_size == 2)
+    select_emit_kernel<uint16_t><<<nq, 256, 0, s>>>(static_cast<const uint16_t*>(keys), key_stride, n, st, T, id_base,
+                                                    cand, score, count);
+  else
+    select_emit_kernel<uint32_t><<<nq, 256, 0, s>>>(static_cast<const uint32_t*>(keys), key_stride, n, st, T, id_base,
+                                                    cand, score, count);
+  BVSS_TRY(post_launch(__func__, s));
+  return BVSS_OK;
+}
+
+}  // namespace bvss
