@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--nq", type=int, default=None)
     ap.add_argument("--T", type=int, default=None)
     ap.add_argument("--k", type=int, default=None)
-    ap.add_argument("--terms", type=int, default=3, choices=[0, 1, 3])
+    ap.add_argument("--terms", type=int, default=0, choices=[0, 1, 3, 255])
     ap.add_argument("--noise", default="per_coord", choices=["per_coord", "total"])
     ap.add_argument("--recall-queries", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -313,7 +313,7 @@ def main_ours(args):
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "u32 popc (scan) / bf16x3 split, fp32 accumulate (refine)",
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32 popc (scan) / scaled fp16 tensor-core Gram, fp32 accumulate + exact fp32 fix-up (refine)",
             "data": f"synthetic (gen/synth.py {cfg.name} recipe, noise_mode={args.noise}), generated on GPU",
             "config": {"workload": (f"{cfg.name}: n={cfg.n} sets, d={cfg.d}, {cfg.nq} query sets, T={T}, k={k}, "
                                     f"m={cfg.m}, s={cfg.s}, L={cfg.L}, {cfg.sketch} sketch"),

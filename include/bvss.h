@@ -75,7 +75,8 @@ typedef struct {
   int32_t device;        /* CUDA device ordinal of this index (shard) */
   uint32_t flags;        /* build flags (BVSS_DEVICE_PTRS | BVSS_VALIDATE_FINITE | BVSS_KEEP_CODES) */
   uint32_t query_batch;  /* queries per internal sub-batch; 0 = auto */
-  uint32_t refine_terms; /* bf16 split terms for the tensor-core Gram: 3 (default) or 1 */
+  uint32_t refine_terms; /* tensor-core Gram on the scaled fp16 split: 0 = default (= 1), 1 = hi*hi,
+                            3 = hi*hi + hi*lo + lo*hi, 255 = no tensor pass (exact fp32 for every candidate) */
 } bvss_params;
 
 typedef struct bvss_index bvss_index;

@@ -61,7 +61,7 @@ def build(force: bool = False, verbose: bool = False, extra=None) -> str:
         if verbose and (r.stdout or r.stderr):
             print(r.stdout + r.stderr)
     if force or not os.path.exists(OUT) or any(os.path.getmtime(o) > os.path.getmtime(OUT) for o in objs):
-        cmd = [cc, *ARCH, "-shared", "--cudart", "static", "-o", OUT, *objs]
+        cmd = [cc, *ARCH, "-shared", "--cudart", "static", "-Xlinker", "--no-undefined", "-o", OUT, *objs]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

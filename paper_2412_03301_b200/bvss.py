@@ -128,7 +128,7 @@ class Index:
     """A device-resident BioVSS index over one database shard (one GPU)."""
 
     def __init__(self, vectors, offsets, *, m, s, L, sketch="binary", seed=0, device=0, keep_codes=False,
-                 validate=False, projection=None, refine_terms=3, query_batch=0):
+                 validate=False, projection=None, refine_terms=0, query_batch=0):
         dev = _is_cuda(vectors)
         if dev != _is_cuda(offsets):
             raise ValueError("vectors and offsets must both be host arrays or both CUDA tensors")

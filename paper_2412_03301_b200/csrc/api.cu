@@ -51,7 +51,9 @@ int post_launch(const char* what, cudaStream_t st) {
 
 // kernels (other translation units)
 int launch_encode(const float* V, int64_t nvec, int d, const uint16_t* Wt, int m, int s, int L, uint32_t* codes,
-                  float* norms, __nv_bfloat16* hi, __nv_bfloat16* lo, int dpad, int num_sms, cudaStream_t st);
+                  float* norms, __half* hs, __half* ls, float* scale, int dpad, int64_t rows, const int64_t* dst_row,
+                  int kcs, int num_sms, cudaStream_t st);
+int refine_kcs(int dpad);
 int launch_finite_check(const float* x, int64_t count, int* bad_dev, int num_sms, cudaStream_t st);
 int launch_sketch(const uint32_t* codes, int m, const int64_t* off, int64_t n, int kind, void* S, int32_t* mass,
                   int64_t cstride, int64_t sstride, int num_sms, cudaStream_t st);
@@ -59,6 +61,9 @@ int launch_unchunk(const void* S, int64_t n_stride, int64_t first, int64_t count
                    cudaStream_t st);
 int launch_scan(int kind, const void* S, const int32_t* mass, int64_t n, int64_t n_stride, int m, const void* SQ,
                 const int32_t* massQ, int nq, void* keys, int64_t key_stride, int num_sms, cudaStream_t st);
+int launch_scan_tc(int kind, const void* S, const int32_t* mass, int64_t n, int64_t n_stride, int m, const void* SQ,
+                   const int32_t* massQ, int nq, void* Qx, int qpad, void* keys, int64_t key_stride, int* work_counter,
+                   int num_sms, cudaStream_t st);
 struct SelectState {
   uint32_t* prefix;
   int64_t* below;
@@ -77,10 +82,10 @@ int launch_select_quota(SelectState st, const int64_t* all_eq, int nq, int world
 int launch_select_tiecount(const int32_t* local_hist, SelectState st, int nq, int64_t* eq_out, cudaStream_t s);
 int launch_select_emit(int key_size, const void* keys, int64_t key_stride, int64_t n, int nq, SelectState st, int T,
                        int64_t id_base, int32_t* cand, int32_t* score, int32_t* count, cudaStream_t s);
-int launch_refine_tc(const __nv_bfloat16* hi, const __nv_bfloat16* lo, const float* vnorm, const int64_t* off,
-                     int dpad, const __nv_bfloat16* qhi, const __nv_bfloat16* qlo, const float* qnorm,
-                     const int64_t* qoff, int max_mq, const int32_t* cand, const int32_t* count, int T, int nq,
-                     int64_t id_base, float* out_h2, int terms, int* work_counter,
+int launch_refine_tc(const __half* hs, const __half* ls, const float* vscale, int64_t prows, const int64_t* pbase,
+                     const float* vnorm, const int64_t* off, int dpad, const __half* qhs, const __half* qls,
+                     const float* qscale, int64_t qrows, const int64_t* qrow, const float* qnorm, const int64_t* qoff, int max_mq, const int32_t* cand,
+                     const int32_t* count, int T, int nq, int64_t id_base, float* out_h2, int terms, int* work_counter,
                      unsigned long long* rows_counter, int num_sms, cudaStream_t st);
 int launch_topk_fixup(const float* approx, const int32_t* cand, const int32_t* count, int T, int k, const float* V,
                       const int64_t* off, int64_t id_base, int d, const float* Qv, const int64_t* qoff,
@@ -97,6 +102,13 @@ __global__ void max_float_kernel(const float* __restrict__ x, int64_t n, unsigne
     m = fmaxf(m, x[i]);
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) atomicMax(out, __float_as_uint(m));  // values >= 0
+}
+// padded refine row of every DB vector: set i's rows start at pbase[i] (8-aligned)
+__global__ void pad_rows_kernel(const int64_t* __restrict__ off, const int64_t* __restrict__ pbase, int64_t n,
+                                int64_t* __restrict__ dst_row) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    for (int64_t v = off[i]; v < off[i + 1]; ++v) dst_row[v] = pbase[i] + (v - off[i]);
 }
 __global__ void count_valid_kernel(const int32_t* __restrict__ cand, int T, int nq, int32_t* __restrict__ count) {
   const int q = blockIdx.x;
@@ -191,8 +203,11 @@ struct bvss_index {
   uint16_t* Wt = nullptr;     // device [s][m]
   float* V = nullptr;         // [nvec][d]
   int64_t* off = nullptr;     // [n+1]
-  __nv_bfloat16* hi = nullptr;
-  __nv_bfloat16* lo = nullptr;
+  __half* hi = nullptr;         // [dpad/64][prows][64] chunk-major, pre-swizzled, 8-aligned sets (refine.cu)
+  __half* lo = nullptr;
+  float* vscale = nullptr;      // [prows] power-of-two scale of each row
+  int64_t prows = 0;            // padded refine rows
+  int64_t* pbase = nullptr;     // [n+1] first padded row of each set
   float* vnorm = nullptr;
   float vmax2 = 0.0f;
   uint32_t* codes = nullptr;  // optional [nvec][m/32]
@@ -218,8 +233,11 @@ struct bvss_search_ctx {
   float* qv = nullptr;
   int64_t* qoff = nullptr;
   float* qnorm = nullptr;
-  __nv_bfloat16* qhi = nullptr;
-  __nv_bfloat16* qlo = nullptr;
+  __half* qhi = nullptr;         // [dpad/64][qrows][64] chunk-major, pre-swizzled, 8-aligned queries
+  __half* qlo = nullptr;
+  float* qscale = nullptr;       // [qrows]
+  int64_t qrows = 0;
+  int64_t* qrow = nullptr;       // [nq] first padded row of each query
   void* keys = nullptr;
   int64_t key_stride = 0;
   SelectState sel{};
@@ -288,12 +306,16 @@ int chunks_per_set(const bvss_index* idx) {
   return idx->sketch == BVSS_SKETCH_BINARY ? static_cast<int>(((idx->m / 32) + 3) / 4) : static_cast<int>(idx->m / 16);
 }
 
-// error-bound constants of the refine arithmetic
+// error-bound constants of the refine arithmetic: scaled fp16
+// split, y = x/s with s a power of two >= max|x|, |y - fp16(y)| <= 2^-11|y| + 2^-25.
 void error_consts(const bvss_index* idx, float* c1, float* c2) {
   const double u23 = std::ldexp(1.0, -23);
   const double dd = static_cast<double>(idx->dpad);
-  const double prod = idx->terms == 3 ? 3.01 * std::ldexp(1.0, -18) : (2.0 * std::ldexp(1.0, -9) + std::ldexp(1.0, -18));
-  const double accum = (3.0 * dd + 64.0) * u23 * 1.01;
+  const double sq = std::sqrt(dd);
+  const int terms = idx->terms == 3 ? 3 : 1;
+  const double prod = terms == 3 ? (4.0 * std::ldexp(1.0, -22) + std::ldexp(1.0, -21) * sq)
+                                 : (std::ldexp(1.0, -10) * 1.001 + std::ldexp(1.0, -22) * sq);
+  const double accum = (terms * dd + 64.0) * u23 * 1.01;
   *c1 = static_cast<float>(2.0 * (prod + accum));
   *c2 = static_cast<float>((dd + 4.0) * u23);
 }
@@ -324,13 +346,30 @@ int prepare_queries(bvss_index* idx, bvss_search_ctx* c, const float* queries, c
     if (sz > max_mq) max_mq = static_cast<int>(sz > (1 << 30) ? (1 << 30) : sz);
   }
   c->max_mq = max_mq;
+  if (max_mq > 256) BVSS_FAIL(BVSS_EUNSUPPORTED, "query sets of more than 256 vectors are not supported in this build");
   const int d = idx->d, dpad = idx->dpad, R = idx->m / 32;
+  // refine operand rows: every query starts on an 8-aligned row (SW128 swizzle phase), +slack for
+  // the N = ceil(m_q/16)*16 rows a tile reads
+  std::vector<int64_t> qrow_h(nq), dst_h(c->nqvec);
+  int64_t run = 0;
+  for (int64_t i = 0; i < nq; ++i) {
+    qrow_h[i] = run;
+    for (int64_t v = qoff_host[i]; v < qoff_host[i + 1]; ++v) dst_h[v] = run + (v - qoff_host[i]);
+    run += (qoff_host[i + 1] - qoff_host[i] + 7) & ~int64_t(7);
+  }
+  c->qrows = run + 256;
   cudaEventRecord(idx->ev[0], idx->stream);
   BVSS_TRY(c->alloc(c->nqvec * d * sizeof(float), reinterpret_cast<void**>(&c->qv)));
   BVSS_TRY(c->alloc((nq + 1) * sizeof(int64_t), reinterpret_cast<void**>(&c->qoff)));
   BVSS_TRY(c->alloc(c->nqvec * sizeof(float), reinterpret_cast<void**>(&c->qnorm)));
-  BVSS_TRY(c->alloc(c->nqvec * dpad * sizeof(__nv_bfloat16), reinterpret_cast<void**>(&c->qhi)));
-  BVSS_TRY(c->alloc(c->nqvec * dpad * sizeof(__nv_bfloat16), reinterpret_cast<void**>(&c->qlo)));
+  BVSS_TRY(c->alloc(c->qrows * dpad * sizeof(__half), reinterpret_cast<void**>(&c->qhi)));
+  BVSS_TRY(c->alloc(c->qrows * dpad * sizeof(__half), reinterpret_cast<void**>(&c->qlo)));
+  BVSS_TRY(c->alloc(c->qrows * sizeof(float), reinterpret_cast<void**>(&c->qscale)));
+  BVSS_TRY(c->alloc(nq * sizeof(int64_t), reinterpret_cast<void**>(&c->qrow)));
+  int64_t* dst_row;
+  BVSS_TRY(c->alloc(c->nqvec * sizeof(int64_t), reinterpret_cast<void**>(&dst_row)));
+  BVSS_CUDA(cudaMemcpyAsync(c->qrow, qrow_h.data(), nq * sizeof(int64_t), cudaMemcpyHostToDevice, idx->stream));
+  BVSS_CUDA(cudaMemcpyAsync(dst_row, dst_h.data(), c->nqvec * sizeof(int64_t), cudaMemcpyHostToDevice, idx->stream));
   BVSS_TRY(to_device(idx, c->qv, queries, c->nqvec * d * sizeof(float), vec_dev));
   BVSS_CUDA(cudaMemcpyAsync(c->qoff, c->qoff_host.data(), (nq + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, idx->stream));
   if (validate) {
@@ -345,8 +384,8 @@ int prepare_queries(bvss_index* idx, bvss_search_ctx* c, const float* queries, c
   }
   BVSS_TRY(c->alloc(c->nqvec * R * sizeof(uint32_t), reinterpret_cast<void**>(&c->qcodes)));
   cudaEventRecord(idx->ev[1], idx->stream);
-  BVSS_TRY(launch_encode(c->qv, c->nqvec, d, idx->Wt, idx->m, idx->s, idx->L, c->qcodes, c->qnorm, c->qhi, c->qlo, dpad,
-                         idx->num_sms, idx->stream));
+  BVSS_TRY(launch_encode(c->qv, c->nqvec, d, idx->Wt, idx->m, idx->s, idx->L, c->qcodes, c->qnorm, c->qhi, c->qlo, c->qscale,
+                         dpad, c->qrows, dst_row, refine_kcs(dpad), idx->num_sms, idx->stream));
   const int cps = chunks_per_set(idx);
   BVSS_TRY(c->alloc(nq * cps * 16, &c->qsk));
   BVSS_TRY(c->alloc(nq * sizeof(int32_t), reinterpret_cast<void**>(&c->qmass)));
@@ -363,11 +402,25 @@ int scan_batch(bvss_index* idx, bvss_search_ctx* c) {
   const int key_size = idx->sketch == BVSS_SKETCH_BINARY ? 2 : 4;
   c->key_stride = (n + 7) & ~int64_t(7);
   BVSS_TRY(c->alloc(static_cast<size_t>(c->nq) * c->key_stride * key_size, &c->keys));
-  BVSS_TRY(launch_scan(idx->sketch, idx->sk, idx->mass, n, n, idx->m, c->qsk, c->qmass, static_cast<int>(c->nq), c->keys,
-                       c->key_stride, idx->num_sms, idx->stream));
+  static const bool simt = getenv("BVSS_SCAN_SIMT") != nullptr;  // developer switch: SIMT popc/dp4a scan
+  if (idx->m % 128 == 0 && !simt) {
+    // tensor-core scan (scan_tc.cu): u8 x u8 -> s32 on tcgen05, queries expanded to [m/16][qpad][16 B]
+    const int qpad = static_cast<int>(ceil_div<int64_t>(c->nq, 256) * 256);
+    void* qx;
+    BVSS_TRY(c->alloc(static_cast<size_t>(idx->m) * qpad, &qx));
+    int* wc;
+    BVSS_TRY(idx->ws.get("scan_counter", sizeof(int), reinterpret_cast<void**>(&wc)));
+    BVSS_TRY(launch_scan_tc(idx->sketch, idx->sk, idx->mass, n, n, idx->m, c->qsk, c->qmass, static_cast<int>(c->nq),
+                            qx, qpad, c->keys, c->key_stride, wc, idx->num_sms, idx->stream));
+    idx->stats.kernel_launches += 2;
+    idx->stats.scan_bytes += static_cast<uint64_t>(ceil_div<int64_t>(c->nq, 256)) * n * chunks_per_set(idx) * 16;
+  } else {
+    BVSS_TRY(launch_scan(idx->sketch, idx->sk, idx->mass, n, n, idx->m, c->qsk, c->qmass, static_cast<int>(c->nq),
+                         c->keys, c->key_stride, idx->num_sms, idx->stream));
+    idx->stats.kernel_launches += 1;
+    idx->stats.scan_bytes += static_cast<uint64_t>(ceil_div<int64_t>(c->nq, 8)) * n * chunks_per_set(idx) * 16;
+  }
   cudaEventRecord(idx->ev[3], idx->stream);
-  idx->stats.kernel_launches += 1;
-  idx->stats.scan_bytes += static_cast<uint64_t>(ceil_div<int64_t>(c->nq, 8)) * n * chunks_per_set(idx) * 16;
   const int nq = static_cast<int>(c->nq);
   BVSS_TRY(c->alloc(nq * sizeof(uint32_t), reinterpret_cast<void**>(&c->sel.prefix)));
   BVSS_TRY(c->alloc(nq * sizeof(int64_t), reinterpret_cast<void**>(&c->sel.below)));
@@ -394,15 +447,16 @@ int emit_refine_topk(bvss_index* idx, bvss_search_ctx* c, int64_t* out_ids_dev, 
   idx->stats.kernel_launches += 1;
   if (!refine) return BVSS_OK;
   int exact_all = 0;
-  if (idx->terms != 0) {
+  if (idx->terms != 0 && c->max_mq <= 128) {  // tensor path: query rows fit the M=128 tile
     BVSS_TRY(c->alloc(static_cast<size_t>(nq) * c->T * sizeof(float), reinterpret_cast<void**>(&c->approx)));
     int* counter;
     BVSS_TRY(idx->ws.get("work_counter", sizeof(int), reinterpret_cast<void**>(&counter)));
     unsigned long long* rows;
     BVSS_TRY(idx->ws.get("rows_counter", sizeof(unsigned long long), reinterpret_cast<void**>(&rows)));
-    BVSS_TRY(launch_refine_tc(idx->hi, idx->lo, idx->vnorm, idx->off, idx->dpad, c->qhi, c->qlo, c->qnorm, c->qoff,
-                              c->max_mq, c->cand, c->count, c->T, nq, c->id_base, c->approx, idx->terms, counter,
-                              rows, idx->num_sms, idx->stream));
+    BVSS_TRY(launch_refine_tc(idx->hi, idx->lo, idx->vscale, idx->prows, idx->pbase, idx->vnorm, idx->off, idx->dpad, c->qhi,
+                              c->qlo, c->qscale, c->qrows,
+                              c->qrow, c->qnorm, c->qoff, c->max_mq, c->cand, c->count, c->T, nq, c->id_base,
+                              c->approx, idx->terms, counter, rows, idx->num_sms, idx->stream));
     idx->stats.kernel_launches += 1;
   } else {
     exact_all = 1;
@@ -500,8 +554,8 @@ int bvss_build_index(const float* vectors, const int64_t* set_offsets, int64_t n
   if (p->L < 1 || p->L > p->m) BVSS_FAIL(BVSS_EINVAL, "L must be in [1, m]");
   if (p->s < 1 || static_cast<int>(p->s) > d || p->s > 32) BVSS_FAIL(BVSS_EINVAL, "s must be in [1, min(d, 32)]");
   if (p->sketch > 1) BVSS_FAIL(BVSS_EINVAL, "unknown sketch kind");
-  if (p->refine_terms != 0 && p->refine_terms != 1 && p->refine_terms != 3 && p->refine_terms != 0xFFFFFFFFu)
-    BVSS_FAIL(BVSS_EINVAL, "refine_terms must be 3, 1 or 0");
+  if (p->refine_terms != 0 && p->refine_terms != 1 && p->refine_terms != 3 && p->refine_terms != 255)
+    BVSS_FAIL(BVSS_EINVAL, "refine_terms must be 0 (default), 1, 3 or 255 (exact)");
   int num_sms = 0;
   BVSS_TRY(check_device(p->device, &num_sms));
   DeviceGuard g(p->device);
@@ -525,7 +579,8 @@ int bvss_build_index(const float* vectors, const int64_t* set_offsets, int64_t n
   idx->L = p->L;
   idx->sketch = p->sketch;
   idx->seed = p->seed;
-  idx->terms = (p->refine_terms == 1 || p->refine_terms == 0) ? static_cast<int>(p->refine_terms) : 3;
+  // 0 = default (1-term fp16 tensor-core pass + exact window), 1, 3, 255 = exact SIMT for every candidate
+  idx->terms = p->refine_terms == 0 ? 1 : (p->refine_terms == 255 ? 0 : static_cast<int>(p->refine_terms));
   idx->query_batch = p->query_batch;
   BVSS_CUDA(cudaStreamCreateWithFlags(&idx->own_stream, cudaStreamNonBlocking));
   idx->stream = idx->own_stream;
@@ -571,8 +626,23 @@ int bvss_build_index(const float* vectors, const int64_t* set_offsets, int64_t n
     BVSS_CUDA(cudaStreamSynchronize(st));
     if (hbad) BVSS_FAIL(BVSS_ENONFINITE, "database vectors contain NaN or Inf");
   }
-  BVSS_TRY(dalloc(static_cast<size_t>(nvec) * idx->dpad * 2, reinterpret_cast<void**>(&idx->hi)));
-  BVSS_TRY(dalloc(static_cast<size_t>(nvec) * idx->dpad * 2, reinterpret_cast<void**>(&idx->lo)));
+  // refine operands: every set starts on an 8-aligned padded row (refine.cu)
+  std::vector<int64_t> pb(n + 1);
+  pb[0] = 0;
+  for (int64_t i = 0; i < n; ++i) pb[i + 1] = pb[i] + ((off_h[i + 1] - off_h[i] + 7) & ~int64_t(7));
+  idx->prows = pb[n];
+  BVSS_TRY(dalloc((n + 1) * 8, reinterpret_cast<void**>(&idx->pbase)));
+  BVSS_CUDA(cudaMemcpyAsync(idx->pbase, pb.data(), (n + 1) * 8, cudaMemcpyHostToDevice, st));
+  BVSS_TRY(dalloc(static_cast<size_t>(idx->prows) * idx->dpad * 2, reinterpret_cast<void**>(&idx->hi)));
+  BVSS_TRY(dalloc(static_cast<size_t>(idx->prows) * idx->dpad * 2, reinterpret_cast<void**>(&idx->lo)));
+  BVSS_TRY(dalloc(static_cast<size_t>(idx->prows) * 4, reinterpret_cast<void**>(&idx->vscale)));
+  BVSS_CUDA(cudaMemsetAsync(idx->vscale, 0, static_cast<size_t>(idx->prows) * 4, st));
+  BVSS_CUDA(cudaMemsetAsync(idx->hi, 0, static_cast<size_t>(idx->prows) * idx->dpad * 2, st));
+  BVSS_CUDA(cudaMemsetAsync(idx->lo, 0, static_cast<size_t>(idx->prows) * idx->dpad * 2, st));
+  int64_t* dst_row;
+  BVSS_TRY(idx->ws.get("dst_row", static_cast<size_t>(nvec) * 8, reinterpret_cast<void**>(&dst_row)));
+  pad_rows_kernel<<<num_sms * 8, 256, 0, st>>>(idx->off, idx->pbase, n, dst_row);
+  BVSS_TRY(post_launch("pad_rows_kernel", st));
   BVSS_TRY(dalloc(static_cast<size_t>(nvec) * 4, reinterpret_cast<void**>(&idx->vnorm)));
   uint32_t* codes = nullptr;
   const bool keep = (p->flags & BVSS_KEEP_CODES) != 0;
@@ -582,8 +652,8 @@ int bvss_build_index(const float* vectors, const int64_t* set_offsets, int64_t n
   } else {
     BVSS_TRY(idx->ws.get("codes", static_cast<size_t>(nvec) * R * 4, reinterpret_cast<void**>(&codes)));
   }
-  BVSS_TRY(launch_encode(idx->V, nvec, d, idx->Wt, p->m, p->s, p->L, codes, idx->vnorm, idx->hi, idx->lo, idx->dpad,
-                         num_sms, st));
+  BVSS_TRY(launch_encode(idx->V, nvec, d, idx->Wt, p->m, p->s, p->L, codes, idx->vnorm, idx->hi, idx->lo, idx->vscale,
+                         idx->dpad, idx->prows, dst_row, refine_kcs(idx->dpad), num_sms, st));
   const int cps = chunks_per_set(idx.get());
   BVSS_TRY(dalloc(static_cast<size_t>(n) * cps * 16, &idx->sk));
   BVSS_TRY(dalloc(static_cast<size_t>(n) * 4, reinterpret_cast<void**>(&idx->mass)));
@@ -597,9 +667,7 @@ int bvss_build_index(const float* vectors, const int64_t* set_offsets, int64_t n
   BVSS_CUDA(cudaMemcpyAsync(&hv, vmax, sizeof(hv), cudaMemcpyDeviceToHost, st));
   BVSS_CUDA(cudaStreamSynchronize(st));
   std::memcpy(&idx->vmax2, &hv, 4);
-  if (!keep) {
-    idx->ws.release();
-  }
+  idx->ws.release();  // build scratch (codes unless kept, padded-row map)
   *out = idx.release();
   return BVSS_OK;
 }
@@ -608,7 +676,8 @@ void bvss_free_index(bvss_index* idx) {
   if (!idx) return;
   DeviceGuard g(idx->device);
   if (idx->stream) cudaStreamSynchronize(idx->stream);
-  void* ptrs[] = {idx->Wt, idx->V, idx->off, idx->hi, idx->lo, idx->vnorm, idx->codes, idx->sk, idx->mass};
+  void* ptrs[] = {idx->Wt,    idx->V,     idx->off,   idx->hi, idx->lo,  idx->vscale,
+                  idx->pbase, idx->vnorm, idx->codes, idx->sk, idx->mass};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   idx->ws.release();
@@ -752,14 +821,15 @@ int bvss_refine(bvss_index* idx, const float* queries, const int64_t* query_offs
   BVSS_TRY(c->alloc(static_cast<size_t>(nq) * k * 8, reinterpret_cast<void**>(&oid)));
   BVSS_TRY(c->alloc(static_cast<size_t>(nq) * k * 4, reinterpret_cast<void**>(&odist)));
   int exact_all = 0;
-  if (idx->terms != 0) {
+  if (idx->terms != 0 && c->max_mq <= 128) {  // tensor path: query rows fit the M=128 tile
     BVSS_TRY(c->alloc(static_cast<size_t>(nq) * T * 4, reinterpret_cast<void**>(&c->approx)));
     BVSS_CUDA(cudaMemsetAsync(c->approx, 0xFF, static_cast<size_t>(nq) * T * 4, idx->stream));  // NaN where unused
     int* counter;
     BVSS_TRY(idx->ws.get("work_counter", sizeof(int), reinterpret_cast<void**>(&counter)));
-    BVSS_TRY(launch_refine_tc(idx->hi, idx->lo, idx->vnorm, idx->off, idx->dpad, c->qhi, c->qlo, c->qnorm, c->qoff,
-                              c->max_mq, c->cand, c->count, T, static_cast<int>(nq), 0, c->approx, idx->terms, counter,
-                              nullptr, idx->num_sms, idx->stream));
+    BVSS_TRY(launch_refine_tc(idx->hi, idx->lo, idx->vscale, idx->prows, idx->pbase, idx->vnorm, idx->off, idx->dpad, c->qhi,
+                              c->qlo, c->qscale, c->qrows,
+                              c->qrow, c->qnorm, c->qoff, c->max_mq, c->cand, c->count, T, static_cast<int>(nq), 0,
+                              c->approx, idx->terms, counter, nullptr, idx->num_sms, idx->stream));
   } else {
     exact_all = 1;
   }
@@ -828,7 +898,7 @@ int bvss_search(bvss_index* idx, const float* queries, const int64_t* query_offs
   BVSS_CUDA(cudaMemcpyAsync(&hr, rows, sizeof(hr), cudaMemcpyDeviceToHost, idx->stream));
   BVSS_CUDA(cudaStreamSynchronize(idx->stream));
   idx->stats.cand_rows = hr;
-  idx->stats.gather_bytes = hr * static_cast<uint64_t>(idx->dpad) * 2u * (idx->terms == 3 ? 2u : 1u);
+  idx->stats.gather_bytes = hr * static_cast<uint64_t>(idx->dpad) * 2u * (idx->terms == 3 ? 2u : (idx->terms == 1 ? 1u : 0u));
   return BVSS_OK;
 }
 

@@ -17,7 +17,8 @@ template <int RM>  // RM = capacity in 32-row groups (m/32 <= RM)
 __global__ void __launch_bounds__(256) flyhash_wta_kernel(
     const float* __restrict__ V, int64_t nvec, int d, const uint16_t* __restrict__ Wt /*[s][m]*/, int m,
     int s, int L, uint32_t* __restrict__ codes /*[nvec][m/32] or null*/, float* __restrict__ norms /*[nvec] or null*/,
-    __nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo /*[nvec][dpad] or null*/, int dpad) {
+    __half* __restrict__ hs, __half* __restrict__ ls /*[KS][rows/8][KCS][8][64] or null*/, float* __restrict__ scale,
+    int dpad, int64_t rows, const int64_t* __restrict__ dst_row, int kcs) {
   extern __shared__ __align__(16) uint8_t smem[];
   uint16_t* sW = reinterpret_cast<uint16_t*>(smem);
   float* sV = reinterpret_cast<float*>(smem + ((static_cast<size_t>(s) * m * 2 + 15) & ~size_t(15)));
@@ -38,13 +39,30 @@ __global__ void __launch_bounds__(256) flyhash_wta_kernel(
       myv[i] = x;
       nrm = __fmaf_rn(x, x, nrm);
     }
-    if (hi != nullptr) {
+    if (hs != nullptr) {
+      // scale: s = 2^e with max|x| <= s (exact power-of-two scaling), y = x / s in [-1, 1]
+      float mx = 0.0f;
+      for (int i = lane; i < d; i += 32) mx = fmaxf(mx, fabsf(myv[i]));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      int ex = 0;
+      if (mx > 0.0f) frexpf(mx, &ex);  // mx = f 2^ex, f in [0.5, 1)
+      const float inv = ldexpf(1.0f, -ex);
+      // super-chunk-major, pre-swizzled (refine.cu): element i of row `row` goes to 128-byte K-chunk
+      // kc = i/64 (super kc/KCS, slot kc%KCS) of its 8-row group, 16-byte unit ((i%64)/8) ^ (row%8)
+      const int64_t row = dst_row ? dst_row[vi] : vi;
+      const int64_t groups = rows >> 3;
+      if (lane == 0) scale[row] = ldexpf(1.0f, ex);
       for (int i = lane; i < dpad; i += 32) {
-        float x = i < d ? myv[i] : 0.0f;
-        __nv_bfloat16 h = __float2bfloat16_rn(x);
-        __nv_bfloat16 l = __float2bfloat16_rn(x - __bfloat162float(h));
-        hi[vi * dpad + i] = h;
-        lo[vi * dpad + i] = l;
+        const float y = i < d ? myv[i] * inv : 0.0f;
+        const __half h = __float2half_rn(y);
+        const __half l = __float2half_rn(y - __half2float(h));
+        const int kc = i >> 6, u = (i >> 3) & 7, e = i & 7;
+        const int ks = kc / kcs, kq = kc % kcs;
+        const int64_t o = ((((static_cast<int64_t>(ks) * groups + (row >> 3)) * kcs + kq) * 8 + (row & 7)) << 6) +
+                          ((u ^ static_cast<int>(row & 7)) << 3) + e;
+        hs[o] = h;
+        ls[o] = l;
       }
     }
     if (norms != nullptr) {
@@ -117,7 +135,8 @@ size_t encode_smem_bytes(int m, int s, int d) {
 }
 
 int launch_encode(const float* V, int64_t nvec, int d, const uint16_t* Wt, int m, int s, int L, uint32_t* codes,
-                  float* norms, __nv_bfloat16* hi, __nv_bfloat16* lo, int dpad, int num_sms, cudaStream_t st) {
+                  float* norms, __half* hs, __half* ls, float* scale, int dpad, int64_t rows, const int64_t* dst_row,
+                  int kcs, int num_sms, cudaStream_t st) {
   if (nvec <= 0) return BVSS_OK;
   const size_t smem = encode_smem_bytes(m, s, d);
   const int R = m / 32;
@@ -127,7 +146,7 @@ int launch_encode(const float* V, int64_t nvec, int d, const uint16_t* Wt, int m
   do {                                                                                                    \
     auto kfn = flyhash_wta_kernel<RMv>;                                                                   \
     BVSS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem))); \
-    kfn<<<grid, 256, smem, st>>>(V, nvec, d, Wt, m, s, L, codes, norms, hi, lo, dpad);                    \
+    kfn<<<grid, 256, smem, st>>>(V, nvec, d, Wt, m, s, L, codes, norms, hs, ls, scale, dpad, rows, dst_row, kcs); \
   } while (0)
   if (R <= 16) BVSS_ENC(16);
   else if (R <= 32) BVSS_ENC(32);

@@ -1,44 +1,70 @@
 // refine.cu — K5: Hausdorff refinement of the T candidates of every query on the
 // 5th-generation tensor cores (Alg 6 lines 19-22; Def 4).
 //
-// For a query Q (m_q vectors) and a run of its candidate sets, the candidate
-// vectors are gathered row by row into 128-row tiles (sets packed back to back,
-// a set may straddle tiles) and the Gram matrix G = V Q^T is formed by
-// tcgen05.mma (M = 128 candidate rows, N = m_q rounded up to 16, K = d) with an
-// fp32 accumulator in TMEM.  Operands are the bf16 split x = hi + lo prepared at
-// build time; terms = 3 issues hi*hi + hi*lo + lo*hi (|error| ~ 3 * 2^-18 |x||y|),
-// terms = 1 issues hi*hi only.  The fused epilogue reads the accumulator with
-// tcgen05.ld and forms D^2 = |v|^2 + |q|^2 - 2g (clamped at 0), the row minima
-// (min over q, per candidate vector), the segmented column minima (min over the
-// vectors of one set, per q), and per set
-//     H^2 = max( max_q min_v D^2 , max_v min_q D^2 )
-// (min/max on squared distances; sqrt is monotone).  K6 then recomputes the
-// final top-k window exactly in fp32 (topk.cu).
+// For a query Q (m_q vectors) and a run of its candidate sets, the Gram matrix
+// G = Q V^T is formed by tcgen05.mma with the QUERY as the A operand (M = 128:
+// the query rows replicated 128/(32*ceil(m_q/32)) times, one replica per TMEM
+// lane quarter) and 256 packed candidate rows as the B operand (N = 256), K = d.
+// Measured on B200 (tools/microbench_umma.cu) a tcgen05.mma costs ~138 cycles
+// whatever N is, so N = 256 candidate rows per instruction is what keeps the
+// tensor pipe off the critical path.  Operands are the scaled fp16 split made at
+// build time, x = s (hi + lo) + r with s a power of two >= max|x|; terms = 1
+// issues hi*hi (|error| <= ~2^-10 |x||y|), terms = 3 hi*hi + hi*lo + lo*hi.
 //
-// CTA = 9 warps: warps 0-3 gather (cp.async, SW128 layout, multi-stage ring),
-// warps 4-7 epilogue (TMEM lanes 0-127 = tile rows), warp 8 owns TMEM and
-// issues the MMAs from one thread.  Accumulators are double-buffered in TMEM so
-// the epilogue of tile i overlaps the MMAs of tile i+1.  Persistent CTAs pull
-// work items (query, up to 128 candidates) from an atomic counter.
+// Epilogue: TMEM lane = query row, column = candidate row.  One warp per
+// candidate set (sets are whole inside a tile): per lane the min over the set's
+// columns of D^2 = |q|^2 + |v|^2 - 2 s_q s_v g (clamped at 0), per column the
+// min over lanes (redux.sync), then
+//     H^2 = max( max_q min_v D^2 , max_v min_q D^2 )
+// with full-mask redux.sync max/min; no shared-memory round trip when m_q <= 32.
+// K6 recomputes the final top-k window exactly in fp32 (topk.cu).
+//
+// Gather.  The fp16 copies are stored super-chunk-major and
+// pre-swizzled: [KS][P/8][KCS][8 rows][64 halves] (KCS consecutive 128-byte
+// K-chunks of each 8-row group together, 16-byte units of row p permuted
+// u -> u ^ (p & 7)).  Every set starts on an 8-aligned padded row, so the
+// (set, super-chunk) slab is ONE contiguous run of ceil8(m) x KCS x 128 bytes
+// and lands, by a single cp.async.bulk, as ready-made SWIZZLE_128B K-major atoms
+// with SBO = KCS x 1 KB.  (Measured: lane-parallel random bulk copies of >= 5 KB
+// reach ~7 TB/s on B200, 2.5 KB copies only ~4 TB/s.)  Queries use the same
+// layout with 8-aligned rows.
+//
+// CTA = 6 warps: warp 0 producer (work items, item tables, tile infos, bulk
+// copies through a stage ring), warp 1 TMEM owner + MMA issuer (one thread),
+// warps 2-5 epilogue.  Accumulators (128 lanes x 256 columns) are
+// double-buffered in TMEM (512 columns); item tables and tile infos are handed
+// over with mbarriers, so the persistent loop has no CTA-wide barrier.
+#include <cstdio>
+#include <cstdlib>
+
 #include "tc.cuh"
 
 namespace bvss {
 
-constexpr int kRows = 128;
-constexpr int kItemCands = 128;
-constexpr int kKChunk = 64;  // bf16 per K-chunk = 128 bytes = one SW128 row
-constexpr int kProd = 128, kEpi = 128;
-constexpr int kRefineThreads = kProd + kEpi + 32;
-constexpr int kMaxN = 256;
+constexpr int kTileRows = 256;   // candidate rows per tile (MMA N)
+constexpr int kItemCands = 128;  // candidates per work item
+constexpr int kKChunk = 64;      // fp16 per K-chunk = 128 bytes = one SW128 row
+constexpr int kEpiWarps = 8;           // warps 2-5 and 8-11 (two per TMEM lane quarter)
+constexpr int kRefineThreads = 32 * 12;  // 0 copy, 1 MMA, 2-5 epilogue, 6 table, 7 tile info, 8-11 epilogue
+constexpr int kMaxQ = 128;       // query rows the tensor path handles (M)
+constexpr int kMaxStages = 4;
+constexpr int kInfoSlots = 4;
+constexpr int kMaxSetsPerTile = kTileRows / 8;
 
 struct RefineArgs {
-  const __nv_bfloat16* hi;
-  const __nv_bfloat16* lo;
-  const float* vnorm;
-  const int64_t* off;
-  int dpad;
-  const __nv_bfloat16* qhi;
-  const __nv_bfloat16* qlo;
+  const __half* hs;      // [KS][prows/8][KCS][8][64] super-chunk-major, pre-swizzled, 8-row-aligned sets
+  const __half* ls;
+  const float* vscale;   // [prows] power-of-two scale of each padded row
+  int64_t pgroups;       // prows / 8
+  const int64_t* pbase;  // [n] first padded row of each set
+  const float* vnorm;    // [nvec] squared norms (unpadded index)
+  const int64_t* off;    // [n+1]
+  int KC, KCS;
+  const __half* qhs;     // [KS][qrows/8][KCS][8][64], 8-aligned queries
+  const __half* qls;
+  const float* qscale;   // [qrows]
+  int64_t qgroups;
+  const int64_t* qrow;   // [nq] first padded row of each query
   const float* qnorm;
   const int64_t* qoff;
   const int32_t* cand;   // [nq][T] global ids (-1 padded)
@@ -46,364 +72,530 @@ struct RefineArgs {
   int T;
   int nq;
   int64_t id_base;
-  float* out_h2;  // [nq][T]
+  float* out_h2;  // [nq][T]; 0 for sets the tensor path does not take (> 256 rows): forces the exact fix-up
   int terms;
-  int nmax;        // max padded N over the batch
   int stages;
   uint32_t stage_bytes;
-  uint32_t a_bytes;  // bytes of one A piece (16 KB)
-  uint32_t b_bytes;  // bytes of one B piece (nmax * 128)
-  uint32_t tmem_cols_per_acc;
+  uint32_t a_bytes;  // one A piece of a stage: 128 rows x KCS x 128 B
+  uint32_t b_bytes;  // one B piece of a stage: 256 rows x KCS x 128 B
   int items_per_query;
   int total_items;
   int* work_counter;
   unsigned long long* rows_counter;  // candidate rows gathered (stats)
+  unsigned long long* prof;          // developer per-role cycle counters (env BVSS_REFINE_PROF) or null
 };
 
-struct RefineSmem {  // small control block after the stage ring
-  float dsm[kRows][33];
-  float carry_r[2][kMaxN];  // double-buffered by tile parity: read [t&1], write [(t+1)&1]
-  float qn[kMaxN];
-  uint32_t hq2s[kRows];
-  float csm[kRows];
-  int32_t rowstart[kItemCands + 1];
-  int64_t vbase[kItemCands];
-  uint64_t full[4];
-  uint64_t empty[4];
+struct ItemTable {
+  int nc;  // candidates in the item; -1 = no more work
+  int q, c0, mq, rep_rows, reps, ntiles;
+  int64_t q0, qrow;
+  int32_t tile_first[kItemCands + 1];  // first table entry of each tile (entries are in tile order)
+  int32_t ent_cand[kItemCands];        // candidate index (within the item) of each entry
+  int16_t ent_col[kItemCands];         // column (B row) where the set starts in its tile
+  int16_t ent_m[kItemCands];           // vectors in the set
+  int64_t ent_vbase[kItemCands];       // first (unpadded) vector index
+  int64_t ent_pbase[kItemCands];       // first padded row
+  float qn[kMaxQ];                     // |q_i|^2
+  float qs2[kMaxQ];                    // 2 * scale of query row i
+};
+
+struct TileInfo {
+  int first, count, pad0, pad1;  // entries of the item table in this tile (pad: 16-byte aligned vn/vs)
+  float vn[kTileRows];       // |v|^2 of each column (candidate row)
+  float vs[kTileRows];       // scale of each column
+};
+
+struct RefineCtl {
+  ItemTable tab[2];
+  TileInfo info[kInfoSlots];
+  uint32_t hq[kEpiWarps][kMaxSetsPerTile];  // general path (m_q > 32): cross-warp partials
+  uint32_t cm[kEpiWarps][kTileRows];
+  uint64_t full[kMaxStages];
+  uint64_t empty[kMaxStages];
   uint64_t tfull[2];
   uint64_t tempty[2];
+  uint64_t tab_full[2];
+  uint64_t tab_empty[2];
+  uint64_t info_full[kInfoSlots];
+  uint64_t info_empty[kInfoSlots];
   uint32_t tmem_base;
-  int item;
-  float carry_h[2];
 };
 
-__device__ __forceinline__ int upper_bound_rows(const int32_t* rs, int nc, int R) {
-  // largest c in [0, nc) with rs[c] <= R  (rs[0] = 0, strictly increasing)
-  int lo = 0, hi = nc;  // invariant: rs[lo] <= R < rs[hi]
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (rs[mid] <= R) lo = mid;
-    else hi = mid;
-  }
-  return lo;
+#define PROF_WAIT(slot, call)                                                        \
+  do {                                                                               \
+    if (a.prof) {                                                                    \
+      const long long t0_ = clock64();                                               \
+      call;                                                                          \
+      if (lane == 0) atomicAdd(&a.prof[slot], (unsigned long long)(clock64() - t0_)); \
+    } else {                                                                         \
+      call;                                                                          \
+    }                                                                                \
+  } while (0)
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// SW128 K-major descriptor with a given stride between 8-row groups (SBO, bytes)
+__device__ __forceinline__ uint64_t sw128_desc_sbo(uint32_t saddr, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(1u) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+  d |= static_cast<uint64_t>(1u) << 46;
+  d |= static_cast<uint64_t>(2u) << 61;
+  return d;
+}
+__device__ __forceinline__ void tmem_ld16f(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  tc::tmem_ld16(taddr, r);
+  tc::tmem_ld_wait();
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
 __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(RefineArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-align the stage ring (SW128 atoms)
+  __shared__ RefineCtl S;
   uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  RefineSmem& S = *reinterpret_cast<RefineSmem*>(ring + static_cast<size_t>(a.stages) * a.stage_bytes);
   const uint32_t ring_s = smem_u32(ring);
-
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int NST = a.stages;
 
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) {
-      tc::mbar_init(&S.full[s], kProd);
+      tc::mbar_init(&S.full[s], 1);
       tc::mbar_init(&S.empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&S.tfull[b], 1);
-      tc::mbar_init(&S.tempty[b], kEpi);
+      tc::mbar_init(&S.tempty[b], kEpiWarps);
+      tc::mbar_init(&S.tab_full[b], 1);
+      tc::mbar_init(&S.tab_empty[b], 4);  // copy producer + MMA warp + epilogue + tile-info warp
+    }
+    for (int s = 0; s < kInfoSlots; ++s) {
+      tc::mbar_init(&S.info_full[s], 1);
+      tc::mbar_init(&S.info_empty[s], kEpiWarps);
     }
     tc::fence_mbar_init();
   }
-  if (warp == 8) tc::tmem_alloc(&S.tmem_base, 2 * a.tmem_cols_per_acc);
+  for (int i = tid; i < kEpiWarps * kTileRows; i += blockDim.x) (&S.cm[0][0])[i] = 0x7f800000u;
+  for (int i = tid; i < kEpiWarps * kMaxSetsPerTile; i += blockDim.x) (&S.hq[0][0])[i] = 0u;
+  if (warp == 1) tc::tmem_alloc(&S.tmem_base, 512);
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = S.tmem_base;
-
-  // pipeline counters (identical sequence in every role)
-  uint32_t kchunk_ctr = 0;  // global K-chunk counter (stage ring)
-  uint32_t tile_ctr = 0;    // global tile counter (TMEM double buffer)
-  const int KC = a.dpad / kKChunk;
-  const uint32_t pieceA = a.a_bytes, pieceB = a.b_bytes;
+  const int KCS = a.KCS, KS = a.KC / a.KCS;
   const bool three = a.terms == 3;
+  const uint32_t sbo = static_cast<uint32_t>(KCS) * 1024u;
+  const long long t_role0 = clock64();
 
-  for (;;) {
-    if (tid == 0) S.item = atomicAdd(a.work_counter, 1);
-    __syncthreads();
-    const int item = S.item;
-    if (item >= a.total_items) break;
-    const int q = item / a.items_per_query;
-    const int c0 = (item % a.items_per_query) * kItemCands;
-    const int cnt = a.count ? a.count[q] : a.T;
-    const int nc = min(kItemCands, cnt - c0);
-    if (nc <= 0) {
-      __syncthreads();
-      continue;
-    }
-    const int64_t q0 = a.qoff[q];
-    const int mq = static_cast<int>(a.qoff[q + 1] - q0);
-    const int Nq = (mq + 15) & ~15;
-    // ---- item table: sizes -> exclusive prefix (warps 0-3), query norms
-    if (tid < kItemCands) {
-      int sz = 0;
-      if (tid < nc) {
-        const int64_t cid = static_cast<int64_t>(a.cand[static_cast<int64_t>(q) * a.T + c0 + tid]) - a.id_base;
-        const int64_t b = a.off[cid];
-        sz = static_cast<int>(a.off[cid + 1] - b);
-        S.vbase[tid] = b;
+  if (warp == 6) {
+    // =========================== item tables (work items, sizes, tile packing) ===========================
+    for (uint32_t it = 0;; ++it) {
+      const int tb = it & 1;
+      ItemTable& t = S.tab[tb];
+      PROF_WAIT(0, tc::mbar_wait(&S.tab_empty[tb], ((it >> 1) & 1u) ^ 1u));
+      int nc = 0, q = 0, c0 = 0;
+      for (;;) {  // next item with at least one candidate
+        int item = 0;
+        if (lane == 0) item = atomicAdd(a.work_counter, 1);
+        item = __shfl_sync(0xffffffffu, item, 0);
+        if (item >= a.total_items) {
+          nc = -1;
+          break;
+        }
+        q = item / a.items_per_query;
+        c0 = (item % a.items_per_query) * kItemCands;
+        const int cnt = a.count ? a.count[q] : a.T;
+        nc = min(kItemCands, cnt - c0);
+        if (nc > 0) break;
       }
-      // block-wide inclusive scan over 128 threads (4 warps) via shuffles + smem
-      int inc = sz;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += t;
+      if (nc < 0) {
+        if (lane == 0) {
+          t.nc = -1;
+          tc::mbar_arrive(&S.tab_full[tb]);
+        }
+        break;
       }
-      if (lane == 31) S.rowstart[warp] = inc;  // temp: warp totals
-      tc::named_bar(1, kItemCands);
-      int wpre = 0;
-      for (int w = 0; w < warp; ++w) wpre += S.rowstart[w];
-      tc::named_bar(1, kItemCands);
-      S.rowstart[tid + 1] = wpre + inc;
-      if (tid == 0) S.rowstart[0] = 0;
-    }
-    for (int j = tid; j < kMaxN; j += blockDim.x) S.qn[j] = (j < mq) ? a.qnorm[q0 + j] : 0.0f;
-    for (int j = tid; j < kRows; j += blockDim.x) S.hq2s[j] = 0u;
-    __syncthreads();
-    const int total_rows = S.rowstart[nc];
-    const int ntiles = (total_rows + kRows - 1) / kRows;
-    if (tid == 0 && a.rows_counter) atomicAdd(a.rows_counter, static_cast<unsigned long long>(total_rows));
-
-    if (warp < 4) {
-      // =========================== producers: cp.async gather ===========================
-      const int u = tid & 7, rsub = tid >> 3;  // 16-byte chunk within the 128-byte row; row group
-      const int lag = NST - 1;
-      uint32_t first_pending = kchunk_ctr;  // oldest K-chunk not yet signalled
-      for (int tile = 0; tile < ntiles; ++tile) {
-        int64_t vrow[8];
+      const int64_t q0 = a.qoff[q];
+      const int mq = static_cast<int>(a.qoff[q + 1] - q0);
+      const int rep_rows = mq <= 32 ? 32 : (mq <= 64 ? 64 : 128);
+      const int64_t qr = a.qrow[q];
+      int msz[kItemCands / 32];
+      int64_t vb[kItemCands / 32], pb[kItemCands / 32];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int R = tile * kRows + rsub + 16 * i;
-          if (R < total_rows) {
-            const int c = upper_bound_rows(S.rowstart, nc, R);
-            vrow[i] = S.vbase[c] + (R - S.rowstart[c]);
-          } else {
-            vrow[i] = -1;
+      for (int i = 0; i < kItemCands / 32; ++i) {
+        const int c = lane + 32 * i;
+        msz[i] = 0;
+        vb[i] = 0;
+        pb[i] = 0;
+        if (c < nc) {
+          const int64_t cid = static_cast<int64_t>(a.cand[static_cast<int64_t>(q) * a.T + c0 + c]) - a.id_base;
+          vb[i] = a.off[cid];
+          msz[i] = static_cast<int>(a.off[cid + 1] - vb[i]);
+          pb[i] = a.pbase[cid];
+          if (msz[i] > kTileRows) a.out_h2[static_cast<int64_t>(q) * a.T + c0 + c] = 0.0f;  // exact path
+        }
+      }
+      for (int j = lane; j < kMaxQ; j += 32) {
+        t.qn[j] = (j < mq) ? a.qnorm[q0 + j] : 0.0f;
+        t.qs2[j] = (j < mq) ? 2.0f * a.qscale[qr + j] : 0.0f;
+      }
+      // greedy packing: sets whole inside 256-row tiles at 8-aligned columns
+      int ntiles = 0, nent = 0, pos = kTileRows;
+      unsigned long long rows = 0;
+      for (int c = 0; c < nc; ++c) {
+        const int m = __shfl_sync(0xffffffffu, msz[c >> 5], c & 31);
+        if (m > kTileRows) continue;
+        const int mp = (m + 7) & ~7;
+        if (pos + ((m + 15) & ~15) > kTileRows) {  // the epilogue reads 16-column chunks from the set start
+          if (lane == 0) t.tile_first[ntiles] = nent;
+          ++ntiles;
+          pos = 0;
+        }
+        if (lane == (c & 31)) {
+          t.ent_cand[nent] = c;
+          t.ent_col[nent] = static_cast<int16_t>(pos);
+          t.ent_m[nent] = static_cast<int16_t>(m);
+          t.ent_vbase[nent] = vb[c >> 5];
+          t.ent_pbase[nent] = pb[c >> 5];
+        }
+        ++nent;
+        pos += mp;
+        rows += static_cast<unsigned long long>(m);
+      }
+      if (lane == 0) {
+        t.tile_first[ntiles] = nent;
+        t.nc = nc;
+        t.q = q;
+        t.c0 = c0;
+        t.mq = mq;
+        t.rep_rows = rep_rows;
+        t.reps = kMaxQ / rep_rows;
+        t.q0 = q0;
+        t.qrow = qr;
+        t.ntiles = ntiles;
+        if (a.rows_counter) atomicAdd(a.rows_counter, rows);
+      }
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&S.tab_full[tb]);  // release: the warp's table writes are visible
+    }
+  } else if (warp == 7) {
+    // =========================== tile infos: |v|^2 and scale of every column ===========================
+    uint32_t tile_ctr = 0;
+    for (uint32_t it = 0;; ++it) {
+      const int tb = it & 1;
+      const ItemTable& t = S.tab[tb];
+      PROF_WAIT(3, tc::mbar_wait(&S.tab_full[tb], (it >> 1) & 1u));
+      if (t.nc < 0) break;
+      const int ntiles = t.ntiles;
+      for (int tile = 0; tile < ntiles; ++tile, ++tile_ctr) {
+        const int e0 = t.tile_first[tile], e1 = t.tile_first[tile + 1];
+        const int slot = tile_ctr % kInfoSlots;
+        TileInfo& inf = S.info[slot];
+        PROF_WAIT(2, tc::mbar_wait(&S.info_empty[slot], ((tile_ctr / kInfoSlots) & 1u) ^ 1u));
+        float vn8[kTileRows / 32], vs8[kTileRows / 32];
+#pragma unroll
+        for (int k = 0; k < kTileRows / 32; ++k) {  // lane owns columns lane + 32k: locate the set, load
+          const int j = lane + 32 * k;
+          int lo = e0, hi = e1;  // largest e with ent_col[e] <= j
+          while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (t.ent_col[mid] <= j) lo = mid;
+            else hi = mid;
+          }
+          const int r = j - t.ent_col[lo];
+          vn8[k] = 0.0f;
+          vs8[k] = 0.0f;
+          if (r < t.ent_m[lo]) {
+            vn8[k] = a.vnorm[t.ent_vbase[lo] + r];
+            vs8[k] = a.vscale[t.ent_pbase[lo] + r];
           }
         }
-        for (int kc = 0; kc < KC; ++kc) {
-          const uint32_t st = kchunk_ctr % NST;
-          tc::mbar_wait(&S.empty[st], ((kchunk_ctr / NST) & 1u) ^ 1u);
+#pragma unroll
+        for (int k = 0; k < kTileRows / 32; ++k) {
+          inf.vn[lane + 32 * k] = vn8[k];
+          inf.vs[lane + 32 * k] = vs8[k];
+        }
+        if (lane == 0) {
+          inf.first = e0;
+          inf.count = e1 - e0;
+        }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&S.info_full[slot]);
+      }
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&S.tab_empty[tb]);
+    }
+  } else if (warp == 0) {
+    // =========================== producer: bulk copies ===========================
+    uint32_t stage_ctr = 0;
+    for (uint32_t it = 0;; ++it) {
+      const int tb = it & 1;
+      const ItemTable& t = S.tab[tb];
+      PROF_WAIT(7, tc::mbar_wait(&S.tab_full[tb], (it >> 1) & 1u));
+      if (t.nc < 0) break;
+      const int ntiles = t.ntiles, mq = t.mq, rep_rows = t.rep_rows, reps = t.reps;
+      const int64_t qr = t.qrow;
+      const uint32_t qbytes = static_cast<uint32_t>((mq + 7) & ~7) / 8u * KCS * 1024u;
+      for (int tile = 0; tile < ntiles; ++tile) {
+        const int e0 = t.tile_first[tile], e1 = t.tile_first[tile + 1];
+        uint32_t bytes = 0;  // B bytes of one piece of one stage
+        for (int e = e0 + lane; e < e1; e += 32) bytes += static_cast<uint32_t>((t.ent_m[e] + 7) & ~7) / 8u * KCS * 1024u;
+        bytes = static_cast<uint32_t>(warp_sum(static_cast<int>(bytes)));
+        const uint32_t stage_tx = (three ? 2u : 1u) * (bytes + static_cast<uint32_t>(reps) * qbytes);
+        for (int ks = 0; ks < KS; ++ks, ++stage_ctr) {
+          const uint32_t st = stage_ctr % NST;
+          PROF_WAIT(1, tc::mbar_wait(&S.empty[st], ((stage_ctr / NST) & 1u) ^ 1u));
           const uint32_t sbase = ring_s + st * a.stage_bytes;
-          const uint32_t a_hi = sbase, a_lo = sbase + pieceA;
-          const uint32_t b_hi = sbase + (three ? 2 : 1) * pieceA, b_lo = b_hi + pieceB;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int r = rsub + 16 * i;
-            const uint32_t o = tc::sw128_off(r, u);
-            const int64_t v = vrow[i];
-            const size_t e = (v >= 0 ? static_cast<size_t>(v) : 0) * a.dpad + kc * kKChunk + u * 8;
-            const uint32_t nb = v >= 0 ? 16u : 0u;
-            tc::cp_async16(a_hi + o, a.hi + e, nb);
-            if (three) tc::cp_async16(a_lo + o, a.lo + e, nb);
+          const uint32_t a_hi = sbase, a_lo = sbase + a.a_bytes;
+          const uint32_t b_hi = sbase + (three ? 2u : 1u) * a.a_bytes, b_lo = b_hi + a.b_bytes;
+          if (lane == 0) mbar_arrive_expect_tx(&S.full[st], stage_tx);
+          __syncwarp();
+          for (int e = e0 + lane; e < e1; e += 32) {
+            const int mp = (t.ent_m[e] + 7) & ~7;
+            const size_t src = ((static_cast<size_t>(ks) * a.pgroups + (t.ent_pbase[e] >> 3)) * KCS) * 8 * kKChunk;
+            const uint32_t nb = static_cast<uint32_t>(mp) / 8u * KCS * 1024u;
+            const uint32_t o = static_cast<uint32_t>(t.ent_col[e]) / 8u * KCS * 1024u;
+            bulk_g2s(b_hi + o, a.hs + src, nb, &S.full[st]);
+            if (three) bulk_g2s(b_lo + o, a.ls + src, nb, &S.full[st]);
           }
-          for (int j = rsub; j < Nq; j += 16) {
-            const uint32_t o = tc::sw128_off(j, u);
-            const bool ok = j < mq;
-            const size_t e = static_cast<size_t>(ok ? q0 + j : 0) * a.dpad + kc * kKChunk + u * 8;
-            tc::cp_async16(b_hi + o, a.qhi + e, ok ? 16u : 0u);
-            if (three) tc::cp_async16(b_lo + o, a.qlo + e, ok ? 16u : 0u);
-          }
-          tc::cp_async_commit();
-          ++kchunk_ctr;
-          // signal chunks that are at least `lag` groups old
-          while (kchunk_ctr - first_pending > static_cast<uint32_t>(lag)) {
-            if (lag >= 3) tc::cp_async_wait<3>();
-            else if (lag == 2) tc::cp_async_wait<2>();
-            else tc::cp_async_wait<1>();
-            tc::fence_proxy_async_smem();
-            tc::mbar_arrive(&S.full[first_pending % NST]);
-            ++first_pending;
+          if (lane >= 32 - reps) {  // query replicas: replica r at A rows r * rep_rows
+            const int r = lane - (32 - reps);
+            const size_t src = ((static_cast<size_t>(ks) * a.qgroups + (qr >> 3)) * KCS) * 8 * kKChunk;
+            const uint32_t o = static_cast<uint32_t>(r * rep_rows) / 8u * KCS * 1024u;
+            bulk_g2s(a_hi + o, a.qhs + src, qbytes, &S.full[st]);
+            if (three) bulk_g2s(a_lo + o, a.qls + src, qbytes, &S.full[st]);
           }
         }
       }
-      tc::cp_async_wait<0>();
-      tc::fence_proxy_async_smem();
-      while (first_pending != kchunk_ctr) {
-        tc::mbar_arrive(&S.full[first_pending % NST]);
-        ++first_pending;
-      }
-    } else if (warp == 8) {
-      // =========================== MMA issuer (one thread) ===========================
-      const uint32_t idesc = tc::idesc_bf16_f32(kRows, Nq);
-      for (int tile = 0; tile < ntiles; ++tile) {
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&S.tab_empty[tb]);
+    }
+  } else if (warp == 1) {
+    // =========================== MMA issuer (one thread) ===========================
+    uint32_t stage_ctr = 0, tile_ctr = 0;
+    const uint32_t idesc = tc::idesc_f16_f32(128, kTileRows);
+    for (uint32_t it = 0;; ++it) {
+      const int tb = it & 1;
+      const ItemTable& t = S.tab[tb];
+      PROF_WAIT(4, tc::mbar_wait(&S.tab_full[tb], (it >> 1) & 1u));
+      const int nc = t.nc;
+      if (nc < 0) break;
+      const int ntiles = t.ntiles;
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&S.tab_empty[tb]);  // the MMA warp needs nothing else from the table
+      for (int tile = 0; tile < ntiles; ++tile, ++tile_ctr) {
         const uint32_t acc = tile_ctr & 1u;
-        tc::mbar_wait(&S.tempty[acc], ((tile_ctr >> 1) & 1u) ^ 1u);
+        PROF_WAIT(5, tc::mbar_wait(&S.tempty[acc], ((tile_ctr >> 1) & 1u) ^ 1u));
         tc::fence_after_sync();
-        const uint32_t d_tmem = tmem + acc * a.tmem_cols_per_acc;
-        for (int kc = 0; kc < KC; ++kc) {
-          const uint32_t st = kchunk_ctr % NST;
-          tc::mbar_wait(&S.full[st], (kchunk_ctr / NST) & 1u);
+        const uint32_t d_tmem = tmem + acc * kTileRows;
+        for (int ks = 0; ks < KS; ++ks, ++stage_ctr) {
+          const uint32_t st = stage_ctr % NST;
+          PROF_WAIT(6, tc::mbar_wait(&S.full[st], (stage_ctr / NST) & 1u));
           tc::fence_after_sync();
           if (lane == 0) {
             const uint32_t sbase = ring_s + st * a.stage_bytes;
-            const uint32_t a_hi = sbase, a_lo = sbase + pieceA;
-            const uint32_t b_hi = sbase + (three ? 2 : 1) * pieceA, b_lo = b_hi + pieceB;
+            const uint32_t a_hi = sbase, a_lo = sbase + a.a_bytes;
+            const uint32_t b_hi = sbase + (three ? 2u : 1u) * a.a_bytes, b_lo = b_hi + a.b_bytes;
+            for (int kc = 0; kc < KCS; ++kc) {
 #pragma unroll
-            for (int kk = 0; kk < kKChunk / 16; ++kk) {
-              const uint32_t koff = kk * 32;
-              const uint32_t accum = (kc | kk) ? 1u : 0u;
-              tc::umma_bf16(d_tmem, tc::sw128_desc(a_hi + koff), tc::sw128_desc(b_hi + koff), idesc, accum);
-              if (three) {
-                tc::umma_bf16(d_tmem, tc::sw128_desc(a_hi + koff), tc::sw128_desc(b_lo + koff), idesc, 1u);
-                tc::umma_bf16(d_tmem, tc::sw128_desc(a_lo + koff), tc::sw128_desc(b_hi + koff), idesc, 1u);
+              for (int kk = 0; kk < kKChunk / 16; ++kk) {
+                const uint32_t koff = kc * 1024u + kk * 32u;
+                const uint32_t accum = (ks | kc | kk) ? 1u : 0u;
+                tc::umma_bf16(d_tmem, sw128_desc_sbo(a_hi + koff, sbo), sw128_desc_sbo(b_hi + koff, sbo), idesc,
+                              accum);
+                if (three) {
+                  tc::umma_bf16(d_tmem, sw128_desc_sbo(a_hi + koff, sbo), sw128_desc_sbo(b_lo + koff, sbo), idesc, 1u);
+                  tc::umma_bf16(d_tmem, sw128_desc_sbo(a_lo + koff, sbo), sw128_desc_sbo(b_hi + koff, sbo), idesc, 1u);
+                }
               }
             }
             tc::umma_commit(&S.empty[st]);
-            if (kc == KC - 1) tc::umma_commit(&S.tfull[acc]);
+            if (ks == KS - 1) tc::umma_commit(&S.tfull[acc]);
           }
           __syncwarp();
-          ++kchunk_ctr;
         }
-        ++tile_ctr;
-      }
-    } else {
-      // =========================== epilogue (warps 4-7) ===========================
-      const int ew = warp - 4;
-      const int r = ew * 32 + lane;  // tile row == TMEM lane
-      const int et = tid - kProd;    // 0..127
-      float* out = a.out_h2 + static_cast<int64_t>(q) * a.T + c0;
-      for (int tile = 0; tile < ntiles; ++tile) {
-        const uint32_t acc = tile_ctr & 1u;
-        const int ts = tile * kRows;
-        const int R = ts + r;
-        const bool valid = R < total_rows;
-        float vn = 0.0f;
-        if (valid) {
-          const int c = upper_bound_rows(S.rowstart, nc, R);
-          vn = a.vnorm[S.vbase[c] + (R - S.rowstart[c])];
-        }
-        const int tile_end = min(total_rows, ts + kRows);
-        const int cf = upper_bound_rows(S.rowstart, nc, ts);
-        const int cl = upper_bound_rows(S.rowstart, nc, tile_end - 1);
-        const int nseg = cl - cf + 1;
-        const bool carry_in = S.rowstart[cf] < ts;
-        const bool carry_out = S.rowstart[cl + 1] > tile_end;
-
-        tc::mbar_wait(&S.tfull[acc], (tile_ctr >> 1) & 1u);
-        tc::fence_after_sync();
-        float cmin = __int_as_float(0x7f800000);
-        const uint32_t tbase = tmem + acc * a.tmem_cols_per_acc + (static_cast<uint32_t>(ew * 32) << 16);
-        for (int cc = 0; cc < Nq; cc += 32) {
-          uint32_t g0[16], g1[16];
-          tc::tmem_ld16(tbase + cc, g0);
-          if (cc + 16 < Nq) tc::tmem_ld16(tbase + cc + 16, g1);
-          tc::tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const int col = cc + j;
-            const uint32_t gb = j < 16 ? g0[j] : g1[j - 16];
-            float d2 = __int_as_float(0x7f800000);
-            if (col < mq && valid) {
-              const float g = __uint_as_float(gb);
-              d2 = fmaxf(vn + S.qn[col] - 2.0f * g, 0.0f);
-              cmin = fminf(cmin, d2);
-            }
-            S.dsm[r][j] = d2;
-          }
-          tc::named_bar(2, kEpi);
-          // segmented column minima for columns cc .. cc+31
-          for (int p = et; p < nseg * 32; p += kEpi) {
-            const int s = p >> 5, j = p & 31, col = cc + j;
-            if (col >= mq) continue;
-            const int c = cf + s;
-            const int rb = max(S.rowstart[c], ts) - ts, re = min(S.rowstart[c + 1], tile_end) - ts;
-            float m = __int_as_float(0x7f800000);
-            for (int rr = rb; rr < re; ++rr) m = fminf(m, S.dsm[rr][j]);
-            if (s == 0 && carry_in) m = fminf(m, S.carry_r[tile & 1][col]);
-            if (s == nseg - 1 && carry_out) S.carry_r[(tile + 1) & 1][col] = m;
-            else atomicMax(&S.hq2s[s], __float_as_uint(m));
-          }
-          tc::named_bar(2, kEpi);
-        }
-        // accumulator fully read: hand the TMEM buffer back to the MMA warp
-        tc::fence_before_sync();
-        tc::mbar_arrive(&S.tempty[acc]);
-        S.csm[r] = valid ? cmin : 0.0f;
-        tc::named_bar(2, kEpi);
-        if (et < nseg) {
-          const int s = et, c = cf + s;
-          const int rb = max(S.rowstart[c], ts) - ts, re = min(S.rowstart[c + 1], tile_end) - ts;
-          float hv = 0.0f;
-          for (int rr = rb; rr < re; ++rr) hv = fmaxf(hv, S.csm[rr]);
-          if (s == 0 && carry_in) hv = fmaxf(hv, S.carry_h[tile & 1]);
-          if (s == nseg - 1 && carry_out) {
-            S.carry_h[(tile + 1) & 1] = hv;
-          } else {
-            const float hq = __uint_as_float(S.hq2s[s]);
-            out[c] = fmaxf(hv, hq);
-          }
-          S.hq2s[s] = 0u;
-        }
-        tc::named_bar(2, kEpi);
-        ++tile_ctr;
       }
     }
-    // keep every role's counters in step (producers/MMA advanced kchunk_ctr, epilogue/MMA tile_ctr)
-    if (warp < 4) tile_ctr += ntiles;
-    else if (warp == 8) { /* both advanced */ }
-    else kchunk_ctr += ntiles * KC;
-    __syncthreads();
+  } else {
+    // =========================== epilogue (warps 2-5, 8-11) ===========================
+    const int ew = warp & 3;                // TMEM lane quarter = query replica rows 32*ew ..
+    const int sub = warp >= 8 ? 1 : 0;      // two warps per lane quarter take alternate sets
+    uint32_t tile_ctr = 0;
+    for (uint32_t it = 0;; ++it) {
+      const int tb = it & 1;
+      const ItemTable& t = S.tab[tb];
+      PROF_WAIT(8, tc::mbar_wait(&S.tab_full[tb], (it >> 1) & 1u));
+      const int nc = t.nc;
+      if (nc < 0) break;
+      const int mq = t.mq, rep_rows = t.rep_rows, ntiles = t.ntiles;
+      const int wpr = rep_rows / 32;          // warps per replica (per sub)
+      const int rep = ew / wpr;               // this warp's replica
+      const int nrep = 4 / wpr;
+      const int qi = (ew % wpr) * 32 + lane;  // query row held by this lane
+      const bool qvalid = qi < mq;
+      const float qn = qvalid ? t.qn[qi] : 0.0f, qs2 = qvalid ? t.qs2[qi] : 0.0f;
+      float* out = a.out_h2 + static_cast<int64_t>(t.q) * a.T + t.c0;
+      for (int tile = 0; tile < ntiles; ++tile, ++tile_ctr) {
+        const uint32_t acc = tile_ctr & 1u;
+        const int slot = tile_ctr % kInfoSlots;
+        const TileInfo& inf = S.info[slot];
+        PROF_WAIT(9, tc::mbar_wait(&S.tfull[acc], (tile_ctr >> 1) & 1u));
+        PROF_WAIT(10, tc::mbar_wait(&S.info_full[slot], (tile_ctr / kInfoSlots) & 1u));
+        tc::fence_after_sync();
+        const uint32_t tbase = tmem + acc * kTileRows + (static_cast<uint32_t>(ew * 32) << 16);
+        const int e0 = inf.first, ne = inf.count;
+        // sets of this tile: replica rep takes sets rep + nrep*k, its two warps (sub) alternate
+        for (int s = rep + nrep * sub; s < ne; s += 2 * nrep) {
+          const int e = e0 + s;
+          const int col0 = t.ent_col[e], m = t.ent_m[e];
+          float rmin = __int_as_float(0x7f800000);  // per lane (query row): min over the set's columns
+          float hv = 0.0f;                          // max over columns of (min over rows)
+          for (int j0 = 0; j0 < m; j0 += 32) {
+            uint32_t g[32];
+            tc::tmem_ld16(tbase + col0 + j0, *reinterpret_cast<uint32_t(*)[16]>(&g[0]));
+            if (j0 + 16 < m) tc::tmem_ld16(tbase + col0 + j0 + 16, *reinterpret_cast<uint32_t(*)[16]>(&g[16]));
+            tc::tmem_ld_wait();
+#pragma unroll
+            for (int j4 = 0; j4 < 32; j4 += 4) {
+              if (j0 + j4 < m) {  // warp-uniform
+                const float4 vn4 = *reinterpret_cast<const float4*>(&inf.vn[col0 + j0 + j4]);
+                const float4 vs4 = *reinterpret_cast<const float4*>(&inf.vs[col0 + j0 + j4]);
+                const float vn[4] = {vn4.x, vn4.y, vn4.z, vn4.w}, vs[4] = {vs4.x, vs4.y, vs4.z, vs4.w};
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                  const int j = j4 + jj;
+                  if (j0 + j < m) {
+                    float d2 = __int_as_float(0x7f800000);
+                    if (qvalid) d2 = fmaxf(qn + vn[jj] - (qs2 * vs[jj]) * __uint_as_float(g[j]), 0.0f);
+                    rmin = fminf(rmin, d2);
+                    const uint32_t cmin = __reduce_min_sync(0xffffffffu, __float_as_uint(d2));
+                    if (wpr == 1) hv = fmaxf(hv, __uint_as_float(cmin));
+                    else if (lane == 0) atomicMin(&S.cm[rep][col0 + j0 + j], cmin);
+                  }
+                }
+              }
+            }
+          }
+          const uint32_t hq = __reduce_max_sync(0xffffffffu, qvalid ? __float_as_uint(rmin) : 0u);
+          if (wpr == 1) {
+            if (lane == 0) out[t.ent_cand[e]] = fmaxf(__uint_as_float(hq), hv);
+          } else if (lane == 0) {
+            atomicMax(&S.hq[rep][s % kMaxSetsPerTile], hq);
+          }
+        }
+        // TMEM reads of this tile are done
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&S.tempty[acc]);
+        if (wpr > 1) {  // combine the warps of each replica, then finalize
+          tc::named_bar(2, 32 * kEpiWarps);
+          if ((ew % wpr) == 0) {  // the replica's first warp (per sub) finalizes its sets
+            for (int s = rep + nrep * sub; s < ne; s += 2 * nrep) {
+              const int e = e0 + s;
+              const int col0 = t.ent_col[e], m = t.ent_m[e];
+              float hv = 0.0f;
+              for (int j = lane; j < m; j += 32) {
+                hv = fmaxf(hv, __uint_as_float(S.cm[rep][col0 + j]));
+                S.cm[rep][col0 + j] = 0x7f800000u;
+              }
+              hv = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(hv)));
+              if (lane == 0) {
+                out[t.ent_cand[e]] = fmaxf(__uint_as_float(S.hq[rep][s % kMaxSetsPerTile]), hv);
+                S.hq[rep][s % kMaxSetsPerTile] = 0u;
+              }
+            }
+          }
+          tc::named_bar(2, 32 * kEpiWarps);
+        }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&S.info_empty[slot]);
+      }
+      __syncwarp();
+      tc::named_bar(3, 32 * kEpiWarps);  // every epilogue warp is done with this item's table
+      if (tid == 64) tc::mbar_arrive(&S.tab_empty[tb]);
+    }
   }
+  if (a.prof && lane == 0 && (warp <= 2 || warp == 6 || warp == 7))
+    atomicAdd(&a.prof[warp <= 2 ? 12 + warp : (warp == 6 ? 15 : 11)], (unsigned long long)(clock64() - t_role0));
   __syncthreads();
-  if (warp == 8) {
+  if (warp == 1) {
     tc::fence_after_sync();
-    tc::tmem_dealloc(tmem, 2 * a.tmem_cols_per_acc);
+    tc::tmem_dealloc(tmem, 512);
   }
 }
 
-size_t refine_smem_bytes(int terms, int nmax, int& stages, uint32_t& stage_bytes) {
-  const uint32_t a_bytes = kRows * 128;
-  const uint32_t b_bytes = static_cast<uint32_t>(nmax) * 128;
+int refine_kcs(int dpad) { return (dpad / kKChunk) % 2 == 0 ? 2 : 1; }
+
+size_t refine_smem_bytes(int terms, int KCS, int& stages, uint32_t& stage_bytes) {
+  const uint32_t a_bytes = 128u * KCS * 128u, b_bytes = kTileRows * KCS * 128u;
   stage_bytes = (terms == 3 ? 2u : 1u) * (a_bytes + b_bytes);
-  stage_bytes = (stage_bytes + 1023u) & ~1023u;
-  const size_t ctrl = (sizeof(RefineSmem) + 127) & ~size_t(127);
+  const size_t ctrl = (sizeof(RefineCtl) + 127) & ~size_t(127);  // static __shared__
   const size_t budget = 227 * 1024 - 1024 - ctrl;
   stages = static_cast<int>(budget / stage_bytes);
-  if (stages > 4) stages = 4;
-  return static_cast<size_t>(stages) * stage_bytes + ctrl + 1024;
+  if (stages > kMaxStages) stages = kMaxStages;
+  return static_cast<size_t>(stages) * stage_bytes + 1024;
 }
 
-int launch_refine_tc(const __nv_bfloat16* hi, const __nv_bfloat16* lo, const float* vnorm, const int64_t* off,
-                     int dpad, const __nv_bfloat16* qhi, const __nv_bfloat16* qlo, const float* qnorm,
-                     const int64_t* qoff, int max_mq, const int32_t* cand, const int32_t* count, int T, int nq,
-                     int64_t id_base, float* out_h2, int terms, int* work_counter,
-                     unsigned long long* rows_counter, int num_sms, cudaStream_t st) {
+int launch_refine_tc(const __half* hs, const __half* ls, const float* vscale, int64_t prows, const int64_t* pbase,
+                     const float* vnorm, const int64_t* off, int dpad, const __half* qhs, const __half* qls,
+                     const float* qscale, int64_t qrows, const int64_t* qrow, const float* qnorm, const int64_t* qoff,
+                     int max_mq, const int32_t* cand, const int32_t* count, int T, int nq, int64_t id_base,
+                     float* out_h2, int terms, int* work_counter, unsigned long long* rows_counter, int num_sms,
+                     cudaStream_t st) {
   if (nq <= 0 || T <= 0) return BVSS_OK;
-  if (max_mq > kMaxN) BVSS_FAIL(BVSS_EUNSUPPORTED, "query set with %d vectors exceeds the %d-row refine tile", max_mq, kMaxN);
+  if (max_mq > kMaxQ) BVSS_FAIL(BVSS_EUNSUPPORTED, "query set with %d vectors exceeds the %d-row tensor tile", max_mq, kMaxQ);
   if (dpad % kKChunk) BVSS_FAIL(BVSS_EINVAL, "dpad must be a multiple of 64");
   RefineArgs a;
-  a.hi = hi; a.lo = lo; a.vnorm = vnorm; a.off = off; a.dpad = dpad;
-  a.qhi = qhi; a.qlo = qlo; a.qnorm = qnorm; a.qoff = qoff;
+  a.hs = hs; a.ls = ls; a.vscale = vscale; a.pgroups = prows / 8; a.pbase = pbase; a.vnorm = vnorm; a.off = off;
+  a.KC = dpad / kKChunk;
+  a.KCS = refine_kcs(dpad);
+  a.qhs = qhs; a.qls = qls; a.qscale = qscale; a.qgroups = qrows / 8; a.qrow = qrow; a.qnorm = qnorm; a.qoff = qoff;
   a.cand = cand; a.count = count; a.T = T; a.nq = nq; a.id_base = id_base; a.out_h2 = out_h2;
-  a.terms = terms == 1 ? 1 : 3;
-  a.nmax = (max_mq + 15) & ~15;
-  if (a.nmax < 16) a.nmax = 16;
+  a.terms = terms == 3 ? 3 : 1;
   int stages;
   uint32_t stage_bytes;
-  const size_t smem = refine_smem_bytes(a.terms, a.nmax, stages, stage_bytes);
-  if (stages < 2) BVSS_FAIL(BVSS_EUNSUPPORTED, "refine tile does not fit shared memory");
+  const size_t smem = refine_smem_bytes(a.terms, a.KCS, stages, stage_bytes);
+  if (stages < 1) BVSS_FAIL(BVSS_EUNSUPPORTED, "refine stage does not fit shared memory");
   a.stages = stages;
   a.stage_bytes = stage_bytes;
-  a.a_bytes = kRows * 128;
-  a.b_bytes = static_cast<uint32_t>(a.nmax) * 128;
-  uint32_t cols = 32;
-  while (cols < static_cast<uint32_t>(a.nmax)) cols <<= 1;
-  a.tmem_cols_per_acc = cols;
+  a.a_bytes = 128u * a.KCS * 128u;
+  a.b_bytes = kTileRows * a.KCS * 128u;
   a.items_per_query = ceil_div(T, kItemCands);
   a.total_items = a.items_per_query * nq;
   a.work_counter = work_counter;
   a.rows_counter = rows_counter;
+  static unsigned long long* prof = nullptr;
+  a.prof = nullptr;
+  if (getenv("BVSS_REFINE_PROF")) {
+    if (!prof) cudaMalloc(&prof, 16 * sizeof(unsigned long long));
+    cudaMemsetAsync(prof, 0, 16 * sizeof(unsigned long long), st);
+    a.prof = prof;
+  }
   BVSS_CUDA(cudaMemsetAsync(work_counter, 0, sizeof(int), st));
   BVSS_CUDA(cudaFuncSetAttribute(refine_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const int grid = a.total_items < num_sms ? a.total_items : num_sms;
   refine_tc_kernel<<<grid, kRefineThreads, smem, st>>>(a);
   BVSS_TRY(post_launch(__func__, st));
+  if (a.prof) {  // developer instrumentation: per-CTA average Mcycles per role
+    unsigned long long h[16];
+    cudaMemcpyAsync(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    const double g = grid;
+    fprintf(stderr,
+            "[refine prof] per CTA Mcycles: copy %.2f (tab %.2f, empty %.2f) | table %.2f (tab_empty %.2f) | info %.2f "
+            "(tab %.2f, info_empty %.2f) | mma %.2f (tab %.2f, tempty %.2f, full %.2f) | epilogue %.2f (tab %.2f, "
+            "tfull %.2f, info %.2f)\n",
+            h[12] / g / 1e6, h[7] / g / 1e6, h[1] / g / 1e6, h[15] / g / 1e6, h[0] / g / 1e6, h[11] / g / 1e6, h[3] / g / 1e6, h[2] / g / 1e6, h[13] / g / 1e6, h[4] / g / 1e6, h[5] / g / 1e6,
+            h[6] / g / 1e6, h[14] / g / 1e6, h[8] / g / 1e6 / kEpiWarps, h[9] / g / 1e6 / kEpiWarps, h[10] / g / 1e6 / kEpiWarps);
+  }
   return BVSS_OK;
 }
 

@@ -5,8 +5,9 @@
 // candidates is found by a 4-round radix select; every candidate whose
 // tensor-core H^2 is within 2E of it (E = the rigorous squared-distance error
 // bound of the refine arithmetic) is recomputed exactly by fp32
-// direct differences sum_k (q_k - v_k)^2 (Def 4 verbatim), and the k smallest
-// exact distances are emitted sorted by (distance, id) (reading R4).  The true
+// direct differences sum_k (q_k - v_k)^2 (Def 4 verbatim; one warp per
+// candidate, set rows on lanes, query rows in register blocks), and the k
+// smallest exact distances are emitted sorted by (distance, id) (reading R4).  The true
 // top-k is always inside the window, so the result does not depend on the
 // tensor-core rounding.  With E = +inf (refine_terms = 0) the kernel is a plain
 // SIMT exact refine of every candidate (correctness anchor).
@@ -15,17 +16,17 @@
 namespace bvss {
 
 constexpr int kTopkThreads = 256;
-constexpr int kMaxColChunk = 1024;
+constexpr int kTopkWarps = kTopkThreads / 32;
+constexpr int kMaxMq = 256;
+constexpr int kIB = 16;  // query rows per register block
+constexpr int kKB = 32;  // dims per register chunk
 
 struct TopkSmem {
   uint32_t hist[256];
-  uint32_t rowmin[256];
-  uint32_t colmin[kMaxColChunk];
+  float rowmin[kTopkWarps][kMaxMq];
   uint32_t wcount;
   uint32_t prefix;
   uint32_t need;
-  float hv;
-  float emax2;
   unsigned long long best;
 };
 
@@ -42,52 +43,84 @@ __device__ __forceinline__ float block_max_f(float v, float* red) {
   return r;
 }
 
-// exact H^2 between query rows [q0, q0+mq) and set rows [v0, v0+mi) in fp32
-__device__ float exact_h2(const float* __restrict__ Q, int64_t q0, int mq, const float* __restrict__ V, int64_t v0,
-                          int mi, int d, TopkSmem& S, float* red) {
-  for (int i = threadIdx.x; i < mq; i += blockDim.x) S.rowmin[i] = 0x7f800000u;
+template <bool VEC>
+__device__ __forceinline__ void load_chunk(const float* __restrict__ p, int kb, int d, bool ok, float (&x)[kKB]) {
+  if (VEC) {
+#pragma unroll
+    for (int e = 0; e < kKB; e += 4) {
+      float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (ok && kb + e < d) t = *reinterpret_cast<const float4*>(p + kb + e);
+      x[e] = t.x; x[e + 1] = t.y; x[e + 2] = t.z; x[e + 3] = t.w;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < kKB; ++e) x[e] = (ok && kb + e < d) ? p[kb + e] : 0.0f;
+  }
+}
+
+// Exact H^2 of Def 4 by fp32 direct differences, one warp: lane j owns set row
+// j (blocks of 32), query rows in register blocks of kIB (uniform, broadcast
+// loads), D^2(i,j) = sum_k (q_ik - v_jk)^2 with FMA; min/max on D^2.
+template <bool VEC>
+__device__ float warp_exact_h2(const float* __restrict__ Q, int mq, const float* __restrict__ Vs, int mi, int d,
+                               float* rowmin) {
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < mq; i += 32) rowmin[i] = __int_as_float(0x7f800000);
+  __syncwarp();
   float hv = 0.0f;
-  for (int vb = 0; vb < mi; vb += kMaxColChunk) {
-    const int vn = min(kMaxColChunk, mi - vb);
-    for (int i = threadIdx.x; i < vn; i += blockDim.x) S.colmin[i] = 0x7f800000u;
-    __syncthreads();
-    const int pairs = mq * vn;
-    for (int p = threadIdx.x; p < pairs; p += blockDim.x) {
-      const int qi = p / vn, vj = p % vn;
-      const float* a = Q + (q0 + qi) * d;
-      const float* b = V + (v0 + vb + vj) * d;
-      float s = 0.0f;
-      if ((d & 3) == 0) {
-        for (int t = 0; t < d; t += 4) {
-          const float4 x = *reinterpret_cast<const float4*>(a + t);
-          const float4 y = *reinterpret_cast<const float4*>(b + t);
-          const float e0 = x.x - y.x, e1 = x.y - y.y, e2 = x.z - y.z, e3 = x.w - y.w;
-          s = __fmaf_rn(e0, e0, s);
-          s = __fmaf_rn(e1, e1, s);
-          s = __fmaf_rn(e2, e2, s);
-          s = __fmaf_rn(e3, e3, s);
-        }
-      } else {
-        for (int t = 0; t < d; ++t) {
-          const float e = a[t] - b[t];
-          s = __fmaf_rn(e, e, s);
+  for (int jb = 0; jb < mi; jb += 32) {
+    const int j = jb + lane;
+    const bool vj = j < mi;
+    const float* vrow = Vs + static_cast<int64_t>(vj ? j : 0) * d;
+    float colmin = __int_as_float(0x7f800000);
+    for (int ib = 0; ib < mq; ib += kIB) {
+      float acc[kIB];
+#pragma unroll
+      for (int ii = 0; ii < kIB; ++ii) acc[ii] = 0.0f;
+      for (int kb = 0; kb < d; kb += kKB) {
+        float v[kKB];
+        load_chunk<VEC>(vrow, kb, d, true, v);
+#pragma unroll
+        for (int ii = 0; ii < kIB; ++ii) {
+          if (ib + ii < mq) {
+            float qv[kKB];
+            load_chunk<VEC>(Q + static_cast<int64_t>(ib + ii) * d, kb, d, true, qv);
+            float s = acc[ii];
+#pragma unroll
+            for (int e = 0; e < kKB; ++e) {
+              const float t = qv[e] - v[e];
+              s = __fmaf_rn(t, t, s);
+            }
+            acc[ii] = s;
+          }
         }
       }
-      const uint32_t u = __float_as_uint(s);  // s >= 0: integer order == float order
-      atomicMin(&S.rowmin[qi], u);
-      atomicMin(&S.colmin[vj], u);
+#pragma unroll
+      for (int ii = 0; ii < kIB; ++ii) {
+        if (ib + ii < mq) {
+          const float a = vj ? acc[ii] : __int_as_float(0x7f800000);
+          colmin = fminf(colmin, a);
+          float m = a;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
+          if (lane == 0) rowmin[ib + ii] = fminf(rowmin[ib + ii], m);
+        }
+      }
     }
-    __syncthreads();
-    float m = 0.0f;
-    for (int i = threadIdx.x; i < vn; i += blockDim.x) m = fmaxf(m, __uint_as_float(S.colmin[i]));
-    hv = fmaxf(hv, block_max_f(m, red));
+    hv = fmaxf(hv, vj ? colmin : 0.0f);
   }
-  float m = 0.0f;
-  for (int i = threadIdx.x; i < mq; i += blockDim.x) m = fmaxf(m, __uint_as_float(S.rowmin[i]));
-  const float hq = block_max_f(m, red);
+  __syncwarp();
+  float hq = 0.0f;
+  for (int i = lane; i < mq; i += 32) hq = fmaxf(hq, rowmin[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    hv = fmaxf(hv, __shfl_xor_sync(0xffffffffu, hv, o));
+    hq = fmaxf(hq, __shfl_xor_sync(0xffffffffu, hq, o));
+  }
   return fmaxf(hq, hv);
 }
 
+template <bool VEC>
 __global__ void __launch_bounds__(kTopkThreads) topk_fixup_kernel(
     const float* __restrict__ approx, const int32_t* __restrict__ cand, const int32_t* __restrict__ count, int T, int k,
     const float* __restrict__ V, const int64_t* __restrict__ off, int64_t id_base, int d, const float* __restrict__ Qv,
@@ -100,13 +133,14 @@ __global__ void __launch_bounds__(kTopkThreads) topk_fixup_kernel(
   __shared__ TopkSmem S;
   __shared__ float red[32];
   const int q = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int cnt = count ? count[q] : T;
   const int64_t q0 = qoff[q];
   const int mq = static_cast<int>(qoff[q + 1] - q0);
   const int kk = min(k, cnt);
   for (int i = threadIdx.x; i < cnt; i += blockDim.x) ap[i] = approx ? approx[static_cast<int64_t>(q) * T + i] : 0.0f;
   if (threadIdx.x == 0) S.wcount = 0;
-  // window threshold W = (k-th smallest approx) + 2E
+  // window threshold W = (k-th smallest tensor-core H^2) + 2E
   float W = __int_as_float(0x7f800000);
   if (!exact_all && kk > 0) {
     float mq2 = 0.0f;
@@ -114,12 +148,11 @@ __global__ void __launch_bounds__(kTopkThreads) topk_fixup_kernel(
     mq2 = block_max_f(mq2, red);
     const float Mq = sqrtf(mq2), Mv = sqrtf(vmax2);
     const float E = c1 * Mq * Mv + c2 * (mq2 + vmax2);
-    // radix select of the kk-th smallest (1-based) over uint keys of approx >= 0
     if (threadIdx.x == 0) {
       S.prefix = 0u;
       S.need = static_cast<uint32_t>(kk);
     }
-    for (int rnd = 0; rnd < 4; ++rnd) {
+    for (int rnd = 0; rnd < 4; ++rnd) {  // radix select of the kk-th smallest (uint order of floats >= 0)
       const int shift = 24 - 8 * rnd;
       for (int i = threadIdx.x; i < 256; i += blockDim.x) S.hist[i] = 0u;
       __syncthreads();
@@ -144,25 +177,23 @@ __global__ void __launch_bounds__(kTopkThreads) topk_fixup_kernel(
       }
       __syncthreads();
     }
-    W = __uint_as_float(S.prefix) + 2.0f * E;
-    W = W * (1.0f + 1e-6f);  // absorb the rounding of the threshold arithmetic itself
+    W = (__uint_as_float(S.prefix) + 2.0f * E) * (1.0f + 1e-6f);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < cnt; i += blockDim.x)
     if (exact_all || ap[i] <= W) win[atomicAdd(&S.wcount, 1u)] = i;
   __syncthreads();
   const int nw = static_cast<int>(S.wcount);
-  // exact recompute of the window
-  for (int w = 0; w < nw; ++w) {
-    const int i = win[w];
-    const int64_t cid = static_cast<int64_t>(cand[static_cast<int64_t>(q) * T + i]) - id_base;
+  // exact recompute of the window: one warp per candidate
+  for (int w = warp; w < nw; w += kTopkWarps) {
+    const int64_t cid = static_cast<int64_t>(cand[static_cast<int64_t>(q) * T + win[w]]) - id_base;
     const int64_t v0 = off[cid];
     const int mi = static_cast<int>(off[cid + 1] - v0);
-    const float h2 = exact_h2(Qv, q0, mq, V, v0, mi, d, S, red);
-    if (threadIdx.x == 0) ex[w] = h2;
-    __syncthreads();
+    const float h2 = warp_exact_h2<VEC>(Qv + q0 * d, mq, V + v0 * d, mi, d, S.rowmin[warp]);
+    if (lane == 0) ex[w] = h2;
   }
   if (threadIdx.x == 0 && fixup_counter) atomicAdd(reinterpret_cast<unsigned long long*>(fixup_counter), nw);
+  __syncthreads();
   // k smallest by (exact, id): k rounds of block argmin on a packed 64-bit key
   for (int r = 0; r < k; ++r) {
     unsigned long long best = ~0ull;
@@ -180,7 +211,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_fixup_kernel(
     }
     if (threadIdx.x == 0) S.best = ~0ull;
     __syncthreads();
-    if ((threadIdx.x & 31) == 0) atomicMin(&S.best, best);
+    if (lane == 0) atomicMin(&S.best, best);
     __syncthreads();
     const unsigned long long b = S.best;
     if (threadIdx.x == 0) {
@@ -194,8 +225,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_fixup_kernel(
         od[r] = sqrtf(__uint_as_float(static_cast<uint32_t>(b >> 32)));
       }
     }
-    // mark the winner as taken
-    if (b != ~0ull) {
+    if (b != ~0ull) {  // mark the winner as taken
       const uint32_t gid = static_cast<uint32_t>(b & 0xffffffffull);
       for (int w = threadIdx.x; w < nw; w += blockDim.x)
         if (static_cast<uint32_t>(cand[static_cast<int64_t>(q) * T + win[w]]) == gid) ex[w] = -1.0f;
@@ -212,10 +242,18 @@ int launch_topk_fixup(const float* approx, const int32_t* cand, const int32_t* c
                       float* out_dist, int nq, int64_t* fixup_counter, cudaStream_t st) {
   if (nq <= 0) return BVSS_OK;
   const size_t smem = topk_smem_bytes(T);
-  if (smem > 200 * 1024) BVSS_FAIL(BVSS_EUNSUPPORTED, "T=%d exceeds the top-k kernel limit (16384)", T);
-  BVSS_CUDA(cudaFuncSetAttribute(topk_fixup_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  topk_fixup_kernel<<<nq, kTopkThreads, smem, st>>>(approx, cand, count, T, k, V, off, id_base, d, Qv, qoff, qnorm,
-                                                   vmax2, c1, c2, exact_all, out_ids, out_dist, fixup_counter);
+  if (smem > 190 * 1024) BVSS_FAIL(BVSS_EUNSUPPORTED, "T=%d exceeds the top-k kernel limit (16384)", T);
+  if (d % 4 == 0) {
+    auto kfn = topk_fixup_kernel<true>;
+    BVSS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    kfn<<<nq, kTopkThreads, smem, st>>>(approx, cand, count, T, k, V, off, id_base, d, Qv, qoff, qnorm, vmax2, c1, c2,
+                                        exact_all, out_ids, out_dist, fixup_counter);
+  } else {
+    auto kfn = topk_fixup_kernel<false>;
+    BVSS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    kfn<<<nq, kTopkThreads, smem, st>>>(approx, cand, count, T, k, V, off, id_base, d, Qv, qoff, qnorm, vmax2, c1, c2,
+                                        exact_all, out_ids, out_dist, fixup_counter);
+  }
   BVSS_TRY(post_launch(__func__, st));
   return BVSS_OK;
 }
