@@ -77,6 +77,11 @@ typedef struct {
   uint32_t query_batch;  /* queries per internal sub-batch; 0 = auto */
   uint32_t refine_terms; /* tensor-core Gram on the scaled fp16 split: 0 = default (= 1), 1 = hi*hi,
                             3 = hi*hi + hi*lo + lo*hi, 255 = no tensor pass (exact fp32 for every candidate) */
+  uint32_t select_mode;  /* bvss_search candidate selection: 0 = auto, 1 = full key rows (scan writes every
+                            score, radix select over them), 2 = sampled threshold (scan emits only scores <=
+                            a per-query threshold estimated on a database sample; exact, with a per-batch
+                            fallback to 1 when the estimate is too low or the buffer overflows).  Auto = 2 when
+                            the tensor-core scan runs (m % 128 == 0) and n >= 65536.  Results are identical. */
 } bvss_params;
 
 typedef struct bvss_index bvss_index;
@@ -99,6 +104,8 @@ typedef struct {
   uint64_t fixup_sets;    /* candidates recomputed by the exact fp32 fix-up */
   int32_t kernel_launches;/* kernels launched by the call */
   int32_t query_batch;
+  uint64_t select_batches;   /* query batches selected on the sampled-threshold path */
+  uint64_t select_fallbacks; /* of those, batches redone on the full-key path */
 } bvss_stats;
 
 /* ---------------------------------------------------------------- core -- */

@@ -41,7 +41,8 @@ class BvssError(RuntimeError):
 class Params(C.Structure):
     _fields_ = [("m", C.c_uint32), ("s", C.c_uint32), ("L", C.c_uint32), ("sketch", C.c_uint32),
                 ("seed", C.c_uint64), ("projection", C.c_void_p), ("device", C.c_int32), ("flags", C.c_uint32),
-                ("query_batch", C.c_uint32), ("refine_terms", C.c_uint32)]
+                ("query_batch", C.c_uint32), ("refine_terms", C.c_uint32),
+                ("select_mode", C.c_uint32)]
 
 
 class Info(C.Structure):
@@ -54,7 +55,8 @@ class Stats(C.Structure):
     _fields_ = [("ms_h2d", C.c_float), ("ms_encode", C.c_float), ("ms_scan", C.c_float), ("ms_select", C.c_float),
                 ("ms_refine", C.c_float), ("ms_topk", C.c_float), ("ms_d2h", C.c_float), ("ms_total", C.c_float),
                 ("scan_bytes", C.c_uint64), ("gather_bytes", C.c_uint64), ("cand_rows", C.c_uint64),
-                ("fixup_sets", C.c_uint64), ("kernel_launches", C.c_int32), ("query_batch", C.c_int32)]
+                ("fixup_sets", C.c_uint64), ("kernel_launches", C.c_int32), ("query_batch", C.c_int32),
+                ("select_batches", C.c_uint64), ("select_fallbacks", C.c_uint64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -128,7 +130,7 @@ class Index:
     """A device-resident BioVSS index over one database shard (one GPU)."""
 
     def __init__(self, vectors, offsets, *, m, s, L, sketch="binary", seed=0, device=0, keep_codes=False,
-                 validate=False, projection=None, refine_terms=0, query_batch=0):
+                 validate=False, projection=None, refine_terms=0, query_batch=0, select_mode=0):
         dev = _is_cuda(vectors)
         if dev != _is_cuda(offsets):
             raise ValueError("vectors and offsets must both be host arrays or both CUDA tensors")
@@ -147,7 +149,8 @@ class Index:
         p = Params(m=m, s=s, L=L, sketch=SKETCH_BINARY if sketch == "binary" else SKETCH_COUNT_U8, seed=seed,
                    projection=(proj.ctypes.data if proj is not None else None), device=device,
                    flags=(DEVICE_PTRS if dev else 0) | (KEEP_CODES if keep_codes else 0) |
-                   (VALIDATE_FINITE if validate else 0), query_batch=query_batch, refine_terms=refine_terms)
+                   (VALIDATE_FINITE if validate else 0), query_batch=query_batch, refine_terms=refine_terms,
+                   select_mode=select_mode)
         self._h = C.c_void_p()
         vp, _k1 = _ptr(vectors)
         op, _k2 = _ptr(offsets)

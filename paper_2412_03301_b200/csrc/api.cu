@@ -63,7 +63,12 @@ int launch_scan(int kind, const void* S, const int32_t* mass, int64_t n, int64_t
                 const int32_t* massQ, int nq, void* keys, int64_t key_stride, int num_sms, cudaStream_t st);
 int launch_scan_tc(int kind, const void* S, const int32_t* mass, int64_t n, int64_t n_stride, int m, const void* SQ,
                    const int32_t* massQ, int nq, void* Qx, int qpad, void* keys, int64_t key_stride, int* work_counter,
-                   int num_sms, cudaStream_t st);
+                   int num_sms, cudaStream_t st, const uint32_t* tau, int32_t* cnt, int32_t* buf_id, uint32_t* buf_key,
+                   int cap, int64_t id_base, bool expand);
+int launch_select_buf(const int32_t* cnt, const uint32_t* bkey, const int32_t* bid, int cap, int teff, int key_bits,
+                      int T, int nq, int32_t* cand, int32_t* count, int* fail, cudaStream_t s);
+int launch_gather_sample(const void* sk, const int32_t* mass, int64_t n, int cps, int64_t ns, void* out,
+                         int32_t* out_mass, int num_sms, cudaStream_t s);
 struct SelectState {
   uint32_t* prefix;
   int64_t* below;
@@ -213,6 +218,10 @@ struct bvss_index {
   uint32_t* codes = nullptr;  // optional [nvec][m/32]
   void* sk = nullptr;         // chunk-major sketches
   int32_t* mass = nullptr;
+  uint32_t select_mode = 0;   // 0 auto, 1 full keys, 2 sampled threshold
+  int64_t ns = 0;             // database sample for the threshold estimate (select_mode 2)
+  void* smp_sk = nullptr;     // chunk-major sketches of the sample
+  int32_t* smp_mass = nullptr;
   size_t owned_bytes = 0;
   Workspace ws;
   bvss_stats stats{};
@@ -240,6 +249,8 @@ struct bvss_search_ctx {
   int64_t* qrow = nullptr;       // [nq] first padded row of each query
   void* keys = nullptr;
   int64_t key_stride = 0;
+  void* qx = nullptr;         // expanded queries of the tensor-core scan
+  int qpad = 0;
   SelectState sel{};
   int32_t* local_hist = nullptr;
   int32_t* cand = nullptr;
@@ -396,22 +407,45 @@ int prepare_queries(bvss_index* idx, bvss_search_ctx* c, const float* queries, c
   return BVSS_OK;
 }
 
-// scan + select (local phases) for a prepared batch; when `global` the caller drives resolve
+bool use_tc_scan(const bvss_index* idx) {
+  static const bool simt = getenv("BVSS_SCAN_SIMT") != nullptr;  // developer switch: SIMT popc/dp4a scan
+  return idx->m % 128 == 0 && !simt;
+}
+
+// tensor-core scan operands: queries expanded to [m/16][qpad][16 B] (scan_tc.cu)
+int expand_alloc(bvss_index* idx, bvss_search_ctx* c) {
+  c->qpad = static_cast<int>(ceil_div<int64_t>(c->nq, 256) * 256);
+  return idx->ws.get("scan_qx", static_cast<size_t>(idx->m) * c->qpad, &c->qx);
+}
+
+int alloc_select_state(bvss_index* idx, bvss_search_ctx* c) {
+  const int nq = static_cast<int>(c->nq);
+  BVSS_TRY(c->alloc(nq * sizeof(uint32_t), reinterpret_cast<void**>(&c->sel.prefix)));
+  BVSS_TRY(c->alloc(nq * sizeof(int64_t), reinterpret_cast<void**>(&c->sel.below)));
+  BVSS_TRY(c->alloc(nq * sizeof(int64_t), reinterpret_cast<void**>(&c->sel.teff)));
+  BVSS_TRY(c->alloc(nq * sizeof(int64_t), reinterpret_cast<void**>(&c->sel.eq)));
+  BVSS_TRY(c->alloc(nq * sizeof(int64_t), reinterpret_cast<void**>(&c->sel.quota)));
+  BVSS_TRY(c->alloc(nq * sizeof(int32_t), reinterpret_cast<void**>(&c->sel.digit)));
+  BVSS_TRY(c->alloc(static_cast<size_t>(nq) * kHistBins * sizeof(int32_t), reinterpret_cast<void**>(&c->local_hist)));
+  c->key_bits = key_bits_for(idx->sketch, idx->m);
+  c->rounds = rounds_for(c->key_bits);
+  c->next_round = 0;
+  return BVSS_OK;
+}
+
+// full-key scan (every score written) + select state init; the caller drives the select rounds
 int scan_batch(bvss_index* idx, bvss_search_ctx* c) {
   const int64_t n = idx->n;
   const int key_size = idx->sketch == BVSS_SKETCH_BINARY ? 2 : 4;
   c->key_stride = (n + 7) & ~int64_t(7);
-  BVSS_TRY(c->alloc(static_cast<size_t>(c->nq) * c->key_stride * key_size, &c->keys));
-  static const bool simt = getenv("BVSS_SCAN_SIMT") != nullptr;  // developer switch: SIMT popc/dp4a scan
-  if (idx->m % 128 == 0 && !simt) {
-    // tensor-core scan (scan_tc.cu): u8 x u8 -> s32 on tcgen05, queries expanded to [m/16][qpad][16 B]
-    const int qpad = static_cast<int>(ceil_div<int64_t>(c->nq, 256) * 256);
-    void* qx;
-    BVSS_TRY(c->alloc(static_cast<size_t>(idx->m) * qpad, &qx));
+  BVSS_TRY(idx->ws.get("keys", static_cast<size_t>(c->nq) * c->key_stride * key_size, &c->keys));
+  if (use_tc_scan(idx)) {
+    BVSS_TRY(expand_alloc(idx, c));
     int* wc;
     BVSS_TRY(idx->ws.get("scan_counter", sizeof(int), reinterpret_cast<void**>(&wc)));
     BVSS_TRY(launch_scan_tc(idx->sketch, idx->sk, idx->mass, n, n, idx->m, c->qsk, c->qmass, static_cast<int>(c->nq),
-                            qx, qpad, c->keys, c->key_stride, wc, idx->num_sms, idx->stream));
+                            c->qx, c->qpad, c->keys, c->key_stride, wc, idx->num_sms, idx->stream, nullptr, nullptr,
+                            nullptr, nullptr, 0, 0, true));
     idx->stats.kernel_launches += 2;
     idx->stats.scan_bytes += static_cast<uint64_t>(ceil_div<int64_t>(c->nq, 256)) * n * chunks_per_set(idx) * 16;
   } else {
@@ -421,22 +455,86 @@ int scan_batch(bvss_index* idx, bvss_search_ctx* c) {
     idx->stats.scan_bytes += static_cast<uint64_t>(ceil_div<int64_t>(c->nq, 8)) * n * chunks_per_set(idx) * 16;
   }
   cudaEventRecord(idx->ev[3], idx->stream);
-  const int nq = static_cast<int>(c->nq);
-  BVSS_TRY(c->alloc(nq * sizeof(uint32_t), reinterpret_cast<void**>(&c->sel.prefix)));
-  BVSS_TRY(c->alloc(nq * sizeof(int64_t), reinterpret_cast<void**>(&c->sel.below)));
-  BVSS_TRY(c->alloc(nq * sizeof(int64_t), reinterpret_cast<void**>(&c->sel.teff)));
-  BVSS_TRY(c->alloc(nq * sizeof(int64_t), reinterpret_cast<void**>(&c->sel.eq)));
-  BVSS_TRY(c->alloc(nq * sizeof(int64_t), reinterpret_cast<void**>(&c->sel.quota)));
-  BVSS_TRY(c->alloc(nq * sizeof(int32_t), reinterpret_cast<void**>(&c->sel.digit)));
-  BVSS_TRY(c->alloc(static_cast<size_t>(nq) * kHistBins * sizeof(int32_t), reinterpret_cast<void**>(&c->local_hist)));
-  BVSS_TRY(launch_select_init(c->sel, nq, c->teff, idx->stream));
-  c->key_bits = key_bits_for(idx->sketch, idx->m);
-  c->rounds = rounds_for(c->key_bits);
-  c->next_round = 0;
+  BVSS_TRY(alloc_select_state(idx, c));
+  BVSS_TRY(launch_select_init(c->sel, static_cast<int>(c->nq), c->teff, idx->stream));
   return BVSS_OK;
 }
 
-int emit_refine_topk(bvss_index* idx, bvss_search_ctx* c, int64_t* out_ids_dev, float* out_dist_dev, bool refine) {
+bool sampled_select_eligible(const bvss_index* idx) {
+  if (!use_tc_scan(idx) || idx->ns == 0) return false;
+  if (idx->select_mode == 2) return true;
+  if (idx->select_mode == 1) return false;
+  return idx->n >= 65536;
+}
+
+// Sampled-threshold selection (select_mode 2) for one prepared batch: the
+// k_s-th smallest key over the database sample estimates a per-query threshold
+// tau_hat that lets ~k_s n / ns >= T keys through; the fused scan emits only keys
+// <= tau_hat and select_buf_kernel picks the exact top-teff (key, id) from them.
+// *ok = false when some query's buffer under- or overflowed (the caller then
+// runs the full-key path for this batch).
+int select_sampled(bvss_index* idx, bvss_search_ctx* c, bool* ok) {
+  const int nq = static_cast<int>(c->nq);
+  const int64_t n = idx->n, ns = idx->ns;
+  const int key_size = idx->sketch == BVSS_SKETCH_BINARY ? 2 : 4;
+  const double f = static_cast<double>(ns) / static_cast<double>(n);
+  const double mu = static_cast<double>(c->teff) * f;
+  int64_t ks = static_cast<int64_t>(std::ceil(mu + 5.0 * std::sqrt(mu) + 4.0));
+  if (ks > ns) ks = ns;
+  int64_t cap = static_cast<int64_t>(std::ceil(2.0 * static_cast<double>(ks) / f)) + 8192;
+  if (cap < c->teff) cap = c->teff;
+  if (cap > n) cap = n;
+  if (const char* e = getenv("BVSS_DEBUG_EMIT_CAP")) cap = atoll(e);  // developer/test switch: force overflows
+  cap = (cap + 7) & ~int64_t(7);
+  BVSS_TRY(expand_alloc(idx, c));
+  int* wc;
+  BVSS_TRY(idx->ws.get("scan_counter", sizeof(int), reinterpret_cast<void**>(&wc)));
+  // 1. scan the sample, full keys
+  const int64_t sstride = (ns + 7) & ~int64_t(7);
+  void* skeys;
+  BVSS_TRY(idx->ws.get("sample_keys", static_cast<size_t>(nq) * sstride * key_size, &skeys));
+  BVSS_TRY(launch_scan_tc(idx->sketch, idx->smp_sk, idx->smp_mass, ns, ns, idx->m, c->qsk, c->qmass, nq, c->qx,
+                          c->qpad, skeys, sstride, wc, idx->num_sms, idx->stream, nullptr, nullptr, nullptr, nullptr, 0,
+                          0, true));
+  // 2. tau_hat = k_s-th smallest sample key (exact radix select on the sample)
+  BVSS_TRY(alloc_select_state(idx, c));
+  BVSS_TRY(launch_select_init(c->sel, nq, ks, idx->stream));
+  for (int r = 0; r < c->rounds; ++r) {
+    BVSS_TRY(launch_select_hist(key_size, skeys, sstride, ns, nq, c->sel, c->key_bits, r, c->local_hist, idx->stream));
+    BVSS_TRY(launch_select_resolve(c->local_hist, c->sel, nq, c->key_bits, r, idx->stream));
+  }
+  // 3. fused scan: emit (id, key) with key <= tau_hat
+  int32_t *cnt, *bid;
+  uint32_t* bkey;
+  BVSS_TRY(idx->ws.get("emit_cnt", nq * sizeof(int32_t), reinterpret_cast<void**>(&cnt)));
+  BVSS_TRY(idx->ws.get("emit_id", static_cast<size_t>(nq) * cap * 4, reinterpret_cast<void**>(&bid)));
+  BVSS_TRY(idx->ws.get("emit_key", static_cast<size_t>(nq) * cap * 4, reinterpret_cast<void**>(&bkey)));
+  BVSS_CUDA(cudaMemsetAsync(cnt, 0, nq * sizeof(int32_t), idx->stream));
+  BVSS_TRY(launch_scan_tc(idx->sketch, idx->sk, idx->mass, n, n, idx->m, c->qsk, c->qmass, nq, c->qx, c->qpad, nullptr,
+                          0, wc, idx->num_sms, idx->stream, c->sel.prefix, cnt, bid, bkey, static_cast<int>(cap),
+                          c->id_base, false));
+  idx->stats.scan_bytes += static_cast<uint64_t>(ceil_div<int64_t>(c->nq, 256)) * (n + ns) * chunks_per_set(idx) * 16;
+  cudaEventRecord(idx->ev[3], idx->stream);
+  // 4. exact top-teff from the buffers
+  BVSS_TRY(c->alloc(static_cast<size_t>(nq) * c->T * sizeof(int32_t), reinterpret_cast<void**>(&c->cand)));
+  BVSS_TRY(c->alloc(nq * sizeof(int32_t), reinterpret_cast<void**>(&c->count)));
+  int* fail;
+  BVSS_TRY(idx->ws.get("select_fail", sizeof(int), reinterpret_cast<void**>(&fail)));
+  BVSS_CUDA(cudaMemsetAsync(fail, 0, sizeof(int), idx->stream));
+  BVSS_TRY(launch_select_buf(cnt, bkey, bid, static_cast<int>(cap), static_cast<int>(c->teff), c->key_bits, c->T, nq,
+                             c->cand, c->count, fail, idx->stream));
+  cudaEventRecord(idx->ev[4], idx->stream);
+  idx->stats.kernel_launches += 4 + 2 * c->rounds;
+  int hf = 0;
+  BVSS_CUDA(cudaMemcpyAsync(&hf, fail, sizeof(int), cudaMemcpyDeviceToHost, idx->stream));
+  BVSS_CUDA(cudaStreamSynchronize(idx->stream));
+  *ok = hf == 0;
+  idx->stats.select_batches += 1;
+  if (!*ok) idx->stats.select_fallbacks += 1;
+  return BVSS_OK;
+}
+
+int emit_candidates(bvss_index* idx, bvss_search_ctx* c) {
   const int nq = static_cast<int>(c->nq);
   const int key_size = idx->sketch == BVSS_SKETCH_BINARY ? 2 : 4;
   BVSS_TRY(c->alloc(static_cast<size_t>(nq) * c->T * sizeof(int32_t), reinterpret_cast<void**>(&c->cand)));
@@ -445,7 +543,12 @@ int emit_refine_topk(bvss_index* idx, bvss_search_ctx* c, int64_t* out_ids_dev, 
                               c->count, idx->stream));
   cudaEventRecord(idx->ev[4], idx->stream);
   idx->stats.kernel_launches += 1;
-  if (!refine) return BVSS_OK;
+  return BVSS_OK;
+}
+
+// refine + top-k over c->cand / c->count
+int refine_topk(bvss_index* idx, bvss_search_ctx* c, int64_t* out_ids_dev, float* out_dist_dev) {
+  const int nq = static_cast<int>(c->nq);
   int exact_all = 0;
   if (idx->terms != 0 && c->max_mq <= 128) {  // tensor path: query rows fit the M=128 tile
     BVSS_TRY(c->alloc(static_cast<size_t>(nq) * c->T * sizeof(float), reinterpret_cast<void**>(&c->approx)));
@@ -494,7 +597,7 @@ int run_select_single(bvss_index* idx, bvss_search_ctx* c) {
 }
 
 int make_ctx(bvss_index* idx, const float* queries, const std::vector<int64_t>& qoff_host, int k, int T,
-             int64_t n_total, uint32_t flags, std::unique_ptr<bvss_search_ctx>& c) {
+             int64_t n_total, uint32_t flags, std::unique_ptr<bvss_search_ctx>& c, bool scan = true) {
   c.reset(new bvss_search_ctx());
   c->idx = idx;
   c->k = k;
@@ -502,7 +605,7 @@ int make_ctx(bvss_index* idx, const float* queries, const std::vector<int64_t>& 
   c->teff = T < n_total ? T : n_total;
   BVSS_TRY(prepare_queries(idx, c.get(), queries, qoff_host, (flags & BVSS_DEVICE_PTRS) != 0,
                            (flags & BVSS_VALIDATE_FINITE) != 0));
-  BVSS_TRY(scan_batch(idx, c.get()));
+  if (scan) BVSS_TRY(scan_batch(idx, c.get()));
   return BVSS_OK;
 }
 
@@ -556,6 +659,7 @@ int bvss_build_index(const float* vectors, const int64_t* set_offsets, int64_t n
   if (p->sketch > 1) BVSS_FAIL(BVSS_EINVAL, "unknown sketch kind");
   if (p->refine_terms != 0 && p->refine_terms != 1 && p->refine_terms != 3 && p->refine_terms != 255)
     BVSS_FAIL(BVSS_EINVAL, "refine_terms must be 0 (default), 1, 3 or 255 (exact)");
+  if (p->select_mode > 2) BVSS_FAIL(BVSS_EINVAL, "select_mode must be 0 (auto), 1 (full keys) or 2 (sampled)");
   int num_sms = 0;
   BVSS_TRY(check_device(p->device, &num_sms));
   DeviceGuard g(p->device);
@@ -582,6 +686,7 @@ int bvss_build_index(const float* vectors, const int64_t* set_offsets, int64_t n
   // 0 = default (1-term fp16 tensor-core pass + exact window), 1, 3, 255 = exact SIMT for every candidate
   idx->terms = p->refine_terms == 0 ? 1 : (p->refine_terms == 255 ? 0 : static_cast<int>(p->refine_terms));
   idx->query_batch = p->query_batch;
+  idx->select_mode = p->select_mode;
   BVSS_CUDA(cudaStreamCreateWithFlags(&idx->own_stream, cudaStreamNonBlocking));
   idx->stream = idx->own_stream;
   for (auto& e : idx->ev) BVSS_CUDA(cudaEventCreate(&e));
@@ -658,6 +763,12 @@ int bvss_build_index(const float* vectors, const int64_t* set_offsets, int64_t n
   BVSS_TRY(dalloc(static_cast<size_t>(n) * cps * 16, &idx->sk));
   BVSS_TRY(dalloc(static_cast<size_t>(n) * 4, reinterpret_cast<void**>(&idx->mass)));
   BVSS_TRY(launch_sketch(codes, p->m, idx->off, n, p->sketch, idx->sk, idx->mass, n, 1, num_sms, st));
+  if (p->m % 128 == 0) {  // strided database sample for the sampled-threshold select
+    idx->ns = n < 16384 ? n : 16384;
+    BVSS_TRY(dalloc(static_cast<size_t>(idx->ns) * cps * 16, &idx->smp_sk));
+    BVSS_TRY(dalloc(static_cast<size_t>(idx->ns) * 4, reinterpret_cast<void**>(&idx->smp_mass)));
+    BVSS_TRY(launch_gather_sample(idx->sk, idx->mass, n, cps, idx->ns, idx->smp_sk, idx->smp_mass, num_sms, st));
+  }
   unsigned int* vmax;
   BVSS_TRY(idx->ws.get("vmax", sizeof(unsigned int), reinterpret_cast<void**>(&vmax)));
   BVSS_CUDA(cudaMemsetAsync(vmax, 0, sizeof(unsigned int), st));
@@ -676,8 +787,8 @@ void bvss_free_index(bvss_index* idx) {
   if (!idx) return;
   DeviceGuard g(idx->device);
   if (idx->stream) cudaStreamSynchronize(idx->stream);
-  void* ptrs[] = {idx->Wt,    idx->V,     idx->off,   idx->hi, idx->lo,  idx->vscale,
-                  idx->pbase, idx->vnorm, idx->codes, idx->sk, idx->mass};
+  void* ptrs[] = {idx->Wt,    idx->V,     idx->off,   idx->hi,   idx->lo,     idx->vscale, idx->pbase,
+                  idx->vnorm, idx->codes, idx->sk,    idx->mass, idx->smp_sk, idx->smp_mass};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   idx->ws.release();
@@ -871,9 +982,16 @@ int bvss_search(bvss_index* idx, const float* queries, const int64_t* query_offs
     std::vector<int64_t> sub(nb + 1);
     for (int64_t i = 0; i <= nb; ++i) sub[i] = qo[b0 + i] - qo[b0];
     std::unique_ptr<bvss_search_ctx> c;
-    BVSS_TRY(make_ctx(idx, queries + qo[b0] * idx->d, sub, k, T, idx->n, flags, c));
-    BVSS_TRY(run_select_single(idx, c.get()));
-    BVSS_TRY(emit_refine_topk(idx, c.get(), oid, odist, true));
+    const bool sampled = sampled_select_eligible(idx);
+    BVSS_TRY(make_ctx(idx, queries + qo[b0] * idx->d, sub, k, T, idx->n, flags, c, !sampled));
+    bool ok = false;
+    if (sampled) BVSS_TRY(select_sampled(idx, c.get(), &ok));
+    if (!ok) {
+      if (sampled) BVSS_TRY(scan_batch(idx, c.get()));
+      BVSS_TRY(run_select_single(idx, c.get()));
+      BVSS_TRY(emit_candidates(idx, c.get()));
+    }
+    BVSS_TRY(refine_topk(idx, c.get(), oid, odist));
     BVSS_TRY(from_device(idx, out_ids + b0 * k, oid, static_cast<size_t>(nb) * k * 8, dev));
     BVSS_TRY(from_device(idx, out_dist + b0 * k, odist, static_cast<size_t>(nb) * k * 4, dev));
     BVSS_CUDA(cudaEventRecord(idx->ev[7], idx->stream));
@@ -959,7 +1077,8 @@ int bvss_dist_finish(bvss_search_ctx* c, const int64_t* all_eq_dev, int32_t worl
   bvss_index* idx = c->idx;
   DeviceGuard g(idx->device);
   BVSS_TRY(launch_select_quota(c->sel, all_eq_dev, static_cast<int>(c->nq), world, rank, idx->stream));
-  BVSS_TRY(emit_refine_topk(idx, c, topk_ids_dev, topk_dist_dev, true));
+  BVSS_TRY(emit_candidates(idx, c));
+  BVSS_TRY(refine_topk(idx, c, topk_ids_dev, topk_dist_dev));
   return BVSS_OK;
 }
 

@@ -32,7 +32,8 @@ constexpr int kScanM = 128;   // database sets per tile
 constexpr int kScanN = 256;   // queries per tile
 constexpr int kScanKB = 128;  // bytes (= u8 elements) per K-chunk
 constexpr int kScanStages = 4;
-constexpr int kScanThreads = 320;
+constexpr int kScanThreads = 448;  // 0 copies, 1 MMA, 2-5 + 10-13 epilogue, 6-9 bit expansion
+constexpr int kScanEpiWarps = 8;
 
 struct ScanArgs {
   int kind;                    // BVSS_SKETCH_BINARY / COUNT_U8
@@ -47,6 +48,13 @@ struct ScanArgs {
   int64_t key_stride;
   int n_tiles, q_tiles;
   int* work_counter;
+  // threshold-emit mode (EMIT = true): keys <= tau[q] are appended to per-query buffers
+  const uint32_t* tau;     // [nq]
+  int32_t* cnt;            // [nq] entries emitted (may exceed cap: overflow)
+  int32_t* buf_id;         // [nq][cap] set ids (+ id_base)
+  uint32_t* buf_key;       // [nq][cap] keys
+  int cap;
+  int64_t id_base;
 };
 
 struct ScanCtl {
@@ -97,7 +105,7 @@ __device__ __forceinline__ uint4 expand16(uint32_t half16) {
   return r;
 }
 
-template <typename KeyT>
+template <typename KeyT, bool EMIT>
 __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ ScanCtl S;
@@ -116,7 +124,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&S.tfull[b], 1);
-      tc::mbar_init(&S.tempty[b], 4);
+      tc::mbar_init(&S.tempty[b], kScanEpiWarps);
     }
     tc::fence_mbar_init();
   }
@@ -152,7 +160,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
         }
       }
     }
-  } else if (warp >= 6) {
+  } else if (warp >= 6 && warp <= 9) {
     // ------------------------------------------- bit expansion (binary mode)
     if (binary) {
       const int r = tid - 192;  // DB row of the tile, 0..127
@@ -207,27 +215,37 @@ __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
       }
     }
   } else {
-    // ------------------------------------------------ epilogue (warps 2-5)
+    // -------------------------------------- epilogue (warps 2-5 and 10-13)
     const int ew = warp & 3;
-    const int row = ew * 32 + lane;  // TMEM lane = DB set of the tile
+    const int half = warp >= 10 ? 1 : 0;  // columns [128 half, 128 half + 128)
+    const int row = ew * 32 + lane;       // TMEM lane = DB set of the tile
     KeyT* keys = static_cast<KeyT*>(a.keys);
     uint32_t tc_ = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x, ++tc_) {
       const int it = w / a.q_tiles, qt = w % a.q_tiles;
       const int64_t i = static_cast<int64_t>(it) * kScanM + row;
-      const int q0 = qt * kScanN;
+      const int q0 = qt * kScanN + half * (kScanN / 2);
       const bool ok = i < a.n;
       const int32_t pi = ok ? a.massS[i] : 0;
       const uint32_t acc = tc_ & 1u;
       tc::mbar_wait(&S.tfull[acc], (tc_ >> 1) & 1u);
       tc::fence_after_sync();
-      const uint32_t tbase = tmem + acc * kScanN + (static_cast<uint32_t>(ew * 32) << 16);
-      for (int c0 = 0; c0 < kScanN; c0 += 32) {
+      const uint32_t tbase = tmem + acc * kScanN + half * (kScanN / 2) + (static_cast<uint32_t>(ew * 32) << 16);
+      for (int c0 = 0; c0 < kScanN / 2; c0 += 32) {
         uint32_t v[32];
         tc::tmem_ld16(tbase + c0, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
         tc::tmem_ld16(tbase + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
+        // query masses (and thresholds) of these 32 columns: warp-uniform loads, overlapped with TMEM
+        int32_t pq[32];
+        uint32_t tq[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int q = q0 + c0 + j;
+          pq[j] = q < a.nq ? __ldg(a.massQ + q) : 0;
+          if (EMIT) tq[j] = q < a.nq ? __ldg(a.tau + q) : 0u;
+        }
         tc::tmem_ld_wait();
-        if (c0 + 32 >= kScanN) {  // accumulator fully read
+        if (c0 + 32 >= kScanN / 2) {  // this warp's half of the accumulator is read
           tc::fence_before_sync();
           __syncwarp();
           if (lane == 0) tc::mbar_arrive(&S.tempty[acc]);
@@ -235,9 +253,22 @@ __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const int q = q0 + c0 + j;
-          if (q < a.nq && ok) {
-            const int32_t key = a.massQ[q] + pi - 2 * static_cast<int32_t>(v[j]);
-            keys[static_cast<int64_t>(q) * a.key_stride + i] = static_cast<KeyT>(key);
+          const int32_t key = pq[j] + pi - 2 * static_cast<int32_t>(v[j]);
+          if (!EMIT) {
+            if (q < a.nq && ok) keys[static_cast<int64_t>(q) * a.key_stride + i] = static_cast<KeyT>(key);
+          } else {
+            const bool pass = ok && q < a.nq && static_cast<uint32_t>(key) <= tq[j];
+            const unsigned mask = __ballot_sync(0xffffffffu, pass);
+            if (mask) {  // warp-uniform: rare (a few keys per thousand)
+              int base = 0;
+              if (lane == 0) base = atomicAdd(a.cnt + q, __popc(mask));
+              base = __shfl_sync(0xffffffffu, base, 0);
+              const int pos = base + __popc(mask & ((1u << lane) - 1u));
+              if (pass && pos < a.cap) {
+                a.buf_id[static_cast<int64_t>(q) * a.cap + pos] = static_cast<int32_t>(a.id_base + i);
+                a.buf_key[static_cast<int64_t>(q) * a.cap + pos] = static_cast<uint32_t>(key);
+              }
+            }
           }
         }
       }
@@ -273,15 +304,19 @@ __global__ void expand_queries_kernel(int kind, const uint4* __restrict__ SQ /*[
   }
 }
 
+// keys mode: keys != null; emit mode: tau != null (cnt must be zeroed by the caller)
 int launch_scan_tc(int kind, const void* S, const int32_t* mass, int64_t n, int64_t n_stride, int m, const void* SQ,
                    const int32_t* massQ, int nq, void* Qx /*workspace [m/16][qpad][16]*/, int qpad, void* keys,
-                   int64_t key_stride, int* work_counter, int num_sms, cudaStream_t st) {
+                   int64_t key_stride, int* work_counter, int num_sms, cudaStream_t st, const uint32_t* tau,
+                   int32_t* cnt, int32_t* buf_id, uint32_t* buf_key, int cap, int64_t id_base, bool expand) {
   if (nq <= 0 || n <= 0) return BVSS_OK;
   if (m % kScanKB) BVSS_FAIL(BVSS_EUNSUPPORTED, "tensor-core scan needs m %% 128 == 0");
   const int cps = kind == BVSS_SKETCH_BINARY ? (((m / 32) + 3) / 4) : m / 16;
-  expand_queries_kernel<<<num_sms * 4, 256, 0, st>>>(kind, static_cast<const uint4*>(SQ), cps, nq, qpad, m,
-                                                     static_cast<uint4*>(Qx));
-  BVSS_TRY(post_launch("expand_queries_kernel", st));
+  if (expand) {
+    expand_queries_kernel<<<num_sms * 4, 256, 0, st>>>(kind, static_cast<const uint4*>(SQ), cps, nq, qpad, m,
+                                                       static_cast<uint4*>(Qx));
+    BVSS_TRY(post_launch("expand_queries_kernel", st));
+  }
   ScanArgs a;
   a.kind = kind;
   a.S = static_cast<const uint4*>(S);
@@ -298,18 +333,30 @@ int launch_scan_tc(int kind, const void* S, const int32_t* mass, int64_t n, int6
   a.n_tiles = static_cast<int>(ceil_div<int64_t>(n, kScanM));
   a.q_tiles = ceil_div(nq, kScanN);
   a.work_counter = work_counter;
+  a.tau = tau;
+  a.cnt = cnt;
+  a.buf_id = buf_id;
+  a.buf_key = buf_key;
+  a.cap = cap;
+  a.id_base = id_base;
   const size_t smem = static_cast<size_t>(kScanStages) * (kScanM + kScanN) * kScanKB + 1024;
   const int total = a.n_tiles * a.q_tiles;
   const int grid = total < num_sms ? total : num_sms;
+#define BVSS_SCAN_LAUNCH(KT, EM)                                                                          \
+  do {                                                                                                    \
+    auto kfn = scan_tc_kernel<KT, EM>;                                                                    \
+    BVSS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem))); \
+    kfn<<<grid, kScanThreads, smem, st>>>(a);                                                             \
+  } while (0)
+  const bool emit = tau != nullptr;
   if (kind == BVSS_SKETCH_BINARY) {
-    BVSS_CUDA(cudaFuncSetAttribute(scan_tc_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
-    scan_tc_kernel<uint16_t><<<grid, kScanThreads, smem, st>>>(a);
+    if (emit) BVSS_SCAN_LAUNCH(uint16_t, true);
+    else BVSS_SCAN_LAUNCH(uint16_t, false);
   } else {
-    BVSS_CUDA(cudaFuncSetAttribute(scan_tc_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
-    scan_tc_kernel<uint32_t><<<grid, kScanThreads, smem, st>>>(a);
+    if (emit) BVSS_SCAN_LAUNCH(uint32_t, true);
+    else BVSS_SCAN_LAUNCH(uint32_t, false);
   }
+#undef BVSS_SCAN_LAUNCH
   BVSS_TRY(post_launch(__func__, st));
   return BVSS_OK;
 }

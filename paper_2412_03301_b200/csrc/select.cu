@@ -324,4 +324,150 @@ int launch_select_emit(int key_size, const void* keys, int64_t key_stride, int64
   return BVSS_OK;
 }
 
+// ------------------------------------------------ sampled-threshold path --
+// The fused scan (scan_tc.cu, EMIT) appends every (id, key) with key <= tau_hat[q]
+// to a per-query buffer, tau_hat being an order statistic of a strided sample of
+// the database chosen so that, with overwhelming probability, at least T database
+// keys are <= tau_hat.  This kernel then selects, exactly, the teff smallest
+// (key, id) pairs of the buffer: an MSB radix select over the key (the teff-th
+// key tau), a second radix select over the ids tied at tau (the quota-th id), and
+// a compaction.  The result equals the full select's set because every key <= the
+// true T-th key is in the buffer whenever cnt >= teff; a buffer with cnt < teff
+// (the sample threshold was too low) or cnt > cap (overflow) is reported in
+// `fail` and the caller redoes the batch on the full key path.  One CTA per query.
+constexpr int kBufThreads = 512;
+
+__device__ __forceinline__ void buf_radix_round(const uint32_t* __restrict__ vals, const uint32_t* __restrict__ keys,
+                                                bool tie_filter, uint32_t tau, int c, int hi, int shift,
+                                                uint32_t prefix, uint32_t* hist, int nbins) {
+  const uint32_t mask = static_cast<uint32_t>(nbins) - 1u;
+  for (int e = threadIdx.x; e < c; e += blockDim.x) {
+    const uint32_t v = vals[e];
+    const bool in = (!tie_filter || keys[e] == tau) && ((hi >= 32) || (v >> hi) == prefix);
+    if (in) atomicAdd(&hist[(v >> shift) & mask], 1u);
+  }
+}
+
+// one warp: first digit where the running count reaches need; returns (digit, count before it)
+__device__ __forceinline__ void buf_find_digit(const uint32_t* hist, int nbins, uint32_t need, uint32_t* out_digit,
+                                               uint32_t* out_before) {
+  const int lane = threadIdx.x & 31;
+  uint32_t run = 0;
+  for (int b0 = 0; b0 < nbins; b0 += 32) {
+    const int b = b0 + lane;
+    const uint32_t v = b < nbins ? hist[b] : 0u;
+    uint32_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    const unsigned hit = __ballot_sync(0xffffffffu, b < nbins && run + inc >= need);
+    if (hit) {
+      const int src = __ffs(hit) - 1;
+      const uint32_t before = run + __shfl_sync(0xffffffffu, inc - v, src);
+      if (lane == 0) {
+        *out_digit = static_cast<uint32_t>(b0 + src);
+        *out_before = before;
+      }
+      return;
+    }
+    run += __shfl_sync(0xffffffffu, inc, 31);
+  }
+  if (lane == 0) {  // unreachable when need <= count in range
+    *out_digit = static_cast<uint32_t>(nbins - 1);
+    *out_before = run;
+  }
+}
+
+// radix select of the need-th smallest value (1-based) among the (filtered) entries
+__device__ uint32_t buf_select(const uint32_t* vals, const uint32_t* keys, bool tie_filter, uint32_t tau, int c,
+                               int bits, uint32_t need, uint32_t* hist, uint32_t* s_dig, uint32_t* s_before,
+                               uint32_t* need_left) {
+  uint32_t prefix = 0;
+  for (int hi = bits; hi > 0;) {
+    const int shift = hi - kHistBits > 0 ? hi - kHistBits : 0;
+    const int width = hi - shift;
+    const int nbins = 1 << width;
+    for (int b = threadIdx.x; b < nbins; b += blockDim.x) hist[b] = 0u;
+    __syncthreads();
+    buf_radix_round(vals, keys, tie_filter, tau, c, hi, shift, prefix, hist, nbins);
+    __syncthreads();
+    if (threadIdx.x < 32) buf_find_digit(hist, nbins, need, s_dig, s_before);
+    __syncthreads();
+    prefix = (prefix << width) | *s_dig;
+    need -= *s_before;
+    __syncthreads();
+    hi = shift;
+  }
+  *need_left = need;
+  return prefix;
+}
+
+__global__ void __launch_bounds__(kBufThreads) select_buf_kernel(const int32_t* __restrict__ cnt,
+                                                                 const uint32_t* __restrict__ bkey,
+                                                                 const int32_t* __restrict__ bid, int cap, int teff,
+                                                                 int key_bits, int T, int32_t* __restrict__ cand,
+                                                                 int32_t* __restrict__ count, int* __restrict__ fail) {
+  __shared__ uint32_t hist[kHistBins];
+  __shared__ uint32_t s_dig, s_before, s_pos;
+  const int q = blockIdx.x;
+  const int c = cnt[q];
+  int32_t* crow = cand + static_cast<int64_t>(q) * T;
+  if (c < teff || c > cap) {
+    if (threadIdx.x == 0) {
+      atomicAdd(fail, 1);
+      count[q] = 0;
+    }
+    return;
+  }
+  const uint32_t* keys = bkey + static_cast<int64_t>(q) * cap;
+  const uint32_t* ids = reinterpret_cast<const uint32_t*>(bid + static_cast<int64_t>(q) * cap);
+  uint32_t quota;
+  const uint32_t tau = buf_select(keys, keys, false, 0u, c, key_bits, static_cast<uint32_t>(teff), hist, &s_dig,
+                                  &s_before, &quota);
+  // quota >= 1 ties at tau are taken, lowest ids first (reading R4)
+  uint32_t dummy;
+  const uint32_t theta = buf_select(ids, keys, true, tau, c, 31, quota, hist, &s_dig, &s_before, &dummy);
+  if (threadIdx.x == 0) s_pos = 0u;
+  __syncthreads();
+  for (int e = threadIdx.x; e < c; e += blockDim.x) {
+    const uint32_t k = keys[e];
+    if (k < tau || (k == tau && ids[e] <= theta)) {
+      const uint32_t pos = atomicAdd(&s_pos, 1u);
+      crow[pos] = static_cast<int32_t>(ids[e]);
+    }
+  }
+  for (int i = teff + threadIdx.x; i < T; i += blockDim.x) crow[i] = -1;
+  if (threadIdx.x == 0) count[q] = teff;
+}
+
+// strided database sample for the threshold estimate: sample j <- set floor(j n / ns)
+__global__ void gather_sample_kernel(const uint4* __restrict__ sk, const int32_t* __restrict__ mass, int64_t n,
+                                     int cps, int64_t ns, uint4* __restrict__ out, int32_t* __restrict__ out_mass) {
+  const int64_t total = ns * cps;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t ch = t / ns, j = t % ns;
+    const int64_t i = j * n / ns;
+    out[ch * ns + j] = sk[ch * n + i];
+    if (ch == 0) out_mass[j] = mass[i];
+  }
+}
+
+int launch_select_buf(const int32_t* cnt, const uint32_t* bkey, const int32_t* bid, int cap, int teff, int key_bits,
+                      int T, int nq, int32_t* cand, int32_t* count, int* fail, cudaStream_t s) {
+  select_buf_kernel<<<nq, kBufThreads, 0, s>>>(cnt, bkey, bid, cap, teff, key_bits, T, cand, count, fail);
+  BVSS_TRY(post_launch(__func__, s));
+  return BVSS_OK;
+}
+
+int launch_gather_sample(const void* sk, const int32_t* mass, int64_t n, int cps, int64_t ns, void* out,
+                         int32_t* out_mass, int num_sms, cudaStream_t s) {
+  gather_sample_kernel<<<num_sms * 4, 256, 0, s>>>(static_cast<const uint4*>(sk), mass, n, cps, ns,
+                                                   static_cast<uint4*>(out), out_mass);
+  BVSS_TRY(post_launch(__func__, s));
+  return BVSS_OK;
+}
+
 }  // namespace bvss

@@ -236,3 +236,52 @@ def test_refine_terms_modes_agree():
     for ids, dist in out[1:]:
         assert np.array_equal(ids, out[0][0])
         assert np.all(dist_close(dist, out[0][1]))
+
+
+# ------------------------------------------------------ selection strategies
+
+def _modes_agree(cfg, data, Ts, env_cap=None, monkeypatch=None):
+    out = {}
+    for mode in (1, 2):
+        idx = B.Index(data["vectors"], data["offsets"], m=cfg.m, s=cfg.s, L=cfg.L, sketch=cfg.sketch, seed=cfg.seed,
+                      select_mode=mode)
+        res = []
+        for T in Ts:
+            ids, dist = idx.search(data["queries"], data["q_offsets"], cfg.k, T)
+            res.append((ids, dist, idx.stats()))
+        out[mode] = res
+        idx.close()
+    for (i1, d1, s1), (i2, d2, s2) in zip(out[1], out[2]):
+        assert s1["select_batches"] == 0
+        assert s2["select_batches"] >= 1
+        assert np.array_equal(i1, i2)
+        assert np.array_equal(d1, d2)
+    return out
+
+
+@pytest.mark.parametrize("name,ov", [("cfg3", dict(n=40000, nq=7, T=400)), ("cfg2", dict(n=20011, nq=5, T=300))])
+def test_sampled_select_equals_full_select(name, ov):
+    """select_mode 2 (sampled threshold, fused scan emission) returns exactly what
+    select_mode 1 (full key rows) returns, and both match the oracle pipeline."""
+    _need_gpu()
+    cfg = synth.get_config(name, **ov)
+    data = synth.to_numpy(synth.generate(cfg, device="cpu"))
+    out = _modes_agree(cfg, data, (cfg.k, cfg.T, 4 * cfg.T))
+    ids, dist, st = out[2][1]
+    oi = O.OracleIndex(data["vectors"], data["offsets"], cfg.m, cfg.s, cfg.L, cfg.seed, sketch=cfg.sketch)
+    V, off = data["vectors"], data["offsets"]
+    for qi in range(3):
+        Q = data["queries"][data["q_offsets"][qi]:data["q_offsets"][qi + 1]]
+        r_ids, r_d = oi.search(Q, cfg.k, cfg.T)
+        check_topk(ids[qi], dist[qi], r_ids, r_d, lambda i: O.hausdorff(Q, V[off[i]:off[i + 1]]))
+
+
+def test_sampled_select_fallback_on_overflow(monkeypatch):
+    """A per-query emission buffer that overflows sends the batch down the full-key
+    path; the answer does not change."""
+    _need_gpu()
+    cfg = synth.get_config("cfg3", n=30000, nq=4, T=300)
+    data = synth.to_numpy(synth.generate(cfg, device="cpu"))
+    monkeypatch.setenv("BVSS_DEBUG_EMIT_CAP", "16")
+    out = _modes_agree(cfg, data, (cfg.T,))
+    assert out[2][0][2]["select_fallbacks"] >= 1
