@@ -95,14 +95,16 @@ def sharded_search(ops, queries, q_offsets, k: int, T: int, n_total: int, group=
             dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)      # C1
             ops.resolve(r, h)
         eq = ops.tie_counts()
-        all_eq = torch.empty((world,) + tuple(eq.shape), dtype=eq.dtype, device=eq.device)
+        # outputs are allocated flat along dim 0 ([world * rows, ...]; gloo requires it) and viewed per rank
+        all_eq = torch.empty((world * eq.shape[0],), dtype=eq.dtype, device=eq.device)
         dist.all_gather_into_tensor(all_eq, eq, group=group)           # C2
+        all_eq = all_eq.view(world, -1)
         ids, dd = ops.finish(all_eq, world, rank)
-        all_ids = torch.empty((world,) + tuple(ids.shape), dtype=ids.dtype, device=ids.device)
-        all_d = torch.empty((world,) + tuple(dd.shape), dtype=dd.dtype, device=dd.device)
+        all_ids = torch.empty((world * ids.shape[0], ids.shape[1]), dtype=ids.dtype, device=ids.device)
+        all_d = torch.empty((world * dd.shape[0], dd.shape[1]), dtype=dd.dtype, device=dd.device)
         dist.all_gather_into_tensor(all_ids, ids, group=group)         # C3
         dist.all_gather_into_tensor(all_d, dd, group=group)
-        return ops.merge(all_ids, all_d, world)                        # K7
+        return ops.merge(all_ids.view(world, *ids.shape), all_d.view(world, *dd.shape), world)  # K7
     finally:
         ops.end()
 
