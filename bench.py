@@ -237,7 +237,7 @@ def main_ours(args):
         times.append(e0.elapsed_time(e1))
         s = idx.stats()
         launches += int(s["kernel_launches"]) + (0 if world == 1 else 1)
-        for key in ("ms_encode", "ms_scan", "ms_select", "ms_refine", "ms_topk", "ms_h2d", "scan_bytes",
+        for key in ("ms_encode", "ms_scan", "ms_select", "ms_refine", "ms_topk", "ms_h2d", "ms_total", "scan_bytes",
                     "gather_bytes", "cand_rows", "fixup_sets"):
             st_sum[key] = st_sum.get(key, 0) + s[key]
     torch.cuda.synchronize()
@@ -253,7 +253,7 @@ def main_ours(args):
     ms_per_step = total_ms / args.steps
     value = cfg.nq / (ms_per_step / 1000.0)
     K = args.steps
-    stages = {kk: st_sum[kk] / K for kk in ("ms_h2d", "ms_encode", "ms_scan", "ms_select", "ms_refine", "ms_topk")}
+    stages = {kk: st_sum[kk] / K for kk in ("ms_h2d", "ms_encode", "ms_scan", "ms_select", "ms_refine", "ms_topk", "ms_total")}
 
     # -------- roofline of the dominant kernel (algorithmic bytes / live event time)
     scan_bytes = st_sum["scan_bytes"] / K

@@ -9,31 +9,43 @@
 // Both are exact in s32 (max 2048 * 255^2 < 2^31), so the keys are bit-identical
 // to the SIMT scan (scan.cu) and to the oracle.
 //
-// Tile = 128 database sets (A, M = 128, one TMEM lane each) x 256 queries
-// (B, N = 256), K = m in 128-byte chunks; a tcgen05.mma costs ~138 cycles
-// whatever N is (tools/microbench_umma.cu), so N = 256 keeps the issue rate at
-// the tensor-core peak.  Operands use the canonical no-swizzle K-major layout:
-// per 16-byte K unit u a [rows][16 B] block (core matrices of 8 rows x 16 B),
-// LBO = rows x 16 B between units, SBO = 128 B between 8-row groups; this is
-// exactly the chunk-major layout the sketches are stored in ([m/16][n][16 B],
-// sketch.cu), so count tiles and the (pre-expanded) query tiles arrive by plain
-// contiguous cp.async.bulk copies, and binary tiles are expanded bit -> byte by
-// four producer warps straight into that layout.
+// Queries are the STATIONARY operand: A = a tile of 128 query sketches (M = 128,
+// one TMEM lane per query), resident in shared memory for a whole work unit when
+// 128 x m bytes fit (m <= 1024), else streamed with B.  B = 256 database sets
+// (N = 256) streamed through a stage ring in 64-byte K-chunks.  The (query
+// tile, database tile) pairs are split into equal contiguous ranges, one per
+// persistent CTA (query-tile-major, so a CTA reloads its query tile at most a
+// few times).
+// Operands use the canonical no-swizzle K-major layout: per 16-byte K unit u a
+// [rows][16 B] block (core matrices of 8 rows x 16 B), LBO = rows x 16 B between
+// units, SBO = 128 B between 8-row groups.  This is the chunk-major layout the
+// sketches are stored in ([m/16][n][16 B], sketch.cu), so count tiles and the
+// pre-expanded query tiles arrive by plain contiguous cp.async.bulk copies, and
+// binary tiles are expanded bit -> byte by eight expander warps (one database
+// set per thread, 128-bit loads prefetched a whole tile ahead in registers).
 //
-// CTA = 10 warps: warp 0 bulk copies (query tile; count-mode DB tile), warp 1
-// TMEM owner + MMA issuer, warps 2-5 epilogue (keys[q][i] = p_Q + p_i - 2 acc,
-// coalesced over sets), warps 6-9 bit expansion (binary mode).  4-stage smem
-// ring, double-buffered TMEM accumulators (2 x 256 columns).
+// Because a TMEM lane is a query, the epilogue thread owns one query: its mass
+// p_Q and threshold tau_Q live in registers and the per-value work is one IMAD
+// and one compare (keys = p_Q + p_i - 2 acc; database masses are warp-uniform
+// 128-bit loads).  Emit mode appends (id, key) for key <= tau_Q with one atomic
+// per (thread, 32 columns) that emit anything.
+//
+// CTA = 14 warps: warp 0 bulk copies (query tile; count-mode / streamed-A
+// stages), warp 1 TMEM owner + MMA issuer, warps 2-5 epilogue (one per TMEM
+// lane quarter, all 256 columns), warps 6-13 bit expansion (binary mode).
+// Double-buffered TMEM accumulators (2 x 256 columns).
 #include "tc.cuh"
 
 namespace bvss {
 
-constexpr int kScanM = 128;   // database sets per tile
-constexpr int kScanN = 256;   // queries per tile
-constexpr int kScanKB = 128;  // bytes (= u8 elements) per K-chunk
-constexpr int kScanStages = 4;
-constexpr int kScanThreads = 448;  // 0 copies, 1 MMA, 2-5 + 10-13 epilogue, 6-9 bit expansion
-constexpr int kScanEpiWarps = 8;
+constexpr int kScanM = 128;    // queries per tile (MMA M, TMEM lanes)
+constexpr int kScanN = 256;    // database sets per tile (MMA N)
+constexpr int kScanKB = 64;    // bytes (= u8 elements) of K per stage
+constexpr int kScanThreads = 448;  // 14 warps (register file: 128 regs/thread)
+constexpr int kScanEpiWarps = 4;
+constexpr int kScanExpWarps = 8;
+constexpr int kScanResidentMaxM = 1024;  // A resident in smem when 128 x m <= 128 KB
+constexpr int kScanRawPer = 8;           // 128-bit raw chunks prefetched per group (expander)
 
 struct ScanArgs {
   int kind;                    // BVSS_SKETCH_BINARY / COUNT_U8
@@ -47,7 +59,6 @@ struct ScanArgs {
   void* keys;                  // [nq][key_stride] uint16 (binary) / uint32 (count)
   int64_t key_stride;
   int n_tiles, q_tiles;
-  int* work_counter;
   // threshold-emit mode (EMIT = true): keys <= tau[q] are appended to per-query buffers
   const uint32_t* tau;     // [nq]
   int32_t* cnt;            // [nq] entries emitted (may exceed cap: overflow)
@@ -57,13 +68,14 @@ struct ScanArgs {
   int64_t id_base;
 };
 
+template <int KS>
 struct ScanCtl {
-  uint64_t full[kScanStages];
-  uint64_t empty[kScanStages];
+  uint64_t full[KS];
+  uint64_t empty[KS];
   uint64_t tfull[2];
   uint64_t tempty[2];
+  uint64_t afull, aempty;
   uint32_t tmem_base;
-  int work[4];  // work ring: (db tile, q tile) pairs claimed by the copy warp
 };
 
 __device__ __forceinline__ void bulk_copy(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -104,28 +116,64 @@ __device__ __forceinline__ uint4 expand16(uint32_t half16) {
   r.w = (((half16 >> 12) & 0xFu) * 0x00204081u) & 0x01010101u;
   return r;
 }
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  tc::tmem_ld16(taddr, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
+  tc::tmem_ld16(taddr + 16, *reinterpret_cast<uint32_t(*)[16]>(&r[16]));
+}
 
-template <typename KeyT, bool EMIT>
+// Work split: the (query tile, database tile) pairs, ordered query-tile-major,
+// are cut into gridDim.x equal contiguous ranges, one per CTA (exact balance;
+// a CTA changes query tile at most a few times).  A "run" is the part of a
+// CTA's range inside one query tile: database tiles [t0, t1) of query tile qt.
+struct ScanRun {
+  int qt, t0, t1;
+};
+struct RunIter {
+  int64_t f, f1;
+  int NT;
+  __device__ RunIter(const ScanArgs& a) {
+    const int64_t W = static_cast<int64_t>(a.q_tiles) * a.n_tiles;
+    f = W * blockIdx.x / gridDim.x;
+    f1 = W * (blockIdx.x + 1) / gridDim.x;
+    NT = a.n_tiles;
+  }
+  __device__ bool next(ScanRun& r) {
+    if (f >= f1) return false;
+    r.qt = static_cast<int>(f / NT);
+    r.t0 = static_cast<int>(f - static_cast<int64_t>(r.qt) * NT);
+    const int64_t left = f1 - f;
+    r.t1 = static_cast<int>(left < NT - r.t0 ? r.t0 + left : NT);
+    f += r.t1 - r.t0;
+    return true;
+  }
+};
+
+template <typename KeyT, bool EMIT, bool RESIDENT, int KS>
 __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ ScanCtl S;
-  uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t ring_s = smem_u32(ring);
-  constexpr uint32_t kA = kScanM * kScanKB, kB = kScanN * kScanKB, kStage = kA + kB;
+  __shared__ ScanCtl<KS> S;
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr uint32_t kBStage = kScanN * kScanKB;                    // 16 KB
+  constexpr uint32_t kAStage = RESIDENT ? 0u : kScanM * kScanKB;    // 8 KB streamed A
+  constexpr uint32_t kStage = kAStage + kBStage;
+  const uint32_t a_res = smem_u32(base);                                                 // resident A
+  const uint32_t ring = a_res + (RESIDENT ? static_cast<uint32_t>(kScanM) * a.m : 0u);  // stage ring
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const bool binary = a.kind == BVSS_SKETCH_BINARY;
-  const int KC = a.m / kScanKB;
-  const int total = a.n_tiles * a.q_tiles;
+  const int KC = a.m / kScanKB;  // stages per tile
 
   if (tid == 0) {
-    for (int s = 0; s < kScanStages; ++s) {
-      tc::mbar_init(&S.full[s], binary ? 1 + 4 : 1);  // copy warp (+ 4 expander warps)
+    const uint32_t fcount = (binary ? kScanExpWarps : 0) + ((!binary || !RESIDENT) ? 1 : 0);
+    for (int s = 0; s < KS; ++s) {
+      tc::mbar_init(&S.full[s], fcount);
       tc::mbar_init(&S.empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&S.tfull[b], 1);
       tc::mbar_init(&S.tempty[b], kScanEpiWarps);
     }
+    tc::mbar_init(&S.afull, 1);
+    tc::mbar_init(&S.aempty, 1);
     tc::fence_mbar_init();
   }
   if (warp == 1) tc::tmem_alloc(&S.tmem_base, 512);
@@ -134,140 +182,236 @@ __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
   tc::fence_after_sync();
   const uint32_t tmem = S.tmem_base;
 
-  // static round-robin over (db tile, q tile), q tile fastest (the db tile stays L2-hot)
   if (warp == 0) {
-    // ---------------------------------------------------------- bulk copies
-    uint32_t sc = 0;
-    for (int w = blockIdx.x; w < total; w += gridDim.x) {
-      const int it = w / a.q_tiles, qt = w % a.q_tiles;
-      const int64_t i0 = static_cast<int64_t>(it) * kScanM;
-      const int q0 = qt * kScanN;
-      const int rows = static_cast<int>(a.n - i0 < kScanM ? a.n - i0 : kScanM);
-      for (int kc = 0; kc < KC; ++kc, ++sc) {
-        const int st = sc % kScanStages;
-        tc::mbar_wait(&S.empty[st], ((sc / kScanStages) & 1u) ^ 1u);
-        const uint32_t sa = ring_s + st * kStage, sb = sa + kA;
-        const uint32_t bytes = 8u * kScanN * 16u + (binary ? 0u : 8u * rows * 16u);
-        if (lane == 0) arrive_expect_tx(&S.full[st], bytes);
+    // ------------------------------------------------------------ bulk copies
+    uint32_t sc = 0, uc = 0;
+    const bool per_stage = !binary || !RESIDENT;
+    RunIter it(a);
+    ScanRun un;
+    for (; it.next(un); ++uc) {
+      const int q0 = un.qt * kScanM;
+      if (RESIDENT) {  // the query tile: m/16 units of [128 rows][16 B]
+        tc::mbar_wait(&S.aempty, (uc & 1u) ^ 1u);
+        if (lane == 0) arrive_expect_tx(&S.afull, static_cast<uint32_t>(kScanM) * a.m);
         __syncwarp();
-        if (lane < 8) {  // query units 8kc .. 8kc+7: [qpad][16 B] blocks of 256 queries
-          const int u = 8 * kc + lane;
-          bulk_copy(sb + lane * kScanN * 16u, a.Qx + static_cast<int64_t>(u) * a.qpad + q0, kScanN * 16u, &S.full[st]);
-        } else if (!binary && lane < 16) {  // count-mode DB units
-          const int uu = lane - 8, u = 8 * kc + uu;
-          bulk_copy(sa + uu * kScanM * 16u, a.S + static_cast<int64_t>(u) * a.n_stride + i0,
-                    static_cast<uint32_t>(rows) * 16u, &S.full[st]);
+        for (int uu = lane; uu < a.m / 16; uu += 32)
+          bulk_copy(a_res + uu * (kScanM * 16u), a.Qx + static_cast<int64_t>(uu) * a.qpad + q0, kScanM * 16u,
+                    &S.afull);
+      }
+      if (!per_stage) continue;
+      for (int t = un.t0; t < un.t1; ++t) {
+        const int64_t i0 = static_cast<int64_t>(t) * kScanN;
+        const int rows = static_cast<int>(a.n - i0 < kScanN ? a.n - i0 : kScanN);
+        for (int kc = 0; kc < KC; ++kc, ++sc) {
+          const int st = sc % KS;
+          tc::mbar_wait(&S.empty[st], ((sc / KS) & 1u) ^ 1u);
+          const uint32_t sa = ring + st * kStage, sb = sa + kAStage;
+          const uint32_t bytes = kAStage + (binary ? 0u : 4u * rows * 16u);
+          if (lane == 0) arrive_expect_tx(&S.full[st], bytes);
+          __syncwarp();
+          if (!RESIDENT && lane < 4) {  // A units 4kc .. 4kc+3
+            const int uu = 4 * kc + lane;
+            bulk_copy(sa + lane * (kScanM * 16u), a.Qx + static_cast<int64_t>(uu) * a.qpad + q0, kScanM * 16u,
+                      &S.full[st]);
+          } else if (!binary && lane >= 4 && lane < 8) {  // count-mode DB units
+            const int uu = 4 * kc + (lane - 4);
+            bulk_copy(sb + (lane - 4) * (kScanN * 16u), a.S + static_cast<int64_t>(uu) * a.n_stride + i0,
+                      static_cast<uint32_t>(rows) * 16u, &S.full[st]);
+          }
         }
       }
     }
-  } else if (warp >= 6 && warp <= 9) {
-    // ------------------------------------------- bit expansion (binary mode)
+  } else if (warp >= 6) {
+    // ------------------------------------------------- bit expansion (binary)
     if (binary) {
-      const int r = tid - 192;  // DB row of the tile, 0..127
-      uint32_t sc = 0;
-      for (int w = blockIdx.x; w < total; w += gridDim.x) {
-        const int it = w / a.q_tiles;
-        const int64_t i = static_cast<int64_t>(it) * kScanM + r;
-        for (int kc = 0; kc < KC; ++kc, ++sc) {
-          const int st = sc % kScanStages;
-          uint4 bits = make_uint4(0, 0, 0, 0);
-          if (i < a.n) bits = a.S[static_cast<int64_t>(kc) * a.n_stride + i];  // 128 bits of K-chunk kc
-          tc::mbar_wait(&S.empty[st], ((sc / kScanStages) & 1u) ^ 1u);
-          const uint32_t sa = ring_s + st * kStage;
-          const uint32_t w4[4] = {bits.x, bits.y, bits.z, bits.w};
+      const int r = tid - 192;  // DB row of the tile, 0..255
+      const int RC = a.m / 128;  // raw 128-bit chunks per set
+      const int G = (RC + kScanRawPer - 1) / kScanRawPer;
+      // flat sequence of (run, tile, group) for this CTA; registers hold one group ahead
+      RunIter it(a);
+      ScanRun un{};
+      bool have = it.next(un);
+      int t = have ? un.t0 : 0, g = 0;
+      uint4 cur[kScanRawPer];
+      auto load_group = [&](int tt, int gg, uint4 (&dst)[kScanRawPer]) {
+        const int64_t i = static_cast<int64_t>(tt) * kScanN + r;
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const uint4 v = expand16((w4[u >> 1] >> (16 * (u & 1))) & 0xFFFFu);
-            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sa + u * kScanM * 16u + r * 16u),
-                         "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-                         : "memory");
-          }
-          tc::fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(&S.full[st]);
+        for (int c = 0; c < kScanRawPer; ++c) {
+          const int rc = gg * kScanRawPer + c;
+          dst[c] = make_uint4(0, 0, 0, 0);
+          if (i < a.n && rc < RC)
+            asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(dst[c].x), "=r"(dst[c].y), "=r"(dst[c].z), "=r"(dst[c].w)
+                         : "l"(a.S + static_cast<int64_t>(rc) * a.n_stride + i));
         }
+      };
+      if (have) load_group(t, g, cur);
+      uint32_t sc = 0;
+      while (have) {
+        // next position in the sequence
+        int nt = t, ng = g + 1;
+        ScanRun nun = un;
+        bool nhave = true;
+        if (ng == G) {
+          ng = 0;
+          ++nt;
+          if (nt >= nun.t1) {
+            nhave = it.next(nun);
+            nt = nun.t0;
+          }
+        }
+        uint4 nxt[kScanRawPer];
+        if (nhave) load_group(nt, ng, nxt);
+#pragma unroll
+        for (int c = 0; c < kScanRawPer; ++c) {
+          if (g * kScanRawPer + c < RC) {
+            const uint32_t w4[4] = {cur[c].x, cur[c].y, cur[c].z, cur[c].w};
+#pragma unroll
+            for (int h = 0; h < 2; ++h, ++sc) {  // two 64-byte stages per 128-bit chunk
+              const int st = sc % KS;
+              tc::mbar_wait(&S.empty[st], ((sc / KS) & 1u) ^ 1u);
+              const uint32_t sb = ring + st * kStage + kAStage;
+#pragma unroll
+              for (int uu = 0; uu < 4; ++uu) {
+                const int unit = 4 * h + uu;
+                const uint4 v = expand16((w4[unit >> 1] >> (16 * (unit & 1))) & 0xFFFFu);
+                asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sb + uu * (kScanN * 16u) + r * 16u),
+                             "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                             : "memory");
+              }
+              tc::fence_proxy_async_smem();
+              __syncwarp();
+              if (lane == 0) tc::mbar_arrive(&S.full[st]);
+            }
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < kScanRawPer; ++c) cur[c] = nxt[c];
+        t = nt;
+        g = ng;
+        un = nun;
+        have = nhave;
       }
     }
   } else if (warp == 1) {
-    // ---------------------------------------------------------- MMA issuer
+    // ------------------------------------------------------------ MMA issuer
     const uint32_t idesc = idesc_u8_s32(kScanM, kScanN);
-    uint32_t sc = 0, tc_ = 0;
-    for (int w = blockIdx.x; w < total; w += gridDim.x, ++tc_) {
-      const uint32_t acc = tc_ & 1u;
-      tc::mbar_wait(&S.tempty[acc], ((tc_ >> 1) & 1u) ^ 1u);
-      tc::fence_after_sync();
-      const uint32_t d = tmem + acc * kScanN;
-      for (int kc = 0; kc < KC; ++kc, ++sc) {
-        const int st = sc % kScanStages;
-        tc::mbar_wait(&S.full[st], (sc / kScanStages) & 1u);
+    uint32_t sc = 0, tc_ = 0, uc = 0;
+    RunIter it(a);
+    ScanRun un;
+    for (; it.next(un); ++uc) {
+      if (RESIDENT) {
+        tc::mbar_wait(&S.afull, uc & 1u);
         tc::fence_after_sync();
-        if (lane == 0) {
-          const uint32_t sa = ring_s + st * kStage, sb = sa + kA;
+      }
+      for (int t = un.t0; t < un.t1; ++t, ++tc_) {
+        const uint32_t acc = tc_ & 1u;
+        tc::mbar_wait(&S.tempty[acc], ((tc_ >> 1) & 1u) ^ 1u);
+        tc::fence_after_sync();
+        const uint32_t d = tmem + acc * kScanN;
+        for (int kc = 0; kc < KC; ++kc, ++sc) {
+          const int st = sc % KS;
+          tc::mbar_wait(&S.full[st], (sc / KS) & 1u);
+          tc::fence_after_sync();
+          if (lane == 0) {
+            const uint32_t sa = ring + st * kStage, sb = sa + kAStage;
 #pragma unroll
-          for (int kk = 0; kk < kScanKB / 32; ++kk) {  // K = 32 bytes = 2 units per instruction
-            umma_u8(d, kmajor_desc(sa + 2 * kk * kScanM * 16u, kScanM * 16u, 128u),
-                    kmajor_desc(sb + 2 * kk * kScanN * 16u, kScanN * 16u, 128u), idesc, (kc | kk) ? 1u : 0u);
+            for (int kk = 0; kk < kScanKB / 32; ++kk) {  // K = 32 bytes = 2 units per instruction
+              const uint64_t ad = RESIDENT ? kmajor_desc(a_res + (4 * kc + 2 * kk) * (kScanM * 16u), kScanM * 16u, 128u)
+                                           : kmajor_desc(sa + 2 * kk * (kScanM * 16u), kScanM * 16u, 128u);
+              umma_u8(d, ad, kmajor_desc(sb + 2 * kk * (kScanN * 16u), kScanN * 16u, 128u), idesc,
+                      (kc | kk) ? 1u : 0u);
+            }
+            tc::umma_commit(&S.empty[st]);
+            if (kc == KC - 1) tc::umma_commit(&S.tfull[acc]);
           }
-          tc::umma_commit(&S.empty[st]);
-          if (kc == KC - 1) tc::umma_commit(&S.tfull[acc]);
+          __syncwarp();
         }
+      }
+      if (RESIDENT) {
+        if (lane == 0) tc::umma_commit(&S.aempty);  // the query tile may be replaced
         __syncwarp();
       }
     }
   } else {
-    // -------------------------------------- epilogue (warps 2-5 and 10-13)
-    const int ew = warp & 3;
-    const int half = warp >= 10 ? 1 : 0;  // columns [128 half, 128 half + 128)
-    const int row = ew * 32 + lane;       // TMEM lane = DB set of the tile
+    // ------------------------------------------------ epilogue (warps 2-5)
+    const int quarter = warp & 3;         // TMEM lane quarter this warp may access
     KeyT* keys = static_cast<KeyT*>(a.keys);
     uint32_t tc_ = 0;
-    for (int w = blockIdx.x; w < total; w += gridDim.x, ++tc_) {
-      const int it = w / a.q_tiles, qt = w % a.q_tiles;
-      const int64_t i = static_cast<int64_t>(it) * kScanM + row;
-      const int q0 = qt * kScanN + half * (kScanN / 2);
-      const bool ok = i < a.n;
-      const int32_t pi = ok ? a.massS[i] : 0;
-      const uint32_t acc = tc_ & 1u;
-      tc::mbar_wait(&S.tfull[acc], (tc_ >> 1) & 1u);
-      tc::fence_after_sync();
-      const uint32_t tbase = tmem + acc * kScanN + half * (kScanN / 2) + (static_cast<uint32_t>(ew * 32) << 16);
-      for (int c0 = 0; c0 < kScanN / 2; c0 += 32) {
-        uint32_t v[32];
-        tc::tmem_ld16(tbase + c0, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
-        tc::tmem_ld16(tbase + c0 + 16, *reinterpret_cast<uint32_t(*)[16]>(&v[16]));
-        // query masses (and thresholds) of these 32 columns: warp-uniform loads, overlapped with TMEM
-        int32_t pq[32];
-        uint32_t tq[32];
+    RunIter it(a);
+    ScanRun un;
+    while (it.next(un)) {
+      const int q = un.qt * kScanM + quarter * 32 + lane;
+      const bool qok = q < a.nq;
+      const int32_t pq = qok ? __ldg(a.massQ + q) : 0;
+      // key <= tau  <=>  p_i - 2 acc <= tau - p_Q   (keys are exact, < 2^31)
+      const int32_t lim = EMIT ? (qok ? static_cast<int32_t>(__ldg(a.tau + q)) - pq : -0x40000000) : 0;
+      for (int t = un.t0; t < un.t1; ++t, ++tc_) {
+        const uint32_t acc = tc_ & 1u;
+        const int64_t i0 = static_cast<int64_t>(t) * kScanN;
+        tc::mbar_wait(&S.tfull[acc], (tc_ >> 1) & 1u);
+        tc::fence_after_sync();
+        const uint32_t tbase = tmem + acc * kScanN + (static_cast<uint32_t>(quarter * 32) << 16);
+#pragma unroll 1
+        for (int c0 = 0; c0 < kScanN; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32(tbase + c0, v);
+          const int64_t ic = i0 + c0;
+          int32_t pi[32];
+          if (ic + 32 <= a.n) {
+            const int4* mp = reinterpret_cast<const int4*>(a.massS + ic);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int q = q0 + c0 + j;
-          pq[j] = q < a.nq ? __ldg(a.massQ + q) : 0;
-          if (EMIT) tq[j] = q < a.nq ? __ldg(a.tau + q) : 0u;
-        }
-        tc::tmem_ld_wait();
-        if (c0 + 32 >= kScanN / 2) {  // this warp's half of the accumulator is read
-          tc::fence_before_sync();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(&S.tempty[acc]);
-        }
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int q = q0 + c0 + j;
-          const int32_t key = pq[j] + pi - 2 * static_cast<int32_t>(v[j]);
-          if (!EMIT) {
-            if (q < a.nq && ok) keys[static_cast<int64_t>(q) * a.key_stride + i] = static_cast<KeyT>(key);
+            for (int j = 0; j < 8; ++j) {
+              const int4 t4 = __ldg(mp + j);
+              pi[4 * j] = t4.x;
+              pi[4 * j + 1] = t4.y;
+              pi[4 * j + 2] = t4.z;
+              pi[4 * j + 3] = t4.w;
+            }
           } else {
-            const bool pass = ok && q < a.nq && static_cast<uint32_t>(key) <= tq[j];
-            const unsigned mask = __ballot_sync(0xffffffffu, pass);
-            if (mask) {  // warp-uniform: rare (a few keys per thousand)
-              int base = 0;
-              if (lane == 0) base = atomicAdd(a.cnt + q, __popc(mask));
-              base = __shfl_sync(0xffffffffu, base, 0);
-              const int pos = base + __popc(mask & ((1u << lane) - 1u));
-              if (pass && pos < a.cap) {
-                a.buf_id[static_cast<int64_t>(q) * a.cap + pos] = static_cast<int32_t>(a.id_base + i);
-                a.buf_key[static_cast<int64_t>(q) * a.cap + pos] = static_cast<uint32_t>(key);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) pi[j] = ic + j < a.n ? __ldg(a.massS + ic + j) : 0x40000000;
+          }
+          tc::tmem_ld_wait();
+          if (c0 + 32 >= kScanN) {  // this warp's lanes of the accumulator are read
+            tc::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&S.tempty[acc]);
+          }
+          if (EMIT) {
+            uint32_t mask = 0;
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              mask |= (pi[j] - 2 * static_cast<int32_t>(v[j]) <= lim ? 1u : 0u) << j;
+            if (mask) {  // rare: a few keys per thousand
+              const int ne = __popc(mask);
+              const int pos0 = atomicAdd(a.cnt + q, ne);
+              int e = 0;
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {  // unrolled: keeps v[] and pi[] in registers
+                if ((mask >> j) & 1u) {
+                  const int pos = pos0 + e++;
+                  if (pos < a.cap) {
+                    const int64_t o = static_cast<int64_t>(q) * a.cap + pos;
+                    a.buf_id[o] = static_cast<int32_t>(a.id_base + ic + j);
+                    a.buf_key[o] = static_cast<uint32_t>(pq + pi[j] - 2 * static_cast<int32_t>(v[j]));
+                  }
+                }
               }
+            }
+          } else if (qok) {
+            KeyT kv[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) kv[j] = static_cast<KeyT>(pq + pi[j] - 2 * static_cast<int32_t>(v[j]));
+            KeyT* row = keys + static_cast<int64_t>(q) * a.key_stride + ic;
+            if (ic + 32 <= a.key_stride) {
+              uint4* dst = reinterpret_cast<uint4*>(row);
+              const uint4* src = reinterpret_cast<const uint4*>(kv);
+#pragma unroll
+              for (int j = 0; j < static_cast<int>(32 * sizeof(KeyT) / 16); ++j) dst[j] = src[j];
+            } else {
+              for (int j = 0; j < 32; ++j)
+                if (ic + j < a.n) row[j] = kv[j];
             }
           }
         }
@@ -310,7 +454,7 @@ int launch_scan_tc(int kind, const void* S, const int32_t* mass, int64_t n, int6
                    int64_t key_stride, int* work_counter, int num_sms, cudaStream_t st, const uint32_t* tau,
                    int32_t* cnt, int32_t* buf_id, uint32_t* buf_key, int cap, int64_t id_base, bool expand) {
   if (nq <= 0 || n <= 0) return BVSS_OK;
-  if (m % kScanKB) BVSS_FAIL(BVSS_EUNSUPPORTED, "tensor-core scan needs m %% 128 == 0");
+  if (m % 128) BVSS_FAIL(BVSS_EUNSUPPORTED, "tensor-core scan needs m %% 128 == 0");
   const int cps = kind == BVSS_SKETCH_BINARY ? (((m / 32) + 3) / 4) : m / 16;
   if (expand) {
     expand_queries_kernel<<<num_sms * 4, 256, 0, st>>>(kind, static_cast<const uint4*>(SQ), cps, nq, qpad, m,
@@ -330,32 +474,49 @@ int launch_scan_tc(int kind, const void* S, const int32_t* mass, int64_t n, int6
   a.m = m;
   a.keys = keys;
   a.key_stride = key_stride;
-  a.n_tiles = static_cast<int>(ceil_div<int64_t>(n, kScanM));
-  a.q_tiles = ceil_div(nq, kScanN);
-  a.work_counter = work_counter;
+  a.n_tiles = static_cast<int>(ceil_div<int64_t>(n, kScanN));
+  a.q_tiles = ceil_div(nq, kScanM);
+  if (qpad < a.q_tiles * kScanM) BVSS_FAIL(BVSS_EINVAL, "scan: query padding %d < %d", qpad, a.q_tiles * kScanM);
   a.tau = tau;
   a.cnt = cnt;
   a.buf_id = buf_id;
   a.buf_key = buf_key;
   a.cap = cap;
   a.id_base = id_base;
-  const size_t smem = static_cast<size_t>(kScanStages) * (kScanM + kScanN) * kScanKB + 1024;
-  const int total = a.n_tiles * a.q_tiles;
-  const int grid = total < num_sms ? total : num_sms;
-#define BVSS_SCAN_LAUNCH(KT, EM)                                                                          \
+  (void)work_counter;
+  constexpr int KS = 6;
+  const bool resident = m <= kScanResidentMaxM;
+  const size_t smem = (resident ? static_cast<size_t>(kScanM) * m + static_cast<size_t>(KS) * kScanN * kScanKB
+                                : static_cast<size_t>(KS) * (kScanM + kScanN) * kScanKB) + 1024;
+  const int64_t work = static_cast<int64_t>(a.n_tiles) * a.q_tiles;
+  const int grid = static_cast<int>(work < num_sms ? work : num_sms);
+#define BVSS_SCAN_LAUNCH(KT, EM, RES)                                                                     \
   do {                                                                                                    \
-    auto kfn = scan_tc_kernel<KT, EM>;                                                                    \
+    auto kfn = scan_tc_kernel<KT, EM, RES, KS>;                                                           \
     BVSS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem))); \
+    cudaFuncAttributes fa;                                                                                \
+    BVSS_CUDA(cudaFuncGetAttributes(&fa, kfn));                                                           \
+    if (fa.maxThreadsPerBlock < kScanThreads)                                                             \
+      BVSS_FAIL(BVSS_ECUDA, "scan_tc_kernel: %d regs/thread, %zu B static smem, %zu B local: max %d threads < %d", \
+                fa.numRegs, fa.sharedSizeBytes, fa.localSizeBytes, fa.maxThreadsPerBlock, kScanThreads); \
     kfn<<<grid, kScanThreads, smem, st>>>(a);                                                             \
+  } while (0)
+#define BVSS_SCAN_LAUNCH2(KT, EM) \
+  do {                            \
+    if (resident)                 \
+      BVSS_SCAN_LAUNCH(KT, EM, true); \
+    else                          \
+      BVSS_SCAN_LAUNCH(KT, EM, false); \
   } while (0)
   const bool emit = tau != nullptr;
   if (kind == BVSS_SKETCH_BINARY) {
-    if (emit) BVSS_SCAN_LAUNCH(uint16_t, true);
-    else BVSS_SCAN_LAUNCH(uint16_t, false);
+    if (emit) BVSS_SCAN_LAUNCH2(uint16_t, true);
+    else BVSS_SCAN_LAUNCH2(uint16_t, false);
   } else {
-    if (emit) BVSS_SCAN_LAUNCH(uint32_t, true);
-    else BVSS_SCAN_LAUNCH(uint32_t, false);
+    if (emit) BVSS_SCAN_LAUNCH2(uint32_t, true);
+    else BVSS_SCAN_LAUNCH2(uint32_t, false);
   }
+#undef BVSS_SCAN_LAUNCH2
 #undef BVSS_SCAN_LAUNCH
   BVSS_TRY(post_launch(__func__, st));
   return BVSS_OK;

@@ -285,3 +285,34 @@ def test_sampled_select_fallback_on_overflow(monkeypatch):
     monkeypatch.setenv("BVSS_DEBUG_EMIT_CAP", "16")
     out = _modes_agree(cfg, data, (cfg.T,))
     assert out[2][0][2]["select_fallbacks"] >= 1
+
+
+@pytest.mark.parametrize("name,ov", [("cfg3", dict(n=7001, nq=300, T=150)), ("cfg2", dict(n=3333, nq=260, T=90, d=64)),
+                                     ("cfg4", dict(n=1500, nq=130, T=60, d=64))])
+def test_filter_many_query_tiles(name, ov):
+    """Several 128-query tiles (ragged), ragged 256-set database tiles, binary and
+    count sketches (m = 1024 resident query tile; m = 2048 streamed): candidates
+    and scores bit-exact against the oracle given the GPU sketches, for the
+    full-key scan and the sampled-threshold fused scan."""
+    _need_gpu()
+    cfg = synth.get_config(name, **ov)
+    data = synth.to_numpy(synth.generate(cfg, device="cpu"))
+    for mode in (1, 2):
+        idx = B.Index(data["vectors"], data["offsets"], m=cfg.m, s=cfg.s, L=cfg.L, sketch=cfg.sketch, seed=cfg.seed,
+                      select_mode=mode)
+        db = idx.export_sketches()
+        qsk = idx.query_sketch(data["queries"], data["q_offsets"])
+        cand, score = idx.filter(data["queries"], data["q_offsets"], cfg.T)
+        ids, dist = idx.search(data["queries"], data["q_offsets"], cfg.k, cfg.T)
+        st = idx.stats()
+        idx.close()
+        for qi in range(cand.shape[0]):
+            sc = _oracle_scores(cfg, qsk[qi], db)
+            ref = np.sort(O.select_top_T(sc, cfg.T))
+            got = cand[qi][cand[qi] >= 0]
+            assert np.array_equal(ref, got), f"mode {mode} query {qi}"
+            assert np.array_equal(score[qi][: got.shape[0]], sc[got])
+        if mode == 1:
+            base = (ids, dist)
+        else:
+            assert np.array_equal(ids, base[0]) and np.array_equal(dist, base[1])
