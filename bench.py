@@ -231,14 +231,18 @@ def main_ours(args):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
+        th0 = time.perf_counter()
         out_ids, out_d = step()
+        th1 = time.perf_counter()
         e1.record()
         torch.cuda.synchronize()
+        if os.environ.get("BVSS_TRACE"):
+            print(f"[bench] step host {1000 * (th1 - th0):.1f} ms, events {e0.elapsed_time(e1):.1f} ms", file=sys.stderr)
         times.append(e0.elapsed_time(e1))
         s = idx.stats()
         launches += int(s["kernel_launches"]) + (0 if world == 1 else 1)
         for key in ("ms_encode", "ms_scan", "ms_select", "ms_refine", "ms_topk", "ms_h2d", "ms_total", "scan_bytes",
-                    "gather_bytes", "cand_rows", "fixup_sets"):
+                    "gather_bytes", "cand_rows", "fixup_sets", "select_batches", "select_fallbacks"):
             st_sum[key] = st_sum.get(key, 0) + s[key]
     torch.cuda.synchronize()
     if world > 1:
@@ -334,6 +338,7 @@ def main_ours(args):
                       "vectors_per_s": round(nvec_shard / (build_ms * 1e-3), 1), "gen_s": round(t_gen, 1),
                       "note": "index build (K1 encode + K9 split/norms + K2 sketch, incl. the D2D copy) per GPU"},
             "fixup_sets_per_step": st_sum["fixup_sets"] / K,
+            "select": {"sampled_batches": st_sum["select_batches"], "fallbacks": st_sum["select_fallbacks"]},
         }
         print(json.dumps(line), flush=True)
     idx.close()

@@ -6,6 +6,7 @@
 //   build : K1 encode (+K9 norms, bf16 split)  ->  K2 sketches
 //   search: K1/K2 on the queries -> K3 scan -> K4 select -> K5 refine -> K6 top-k
 #include <algorithm>
+#include <chrono>
 #include <cstdarg>
 #include <cstdlib>
 #include <cstdio>
@@ -67,6 +68,8 @@ int launch_scan_tc(int kind, const void* S, const int32_t* mass, int64_t n, int6
                    int cap, int64_t id_base, bool expand);
 int launch_select_buf(const int32_t* cnt, const uint32_t* bkey, const int32_t* bid, int cap, int teff, int key_bits,
                       int T, int nq, int32_t* cand, int32_t* count, int* fail, cudaStream_t s);
+int launch_expand_db_fp4(const void* S, int64_t n, int64_t n_stride, int m, void* X, int num_sms, cudaStream_t st);
+int scan_tc_units(int kind, int m);
 int launch_gather_sample(const void* sk, const int32_t* mass, int64_t n, int cps, int64_t ns, void* out,
                          int32_t* out_mass, int num_sms, cudaStream_t s);
 struct SelectState {
@@ -221,6 +224,8 @@ struct bvss_index {
   uint32_t select_mode = 0;   // 0 auto, 1 full keys, 2 sampled threshold
   int64_t ns = 0;             // database sample for the threshold estimate (select_mode 2)
   void* smp_sk = nullptr;     // chunk-major sketches of the sample
+  void* skx = nullptr;        // binary: tensor-core scan operand, FP4 expansion [m/32][n][16 B] (scan_tc.cu)
+  void* smp_skx = nullptr;    // the same for the sample
   int32_t* smp_mass = nullptr;
   size_t owned_bytes = 0;
   Workspace ws;
@@ -409,13 +414,18 @@ int prepare_queries(bvss_index* idx, bvss_search_ctx* c, const float* queries, c
 
 bool use_tc_scan(const bvss_index* idx) {
   static const bool simt = getenv("BVSS_SCAN_SIMT") != nullptr;  // developer switch: SIMT popc/dp4a scan
-  return idx->m % 128 == 0 && !simt;
+  return idx->m % (idx->sketch == BVSS_SKETCH_BINARY ? 256 : 128) == 0 && !simt;
+}
+// database operand of the tensor-core scan (binary: FP4 expansion; count: the counters themselves)
+const void* scan_operand(const bvss_index* idx, bool sample) {
+  if (idx->sketch == BVSS_SKETCH_BINARY) return sample ? idx->smp_skx : idx->skx;
+  return sample ? idx->smp_sk : idx->sk;
 }
 
 // tensor-core scan operands: queries expanded to [m/16][qpad][16 B] (scan_tc.cu)
 int expand_alloc(bvss_index* idx, bvss_search_ctx* c) {
-  c->qpad = static_cast<int>(ceil_div<int64_t>(c->nq, 256) * 256);
-  return idx->ws.get("scan_qx", static_cast<size_t>(idx->m) * c->qpad, &c->qx);
+  c->qpad = static_cast<int>(ceil_div<int64_t>(c->nq, 128) * 128);
+  return idx->ws.get("scan_qx", static_cast<size_t>(scan_tc_units(idx->sketch, idx->m)) * 16 * c->qpad, &c->qx);
 }
 
 int alloc_select_state(bvss_index* idx, bvss_search_ctx* c) {
@@ -443,7 +453,7 @@ int scan_batch(bvss_index* idx, bvss_search_ctx* c) {
     BVSS_TRY(expand_alloc(idx, c));
     int* wc;
     BVSS_TRY(idx->ws.get("scan_counter", sizeof(int), reinterpret_cast<void**>(&wc)));
-    BVSS_TRY(launch_scan_tc(idx->sketch, idx->sk, idx->mass, n, n, idx->m, c->qsk, c->qmass, static_cast<int>(c->nq),
+    BVSS_TRY(launch_scan_tc(idx->sketch, scan_operand(idx, false), idx->mass, n, n, idx->m, c->qsk, c->qmass, static_cast<int>(c->nq),
                             c->qx, c->qpad, c->keys, c->key_stride, wc, idx->num_sms, idx->stream, nullptr, nullptr,
                             nullptr, nullptr, 0, 0, true));
     idx->stats.kernel_launches += 2;
@@ -493,7 +503,7 @@ int select_sampled(bvss_index* idx, bvss_search_ctx* c, bool* ok) {
   const int64_t sstride = (ns + 7) & ~int64_t(7);
   void* skeys;
   BVSS_TRY(idx->ws.get("sample_keys", static_cast<size_t>(nq) * sstride * key_size, &skeys));
-  BVSS_TRY(launch_scan_tc(idx->sketch, idx->smp_sk, idx->smp_mass, ns, ns, idx->m, c->qsk, c->qmass, nq, c->qx,
+  BVSS_TRY(launch_scan_tc(idx->sketch, scan_operand(idx, true), idx->smp_mass, ns, ns, idx->m, c->qsk, c->qmass, nq, c->qx,
                           c->qpad, skeys, sstride, wc, idx->num_sms, idx->stream, nullptr, nullptr, nullptr, nullptr, 0,
                           0, true));
   // 2. tau_hat = k_s-th smallest sample key (exact radix select on the sample)
@@ -510,7 +520,7 @@ int select_sampled(bvss_index* idx, bvss_search_ctx* c, bool* ok) {
   BVSS_TRY(idx->ws.get("emit_id", static_cast<size_t>(nq) * cap * 4, reinterpret_cast<void**>(&bid)));
   BVSS_TRY(idx->ws.get("emit_key", static_cast<size_t>(nq) * cap * 4, reinterpret_cast<void**>(&bkey)));
   BVSS_CUDA(cudaMemsetAsync(cnt, 0, nq * sizeof(int32_t), idx->stream));
-  BVSS_TRY(launch_scan_tc(idx->sketch, idx->sk, idx->mass, n, n, idx->m, c->qsk, c->qmass, nq, c->qx, c->qpad, nullptr,
+  BVSS_TRY(launch_scan_tc(idx->sketch, scan_operand(idx, false), idx->mass, n, n, idx->m, c->qsk, c->qmass, nq, c->qx, c->qpad, nullptr,
                           0, wc, idx->num_sms, idx->stream, c->sel.prefix, cnt, bid, bkey, static_cast<int>(cap),
                           c->id_base, false));
   idx->stats.scan_bytes += static_cast<uint64_t>(ceil_div<int64_t>(c->nq, 256)) * (n + ns) * chunks_per_set(idx) * 16;
@@ -763,11 +773,18 @@ int bvss_build_index(const float* vectors, const int64_t* set_offsets, int64_t n
   BVSS_TRY(dalloc(static_cast<size_t>(n) * cps * 16, &idx->sk));
   BVSS_TRY(dalloc(static_cast<size_t>(n) * 4, reinterpret_cast<void**>(&idx->mass)));
   BVSS_TRY(launch_sketch(codes, p->m, idx->off, n, p->sketch, idx->sk, idx->mass, n, 1, num_sms, st));
-  if (p->m % 128 == 0) {  // strided database sample for the sampled-threshold select
+  if (use_tc_scan(idx.get())) {
+    // strided database sample for the sampled-threshold select
     idx->ns = n < 16384 ? n : 16384;
     BVSS_TRY(dalloc(static_cast<size_t>(idx->ns) * cps * 16, &idx->smp_sk));
     BVSS_TRY(dalloc(static_cast<size_t>(idx->ns) * 4, reinterpret_cast<void**>(&idx->smp_mass)));
     BVSS_TRY(launch_gather_sample(idx->sk, idx->mass, n, cps, idx->ns, idx->smp_sk, idx->smp_mass, num_sms, st));
+    if (p->sketch == BVSS_SKETCH_BINARY) {  // FP4 tensor-core operands (m/2 bytes per set)
+      BVSS_TRY(dalloc(static_cast<size_t>(n) * p->m / 2, &idx->skx));
+      BVSS_TRY(dalloc(static_cast<size_t>(idx->ns) * p->m / 2, &idx->smp_skx));
+      BVSS_TRY(launch_expand_db_fp4(idx->sk, n, n, p->m, idx->skx, num_sms, st));
+      BVSS_TRY(launch_expand_db_fp4(idx->smp_sk, idx->ns, idx->ns, p->m, idx->smp_skx, num_sms, st));
+    }
   }
   unsigned int* vmax;
   BVSS_TRY(idx->ws.get("vmax", sizeof(unsigned int), reinterpret_cast<void**>(&vmax)));
@@ -788,7 +805,8 @@ void bvss_free_index(bvss_index* idx) {
   DeviceGuard g(idx->device);
   if (idx->stream) cudaStreamSynchronize(idx->stream);
   void* ptrs[] = {idx->Wt,    idx->V,     idx->off,   idx->hi,   idx->lo,     idx->vscale, idx->pbase,
-                  idx->vnorm, idx->codes, idx->sk,    idx->mass, idx->smp_sk, idx->smp_mass};
+                  idx->vnorm, idx->codes, idx->sk,    idx->mass, idx->smp_sk, idx->smp_mass,
+                  idx->skx,   idx->smp_skx};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   idx->ws.release();
@@ -957,6 +975,7 @@ int bvss_refine(bvss_index* idx, const float* queries, const int64_t* query_offs
 
 int bvss_search(bvss_index* idx, const float* queries, const int64_t* query_offsets, int64_t nq, int32_t k, int32_t T,
                 int64_t* out_ids, float* out_dist, uint32_t flags) {
+  const auto t_entry = std::chrono::steady_clock::now();
   BVSS_TRY(validate_search(idx, queries, query_offsets, nq, k, T));
   if (!out_ids || !out_dist) BVSS_FAIL(BVSS_EINVAL, "null output");
   DeviceGuard g(idx->device);
@@ -977,8 +996,15 @@ int bvss_search(bvss_index* idx, const float* queries, const int64_t* query_offs
   float ms[6] = {0, 0, 0, 0, 0, 0};
   float tot = 0.0f;
   uint64_t fixups = 0;
+  static const bool trace = getenv("BVSS_TRACE") != nullptr;  // developer switch: host-side phase timing
+  auto now_us = [] { return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+  const double t_start = now_us();
+  if (trace)
+    fprintf(stderr, "[bvss] search entry -> batches %.0f us\n",
+            std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_entry).count());
   for (int64_t b0 = 0; b0 < nq; b0 += B) {
     const int64_t nb = (b0 + B <= nq) ? B : nq - b0;
+    const double t_b = now_us();
     std::vector<int64_t> sub(nb + 1);
     for (int64_t i = 0; i <= nb; ++i) sub[i] = qo[b0 + i] - qo[b0];
     std::unique_ptr<bvss_search_ctx> c;
@@ -991,7 +1017,9 @@ int bvss_search(bvss_index* idx, const float* queries, const int64_t* query_offs
       BVSS_TRY(run_select_single(idx, c.get()));
       BVSS_TRY(emit_candidates(idx, c.get()));
     }
+    const double t_sel = now_us();
     BVSS_TRY(refine_topk(idx, c.get(), oid, odist));
+    const double t_ref = now_us();
     BVSS_TRY(from_device(idx, out_ids + b0 * k, oid, static_cast<size_t>(nb) * k * 8, dev));
     BVSS_TRY(from_device(idx, out_dist + b0 * k, odist, static_cast<size_t>(nb) * k * 4, dev));
     BVSS_CUDA(cudaEventRecord(idx->ev[7], idx->stream));
@@ -1003,7 +1031,11 @@ int bvss_search(bvss_index* idx, const float* queries, const int64_t* query_offs
     BVSS_CUDA(cudaMemcpyAsync(&hf, fix, sizeof(hf), cudaMemcpyDeviceToHost, idx->stream));
     BVSS_CUDA(cudaStreamSynchronize(idx->stream));
     fixups += static_cast<uint64_t>(hf);
+    if (trace)
+      fprintf(stderr, "[bvss] batch %lld: host issue->select %.0f us, refine issue %.0f us, wait %.0f us; gpu %.0f us\n",
+              static_cast<long long>(b0), t_sel - t_b, t_ref - t_sel, now_us() - t_ref, 1000.0 * ev_ms(idx, 0, 7));
   }
+  if (trace) fprintf(stderr, "[bvss] search host total %.0f us\n", now_us() - t_start);
   idx->stats.ms_h2d = ms[0];
   idx->stats.ms_encode = ms[1];
   idx->stats.ms_scan = ms[2];

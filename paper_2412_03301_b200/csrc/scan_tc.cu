@@ -1,61 +1,71 @@
 // scan_tc.cu — K3 on the 5th-generation tensor cores: the filter scan of Alg 6
-// lines 10-13 as an exact unsigned-integer GEMM (tcgen05.mma
-// kind::i8, u8 x u8 -> s32 accumulated in TMEM).
+// lines 10-13 as an exact GEMM between query sketches and database
+// sketches, accumulated in TMEM.
 //
-//   binary : popc(S_Q AND S_i) = sum_j b_Q[j] b_i[j] with every sketch bit expanded
-//            to a 0/1 byte; Hamming = p_Q + p_i - 2 popc(AND)          (reading R1)
-//   count  : <C_Q, C_i> = sum_j C_Q[j] C_i[j] on the uint8 counters;
-//            L2^2 = |C_Q|^2 + |C_i|^2 - 2 <C_Q, C_i>                      (reading R2)
-// Both are exact in s32 (max 2048 * 255^2 < 2^31), so the keys are bit-identical
-// to the SIMT scan (scan.cu) and to the oracle.
+//   binary : popc(S_Q AND S_i) = sum_j b_Q[j] b_i[j].  Every sketch bit is an
+//            e2m1 (FP4) element, 1.0 or 0.0, and the product runs as
+//            tcgen05.mma kind::mxf4 with all block scales = 1.0 (ue8m0 127):
+//            products are 0/1 and the fp32 sums are integers <= m < 2^24, so
+//            the count is exact.  Hamming = p_Q + p_i - 2 popc(AND)   (reading R1)
+//   count  : <C_Q, C_i> = sum_j C_Q[j] C_i[j] on the uint8 counters, kind::i8
+//            (u8 x u8 -> s32); L2^2 = |C_Q|^2 + |C_i|^2 - 2 <C_Q, C_i>  (reading R2)
+// Both are exact, so the keys are bit-identical to the SIMT scan (scan.cu) and
+// to the oracle.  Measured on B200 (tools/microbench_scan_mma.cu): kind::mxf4
+// M=128 N=240 K=64 issues every ~154 cycles (12.8k MAC/clk/SM), kind::i8 M=128
+// N=256 K=32 every ~161 cycles (6.5k MAC/clk/SM).
+//
+// Operands use the canonical no-swizzle K-major layout: per 16-byte K unit u a
+// [rows][16 B] block (core matrices of 8 rows x 16 B), LBO = rows x 16 B
+// between units, SBO = 128 B between 8-row groups.  The index stores the
+// database operand in exactly this layout ([units][n][16 B]: the FP4 expansion
+// of the binary sketches, made once at build time, or the count sketches), so
+// every tile arrives by plain contiguous cp.async.bulk copies and no SM time is
+// spent on bit expansion.
 //
 // Queries are the STATIONARY operand: A = a tile of 128 query sketches (M = 128,
-// one TMEM lane per query), resident in shared memory for a whole work unit when
-// 128 x m bytes fit (m <= 1024), else streamed with B.  B = 256 database sets
-// (N = 256) streamed through a stage ring in 64-byte K-chunks.  The (query
-// tile, database tile) pairs are split into equal contiguous ranges, one per
+// one TMEM lane per query), resident in shared memory while it fits (else
+// streamed with B).  B = kN database sets (N = 240 FP4 / 256 i8) streamed
+// through a stage ring, 128 bytes of K per stage (4 MMAs).  The (query tile,
+// database tile) pairs are split into equal contiguous ranges, one per
 // persistent CTA (query-tile-major, so a CTA reloads its query tile at most a
 // few times).
-// Operands use the canonical no-swizzle K-major layout: per 16-byte K unit u a
-// [rows][16 B] block (core matrices of 8 rows x 16 B), LBO = rows x 16 B between
-// units, SBO = 128 B between 8-row groups.  This is the chunk-major layout the
-// sketches are stored in ([m/16][n][16 B], sketch.cu), so count tiles and the
-// pre-expanded query tiles arrive by plain contiguous cp.async.bulk copies, and
-// binary tiles are expanded bit -> byte by eight expander warps (one database
-// set per thread, 128-bit loads prefetched a whole tile ahead in registers).
 //
 // Because a TMEM lane is a query, the epilogue thread owns one query: its mass
-// p_Q and threshold tau_Q live in registers and the per-value work is one IMAD
-// and one compare (keys = p_Q + p_i - 2 acc; database masses are warp-uniform
-// 128-bit loads).  Emit mode appends (id, key) for key <= tau_Q with one atomic
-// per (thread, 32 columns) that emit anything.
+// p_Q and threshold tau_Q live in registers and the per-value work is one FFMA
+// (IMAD for i8) and one compare: p_i - 2 acc <= tau_Q - p_Q (database masses
+// come from a shared-memory slot the producer fills per tile; all values are
+// exact integers in fp32).  Emit mode appends (id, key)
+// for key <= tau_Q: a first pass over the tile's columns builds per-column pass
+// bits, one atomic per (thread, tile) reserves the buffer range, and a second
+// TMEM pass writes the entries.
 //
-// CTA = 14 warps: warp 0 bulk copies (query tile; count-mode / streamed-A
-// stages), warp 1 TMEM owner + MMA issuer, warps 2-5 epilogue (one per TMEM
-// lane quarter, all 256 columns), warps 6-13 bit expansion (binary mode).
-// Double-buffered TMEM accumulators (2 x 256 columns).
+// CTA = 10 warps: warp 0 producer (query tile, stage copies, database masses),
+// warp 1 TMEM owner + MMA issuer, warps 2-9 epilogue (two per TMEM lane
+// quarter, each half of the columns).  Double-buffered TMEM accumulators (2 x kN columns; FP4 keeps its
+// block scales in the last 32 columns).
+#include <cstdlib>
+#include <type_traits>
+
 #include "tc.cuh"
 
 namespace bvss {
 
-constexpr int kScanM = 128;    // queries per tile (MMA M, TMEM lanes)
-constexpr int kScanN = 256;    // database sets per tile (MMA N)
-constexpr int kScanKB = 64;    // bytes (= u8 elements) of K per stage
-constexpr int kScanThreads = 448;  // 14 warps (register file: 128 regs/thread)
-constexpr int kScanEpiWarps = 4;
-constexpr int kScanExpWarps = 8;
-constexpr int kScanResidentMaxM = 1024;  // A resident in smem when 128 x m <= 128 KB
-constexpr int kScanRawPer = 8;           // 128-bit raw chunks prefetched per group (expander)
+constexpr int kScanM = 128;        // queries per tile (MMA M, TMEM lanes)
+constexpr int kScanStageB = 128;   // bytes of K per row per stage (8 units of 16 B, 4 MMAs)
+constexpr int kScanThreads = 320;
+constexpr int kScanEpiWarps = 8;
+constexpr int kScanSmemBudget = 220 * 1024;
+constexpr int kScanMaxStages = 8;
+constexpr uint32_t kScaleOne = 0x7F7F7F7Fu;  // four ue8m0 scale factors = 2^0
 
 struct ScanArgs {
-  int kind;                    // BVSS_SKETCH_BINARY / COUNT_U8
-  const uint4* S;              // DB sketches chunk-major: binary [m/128][n][16B bits], count [m/16][n][16B]
+  const uint4* S;              // DB operand [U][n_stride][16 B] (FP4 expansion or u8 counters)
   const int32_t* massS;        // [n]
   int64_t n, n_stride;
-  const uint4* Qx;             // expanded queries [m/16][qpad][16 B]
+  const uint4* Qx;             // query operand [U][qpad][16 B]
   const int32_t* massQ;        // [nq]
   int nq, qpad;
-  int m;
+  int U;                       // 16-byte K units per row
   void* keys;                  // [nq][key_stride] uint16 (binary) / uint32 (count)
   int64_t key_stride;
   int n_tiles, q_tiles;
@@ -68,14 +78,17 @@ struct ScanArgs {
   int64_t id_base;
 };
 
-template <int KS>
+template <int KS, int N>
 struct ScanCtl {
   uint64_t full[KS];
   uint64_t empty[KS];
   uint64_t tfull[2];
   uint64_t tempty[2];
   uint64_t afull, aempty;
+  uint64_t mfull[2], mempty[2];  // database masses of a tile (producer -> epilogue)
   uint32_t tmem_base;
+  __align__(16) uint32_t mass[2][256];  // FP4: float bits; i8: int
+  uint32_t emit_mask[kScanEpiWarps][4][32];  // emit pass-1 bits [warp][chunk][lane]
 };
 
 __device__ __forceinline__ void bulk_copy(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -95,8 +108,13 @@ __device__ __forceinline__ uint64_t kmajor_desc(uint32_t saddr, uint32_t lbo, ui
   d |= static_cast<uint64_t>(1u) << 46;  // version (sm_100)
   return d;                              // layout type 0 = SWIZZLE_NONE
 }
+// instruction descriptors: kind::i8 (u8 x u8 -> s32) and kind::mxf4 (e2m1 x e2m1, ue8m0 scales -> f32)
 __host__ __device__ __forceinline__ uint32_t idesc_u8_s32(int M, int N) {
   return (2u << 4) | (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
+}
+__host__ __device__ __forceinline__ uint32_t idesc_mxf4(int M, int N) {
+  return (1u << 7) | (1u << 10) | (static_cast<uint32_t>(N >> 3) << 17) | (1u << 23) |
+         (static_cast<uint32_t>(M >> 4) << 24);
 }
 __device__ __forceinline__ void umma_u8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                         uint32_t accumulate) {
@@ -107,14 +125,22 @@ __device__ __forceinline__ void umma_u8(uint32_t d_tmem, uint64_t a_desc, uint64
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-// 16 sketch bits -> 16 bytes of 0/1 (bit b of the half -> byte b, little-endian)
-__device__ __forceinline__ uint4 expand16(uint32_t half16) {
-  uint4 r;
-  r.x = ((half16 & 0xFu) * 0x00204081u) & 0x01010101u;
-  r.y = (((half16 >> 4) & 0xFu) * 0x00204081u) & 0x01010101u;
-  r.z = (((half16 >> 8) & 0xFu) * 0x00204081u) & 0x01010101u;
-  r.w = (((half16 >> 12) & 0xFu) * 0x00204081u) & 0x01010101u;
-  return r;
+__device__ __forceinline__ void umma_fp4(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                         uint32_t accumulate, uint32_t sfa, uint32_t sfb) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb)
+      : "memory");
+}
+// 8 sketch bits -> 8 e2m1 nibbles (bit e -> nibble e: 0x2 = 1.0 or 0x0)
+__host__ __device__ __forceinline__ uint32_t bits8_to_fp4(uint32_t b) {
+  uint32_t x = b & 0xFFu;
+  x = (x | (x << 12)) & 0x000F000Fu;
+  x = (x | (x << 6)) & 0x03030303u;
+  x = (x | (x << 3)) & 0x11111111u;
+  return x << 1;
 }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   tc::tmem_ld16(taddr, *reinterpret_cast<uint32_t(*)[16]>(&r[0]));
@@ -148,29 +174,33 @@ struct RunIter {
   }
 };
 
-template <typename KeyT, bool EMIT, bool RESIDENT, int KS>
+// FP4 = binary sketches (kind::mxf4, N = 240, uint16 keys); else count sketches (kind::i8, N = 256, uint32 keys)
+template <bool FP4, bool EMIT, bool RESIDENT, int KS>
 __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ ScanCtl<KS> S;
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr uint32_t kBStage = kScanN * kScanKB;                    // 16 KB
-  constexpr uint32_t kAStage = RESIDENT ? 0u : kScanM * kScanKB;    // 8 KB streamed A
+  using KeyT = typename std::conditional<FP4, uint16_t, uint32_t>::type;
+  constexpr int N = FP4 ? 240 : 256;
+  constexpr uint32_t kBStage = N * kScanStageB;
+  constexpr uint32_t kAStage = RESIDENT ? 0u : kScanM * kScanStageB;
   constexpr uint32_t kStage = kAStage + kBStage;
-  const uint32_t a_res = smem_u32(base);                                                 // resident A
-  const uint32_t ring = a_res + (RESIDENT ? static_cast<uint32_t>(kScanM) * a.m : 0u);  // stage ring
+  constexpr uint32_t kAcc = FP4 ? 240u : 256u;  // accumulator buffer b at columns [b kAcc, b kAcc + N)
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ ScanCtl<KS, N> S;
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t a_res = smem_u32(base);
+  const uint32_t ring = a_res + (RESIDENT ? static_cast<uint32_t>(kScanM) * a.U * 16u : 0u);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const bool binary = a.kind == BVSS_SKETCH_BINARY;
-  const int KC = a.m / kScanKB;  // stages per tile
+  const int KC = a.U / 8;  // stages per tile
 
   if (tid == 0) {
-    const uint32_t fcount = (binary ? kScanExpWarps : 0) + ((!binary || !RESIDENT) ? 1 : 0);
     for (int s = 0; s < KS; ++s) {
-      tc::mbar_init(&S.full[s], fcount);
+      tc::mbar_init(&S.full[s], 1);
       tc::mbar_init(&S.empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&S.tfull[b], 1);
       tc::mbar_init(&S.tempty[b], kScanEpiWarps);
+      tc::mbar_init(&S.mfull[b], 32);
+      tc::mbar_init(&S.mempty[b], kScanEpiWarps);
     }
     tc::mbar_init(&S.afull, 1);
     tc::mbar_init(&S.aempty, 1);
@@ -181,121 +211,67 @@ __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tmem = S.tmem_base;
+  if (FP4 && warp >= 2 && warp < 6) {  // block scales = 1.0 in columns [480, 512) of every lane
+    const uint32_t taddr = tmem + (static_cast<uint32_t>((warp & 3) * 32) << 16) + 480u;
+#pragma unroll 1
+    for (int c = 0; c < 32; ++c)
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr + c), "r"(kScaleOne) : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
 
   if (warp == 0) {
-    // ------------------------------------------------------------ bulk copies
-    uint32_t sc = 0, uc = 0;
-    const bool per_stage = !binary || !RESIDENT;
+    // ------------------------------------------------------------- producer
+    uint32_t sc = 0, uc = 0, tc_ = 0;
     RunIter it(a);
     ScanRun un;
     for (; it.next(un); ++uc) {
       const int q0 = un.qt * kScanM;
-      if (RESIDENT) {  // the query tile: m/16 units of [128 rows][16 B]
+      if (RESIDENT) {  // the query tile: U units of [128 rows][16 B]
         tc::mbar_wait(&S.aempty, (uc & 1u) ^ 1u);
-        if (lane == 0) arrive_expect_tx(&S.afull, static_cast<uint32_t>(kScanM) * a.m);
+        if (lane == 0) arrive_expect_tx(&S.afull, static_cast<uint32_t>(kScanM) * a.U * 16u);
         __syncwarp();
-        for (int uu = lane; uu < a.m / 16; uu += 32)
+        for (int uu = lane; uu < a.U; uu += 32)
           bulk_copy(a_res + uu * (kScanM * 16u), a.Qx + static_cast<int64_t>(uu) * a.qpad + q0, kScanM * 16u,
                     &S.afull);
       }
-      if (!per_stage) continue;
-      for (int t = un.t0; t < un.t1; ++t) {
-        const int64_t i0 = static_cast<int64_t>(t) * kScanN;
-        const int rows = static_cast<int>(a.n - i0 < kScanN ? a.n - i0 : kScanN);
+      for (int t = un.t0; t < un.t1; ++t, ++tc_) {
+        const int64_t i0 = static_cast<int64_t>(t) * N;
+        const int rows = static_cast<int>(a.n - i0 < N ? a.n - i0 : N);
+        {  // masses of the tile's sets -> smem slot tc_ & 1 (columns past n get a huge mass: never selected)
+          const uint32_t slot = tc_ & 1u;
+          tc::mbar_wait(&S.mempty[slot], ((tc_ >> 1) & 1u) ^ 1u);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int c = lane * 8 + j;
+            const int32_t mv = (c < rows) ? __ldg(a.massS + i0 + c) : 0x40000000;  // huge: never selected
+            S.mass[slot][c] = FP4 ? __float_as_uint(static_cast<float>(mv)) : static_cast<uint32_t>(mv);
+          }
+          tc::mbar_arrive(&S.mfull[slot]);
+        }
         for (int kc = 0; kc < KC; ++kc, ++sc) {
           const int st = sc % KS;
           tc::mbar_wait(&S.empty[st], ((sc / KS) & 1u) ^ 1u);
           const uint32_t sa = ring + st * kStage, sb = sa + kAStage;
-          const uint32_t bytes = kAStage + (binary ? 0u : 4u * rows * 16u);
-          if (lane == 0) arrive_expect_tx(&S.full[st], bytes);
+          if (lane == 0) arrive_expect_tx(&S.full[st], kAStage + 8u * rows * 16u);
           __syncwarp();
-          if (!RESIDENT && lane < 4) {  // A units 4kc .. 4kc+3
-            const int uu = 4 * kc + lane;
-            bulk_copy(sa + lane * (kScanM * 16u), a.Qx + static_cast<int64_t>(uu) * a.qpad + q0, kScanM * 16u,
-                      &S.full[st]);
-          } else if (!binary && lane >= 4 && lane < 8) {  // count-mode DB units
-            const int uu = 4 * kc + (lane - 4);
-            bulk_copy(sb + (lane - 4) * (kScanN * 16u), a.S + static_cast<int64_t>(uu) * a.n_stride + i0,
+          if (lane < 8) {  // DB units 8kc .. 8kc+7
+            const int uu = 8 * kc + lane;
+            bulk_copy(sb + lane * (N * 16u), a.S + static_cast<int64_t>(uu) * a.n_stride + i0,
                       static_cast<uint32_t>(rows) * 16u, &S.full[st]);
+          } else if (!RESIDENT && lane < 16) {  // streamed A units
+            const int uu = 8 * kc + (lane - 8);
+            bulk_copy(sa + (lane - 8) * (kScanM * 16u), a.Qx + static_cast<int64_t>(uu) * a.qpad + q0, kScanM * 16u,
+                      &S.full[st]);
           }
         }
-      }
-    }
-  } else if (warp >= 6) {
-    // ------------------------------------------------- bit expansion (binary)
-    if (binary) {
-      const int r = tid - 192;  // DB row of the tile, 0..255
-      const int RC = a.m / 128;  // raw 128-bit chunks per set
-      const int G = (RC + kScanRawPer - 1) / kScanRawPer;
-      // flat sequence of (run, tile, group) for this CTA; registers hold one group ahead
-      RunIter it(a);
-      ScanRun un{};
-      bool have = it.next(un);
-      int t = have ? un.t0 : 0, g = 0;
-      uint4 cur[kScanRawPer];
-      auto load_group = [&](int tt, int gg, uint4 (&dst)[kScanRawPer]) {
-        const int64_t i = static_cast<int64_t>(tt) * kScanN + r;
-#pragma unroll
-        for (int c = 0; c < kScanRawPer; ++c) {
-          const int rc = gg * kScanRawPer + c;
-          dst[c] = make_uint4(0, 0, 0, 0);
-          if (i < a.n && rc < RC)
-            asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                         : "=r"(dst[c].x), "=r"(dst[c].y), "=r"(dst[c].z), "=r"(dst[c].w)
-                         : "l"(a.S + static_cast<int64_t>(rc) * a.n_stride + i));
-        }
-      };
-      if (have) load_group(t, g, cur);
-      uint32_t sc = 0;
-      while (have) {
-        // next position in the sequence
-        int nt = t, ng = g + 1;
-        ScanRun nun = un;
-        bool nhave = true;
-        if (ng == G) {
-          ng = 0;
-          ++nt;
-          if (nt >= nun.t1) {
-            nhave = it.next(nun);
-            nt = nun.t0;
-          }
-        }
-        uint4 nxt[kScanRawPer];
-        if (nhave) load_group(nt, ng, nxt);
-#pragma unroll
-        for (int c = 0; c < kScanRawPer; ++c) {
-          if (g * kScanRawPer + c < RC) {
-            const uint32_t w4[4] = {cur[c].x, cur[c].y, cur[c].z, cur[c].w};
-#pragma unroll
-            for (int h = 0; h < 2; ++h, ++sc) {  // two 64-byte stages per 128-bit chunk
-              const int st = sc % KS;
-              tc::mbar_wait(&S.empty[st], ((sc / KS) & 1u) ^ 1u);
-              const uint32_t sb = ring + st * kStage + kAStage;
-#pragma unroll
-              for (int uu = 0; uu < 4; ++uu) {
-                const int unit = 4 * h + uu;
-                const uint4 v = expand16((w4[unit >> 1] >> (16 * (unit & 1))) & 0xFFFFu);
-                asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(sb + uu * (kScanN * 16u) + r * 16u),
-                             "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-                             : "memory");
-              }
-              tc::fence_proxy_async_smem();
-              __syncwarp();
-              if (lane == 0) tc::mbar_arrive(&S.full[st]);
-            }
-          }
-        }
-#pragma unroll
-        for (int c = 0; c < kScanRawPer; ++c) cur[c] = nxt[c];
-        t = nt;
-        g = ng;
-        un = nun;
-        have = nhave;
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    const uint32_t idesc = idesc_u8_s32(kScanM, kScanN);
+    const uint32_t idesc = FP4 ? idesc_mxf4(kScanM, N) : idesc_u8_s32(kScanM, N);
     uint32_t sc = 0, tc_ = 0, uc = 0;
     RunIter it(a);
     ScanRun un;
@@ -308,7 +284,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
         const uint32_t acc = tc_ & 1u;
         tc::mbar_wait(&S.tempty[acc], ((tc_ >> 1) & 1u) ^ 1u);
         tc::fence_after_sync();
-        const uint32_t d = tmem + acc * kScanN;
+        const uint32_t d = tmem + acc * kAcc;
         for (int kc = 0; kc < KC; ++kc, ++sc) {
           const int st = sc % KS;
           tc::mbar_wait(&S.full[st], (sc / KS) & 1u);
@@ -316,11 +292,13 @@ __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
           if (lane == 0) {
             const uint32_t sa = ring + st * kStage, sb = sa + kAStage;
 #pragma unroll
-            for (int kk = 0; kk < kScanKB / 32; ++kk) {  // K = 32 bytes = 2 units per instruction
-              const uint64_t ad = RESIDENT ? kmajor_desc(a_res + (4 * kc + 2 * kk) * (kScanM * 16u), kScanM * 16u, 128u)
+            for (int kk = 0; kk < 4; ++kk) {  // 32 bytes of K (2 units) per instruction
+              const uint64_t ad = RESIDENT ? kmajor_desc(a_res + (8 * kc + 2 * kk) * (kScanM * 16u), kScanM * 16u, 128u)
                                            : kmajor_desc(sa + 2 * kk * (kScanM * 16u), kScanM * 16u, 128u);
-              umma_u8(d, ad, kmajor_desc(sb + 2 * kk * (kScanN * 16u), kScanN * 16u, 128u), idesc,
-                      (kc | kk) ? 1u : 0u);
+              const uint64_t bd = kmajor_desc(sb + 2 * kk * (N * 16u), N * 16u, 128u);
+              const uint32_t accum = (kc | kk) ? 1u : 0u;
+              if (FP4) umma_fp4(d, ad, bd, idesc, accum, tmem + 480u, tmem + 496u);
+              else umma_u8(d, ad, bd, idesc, accum);
             }
             tc::umma_commit(&S.empty[st]);
             if (kc == KC - 1) tc::umma_commit(&S.tfull[acc]);
@@ -334,8 +312,10 @@ __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
       }
     }
   } else {
-    // ------------------------------------------------ epilogue (warps 2-5)
-    const int quarter = warp & 3;         // TMEM lane quarter this warp may access
+    // ------------------------------------------------ epilogue (warps 2-9)
+    const int quarter = warp & 3;           // TMEM lane quarter this warp may access
+    const int half = (warp - 2) >> 2;       // columns [cb, ce): [0, 128) or [128, N)
+    const int cb = half * 128, ce = half ? N : 128;
     KeyT* keys = static_cast<KeyT*>(a.keys);
     uint32_t tc_ = 0;
     RunIter it(a);
@@ -344,74 +324,123 @@ __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
       const int q = un.qt * kScanM + quarter * 32 + lane;
       const bool qok = q < a.nq;
       const int32_t pq = qok ? __ldg(a.massQ + q) : 0;
-      // key <= tau  <=>  p_i - 2 acc <= tau - p_Q   (keys are exact, < 2^31)
+      // key <= tau  <=>  p_i - 2 acc <= tau - p_Q   (keys are exact integers < 2^24 (FP4) / 2^31 (i8))
       const int32_t lim = EMIT ? (qok ? static_cast<int32_t>(__ldg(a.tau + q)) - pq : -0x40000000) : 0;
+      const float limf = static_cast<float>(lim);
+      const float pqf = static_cast<float>(pq);
       for (int t = un.t0; t < un.t1; ++t, ++tc_) {
         const uint32_t acc = tc_ & 1u;
-        const int64_t i0 = static_cast<int64_t>(t) * kScanN;
+        const int64_t i0 = static_cast<int64_t>(t) * N;
+        tc::mbar_wait(&S.mfull[acc], (tc_ >> 1) & 1u);
         tc::mbar_wait(&S.tfull[acc], (tc_ >> 1) & 1u);
         tc::fence_after_sync();
-        const uint32_t tbase = tmem + acc * kScanN + (static_cast<uint32_t>(quarter * 32) << 16);
+        const uint32_t tbase = tmem + acc * kAcc + (static_cast<uint32_t>(quarter * 32) << 16);
+        // masses: float (FP4: the accumulator is an exact integer-valued f32) or int (i8: s32 accumulator)
+        auto load_mass = [&](int c0, uint32_t (&pi)[32]) {
+          const uint4* mp = reinterpret_cast<const uint4*>(&S.mass[acc][c0]);  // warp-uniform: broadcast
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint4 t4 = mp[j];
+            pi[4 * j] = t4.x;
+            pi[4 * j + 1] = t4.y;
+            pi[4 * j + 2] = t4.z;
+            pi[4 * j + 3] = t4.w;
+          }
+        };
+        auto load_acc = [&](int c0, uint32_t (&v)[32]) {
+          if (c0 + 32 <= N) {
+            tmem_ld32(tbase + c0, v);
+          } else {  // last chunk of an N = 240 tile: 16 columns (the masses of columns >= N are huge)
+            tc::tmem_ld16(tbase + c0, *reinterpret_cast<uint32_t(*)[16]>(&v[0]));
+#pragma unroll
+            for (int j = 16; j < 32; ++j) v[j] = 0u;
+          }
+        };
+        // p_i - 2 acc (exact) and the pass test against lim
+        auto partial = [&](uint32_t pi, uint32_t v) -> float { return fmaf(-2.0f, __uint_as_float(v), __uint_as_float(pi)); };
+        auto passes = [&](uint32_t pi, uint32_t v) -> bool {
+          if (FP4) return partial(pi, v) <= limf;
+          return static_cast<int32_t>(pi) - 2 * static_cast<int32_t>(v) <= lim;
+        };
+        auto key_of = [&](uint32_t pi, uint32_t v) -> uint32_t {
+          if (FP4) return __float_as_uint(pqf + partial(pi, v) + 8388608.0f) - 0x4B000000u;  // exact int < 2^23
+          return static_cast<uint32_t>(pq + static_cast<int32_t>(pi) - 2 * static_cast<int32_t>(v));
+        };
+        auto release = [&]() {  // this warp's lanes/columns of the accumulator (and the masses) are read
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) {
+            tc::mbar_arrive(&S.tempty[acc]);
+            tc::mbar_arrive(&S.mempty[acc]);
+          }
+        };
+        if (EMIT) {
+          // pass 1: which keys pass (one bit per column), then ONE atomic per thread per tile;
+          // pass 2 re-reads only the chunks where some lane emits and writes those entries
+          uint32_t(*masks)[32] = S.emit_mask[warp - 2];
+          int ne = 0;
 #pragma unroll 1
-        for (int c0 = 0; c0 < kScanN; c0 += 32) {
-          uint32_t v[32];
-          tmem_ld32(tbase + c0, v);
-          const int64_t ic = i0 + c0;
-          int32_t pi[32];
-          if (ic + 32 <= a.n) {
-            const int4* mp = reinterpret_cast<const int4*>(a.massS + ic);
+          for (int c0 = cb; c0 < ce; c0 += 32) {
+            uint32_t v[32], pi[32];
+            load_acc(c0, v);
+            load_mass(c0, pi);
+            tc::tmem_ld_wait();
+            uint32_t mk = 0;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const int4 t4 = __ldg(mp + j);
-              pi[4 * j] = t4.x;
-              pi[4 * j + 1] = t4.y;
-              pi[4 * j + 2] = t4.z;
-              pi[4 * j + 3] = t4.w;
-            }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) pi[j] = ic + j < a.n ? __ldg(a.massS + ic + j) : 0x40000000;
+            for (int j = 0; j < 32; ++j) mk |= (passes(pi[j], v[j]) ? 1u : 0u) << j;
+            masks[(c0 - cb) >> 5][lane] = mk;
+            ne += __popc(mk);
           }
-          tc::tmem_ld_wait();
-          if (c0 + 32 >= kScanN) {  // this warp's lanes of the accumulator are read
-            tc::fence_before_sync();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&S.tempty[acc]);
-          }
-          if (EMIT) {
-            uint32_t mask = 0;
+          int pos = 0;
+          if (ne) pos = atomicAdd(a.cnt + q, ne);
+#pragma unroll 1
+          for (int c0 = cb; c0 < ce; c0 += 32) {
+            const uint32_t mk = masks[(c0 - cb) >> 5][lane];
+            if (__any_sync(0xffffffffu, mk != 0u)) {  // warp-uniform (tcgen05.ld is warp-collective)
+              uint32_t v[32], pi[32];
+              load_acc(c0, v);
+              load_mass(c0, pi);
+              tc::tmem_ld_wait();
+              const int64_t ic = i0 + c0;
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              mask |= (pi[j] - 2 * static_cast<int32_t>(v[j]) <= lim ? 1u : 0u) << j;
-            if (mask) {  // rare: a few keys per thousand
-              const int ne = __popc(mask);
-              const int pos0 = atomicAdd(a.cnt + q, ne);
-              int e = 0;
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {  // unrolled: keeps v[] and pi[] in registers
-                if ((mask >> j) & 1u) {
-                  const int pos = pos0 + e++;
-                  if (pos < a.cap) {
+              for (int j = 0; j < 32; ++j) {  // warp-uniform skip of empty columns: no divergent reconvergence
+                const bool e = (mk >> j) & 1u;
+                if (__ballot_sync(0xffffffffu, e)) {
+                  if (e && pos < a.cap) {
                     const int64_t o = static_cast<int64_t>(q) * a.cap + pos;
                     a.buf_id[o] = static_cast<int32_t>(a.id_base + ic + j);
-                    a.buf_key[o] = static_cast<uint32_t>(pq + pi[j] - 2 * static_cast<int32_t>(v[j]));
+                    a.buf_key[o] = key_of(pi[j], v[j]);
                   }
+                  pos += e ? 1 : 0;
                 }
               }
             }
-          } else if (qok) {
-            KeyT kv[32];
+          }
+          release();
+        } else {
+#pragma unroll 1
+          for (int c0 = cb; c0 < ce; c0 += 32) {
+            uint32_t v[32], pi[32];
+            load_acc(c0, v);
+            load_mass(c0, pi);
+            tc::tmem_ld_wait();
+            if (c0 + 32 >= ce) release();
+            if (qok) {
+              const int64_t ic = i0 + c0;
+              KeyT kv[32];
 #pragma unroll
-            for (int j = 0; j < 32; ++j) kv[j] = static_cast<KeyT>(pq + pi[j] - 2 * static_cast<int32_t>(v[j]));
-            KeyT* row = keys + static_cast<int64_t>(q) * a.key_stride + ic;
-            if (ic + 32 <= a.key_stride) {
-              uint4* dst = reinterpret_cast<uint4*>(row);
-              const uint4* src = reinterpret_cast<const uint4*>(kv);
+              for (int j = 0; j < 32; ++j) kv[j] = static_cast<KeyT>(key_of(pi[j], v[j]));
+              KeyT* row = keys + static_cast<int64_t>(q) * a.key_stride + ic;
+              const int cols = c0 + 32 <= N ? 32 : N - c0;
+              if (cols == 32 && ic + 32 <= a.key_stride) {
+                uint4* dst = reinterpret_cast<uint4*>(row);
+                const uint4* src = reinterpret_cast<const uint4*>(kv);
 #pragma unroll
-              for (int j = 0; j < static_cast<int>(32 * sizeof(KeyT) / 16); ++j) dst[j] = src[j];
-            } else {
-              for (int j = 0; j < 32; ++j)
-                if (ic + j < a.n) row[j] = kv[j];
+                for (int j = 0; j < static_cast<int>(32 * sizeof(KeyT) / 16); ++j) dst[j] = src[j];
+              } else {
+                for (int j = 0; j < cols; ++j)
+                  if (ic + j < a.n) row[j] = kv[j];
+              }
             }
           }
         }
@@ -425,21 +454,19 @@ __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
   }
 }
 
-// queries -> [m/16][qpad][16 B] (binary: bits expanded to 0/1 bytes; count: the uint8 counters)
+// queries -> [U][qpad][16 B]: binary -> FP4 nibbles (32 bits per unit), count -> the uint8 counters (16 per unit)
 __global__ void expand_queries_kernel(int kind, const uint4* __restrict__ SQ /*[nq][cps] row-major chunks*/, int cps,
-                                      int nq, int qpad, int m, uint4* __restrict__ Qx) {
-  const int units = m / 16;
-  const int64_t total = static_cast<int64_t>(units) * qpad;
+                                      int nq, int qpad, int U, uint4* __restrict__ Qx) {
+  const int64_t total = static_cast<int64_t>(U) * qpad;
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int q = static_cast<int>(t % qpad), u = static_cast<int>(t / qpad);
     uint4 out = make_uint4(0, 0, 0, 0);
     if (q < nq) {
       if (kind == BVSS_SKETCH_BINARY) {
-        const uint4 c = SQ[static_cast<int64_t>(q) * cps + (u >> 3)];  // 128-bit chunk holding unit u
-        const uint32_t w4[4] = {c.x, c.y, c.z, c.w};
-        const int uu = u & 7;
-        out = expand16((w4[uu >> 1] >> (16 * (uu & 1))) & 0xFFFFu);
+        const uint32_t* row = reinterpret_cast<const uint32_t*>(SQ + static_cast<int64_t>(q) * cps);
+        const uint32_t w = row[u];  // sketch bits 32u .. 32u + 31
+        out = make_uint4(bits8_to_fp4(w), bits8_to_fp4(w >> 8), bits8_to_fp4(w >> 16), bits8_to_fp4(w >> 24));
       } else {
         out = SQ[static_cast<int64_t>(q) * cps + u];
       }
@@ -448,21 +475,78 @@ __global__ void expand_queries_kernel(int kind, const uint4* __restrict__ SQ /*[
   }
 }
 
-// keys mode: keys != null; emit mode: tau != null (cnt must be zeroed by the caller)
+// binary database sketches, chunk-major [m/128][n_stride][16 B] -> FP4 operand [m/32][n][16 B]
+__global__ void expand_db_fp4_kernel(const uint4* __restrict__ S, int64_t n, int64_t n_stride, int U,
+                                     uint4* __restrict__ X) {
+  const int64_t total = static_cast<int64_t>(U) * n;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = t % n;
+    const int u = static_cast<int>(t / n);
+    const uint32_t* ch = reinterpret_cast<const uint32_t*>(S + static_cast<int64_t>(u >> 2) * n_stride + i);
+    const uint32_t w = ch[u & 3];
+    X[t] = make_uint4(bits8_to_fp4(w), bits8_to_fp4(w >> 8), bits8_to_fp4(w >> 16), bits8_to_fp4(w >> 24));
+  }
+}
+
+// 16-byte K units per row of the tensor-core operand
+int scan_tc_units(int kind, int m) { return kind == BVSS_SKETCH_BINARY ? m / 32 : m / 16; }
+
+int launch_expand_db_fp4(const void* S, int64_t n, int64_t n_stride, int m, void* X, int num_sms, cudaStream_t st) {
+  if (n <= 0) return BVSS_OK;
+  expand_db_fp4_kernel<<<num_sms * 8, 256, 0, st>>>(static_cast<const uint4*>(S), n, n_stride, m / 32,
+                                                    static_cast<uint4*>(X));
+  BVSS_TRY(post_launch(__func__, st));
+  return BVSS_OK;
+}
+
+template <bool FP4, bool EMIT, bool RES, int KS>
+static int launch_one(const ScanArgs& a, size_t smem, int grid, cudaStream_t st) {
+  auto kfn = scan_tc_kernel<FP4, EMIT, RES, KS>;
+  BVSS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  kfn<<<grid, kScanThreads, smem, st>>>(a);
+  return BVSS_OK;
+}
+template <bool FP4, bool EMIT>
+static int launch_res(const ScanArgs& a, bool resident, int ks, size_t smem, int grid, cudaStream_t st) {
+  // stage counts: 4..8 resident, 3..6 streamed (chosen by the smem budget)
+  if (resident) {
+    switch (ks) {
+      case 8: return launch_one<FP4, EMIT, true, 8>(a, smem, grid, st);
+      case 7: return launch_one<FP4, EMIT, true, 7>(a, smem, grid, st);
+      case 6: return launch_one<FP4, EMIT, true, 6>(a, smem, grid, st);
+      case 5: return launch_one<FP4, EMIT, true, 5>(a, smem, grid, st);
+      default: return launch_one<FP4, EMIT, true, 4>(a, smem, grid, st);
+    }
+  }
+  switch (ks) {
+    case 6: return launch_one<FP4, EMIT, false, 6>(a, smem, grid, st);
+    case 5: return launch_one<FP4, EMIT, false, 5>(a, smem, grid, st);
+    case 4: return launch_one<FP4, EMIT, false, 4>(a, smem, grid, st);
+    default: return launch_one<FP4, EMIT, false, 3>(a, smem, grid, st);
+  }
+}
+
+// keys mode: keys != null; emit mode: tau != null (cnt must be zeroed by the caller).
+// S: the DB operand [U][n_stride][16 B]; SQ: query sketches (row-major chunks) expanded into Qx
+// ([U][qpad][16 B], qpad >= ceil(nq/128)*128) unless expand == false (Qx already holds them).
 int launch_scan_tc(int kind, const void* S, const int32_t* mass, int64_t n, int64_t n_stride, int m, const void* SQ,
-                   const int32_t* massQ, int nq, void* Qx /*workspace [m/16][qpad][16]*/, int qpad, void* keys,
-                   int64_t key_stride, int* work_counter, int num_sms, cudaStream_t st, const uint32_t* tau,
-                   int32_t* cnt, int32_t* buf_id, uint32_t* buf_key, int cap, int64_t id_base, bool expand) {
+                   const int32_t* massQ, int nq, void* Qx, int qpad, void* keys, int64_t key_stride, int* work_counter,
+                   int num_sms, cudaStream_t st, const uint32_t* tau, int32_t* cnt, int32_t* buf_id, uint32_t* buf_key,
+                   int cap, int64_t id_base, bool expand) {
+  (void)work_counter;
   if (nq <= 0 || n <= 0) return BVSS_OK;
-  if (m % 128) BVSS_FAIL(BVSS_EUNSUPPORTED, "tensor-core scan needs m %% 128 == 0");
-  const int cps = kind == BVSS_SKETCH_BINARY ? (((m / 32) + 3) / 4) : m / 16;
+  const bool fp4 = kind == BVSS_SKETCH_BINARY;
+  const int U = scan_tc_units(kind, m);
+  if (U % 8) BVSS_FAIL(BVSS_EUNSUPPORTED, "tensor-core scan needs m %% %d == 0", fp4 ? 256 : 128);
+  const int cps = fp4 ? (((m / 32) + 3) / 4) : m / 16;
+  if (qpad < ceil_div(nq, kScanM) * kScanM) BVSS_FAIL(BVSS_EINVAL, "scan: query padding %d too small", qpad);
   if (expand) {
-    expand_queries_kernel<<<num_sms * 4, 256, 0, st>>>(kind, static_cast<const uint4*>(SQ), cps, nq, qpad, m,
+    expand_queries_kernel<<<num_sms * 4, 256, 0, st>>>(kind, static_cast<const uint4*>(SQ), cps, nq, qpad, U,
                                                        static_cast<uint4*>(Qx));
     BVSS_TRY(post_launch("expand_queries_kernel", st));
   }
   ScanArgs a;
-  a.kind = kind;
   a.S = static_cast<const uint4*>(S);
   a.massS = mass;
   a.n = n;
@@ -471,53 +555,44 @@ int launch_scan_tc(int kind, const void* S, const int32_t* mass, int64_t n, int6
   a.massQ = massQ;
   a.nq = nq;
   a.qpad = qpad;
-  a.m = m;
+  a.U = U;
   a.keys = keys;
   a.key_stride = key_stride;
-  a.n_tiles = static_cast<int>(ceil_div<int64_t>(n, kScanN));
+  const int N = fp4 ? 240 : 256;
+  a.n_tiles = static_cast<int>(ceil_div<int64_t>(n, N));
   a.q_tiles = ceil_div(nq, kScanM);
-  if (qpad < a.q_tiles * kScanM) BVSS_FAIL(BVSS_EINVAL, "scan: query padding %d < %d", qpad, a.q_tiles * kScanM);
   a.tau = tau;
   a.cnt = cnt;
   a.buf_id = buf_id;
   a.buf_key = buf_key;
   a.cap = cap;
   a.id_base = id_base;
-  (void)work_counter;
-  constexpr int KS = 6;
-  const bool resident = m <= kScanResidentMaxM;
-  const size_t smem = (resident ? static_cast<size_t>(kScanM) * m + static_cast<size_t>(KS) * kScanN * kScanKB
-                                : static_cast<size_t>(KS) * (kScanM + kScanN) * kScanKB) + 1024;
+  const size_t a_bytes = static_cast<size_t>(kScanM) * U * 16;
+  const size_t b_stage = static_cast<size_t>(N) * kScanStageB;
+  bool resident = a_bytes + 4 * b_stage <= static_cast<size_t>(kScanSmemBudget);
+  int ks;
+  size_t smem;
+  if (resident) {
+    ks = static_cast<int>((kScanSmemBudget - a_bytes) / b_stage);
+    if (ks > kScanMaxStages) ks = kScanMaxStages;
+    smem = a_bytes + ks * b_stage + 1024;
+  } else {
+    const size_t stage = b_stage + static_cast<size_t>(kScanM) * kScanStageB;
+    ks = static_cast<int>(kScanSmemBudget / stage);
+    if (ks > 6) ks = 6;
+    if (ks < 3) BVSS_FAIL(BVSS_EUNSUPPORTED, "scan: stage ring does not fit");
+    smem = ks * stage + 1024;
+  }
   const int64_t work = static_cast<int64_t>(a.n_tiles) * a.q_tiles;
   const int grid = static_cast<int>(work < num_sms ? work : num_sms);
-#define BVSS_SCAN_LAUNCH(KT, EM, RES)                                                                     \
-  do {                                                                                                    \
-    auto kfn = scan_tc_kernel<KT, EM, RES, KS>;                                                           \
-    BVSS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem))); \
-    cudaFuncAttributes fa;                                                                                \
-    BVSS_CUDA(cudaFuncGetAttributes(&fa, kfn));                                                           \
-    if (fa.maxThreadsPerBlock < kScanThreads)                                                             \
-      BVSS_FAIL(BVSS_ECUDA, "scan_tc_kernel: %d regs/thread, %zu B static smem, %zu B local: max %d threads < %d", \
-                fa.numRegs, fa.sharedSizeBytes, fa.localSizeBytes, fa.maxThreadsPerBlock, kScanThreads); \
-    kfn<<<grid, kScanThreads, smem, st>>>(a);                                                             \
-  } while (0)
-#define BVSS_SCAN_LAUNCH2(KT, EM) \
-  do {                            \
-    if (resident)                 \
-      BVSS_SCAN_LAUNCH(KT, EM, true); \
-    else                          \
-      BVSS_SCAN_LAUNCH(KT, EM, false); \
-  } while (0)
   const bool emit = tau != nullptr;
-  if (kind == BVSS_SKETCH_BINARY) {
-    if (emit) BVSS_SCAN_LAUNCH2(uint16_t, true);
-    else BVSS_SCAN_LAUNCH2(uint16_t, false);
+  if (fp4) {
+    if (emit) BVSS_TRY((launch_res<true, true>(a, resident, ks, smem, grid, st)));
+    else BVSS_TRY((launch_res<true, false>(a, resident, ks, smem, grid, st)));
   } else {
-    if (emit) BVSS_SCAN_LAUNCH2(uint32_t, true);
-    else BVSS_SCAN_LAUNCH2(uint32_t, false);
+    if (emit) BVSS_TRY((launch_res<false, true>(a, resident, ks, smem, grid, st)));
+    else BVSS_TRY((launch_res<false, false>(a, resident, ks, smem, grid, st)));
   }
-#undef BVSS_SCAN_LAUNCH2
-#undef BVSS_SCAN_LAUNCH
   BVSS_TRY(post_launch(__func__, st));
   return BVSS_OK;
 }
