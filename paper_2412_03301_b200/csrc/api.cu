@@ -98,7 +98,7 @@ int launch_refine_tc(const __half* hs, const __half* ls, const float* vscale, in
 int launch_topk_fixup(const float* approx, const int32_t* cand, const int32_t* count, int T, int k, const float* V,
                       const int64_t* off, int64_t id_base, int d, const float* Qv, const int64_t* qoff,
                       const float* qnorm, float vmax2, float c1, float c2, int exact_all, int64_t* out_ids,
-                      float* out_dist, int nq, int64_t* fixup_counter, cudaStream_t st);
+                      float* out_dist, int nq, int64_t* fixup_counter, void* scratch, cudaStream_t st);
 int launch_merge_topk(const int64_t* ids, const float* dist, int P, int64_t nq, int k, int64_t* out_ids,
                       float* out_dist, cudaStream_t st);
 
@@ -580,9 +580,11 @@ int refine_topk(bvss_index* idx, bvss_search_ctx* c, int64_t* out_ids_dev, float
   int64_t* fix;
   BVSS_TRY(idx->ws.get("fixup_counter", sizeof(int64_t), reinterpret_cast<void**>(&fix)));
   BVSS_CUDA(cudaMemsetAsync(fix, 0, sizeof(int64_t), idx->stream));
+  void* scratch;
+  BVSS_TRY(idx->ws.get("topk_scratch", static_cast<size_t>(nq) * c->T * 8, &scratch));
   BVSS_TRY(launch_topk_fixup(c->approx, c->cand, c->count, c->T, c->k, idx->V, idx->off, c->id_base, idx->d, c->qv,
                              c->qoff, c->qnorm, idx->vmax2, c1, c2, exact_all, out_ids_dev, out_dist_dev, nq, fix,
-                             idx->stream));
+                             scratch, idx->stream));
   cudaEventRecord(idx->ev[6], idx->stream);
   idx->stats.kernel_launches += 1;
   return BVSS_OK;
@@ -964,8 +966,11 @@ int bvss_refine(bvss_index* idx, const float* queries, const int64_t* query_offs
   }
   float c1, c2;
   error_consts(idx, &c1, &c2);
+  void* scratch;
+  BVSS_TRY(idx->ws.get("topk_scratch", static_cast<size_t>(nq) * T * 8, &scratch));
   BVSS_TRY(launch_topk_fixup(c->approx, c->cand, c->count, T, k, idx->V, idx->off, 0, idx->d, c->qv, c->qoff, c->qnorm,
-                             idx->vmax2, c1, c2, exact_all, oid, odist, static_cast<int>(nq), nullptr, idx->stream));
+                             idx->vmax2, c1, c2, exact_all, oid, odist, static_cast<int>(nq), nullptr, scratch,
+                             idx->stream));
   BVSS_TRY(from_device(idx, out_ids, oid, static_cast<size_t>(nq) * k * 8, dev));
   BVSS_TRY(from_device(idx, out_dist, odist, static_cast<size_t>(nq) * k * 4, dev));
   if (out_approx && c->approx) BVSS_TRY(from_device(idx, out_approx, c->approx, static_cast<size_t>(nq) * T * 4, dev));

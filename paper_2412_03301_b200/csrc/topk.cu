@@ -11,7 +11,7 @@
 // top-k is always inside the window, so the result does not depend on the
 // tensor-core rounding.  With E = +inf (refine_terms = 0) the kernel is a plain
 // SIMT exact refine of every candidate (correctness anchor).
-#include "common.cuh"
+#include "tc.cuh"
 
 namespace bvss {
 
@@ -234,13 +234,342 @@ __global__ void __launch_bounds__(kTopkThreads) topk_fixup_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------
+// K6 v2: the same window rule, with the exact recompute run by the whole CTA on
+// shared-memory tiles.  Per query (one CTA, 256 threads):
+//   1. radix select of the k-th smallest tensor-core H^2 (4 x 8-bit rounds,
+//      smem histogram, warp-parallel digit search) and the window
+//      W = H^2_(k) + 2E; the window's candidate slots go to global scratch;
+//   2. for every window candidate, Def 4 by fp32 direct differences: the query
+//      rows (resident, blocks of RB rows) and the candidate's rows (RB-row
+//      blocks, cp.async staging; two CTAs per SM overlap staging and math) are
+//      tiles in smem; each thread
+//      owns 2 x 2 (query row, set row) pairs over a slice of the d dimensions
+//      (the slices cover d as evenly as the pair count allows), partial sums
+//      meet in smem, and the row / column minima of D^2 are kept with
+//      shared-memory atomicMin on the (non-negative) float bits;
+//   3. the k smallest exact distances by (distance, id).
+constexpr int kTxThreads = 256;
+
+struct TxSmem {
+  uint32_t hist[256];
+  uint32_t rowmin[256];   // min_v D^2 of each query row (kMaxMq)
+  uint32_t colmin[32];    // min_q D^2 of each set row of the current block
+  uint32_t prefix, need, wcount;
+  float hv;
+  unsigned long long best;
+};
+
+__device__ __forceinline__ void stage_rows(float* dst, int stride4, const float* __restrict__ src, int rows, int d,
+                                           int d4) {
+  // rows x d fp32 -> smem rows of stride4 float4 (zero-padded to d4 float4); 16-byte cp.async when d % 4 == 0
+  if ((d & 3) == 0) {
+    const int total = rows * d4;
+    for (int t = threadIdx.x; t < total; t += blockDim.x) {
+      const int r = t / d4, c = t - r * d4;
+      tc::cp_async16(smem_u32(dst + (static_cast<int64_t>(r) * stride4 + c) * 4), src + static_cast<int64_t>(r) * d + 4 * c, 16);
+    }
+  } else {
+    const int total = rows * d4 * 4;
+    for (int t = threadIdx.x; t < total; t += blockDim.x) {
+      const int r = t / (d4 * 4), c = t - r * (d4 * 4);
+      dst[static_cast<int64_t>(r) * stride4 * 4 + c] = c < d ? src[static_cast<int64_t>(r) * d + c] : 0.0f;
+    }
+  }
+  tc::cp_async_commit();
+}
+
+__global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
+    const float* __restrict__ approx, const int32_t* __restrict__ cand, const int32_t* __restrict__ count, int T, int k,
+    const float* __restrict__ V, const int64_t* __restrict__ off, int64_t id_base, int d, int d4, int stride4, int RB,
+    const float* __restrict__ Qv, const int64_t* __restrict__ qoff, const float* __restrict__ qnorm, float vmax2,
+    float c1, float c2, int exact_all, int32_t* __restrict__ win_g, float* __restrict__ ex_g,
+    int64_t* __restrict__ out_ids, float* __restrict__ out_dist, int64_t* __restrict__ fixup_counter) {
+  extern __shared__ __align__(16) float txs[];
+  float* Qs = txs;                                          // [RB][stride4*4]
+  float* Vs0 = Qs + static_cast<int64_t>(RB) * stride4 * 4;   // [RB][stride4*4]
+  float* red = Vs0 + static_cast<int64_t>(RB) * stride4 * 4;  // [kTxThreads][4] partial sums
+  __shared__ TxSmem S;
+  __shared__ float bred[32];
+  const int q = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int cnt = count ? count[q] : T;
+  const int64_t q0 = qoff[q];
+  const int mq = static_cast<int>(qoff[q + 1] - q0);
+  const int kk = min(k, cnt);
+  const float* ap = approx ? approx + static_cast<int64_t>(q) * T : nullptr;
+  const int32_t* cq = cand + static_cast<int64_t>(q) * T;
+  int32_t* win = win_g + static_cast<int64_t>(q) * T;
+  float* ex = ex_g + static_cast<int64_t>(q) * T;
+  if (tid == 0) S.wcount = 0;
+  // ---- 1. window
+  float W = __int_as_float(0x7f800000);
+  if (!exact_all && kk > 0) {
+    float mq2 = 0.0f;
+    for (int i = tid; i < mq; i += blockDim.x) mq2 = fmaxf(mq2, qnorm[q0 + i]);
+    mq2 = block_max_f(mq2, bred);
+    const float E = c1 * sqrtf(mq2) * sqrtf(vmax2) + c2 * (mq2 + vmax2);
+    uint32_t pre = 0u, need = static_cast<uint32_t>(kk);
+    constexpr int kReg = 8;  // candidates held in registers per thread (cnt <= 2048); beyond: re-read
+    uint32_t ur[kReg];
+#pragma unroll
+    for (int e = 0; e < kReg; ++e) {
+      const int i = tid + e * kTxThreads;
+      ur[e] = i < cnt ? __float_as_uint(ap[i]) : 0xFFFFFFFFu;
+    }
+    for (int rnd = 0; rnd < 4; ++rnd) {  // radix select of the kk-th smallest (uint order of floats >= 0)
+      const int shift = 24 - 8 * rnd;
+      S.hist[tid] = 0u;
+      __syncthreads();
+#pragma unroll
+      for (int e = 0; e < kReg; ++e) {
+        const uint32_t u = ur[e];
+        if (tid + e * kTxThreads < cnt && (rnd == 0 || (u >> (shift + 8)) == pre))
+          atomicAdd(&S.hist[(u >> shift) & 255u], 1u);
+      }
+      for (int i = tid + kReg * kTxThreads; i < cnt; i += blockDim.x) {
+        const uint32_t u = __float_as_uint(ap[i]);
+        if (rnd == 0 || (u >> (shift + 8)) == pre) atomicAdd(&S.hist[(u >> shift) & 255u], 1u);
+      }
+      __syncthreads();
+      if (warp == 0) {  // lane l owns bins 8l .. 8l+7
+        uint32_t h[8], sum = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) {
+          h[b] = S.hist[8 * lane + b];
+          sum += h[b];
+        }
+        uint32_t incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += t;
+        }
+        const uint32_t excl = incl - sum;
+        const unsigned hit = __ballot_sync(0xffffffffu, incl >= need && excl < need);
+        const int owner = __ffs(hit) - 1;
+        if (lane == owner) {
+          uint32_t run = excl;
+          int dsel = 8 * lane + 7;
+#pragma unroll
+          for (int b = 0; b < 8; ++b) {
+            if (run + h[b] >= need) {
+              dsel = 8 * lane + b;
+              break;
+            }
+            run += h[b];
+          }
+          S.prefix = (pre << 8) | static_cast<uint32_t>(dsel);
+          S.need = need - run;
+        }
+      }
+      __syncthreads();
+      pre = S.prefix;
+      need = S.need;
+    }
+    W = (__uint_as_float(pre) + 2.0f * E) * (1.0f + 1e-6f);
+  }
+  __syncthreads();
+  if (exact_all) {
+    for (int i = tid; i < cnt; i += blockDim.x) win[i] = i;
+    if (tid == 0) S.wcount = cnt;
+  } else {
+    for (int i = tid; i < cnt; i += blockDim.x)
+      if (ap[i] <= W) win[atomicAdd(&S.wcount, 1u)] = i;
+  }
+  __syncthreads();
+  const int nw = static_cast<int>(S.wcount);
+  if (tid == 0 && fixup_counter) atomicAdd(reinterpret_cast<unsigned long long*>(fixup_counter), nw);
+  // ---- 2. exact H^2 of every window candidate
+  const int nqb = (mq + RB - 1) / RB;
+  const int rowsq0 = min(RB, mq);
+  if (nqb == 1) stage_rows(Qs, stride4, Qv + q0 * d, rowsq0, d, d4);
+  for (int i = tid; i < mq; i += blockDim.x) S.rowmin[i] = 0x7f800000u;
+  if (tid < 32) S.colmin[tid] = 0x7f800000u;
+  if (tid == 0) S.hv = 0.0f;
+  // job sequence: (window entry w, set-row block vb); the next job's rows are staged while this one computes
+  auto job_rows = [&](int w, int vb, const float** src, int* rows) {
+    const int64_t cid = static_cast<int64_t>(cq[win[w]]) - id_base;
+    const int64_t v0 = off[cid];
+    const int mi = static_cast<int>(off[cid + 1] - v0);
+    *src = V + (v0 + static_cast<int64_t>(vb) * RB) * d;
+    *rows = min(RB, mi - vb * RB);
+    return mi;
+  };
+  int w = 0, vb = 0;
+  while (w < nw) {
+    const float* src;
+    int rowsv;
+    const int mi = job_rows(w, vb, &src, &rowsv);
+    int nw_ = w, nvb = vb + 1;  // next job
+    if (nvb * RB >= mi) {
+      nw_ = w + 1;
+      nvb = 0;
+    }
+    stage_rows(Vs0, stride4, src, rowsv, d, d4);  // (two CTAs per SM overlap one's staging with the other's math)
+    tc::cp_async_wait<0>();
+    __syncthreads();
+    const float* Vb = Vs0;
+    for (int qb = 0; qb < nqb; ++qb) {
+      const int rowsq = min(RB, mq - qb * RB);
+      if (nqb > 1) {  // query blocks restaged per (candidate block, query block): only for m_q > RB
+        __syncthreads();
+        stage_rows(Qs, stride4, Qv + (q0 + static_cast<int64_t>(qb) * RB) * d, rowsq, d, d4);
+        tc::cp_async_wait<0>();
+        __syncthreads();
+      }
+      const int ti_n = (rowsq + 1) >> 1, tj_n = (rowsv + 1) >> 1;
+      const int ntile = ti_n * tj_n;
+      const int dsplit = max(1, min(kTxThreads / ntile, d4));
+      const int tile = tid % ntile, split = tid / ntile;
+      float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      if (split < dsplit) {
+        const int i0 = (tile / tj_n) * 2, j0 = (tile % tj_n) * 2;
+        const int i1 = min(i0 + 1, rowsq - 1), j1 = min(j0 + 1, rowsv - 1);
+        const float4* qa = reinterpret_cast<const float4*>(Qs) + i0 * stride4;
+        const float4* qb4 = reinterpret_cast<const float4*>(Qs) + i1 * stride4;
+        const float4* va = reinterpret_cast<const float4*>(Vb) + j0 * stride4;
+        const float4* vb4 = reinterpret_cast<const float4*>(Vb) + j1 * stride4;
+        const int kb = split * d4 / dsplit, ke = (split + 1) * d4 / dsplit;
+        for (int c = kb; c < ke; ++c) {
+          const float4 x0 = qa[c], x1 = qb4[c], y0 = va[c], y1 = vb4[c];
+#define BVSS_DD(A, X, Y)                                  \
+  {                                                       \
+    float t_ = X.x - Y.x;                                 \
+    A = __fmaf_rn(t_, t_, A);                             \
+    t_ = X.y - Y.y;                                       \
+    A = __fmaf_rn(t_, t_, A);                             \
+    t_ = X.z - Y.z;                                       \
+    A = __fmaf_rn(t_, t_, A);                             \
+    t_ = X.w - Y.w;                                       \
+    A = __fmaf_rn(t_, t_, A);                             \
+  }
+          BVSS_DD(acc[0], x0, y0)
+          BVSS_DD(acc[1], x0, y1)
+          BVSS_DD(acc[2], x1, y0)
+          BVSS_DD(acc[3], x1, y1)
+#undef BVSS_DD
+        }
+      }
+      if (dsplit > 1) {
+        reinterpret_cast<float4*>(red)[tid] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        __syncthreads();
+        if (tid < ntile) {
+          for (int sp = 1; sp < dsplit; ++sp) {
+            const float4 r = reinterpret_cast<const float4*>(red)[sp * ntile + tid];
+            acc[0] += r.x;
+            acc[1] += r.y;
+            acc[2] += r.z;
+            acc[3] += r.w;
+          }
+        }
+      }
+      if (tid < ntile) {
+        const int i0 = (tid / tj_n) * 2, j0 = (tid % tj_n) * 2;
+        const bool iv1 = i0 + 1 < rowsq, jv1 = j0 + 1 < rowsv;
+        const float r0 = fminf(acc[0], jv1 ? acc[1] : acc[0]);
+        atomicMin(&S.rowmin[qb * RB + i0], __float_as_uint(r0));
+        if (iv1) atomicMin(&S.rowmin[qb * RB + i0 + 1], __float_as_uint(fminf(acc[2], jv1 ? acc[3] : acc[2])));
+        atomicMin(&S.colmin[j0], __float_as_uint(fminf(acc[0], iv1 ? acc[2] : acc[0])));
+        if (jv1) atomicMin(&S.colmin[j0 + 1], __float_as_uint(fminf(acc[1], iv1 ? acc[3] : acc[1])));
+      }
+      __syncthreads();
+    }
+    // fold this set-row block: H_v part = max over its rows of the column minima
+    if (warp == 0) {
+      float cm = lane < rowsv ? __uint_as_float(S.colmin[lane]) : 0.0f;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) cm = fmaxf(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+      S.colmin[lane] = 0x7f800000u;
+      if (lane == 0) S.hv = fmaxf(S.hv, cm);
+    }
+    if (nw_ != w) {  // candidate done: H^2 = max(max_q min_v D^2, max_v min_q D^2)
+      __syncthreads();
+      float hq = 0.0f;
+      for (int i = tid; i < mq; i += blockDim.x) {
+        hq = fmaxf(hq, __uint_as_float(S.rowmin[i]));
+        S.rowmin[i] = 0x7f800000u;
+      }
+      hq = block_max_f(hq, bred);
+      if (tid == 0) {
+        ex[w] = fmaxf(hq, S.hv);
+        S.hv = 0.0f;
+      }
+    }
+    __syncthreads();
+    w = nw_;
+    vb = nvb;
+  }
+  __syncthreads();
+  // ---- 3. the k smallest by (exact H^2, id)
+  for (int r = 0; r < k; ++r) {
+    unsigned long long best = ~0ull;
+    for (int x = tid; x < nw; x += blockDim.x) {
+      const float e = ex[x];
+      if (e < 0.0f) continue;  // taken
+      const uint32_t gid = static_cast<uint32_t>(cq[win[x]]);
+      const unsigned long long key = (static_cast<unsigned long long>(__float_as_uint(e)) << 32) | gid;
+      best = key < best ? key : best;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
+      best = t < best ? t : best;
+    }
+    if (tid == 0) S.best = ~0ull;
+    __syncthreads();
+    if (lane == 0) atomicMin(&S.best, best);
+    __syncthreads();
+    const unsigned long long b = S.best;
+    if (tid == 0) {
+      int64_t* oi = out_ids + static_cast<int64_t>(q) * k;
+      float* od = out_dist + static_cast<int64_t>(q) * k;
+      if (b == ~0ull) {
+        oi[r] = -1;
+        od[r] = __int_as_float(0x7f800000);
+      } else {
+        oi[r] = static_cast<int64_t>(static_cast<uint32_t>(b & 0xffffffffull));
+        od[r] = sqrtf(__uint_as_float(static_cast<uint32_t>(b >> 32)));
+      }
+    }
+    if (b != ~0ull) {  // mark the winner as taken
+      const uint32_t gid = static_cast<uint32_t>(b & 0xffffffffull);
+      for (int x = tid; x < nw; x += blockDim.x)
+        if (static_cast<uint32_t>(cq[win[x]]) == gid) ex[x] = -1.0f;
+    }
+    __syncthreads();
+  }
+}
+
 size_t topk_smem_bytes(int T) { return static_cast<size_t>(T) * 12; }
+
+// shared memory of topk_exact_kernel for row blocks of RB rows
+static size_t tx_smem(int stride4, int RB) {
+  return (2 * static_cast<size_t>(RB) * stride4 + kTxThreads) * 16;
+}
 
 int launch_topk_fixup(const float* approx, const int32_t* cand, const int32_t* count, int T, int k, const float* V,
                       const int64_t* off, int64_t id_base, int d, const float* Qv, const int64_t* qoff,
                       const float* qnorm, float vmax2, float c1, float c2, int exact_all, int64_t* out_ids,
-                      float* out_dist, int nq, int64_t* fixup_counter, cudaStream_t st) {
+                      float* out_dist, int nq, int64_t* fixup_counter, void* scratch /*[nq][T] x 8 B*/, cudaStream_t st) {
   if (nq <= 0) return BVSS_OK;
+  if (k > T) BVSS_FAIL(BVSS_EINVAL, "k > T");
+  const int d4 = (d + 3) / 4;
+  const int stride4 = (d4 & 1) ? d4 + 2 : d4 + 1;  // odd stride in float4: conflict-free row-parallel reads
+  int RB = 32;
+  while (RB > 4 && tx_smem(stride4, RB) > 110 * 1024) RB >>= 1;  // two CTAs per SM
+  if (scratch && tx_smem(stride4, RB) <= 110 * 1024) {
+    const size_t smem = tx_smem(stride4, RB);
+    int32_t* win = static_cast<int32_t*>(scratch);
+    float* ex = reinterpret_cast<float*>(win + static_cast<int64_t>(nq) * T);
+    BVSS_CUDA(cudaFuncSetAttribute(topk_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    topk_exact_kernel<<<nq, kTxThreads, smem, st>>>(approx, cand, count, T, k, V, off, id_base, d, d4, stride4, RB, Qv,
+                                                    qoff, qnorm, vmax2, c1, c2, exact_all, win, ex, out_ids, out_dist,
+                                                    fixup_counter);
+    BVSS_TRY(post_launch("topk_exact_kernel", st));
+    return BVSS_OK;
+  }
+  // very wide vectors: the warp-per-candidate kernel (global-memory operands)
   const size_t smem = topk_smem_bytes(T);
   if (smem > 190 * 1024) BVSS_FAIL(BVSS_EUNSUPPORTED, "T=%d exceeds the top-k kernel limit (16384)", T);
   if (d % 4 == 0) {
