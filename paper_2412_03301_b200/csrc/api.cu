@@ -556,6 +556,56 @@ int emit_candidates(bvss_index* idx, bvss_search_ctx* c) {
   return BVSS_OK;
 }
 
+// Full-key candidate selection for a prepared batch, in sub-batches whose key rows fit 4 GB: the
+// fallback of the sampled-threshold path (same result, more memory traffic).
+int fallback_full(bvss_index* idx, bvss_search_ctx* c) {
+  const int nq = static_cast<int>(c->nq);
+  const int64_t n = idx->n;
+  const int key_size = idx->sketch == BVSS_SKETCH_BINARY ? 2 : 4;
+  const int64_t key_stride = (n + 7) & ~int64_t(7);
+  int64_t sub = static_cast<int64_t>((4.0 * (1ull << 30)) / (static_cast<double>(key_stride) * key_size));
+  if (sub < 1) sub = 1;
+  if (sub > nq) sub = nq;
+  void* keys;
+  BVSS_TRY(idx->ws.get("keys", static_cast<size_t>(sub) * key_stride * key_size, &keys));
+  BVSS_TRY(alloc_select_state(idx, c));
+  BVSS_TRY(c->alloc(static_cast<size_t>(nq) * c->T * sizeof(int32_t), reinterpret_cast<void**>(&c->cand)));
+  BVSS_TRY(c->alloc(nq * sizeof(int32_t), reinterpret_cast<void**>(&c->count)));
+  BVSS_TRY(expand_alloc(idx, c));
+  int* wc;
+  BVSS_TRY(idx->ws.get("scan_counter", sizeof(int), reinterpret_cast<void**>(&wc)));
+  const int cps = chunks_per_set(idx);
+  for (int q0 = 0; q0 < nq; q0 += static_cast<int>(sub)) {
+    const int ns = static_cast<int>(q0 + sub <= nq ? sub : nq - q0);
+    const void* sq = static_cast<const uint8_t*>(c->qsk) + static_cast<size_t>(q0) * cps * 16;
+    if (use_tc_scan(idx)) {
+      BVSS_TRY(launch_scan_tc(idx->sketch, scan_operand(idx, false), idx->mass, n, n, idx->m, sq, c->qmass + q0, ns,
+                              c->qx, c->qpad, keys, key_stride, wc, idx->num_sms, idx->stream, nullptr, nullptr,
+                              nullptr, nullptr, 0, 0, true));
+    } else {
+      BVSS_TRY(launch_scan(idx->sketch, idx->sk, idx->mass, n, n, idx->m, sq, c->qmass + q0, ns, keys, key_stride,
+                           idx->num_sms, idx->stream));
+    }
+    SelectState s2 = c->sel;
+    s2.prefix += q0;
+    s2.below += q0;
+    s2.teff += q0;
+    s2.eq += q0;
+    s2.quota += q0;
+    s2.digit += q0;
+    BVSS_TRY(launch_select_init(s2, ns, c->teff, idx->stream));
+    for (int r = 0; r < c->rounds; ++r) {
+      BVSS_TRY(launch_select_hist(key_size, keys, key_stride, n, ns, s2, c->key_bits, r, c->local_hist, idx->stream));
+      BVSS_TRY(launch_select_resolve(c->local_hist, s2, ns, c->key_bits, r, idx->stream));
+    }
+    BVSS_TRY(launch_select_emit(key_size, keys, key_stride, n, ns, s2, c->T, c->id_base,
+                                c->cand + static_cast<int64_t>(q0) * c->T, nullptr, c->count + q0, idx->stream));
+    idx->stats.kernel_launches += 4 + 2 * c->rounds;
+  }
+  cudaEventRecord(idx->ev[4], idx->stream);
+  return BVSS_OK;
+}
+
 // refine + top-k over c->cand / c->count
 int refine_topk(bvss_index* idx, bvss_search_ctx* c, int64_t* out_ids_dev, float* out_dist_dev) {
   const int nq = static_cast<int>(c->nq);
@@ -630,8 +680,12 @@ int validate_search(bvss_index* idx, const float* q, const int64_t* qo, int64_t 
   return BVSS_OK;
 }
 
+bool sampled_select_eligible(const bvss_index* idx);
+
 int64_t batch_size(const bvss_index* idx, int64_t nq) {
   if (idx->query_batch) return idx->query_batch < nq ? idx->query_batch : nq;
+  // sampled-threshold selection needs no key rows (its fallback runs in sub-batches): large batches
+  if (sampled_select_eligible(idx)) return nq < 16384 ? nq : 16384;
   const int key_size = idx->sketch == BVSS_SKETCH_BINARY ? 2 : 4;
   const double per_q = static_cast<double>((idx->n + 7) & ~int64_t(7)) * key_size;
   int64_t b = static_cast<int64_t>((4.0 * (1ull << 30)) / per_q);
@@ -1018,9 +1072,12 @@ int bvss_search(bvss_index* idx, const float* queries, const int64_t* query_offs
     bool ok = false;
     if (sampled) BVSS_TRY(select_sampled(idx, c.get(), &ok));
     if (!ok) {
-      if (sampled) BVSS_TRY(scan_batch(idx, c.get()));
-      BVSS_TRY(run_select_single(idx, c.get()));
-      BVSS_TRY(emit_candidates(idx, c.get()));
+      if (sampled) {
+        BVSS_TRY(fallback_full(idx, c.get()));
+      } else {
+        BVSS_TRY(run_select_single(idx, c.get()));
+        BVSS_TRY(emit_candidates(idx, c.get()));
+      }
     }
     const double t_sel = now_us();
     BVSS_TRY(refine_topk(idx, c.get(), oid, odist));

@@ -147,47 +147,55 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   tc::tmem_ld16(taddr + 16, *reinterpret_cast<uint32_t(*)[16]>(&r[16]));
 }
 
-// Work split: the (query tile, database tile) pairs, ordered query-tile-major,
-// are cut into gridDim.x equal contiguous ranges, one per CTA (exact balance;
-// a CTA changes query tile at most a few times).  A "run" is the part of a
-// CTA's range inside one query tile: database tiles [t0, t1) of query tile qt.
-struct ScanRun {
-  int qt, t0, t1;
-};
-struct RunIter {
-  int64_t f, f1;
-  int NT;
-  __device__ RunIter(const ScanArgs& a) {
+// Work split: the (query tile, database tile) pairs are ordered by the
+// STATIONARY operand -- query-tile-major when the query tile stays in smem
+// (MODE_ARES / MODE_STREAM), database-tile-major when the database tile does
+// (MODE_BRES) -- and cut into gridDim.x equal contiguous ranges, one per CTA
+// (exact balance).  A "run" is a maximal stretch of a CTA's range with the same
+// stationary tile; the stationary operand is loaded once per run.
+enum { MODE_ARES = 0, MODE_STREAM = 1, MODE_BRES = 2 };
+
+struct TileSeq {
+  int64_t f, f0, f1;
+  int inner;
+  bool dbmajor;
+  __device__ TileSeq(const ScanArgs& a, bool db_major) {
     const int64_t W = static_cast<int64_t>(a.q_tiles) * a.n_tiles;
-    f = W * blockIdx.x / gridDim.x;
+    f0 = f = W * blockIdx.x / gridDim.x;
     f1 = W * (blockIdx.x + 1) / gridDim.x;
-    NT = a.n_tiles;
+    inner = db_major ? a.q_tiles : a.n_tiles;
+    dbmajor = db_major;
   }
-  __device__ bool next(ScanRun& r) {
+  // next tile (qt, t); first / last = first / last tile of its run
+  __device__ bool next(int& qt, int& t, bool& first, bool& last) {
     if (f >= f1) return false;
-    r.qt = static_cast<int>(f / NT);
-    r.t0 = static_cast<int>(f - static_cast<int64_t>(r.qt) * NT);
-    const int64_t left = f1 - f;
-    r.t1 = static_cast<int>(left < NT - r.t0 ? r.t0 + left : NT);
-    f += r.t1 - r.t0;
+    const int64_t key = f / inner;
+    const int pos = static_cast<int>(f - key * inner);
+    qt = dbmajor ? pos : static_cast<int>(key);
+    t = dbmajor ? static_cast<int>(key) : pos;
+    first = pos == 0 || f == f0;
+    ++f;
+    last = f >= f1 || (f % inner) == 0;
     return true;
   }
 };
 
 // FP4 = binary sketches (kind::mxf4, N = 240, uint16 keys); else count sketches (kind::i8, N = 256, uint32 keys)
-template <bool FP4, bool EMIT, bool RESIDENT, int KS>
+template <bool FP4, bool EMIT, int MODE, int KS>
 __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
   using KeyT = typename std::conditional<FP4, uint16_t, uint32_t>::type;
   constexpr int N = FP4 ? 240 : 256;
-  constexpr uint32_t kBStage = N * kScanStageB;
-  constexpr uint32_t kAStage = RESIDENT ? 0u : kScanM * kScanStageB;
+  constexpr bool ARES = MODE == MODE_ARES, BRES = MODE == MODE_BRES;
+  constexpr uint32_t kBStage = BRES ? 0u : N * kScanStageB;
+  constexpr uint32_t kAStage = ARES ? 0u : kScanM * kScanStageB;
   constexpr uint32_t kStage = kAStage + kBStage;
   constexpr uint32_t kAcc = FP4 ? 240u : 256u;  // accumulator buffer b at columns [b kAcc, b kAcc + N)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ ScanCtl<KS, N> S;
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t a_res = smem_u32(base);
-  const uint32_t ring = a_res + (RESIDENT ? static_cast<uint32_t>(kScanM) * a.U * 16u : 0u);
+  const uint32_t res = smem_u32(base);  // the resident (stationary) tile
+  const uint32_t ring =
+      res + (ARES ? static_cast<uint32_t>(kScanM) * a.U * 16u : (BRES ? static_cast<uint32_t>(N) * a.U * 16u : 0u));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int KC = a.U / 8;  // stages per tile
 
@@ -224,92 +232,100 @@ __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
 
   if (warp == 0) {
     // ------------------------------------------------------------- producer
-    uint32_t sc = 0, uc = 0, tc_ = 0;
-    RunIter it(a);
-    ScanRun un;
-    for (; it.next(un); ++uc) {
-      const int q0 = un.qt * kScanM;
-      if (RESIDENT) {  // the query tile: U units of [128 rows][16 B]
-        tc::mbar_wait(&S.aempty, (uc & 1u) ^ 1u);
-        if (lane == 0) arrive_expect_tx(&S.afull, static_cast<uint32_t>(kScanM) * a.U * 16u);
+    uint32_t sc = 0, rc = 0, tc_ = 0;
+    TileSeq seq(a, BRES);
+    int qt, t;
+    bool first, last;
+    while (seq.next(qt, t, first, last)) {
+      const int q0 = qt * kScanM;
+      const int64_t i0 = static_cast<int64_t>(t) * N;
+      const int rows = static_cast<int>(a.n - i0 < N ? a.n - i0 : N);
+      if (first && !(MODE == MODE_STREAM)) {  // the stationary tile of this run: U units of [rows][16 B]
+        tc::mbar_wait(&S.aempty, (rc & 1u) ^ 1u);
+        const uint32_t rrows = ARES ? kScanM : N;
+        if (lane == 0) arrive_expect_tx(&S.afull, (ARES ? kScanM : rows) * a.U * 16u);
         __syncwarp();
-        for (int uu = lane; uu < a.U; uu += 32)
-          bulk_copy(a_res + uu * (kScanM * 16u), a.Qx + static_cast<int64_t>(uu) * a.qpad + q0, kScanM * 16u,
-                    &S.afull);
+        for (int uu = lane; uu < a.U; uu += 32) {
+          if (ARES)
+            bulk_copy(res + uu * (rrows * 16u), a.Qx + static_cast<int64_t>(uu) * a.qpad + q0, kScanM * 16u, &S.afull);
+          else
+            bulk_copy(res + uu * (rrows * 16u), a.S + static_cast<int64_t>(uu) * a.n_stride + i0,
+                      static_cast<uint32_t>(rows) * 16u, &S.afull);
+        }
+        ++rc;
       }
-      for (int t = un.t0; t < un.t1; ++t, ++tc_) {
-        const int64_t i0 = static_cast<int64_t>(t) * N;
-        const int rows = static_cast<int>(a.n - i0 < N ? a.n - i0 : N);
-        {  // masses of the tile's sets -> smem slot tc_ & 1 (columns past n get a huge mass: never selected)
-          const uint32_t slot = tc_ & 1u;
-          tc::mbar_wait(&S.mempty[slot], ((tc_ >> 1) & 1u) ^ 1u);
+      {  // masses of the tile's sets -> smem slot tc_ & 1 (columns past n get a huge mass: never selected)
+        const uint32_t slot = tc_ & 1u;
+        tc::mbar_wait(&S.mempty[slot], ((tc_ >> 1) & 1u) ^ 1u);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int c = lane * 8 + j;
-            const int32_t mv = (c < rows) ? __ldg(a.massS + i0 + c) : 0x40000000;  // huge: never selected
-            S.mass[slot][c] = FP4 ? __float_as_uint(static_cast<float>(mv)) : static_cast<uint32_t>(mv);
-          }
-          tc::mbar_arrive(&S.mfull[slot]);
+        for (int j = 0; j < 8; ++j) {
+          const int c = lane * 8 + j;
+          const int32_t mv = (c < rows) ? __ldg(a.massS + i0 + c) : 0x40000000;  // huge: never selected
+          S.mass[slot][c] = FP4 ? __float_as_uint(static_cast<float>(mv)) : static_cast<uint32_t>(mv);
         }
-        for (int kc = 0; kc < KC; ++kc, ++sc) {
-          const int st = sc % KS;
-          tc::mbar_wait(&S.empty[st], ((sc / KS) & 1u) ^ 1u);
-          const uint32_t sa = ring + st * kStage, sb = sa + kAStage;
-          if (lane == 0) arrive_expect_tx(&S.full[st], kAStage + 8u * rows * 16u);
-          __syncwarp();
-          if (lane < 8) {  // DB units 8kc .. 8kc+7
-            const int uu = 8 * kc + lane;
-            bulk_copy(sb + lane * (N * 16u), a.S + static_cast<int64_t>(uu) * a.n_stride + i0,
-                      static_cast<uint32_t>(rows) * 16u, &S.full[st]);
-          } else if (!RESIDENT && lane < 16) {  // streamed A units
-            const int uu = 8 * kc + (lane - 8);
-            bulk_copy(sa + (lane - 8) * (kScanM * 16u), a.Qx + static_cast<int64_t>(uu) * a.qpad + q0, kScanM * 16u,
-                      &S.full[st]);
-          }
+        tc::mbar_arrive(&S.mfull[slot]);
+      }
+      for (int kc = 0; kc < KC; ++kc, ++sc) {
+        const int st = sc % KS;
+        tc::mbar_wait(&S.empty[st], ((sc / KS) & 1u) ^ 1u);
+        const uint32_t sa = ring + st * kStage, sb = sa + kAStage;
+        if (lane == 0) arrive_expect_tx(&S.full[st], kAStage + (BRES ? 0u : 8u * rows * 16u));
+        __syncwarp();
+        if (!BRES && lane < 8) {  // DB units 8kc .. 8kc+7
+          const int uu = 8 * kc + lane;
+          bulk_copy(sb + lane * (N * 16u), a.S + static_cast<int64_t>(uu) * a.n_stride + i0,
+                    static_cast<uint32_t>(rows) * 16u, &S.full[st]);
+        } else if (!ARES && lane >= 8 && lane < 16) {  // streamed A units
+          const int uu = 8 * kc + (lane - 8);
+          bulk_copy(sa + (lane - 8) * (kScanM * 16u), a.Qx + static_cast<int64_t>(uu) * a.qpad + q0, kScanM * 16u,
+                    &S.full[st]);
         }
       }
+      ++tc_;
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     const uint32_t idesc = FP4 ? idesc_mxf4(kScanM, N) : idesc_u8_s32(kScanM, N);
-    uint32_t sc = 0, tc_ = 0, uc = 0;
-    RunIter it(a);
-    ScanRun un;
-    for (; it.next(un); ++uc) {
-      if (RESIDENT) {
-        tc::mbar_wait(&S.afull, uc & 1u);
+    uint32_t sc = 0, tc_ = 0, rc = 0;
+    TileSeq seq(a, BRES);
+    int qt, t;
+    bool first, last;
+    while (seq.next(qt, t, first, last)) {
+      if (first && MODE != MODE_STREAM) {
+        tc::mbar_wait(&S.afull, rc & 1u);
         tc::fence_after_sync();
       }
-      for (int t = un.t0; t < un.t1; ++t, ++tc_) {
-        const uint32_t acc = tc_ & 1u;
-        tc::mbar_wait(&S.tempty[acc], ((tc_ >> 1) & 1u) ^ 1u);
+      const uint32_t acc = tc_ & 1u;
+      tc::mbar_wait(&S.tempty[acc], ((tc_ >> 1) & 1u) ^ 1u);
+      tc::fence_after_sync();
+      const uint32_t d = tmem + acc * kAcc;
+      for (int kc = 0; kc < KC; ++kc, ++sc) {
+        const int st = sc % KS;
+        tc::mbar_wait(&S.full[st], (sc / KS) & 1u);
         tc::fence_after_sync();
-        const uint32_t d = tmem + acc * kAcc;
-        for (int kc = 0; kc < KC; ++kc, ++sc) {
-          const int st = sc % KS;
-          tc::mbar_wait(&S.full[st], (sc / KS) & 1u);
-          tc::fence_after_sync();
-          if (lane == 0) {
-            const uint32_t sa = ring + st * kStage, sb = sa + kAStage;
+        if (lane == 0) {
+          const uint32_t sa = ring + st * kStage, sb = sa + kAStage;
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {  // 32 bytes of K (2 units) per instruction
-              const uint64_t ad = RESIDENT ? kmajor_desc(a_res + (8 * kc + 2 * kk) * (kScanM * 16u), kScanM * 16u, 128u)
-                                           : kmajor_desc(sa + 2 * kk * (kScanM * 16u), kScanM * 16u, 128u);
-              const uint64_t bd = kmajor_desc(sb + 2 * kk * (N * 16u), N * 16u, 128u);
-              const uint32_t accum = (kc | kk) ? 1u : 0u;
-              if (FP4) umma_fp4(d, ad, bd, idesc, accum, tmem + 480u, tmem + 496u);
-              else umma_u8(d, ad, bd, idesc, accum);
-            }
-            tc::umma_commit(&S.empty[st]);
-            if (kc == KC - 1) tc::umma_commit(&S.tfull[acc]);
+          for (int kk = 0; kk < 4; ++kk) {  // 32 bytes of K (2 units) per instruction
+            const uint32_t u = 8 * kc + 2 * kk;
+            const uint64_t ad = ARES ? kmajor_desc(res + u * (kScanM * 16u), kScanM * 16u, 128u)
+                                     : kmajor_desc(sa + 2 * kk * (kScanM * 16u), kScanM * 16u, 128u);
+            const uint64_t bd = BRES ? kmajor_desc(res + u * (N * 16u), N * 16u, 128u)
+                                     : kmajor_desc(sb + 2 * kk * (N * 16u), N * 16u, 128u);
+            const uint32_t accum = (kc | kk) ? 1u : 0u;
+            if (FP4) umma_fp4(d, ad, bd, idesc, accum, tmem + 480u, tmem + 496u);
+            else umma_u8(d, ad, bd, idesc, accum);
           }
-          __syncwarp();
+          tc::umma_commit(&S.empty[st]);
+          if (kc == KC - 1) {
+            tc::umma_commit(&S.tfull[acc]);
+            if (last && MODE != MODE_STREAM) tc::umma_commit(&S.aempty);  // the stationary tile may be replaced
+          }
         }
-      }
-      if (RESIDENT) {
-        if (lane == 0) tc::umma_commit(&S.aempty);  // the query tile may be replaced
         __syncwarp();
       }
+      if (first && MODE != MODE_STREAM) ++rc;
+      ++tc_;
     }
   } else {
     // ------------------------------------------------ epilogue (warps 2-9)
@@ -318,17 +334,26 @@ __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
     const int cb = half * 128, ce = half ? N : 128;
     KeyT* keys = static_cast<KeyT*>(a.keys);
     uint32_t tc_ = 0;
-    RunIter it(a);
-    ScanRun un;
-    while (it.next(un)) {
-      const int q = un.qt * kScanM + quarter * 32 + lane;
-      const bool qok = q < a.nq;
-      const int32_t pq = qok ? __ldg(a.massQ + q) : 0;
-      // key <= tau  <=>  p_i - 2 acc <= tau - p_Q   (keys are exact integers < 2^24 (FP4) / 2^31 (i8))
-      const int32_t lim = EMIT ? (qok ? static_cast<int32_t>(__ldg(a.tau + q)) - pq : -0x40000000) : 0;
-      const float limf = static_cast<float>(lim);
-      const float pqf = static_cast<float>(pq);
-      for (int t = un.t0; t < un.t1; ++t, ++tc_) {
+    TileSeq seq(a, BRES);
+    int qt, t;
+    bool first, last;
+    int qcur = -1;
+    int32_t pq = 0, lim = 0;
+    float limf = 0.0f, pqf = 0.0f;
+    bool qok = false;
+    int q = 0;
+    while (seq.next(qt, t, first, last)) {
+      if (qt != qcur) {
+        qcur = qt;
+        q = qt * kScanM + quarter * 32 + lane;
+        qok = q < a.nq;
+        pq = qok ? __ldg(a.massQ + q) : 0;
+        // key <= tau  <=>  p_i - 2 acc <= tau - p_Q   (keys are exact integers < 2^24 (FP4) / 2^31 (i8))
+        lim = EMIT ? (qok ? static_cast<int32_t>(__ldg(a.tau + q)) - pq : -0x40000000) : 0;
+        limf = static_cast<float>(lim);
+        pqf = static_cast<float>(pq);
+      }
+      {
         const uint32_t acc = tc_ & 1u;
         const int64_t i0 = static_cast<int64_t>(t) * N;
         tc::mbar_wait(&S.mfull[acc], (tc_ >> 1) & 1u);
@@ -385,34 +410,33 @@ __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
             load_acc(c0, v);
             load_mass(c0, pi);
             tc::tmem_ld_wait();
-            uint32_t mk = 0;
+            uint32_t m4[4] = {0u, 0u, 0u, 0u};  // four independent OR chains
 #pragma unroll
-            for (int j = 0; j < 32; ++j) mk |= (passes(pi[j], v[j]) ? 1u : 0u) << j;
+            for (int j = 0; j < 32; ++j) m4[j & 3] |= (passes(pi[j], v[j]) ? 1u : 0u) << j;
+            const uint32_t mk = (m4[0] | m4[1]) | (m4[2] | m4[3]);
             masks[(c0 - cb) >> 5][lane] = mk;
             ne += __popc(mk);
           }
           int pos = 0;
           if (ne) pos = atomicAdd(a.cnt + q, ne);
+          // pass 2: only the columns where some lane emits, one TMEM column (all 32 lanes) per load
 #pragma unroll 1
           for (int c0 = cb; c0 < ce; c0 += 32) {
             const uint32_t mk = masks[(c0 - cb) >> 5][lane];
-            if (__any_sync(0xffffffffu, mk != 0u)) {  // warp-uniform (tcgen05.ld is warp-collective)
-              uint32_t v[32], pi[32];
-              load_acc(c0, v);
-              load_mass(c0, pi);
+            uint32_t cols = __reduce_or_sync(0xffffffffu, mk);  // warp-uniform
+            while (cols) {
+              const int j = __ffs(cols) - 1;
+              cols &= cols - 1;
+              uint32_t vj;
+              asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(vj) : "r"(tbase + c0 + j) : "memory");
               tc::tmem_ld_wait();
-              const int64_t ic = i0 + c0;
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {  // warp-uniform skip of empty columns: no divergent reconvergence
-                const bool e = (mk >> j) & 1u;
-                if (__ballot_sync(0xffffffffu, e)) {
-                  if (e && pos < a.cap) {
-                    const int64_t o = static_cast<int64_t>(q) * a.cap + pos;
-                    a.buf_id[o] = static_cast<int32_t>(a.id_base + ic + j);
-                    a.buf_key[o] = key_of(pi[j], v[j]);
-                  }
-                  pos += e ? 1 : 0;
+              if ((mk >> j) & 1u) {
+                if (pos < a.cap) {
+                  const int64_t o = static_cast<int64_t>(q) * a.cap + pos;
+                  a.buf_id[o] = static_cast<int32_t>(a.id_base + i0 + c0 + j);
+                  a.buf_key[o] = key_of(S.mass[acc][c0 + j], vj);
                 }
+                ++pos;
               }
             }
           }
@@ -445,6 +469,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
           }
         }
       }
+      ++tc_;
     }
   }
   __syncthreads();
@@ -500,31 +525,29 @@ int launch_expand_db_fp4(const void* S, int64_t n, int64_t n_stride, int m, void
   return BVSS_OK;
 }
 
-template <bool FP4, bool EMIT, bool RES, int KS>
+template <bool FP4, bool EMIT, int MODE, int KS>
 static int launch_one(const ScanArgs& a, size_t smem, int grid, cudaStream_t st) {
-  auto kfn = scan_tc_kernel<FP4, EMIT, RES, KS>;
+  auto kfn = scan_tc_kernel<FP4, EMIT, MODE, KS>;
   BVSS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   kfn<<<grid, kScanThreads, smem, st>>>(a);
   return BVSS_OK;
 }
-template <bool FP4, bool EMIT>
-static int launch_res(const ScanArgs& a, bool resident, int ks, size_t smem, int grid, cudaStream_t st) {
-  // stage counts: 4..8 resident, 3..6 streamed (chosen by the smem budget)
-  if (resident) {
-    switch (ks) {
-      case 8: return launch_one<FP4, EMIT, true, 8>(a, smem, grid, st);
-      case 7: return launch_one<FP4, EMIT, true, 7>(a, smem, grid, st);
-      case 6: return launch_one<FP4, EMIT, true, 6>(a, smem, grid, st);
-      case 5: return launch_one<FP4, EMIT, true, 5>(a, smem, grid, st);
-      default: return launch_one<FP4, EMIT, true, 4>(a, smem, grid, st);
-    }
-  }
+template <bool FP4, bool EMIT, int MODE>
+static int launch_ks(const ScanArgs& a, int ks, size_t smem, int grid, cudaStream_t st) {
   switch (ks) {
-    case 6: return launch_one<FP4, EMIT, false, 6>(a, smem, grid, st);
-    case 5: return launch_one<FP4, EMIT, false, 5>(a, smem, grid, st);
-    case 4: return launch_one<FP4, EMIT, false, 4>(a, smem, grid, st);
-    default: return launch_one<FP4, EMIT, false, 3>(a, smem, grid, st);
+    case 8: return launch_one<FP4, EMIT, MODE, 8>(a, smem, grid, st);
+    case 7: return launch_one<FP4, EMIT, MODE, 7>(a, smem, grid, st);
+    case 6: return launch_one<FP4, EMIT, MODE, 6>(a, smem, grid, st);
+    case 5: return launch_one<FP4, EMIT, MODE, 5>(a, smem, grid, st);
+    case 4: return launch_one<FP4, EMIT, MODE, 4>(a, smem, grid, st);
+    default: return launch_one<FP4, EMIT, MODE, 3>(a, smem, grid, st);
   }
+}
+template <bool FP4, bool EMIT>
+static int launch_mode(const ScanArgs& a, int mode, int ks, size_t smem, int grid, cudaStream_t st) {
+  if (mode == MODE_BRES) return launch_ks<FP4, EMIT, MODE_BRES>(a, ks, smem, grid, st);
+  if (mode == MODE_ARES) return launch_ks<FP4, EMIT, MODE_ARES>(a, ks, smem, grid, st);
+  return launch_ks<FP4, EMIT, MODE_STREAM>(a, ks, smem, grid, st);
 }
 
 // keys mode: keys != null; emit mode: tau != null (cnt must be zeroed by the caller).
@@ -567,31 +590,33 @@ int launch_scan_tc(int kind, const void* S, const int32_t* mass, int64_t n, int6
   a.buf_key = buf_key;
   a.cap = cap;
   a.id_base = id_base;
-  const size_t a_bytes = static_cast<size_t>(kScanM) * U * 16;
-  const size_t b_stage = static_cast<size_t>(N) * kScanStageB;
-  bool resident = a_bytes + 4 * b_stage <= static_cast<size_t>(kScanSmemBudget);
-  int ks;
-  size_t smem;
-  if (resident) {
-    ks = static_cast<int>((kScanSmemBudget - a_bytes) / b_stage);
-    if (ks > kScanMaxStages) ks = kScanMaxStages;
-    smem = a_bytes + ks * b_stage + 1024;
-  } else {
-    const size_t stage = b_stage + static_cast<size_t>(kScanM) * kScanStageB;
-    ks = static_cast<int>(kScanSmemBudget / stage);
-    if (ks > 6) ks = 6;
-    if (ks < 3) BVSS_FAIL(BVSS_EUNSUPPORTED, "scan: stage ring does not fit");
-    smem = ks * stage + 1024;
+  // operand residency: the database tile stationary (A streamed from L2) when it fits, else the query
+  // tile, else both streamed; the stage ring takes the rest of the shared-memory budget
+  const size_t a_tile = static_cast<size_t>(kScanM) * U * 16, b_tile = static_cast<size_t>(N) * U * 16;
+  const size_t a_stage = static_cast<size_t>(kScanM) * kScanStageB, b_stage = static_cast<size_t>(N) * kScanStageB;
+  const size_t budget = kScanSmemBudget;
+  int mode = MODE_STREAM;
+  if (b_tile + 4 * a_stage <= budget) mode = MODE_BRES;
+  else if (a_tile + 4 * b_stage <= budget) mode = MODE_ARES;
+  if (const char* e = getenv("BVSS_SCAN_MODE")) {  // developer switch (0 = query tile resident, 1 = streamed)
+    const int want = atoi(e);
+    if (want == MODE_STREAM || (want == MODE_ARES && a_tile + 4 * b_stage <= budget)) mode = want;
   }
+  const size_t fixed = mode == MODE_BRES ? b_tile : (mode == MODE_ARES ? a_tile : 0);
+  const size_t stage = (mode == MODE_BRES ? 0 : b_stage) + (mode == MODE_ARES ? 0 : a_stage);
+  int ks = static_cast<int>((budget - fixed) / stage);
+  if (ks > kScanMaxStages) ks = kScanMaxStages;
+  if (ks < 3) BVSS_FAIL(BVSS_EUNSUPPORTED, "scan: stage ring does not fit");
+  const size_t smem = fixed + ks * stage + 1024;
   const int64_t work = static_cast<int64_t>(a.n_tiles) * a.q_tiles;
   const int grid = static_cast<int>(work < num_sms ? work : num_sms);
   const bool emit = tau != nullptr;
   if (fp4) {
-    if (emit) BVSS_TRY((launch_res<true, true>(a, resident, ks, smem, grid, st)));
-    else BVSS_TRY((launch_res<true, false>(a, resident, ks, smem, grid, st)));
+    if (emit) BVSS_TRY((launch_mode<true, true>(a, mode, ks, smem, grid, st)));
+    else BVSS_TRY((launch_mode<true, false>(a, mode, ks, smem, grid, st)));
   } else {
-    if (emit) BVSS_TRY((launch_res<false, true>(a, resident, ks, smem, grid, st)));
-    else BVSS_TRY((launch_res<false, false>(a, resident, ks, smem, grid, st)));
+    if (emit) BVSS_TRY((launch_mode<false, true>(a, mode, ks, smem, grid, st)));
+    else BVSS_TRY((launch_mode<false, false>(a, mode, ks, smem, grid, st)));
   }
   BVSS_TRY(post_launch(__func__, st));
   return BVSS_OK;

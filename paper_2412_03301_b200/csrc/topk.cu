@@ -423,9 +423,11 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
       const int dsplit = max(1, min(kTxThreads / ntile, d4));
       const int tile = tid % ntile, split = tid / ntile;
       float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      // thread (tile, split): query rows {it, it + ti_n}, set rows {jt, jt + tj_n} (consecutive lanes take
+      // consecutive set rows: conflict-free 16-byte reads at the odd row stride), dims of slice `split`
       if (split < dsplit) {
-        const int i0 = (tile / tj_n) * 2, j0 = (tile % tj_n) * 2;
-        const int i1 = min(i0 + 1, rowsq - 1), j1 = min(j0 + 1, rowsv - 1);
+        const int i0 = tile / tj_n, j0 = tile % tj_n;
+        const int i1 = min(i0 + ti_n, rowsq - 1), j1 = min(j0 + tj_n, rowsv - 1);
         const float4* qa = reinterpret_cast<const float4*>(Qs) + i0 * stride4;
         const float4* qb4 = reinterpret_cast<const float4*>(Qs) + i1 * stride4;
         const float4* va = reinterpret_cast<const float4*>(Vb) + j0 * stride4;
@@ -465,13 +467,13 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
         }
       }
       if (tid < ntile) {
-        const int i0 = (tid / tj_n) * 2, j0 = (tid % tj_n) * 2;
-        const bool iv1 = i0 + 1 < rowsq, jv1 = j0 + 1 < rowsv;
+        const int i0 = tid / tj_n, j0 = tid % tj_n;
+        const bool iv1 = i0 + ti_n < rowsq, jv1 = j0 + tj_n < rowsv;
         const float r0 = fminf(acc[0], jv1 ? acc[1] : acc[0]);
         atomicMin(&S.rowmin[qb * RB + i0], __float_as_uint(r0));
-        if (iv1) atomicMin(&S.rowmin[qb * RB + i0 + 1], __float_as_uint(fminf(acc[2], jv1 ? acc[3] : acc[2])));
+        if (iv1) atomicMin(&S.rowmin[qb * RB + i0 + ti_n], __float_as_uint(fminf(acc[2], jv1 ? acc[3] : acc[2])));
         atomicMin(&S.colmin[j0], __float_as_uint(fminf(acc[0], iv1 ? acc[2] : acc[0])));
-        if (jv1) atomicMin(&S.colmin[j0 + 1], __float_as_uint(fminf(acc[1], iv1 ? acc[3] : acc[1])));
+        if (jv1) atomicMin(&S.colmin[j0 + tj_n], __float_as_uint(fminf(acc[1], iv1 ? acc[3] : acc[1])));
       }
       __syncthreads();
     }
