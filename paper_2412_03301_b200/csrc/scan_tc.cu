@@ -39,9 +39,9 @@
 // bits, one atomic per (thread, tile) reserves the buffer range, and a second
 // TMEM pass writes the entries.
 //
-// CTA = 10 warps: warp 0 producer (query tile, stage copies, database masses),
-// warp 1 TMEM owner + MMA issuer, warps 2-9 epilogue (two per TMEM lane
-// quarter, each half of the columns).  Double-buffered TMEM accumulators (2 x kN columns; FP4 keeps its
+// CTA = 14 warps: warp 0 producer (query tile, stage copies, database masses),
+// warp 1 TMEM owner + MMA issuer, warps 2-13 epilogue (three per TMEM lane
+// quarter, 96 columns each).  Double-buffered TMEM accumulators (2 x kN columns; FP4 keeps its
 // block scales in the last 32 columns).
 #include <cstdlib>
 #include <type_traits>
@@ -52,8 +52,9 @@ namespace bvss {
 
 constexpr int kScanM = 128;        // queries per tile (MMA M, TMEM lanes)
 constexpr int kScanStageB = 128;   // bytes of K per row per stage (8 units of 16 B, 4 MMAs)
-constexpr int kScanThreads = 320;
-constexpr int kScanEpiWarps = 8;
+constexpr int kScanThreads = 448;  // 14 warps: 128 registers per thread
+constexpr int kScanEpiWarps = 12;
+constexpr int kScanEpiCols = 96;  // columns per epilogue warp (three per TMEM lane quarter)
 constexpr int kScanSmemBudget = 220 * 1024;
 constexpr int kScanMaxStages = 8;
 constexpr uint32_t kScaleOne = 0x7F7F7F7Fu;  // four ue8m0 scale factors = 2^0
@@ -88,7 +89,7 @@ struct ScanCtl {
   uint64_t mfull[2], mempty[2];  // database masses of a tile (producer -> epilogue)
   uint32_t tmem_base;
   __align__(16) uint32_t mass[2][256];  // FP4: float bits; i8: int
-  uint32_t emit_mask[kScanEpiWarps][4][32];  // emit pass-1 bits [warp][chunk][lane]
+  uint32_t emit_mask[kScanEpiWarps][kScanEpiCols / 32][32];  // emit pass-1 bits [warp][chunk][lane]
 };
 
 __device__ __forceinline__ void bulk_copy(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -328,10 +329,10 @@ __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
       ++tc_;
     }
   } else {
-    // ------------------------------------------------ epilogue (warps 2-9)
+    // ------------------------------------------------ epilogue (warps 2-13)
     const int quarter = warp & 3;           // TMEM lane quarter this warp may access
-    const int half = (warp - 2) >> 2;       // columns [cb, ce): [0, 128) or [128, N)
-    const int cb = half * 128, ce = half ? N : 128;
+    const int part = (warp - 2) >> 2;       // columns [cb, ce): [0, 96), [96, 192), [192, N)
+    const int cb = part * kScanEpiCols, ce = min(N, cb + kScanEpiCols);
     KeyT* keys = static_cast<KeyT*>(a.keys);
     uint32_t tc_ = 0;
     TileSeq seq(a, BRES);
@@ -413,7 +414,8 @@ __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
             uint32_t m4[4] = {0u, 0u, 0u, 0u};  // four independent OR chains
 #pragma unroll
             for (int j = 0; j < 32; ++j) m4[j & 3] |= (passes(pi[j], v[j]) ? 1u : 0u) << j;
-            const uint32_t mk = (m4[0] | m4[1]) | (m4[2] | m4[3]);
+            uint32_t mk = (m4[0] | m4[1]) | (m4[2] | m4[3]);
+            if (ce - c0 < 32) mk &= (1u << (ce - c0)) - 1u;  // columns of the next warp's range
             masks[(c0 - cb) >> 5][lane] = mk;
             ne += __popc(mk);
           }
@@ -424,19 +426,34 @@ __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
           for (int c0 = cb; c0 < ce; c0 += 32) {
             const uint32_t mk = masks[(c0 - cb) >> 5][lane];
             uint32_t cols = __reduce_or_sync(0xffffffffu, mk);  // warp-uniform
-            while (cols) {
-              const int j = __ffs(cols) - 1;
-              cols &= cols - 1;
-              uint32_t vj;
-              asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(vj) : "r"(tbase + c0 + j) : "memory");
+            while (cols) {  // up to 4 columns per TMEM round trip
+              int jb[4];
+              int nb = 0;
+#pragma unroll
+              for (int b = 0; b < 4; ++b) {
+                jb[b] = cols ? __ffs(cols) - 1 : jb[0];
+                if (cols) ++nb;
+                cols &= cols - 1;
+              }
+              uint32_t vb[4];
+#pragma unroll
+              for (int b = 0; b < 4; ++b)
+                asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];"
+                             : "=r"(vb[b])
+                             : "r"(tbase + c0 + jb[b])
+                             : "memory");
               tc::tmem_ld_wait();
-              if ((mk >> j) & 1u) {
-                if (pos < a.cap) {
-                  const int64_t o = static_cast<int64_t>(q) * a.cap + pos;
-                  a.buf_id[o] = static_cast<int32_t>(a.id_base + i0 + c0 + j);
-                  a.buf_key[o] = key_of(S.mass[acc][c0 + j], vj);
+#pragma unroll
+              for (int b = 0; b < 4; ++b) {
+                const int j = jb[b];
+                if (b < nb && ((mk >> j) & 1u)) {
+                  if (pos < a.cap) {
+                    const int64_t o = static_cast<int64_t>(q) * a.cap + pos;
+                    a.buf_id[o] = static_cast<int32_t>(a.id_base + i0 + c0 + j);
+                    a.buf_key[o] = key_of(S.mass[acc][c0 + j], vb[b]);
+                  }
+                  ++pos;
                 }
-                ++pos;
               }
             }
           }
@@ -455,7 +472,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
 #pragma unroll
               for (int j = 0; j < 32; ++j) kv[j] = static_cast<KeyT>(key_of(pi[j], v[j]));
               KeyT* row = keys + static_cast<int64_t>(q) * a.key_stride + ic;
-              const int cols = c0 + 32 <= N ? 32 : N - c0;
+              const int cols = c0 + 32 <= ce ? 32 : ce - c0;
               if (cols == 32 && ic + 32 <= a.key_stride) {
                 uint4* dst = reinterpret_cast<uint4*>(row);
                 const uint4* src = reinterpret_cast<const uint4*>(kv);
