@@ -98,7 +98,7 @@ typedef struct {
 typedef struct {
   /* per-stage device time of the most recent bvss_search / bvss_filter / bvss_refine, ms */
   float ms_h2d, ms_encode, ms_scan, ms_select, ms_refine, ms_topk, ms_d2h, ms_total;
-  uint64_t scan_bytes;    /* sketch bytes streamed by the scan kernel (algorithmic) */
+  uint64_t scan_bytes;    /* database-operand bytes the scan kernel streams (FP4/u8 tiles; algorithmic) */
   uint64_t gather_bytes;  /* candidate-vector bytes gathered by the refine kernel (algorithmic) */
   uint64_t cand_rows;     /* candidate vectors refined */
   uint64_t fixup_sets;    /* candidates recomputed by the exact fp32 fix-up */
@@ -106,6 +106,7 @@ typedef struct {
   int32_t query_batch;
   uint64_t select_batches;   /* query batches selected on the sampled-threshold path */
   uint64_t select_fallbacks; /* of those, batches redone on the full-key path */
+  uint64_t scan_macs;        /* (query sketch bit, database sketch bit) products of the scan (nq x n x m) */
 } bvss_stats;
 
 /* ---------------------------------------------------------------- core -- */
@@ -168,6 +169,16 @@ BVSS_API int bvss_filter(bvss_index* idx, const float* queries, const int64_t* q
 BVSS_API int bvss_refine(bvss_index* idx, const float* queries, const int64_t* query_offsets, int64_t nq,
                 const int32_t* cand, int32_t T, int32_t k, int64_t* out_ids, float* out_dist,
                 float* out_approx, uint32_t flags);
+/* Brute force (K8; "precise calculations according to Definition 4"):
+ * the exact top-k Hausdorff neighbours among sets [0, set_limit) (set_limit
+ * <= 0 or > n means all n sets), for recall ground truth.  Runs the refine
+ * path (tensor-core Hausdorff + exact fp32 fix-up window, exact by the window
+ * rule) over chunks of 8192 sets and merges the chunk top-k lists (K7).
+ *   out_ids [nq][k] int64, out_dist [nq][k] fp32, sorted by (distance, id),
+ *   padded with (-1, +inf) when set_limit < k.
+ * Errors: as bvss_search. */
+BVSS_API int bvss_bruteforce(bvss_index* idx, const float* queries, const int64_t* query_offsets, int64_t nq,
+                    int64_t set_limit, int32_t k, int64_t* out_ids, float* out_dist, uint32_t flags);
 /* Squared-distance error bound E used by the fix-up window for a query whose
  * largest vector norm is qnorm_max. */
 BVSS_API double bvss_refine_error_bound(const bvss_index* idx, double qnorm_max);

@@ -26,7 +26,7 @@ DEVICE_PTRS, VALIDATE_FINITE, KEEP_CODES = 0x1, 0x2, 0x4
 EXPORTS = (
     "bvss_build_index", "bvss_search", "bvss_free_index", "bvss_last_error", "bvss_get_info", "bvss_get_stats",
     "bvss_set_stream", "bvss_device_count", "bvss_export_projection", "bvss_export_codes", "bvss_export_sketches",
-    "bvss_query_sketch", "bvss_filter", "bvss_refine", "bvss_refine_error_bound", "bvss_dist_begin",
+    "bvss_query_sketch", "bvss_filter", "bvss_refine", "bvss_bruteforce", "bvss_refine_error_bound", "bvss_dist_begin",
     "bvss_dist_hist", "bvss_dist_resolve", "bvss_dist_tie_counts", "bvss_dist_finish", "bvss_merge_topk",
     "bvss_dist_end",
 )
@@ -56,7 +56,7 @@ class Stats(C.Structure):
                 ("ms_refine", C.c_float), ("ms_topk", C.c_float), ("ms_d2h", C.c_float), ("ms_total", C.c_float),
                 ("scan_bytes", C.c_uint64), ("gather_bytes", C.c_uint64), ("cand_rows", C.c_uint64),
                 ("fixup_sets", C.c_uint64), ("kernel_launches", C.c_int32), ("query_batch", C.c_int32),
-                ("select_batches", C.c_uint64), ("select_fallbacks", C.c_uint64)]
+                ("select_batches", C.c_uint64), ("select_fallbacks", C.c_uint64), ("scan_macs", C.c_uint64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -83,6 +83,7 @@ def _load():
         "bvss_query_sketch": (C.c_int, [VP, P, P, I64, P, P, U32]),
         "bvss_filter": (C.c_int, [VP, P, P, I64, I32, P, P, U32]),
         "bvss_refine": (C.c_int, [VP, P, P, I64, P, I32, I32, P, P, P, U32]),
+        "bvss_bruteforce": (C.c_int, [VP, P, P, I64, I64, I32, P, P, U32]),
         "bvss_refine_error_bound": (C.c_double, [VP, C.c_double]),
         "bvss_dist_begin": (C.c_int, [VP, P, P, I64, I32, I32, I64, U32, C.POINTER(VP), C.POINTER(I32)]),
         "bvss_dist_hist": (C.c_int, [VP, I32, P]),
@@ -226,6 +227,17 @@ class Index:
         _check(lib.bvss_refine(self._h, qp, op, nq, cp, T, k, _ptr(ids)[0], _ptr(dist)[0],
                                _ptr(approx)[0] if approx is not None else None, fl))
         return ids, dist, approx
+
+    def bruteforce(self, queries, q_offsets, k, set_limit=0):
+        """bvss_bruteforce (K8): exact top-k over sets [0, set_limit) (all when 0)."""
+        queries, q_offsets, dev, nq = self._queries(queries, q_offsets)
+        fl = self._bind_stream([queries])
+        ids = self._alloc(dev, (nq, k), np.int64)
+        dist = self._alloc(dev, (nq, k), np.float32)
+        qp, _a = _ptr(queries)
+        op, _b = _ptr(q_offsets)
+        _check(lib.bvss_bruteforce(self._h, qp, op, nq, int(set_limit), k, _ptr(ids)[0], _ptr(dist)[0], fl))
+        return ids, dist
 
     def query_sketch(self, queries, q_offsets, with_codes=False):
         queries, q_offsets, dev, nq = self._queries(queries, q_offsets)

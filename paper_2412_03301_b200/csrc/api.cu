@@ -70,6 +70,7 @@ int launch_select_buf(const int32_t* cnt, const uint32_t* bkey, const int32_t* b
                       int T, int nq, int32_t* cand, int32_t* count, int* fail, cudaStream_t s);
 int launch_expand_db_fp4(const void* S, int64_t n, int64_t n_stride, int m, void* X, int num_sms, cudaStream_t st);
 int scan_tc_units(int kind, int m);
+uint64_t scan_tc_db_bytes(int kind, int m, int64_t n, int nq, int num_sms);
 int launch_gather_sample(const void* sk, const int32_t* mass, int64_t n, int cps, int64_t ns, void* out,
                          int32_t* out_mass, int num_sms, cudaStream_t s);
 struct SelectState {
@@ -130,6 +131,18 @@ __global__ void count_valid_kernel(const int32_t* __restrict__ cand, int T, int 
     int t = 0;
     for (int w = 0; w < (blockDim.x >> 5); ++w) t += s[w];
     count[q] = t;
+  }
+}
+
+// candidate rows of one brute-force chunk: cand[q][i] = c0 + i (i < cnt), count[q] = cnt
+__global__ void fill_range_kernel(int32_t* __restrict__ cand, int32_t* __restrict__ count, int nq, int T, int64_t c0,
+                                  int cnt) {
+  const int64_t total = static_cast<int64_t>(nq) * T;
+  for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int i = static_cast<int>(t % T);
+    cand[t] = i < cnt ? static_cast<int32_t>(c0 + i) : -1;
+    if (i == 0) count[t / T] = cnt;
   }
 }
 
@@ -457,12 +470,14 @@ int scan_batch(bvss_index* idx, bvss_search_ctx* c) {
                             c->qx, c->qpad, c->keys, c->key_stride, wc, idx->num_sms, idx->stream, nullptr, nullptr,
                             nullptr, nullptr, 0, 0, true));
     idx->stats.kernel_launches += 2;
-    idx->stats.scan_bytes += static_cast<uint64_t>(ceil_div<int64_t>(c->nq, 256)) * n * chunks_per_set(idx) * 16;
+    idx->stats.scan_bytes += scan_tc_db_bytes(idx->sketch, idx->m, n, static_cast<int>(c->nq), idx->num_sms);
+    idx->stats.scan_macs += static_cast<uint64_t>(c->nq) * n * idx->m;
   } else {
     BVSS_TRY(launch_scan(idx->sketch, idx->sk, idx->mass, n, n, idx->m, c->qsk, c->qmass, static_cast<int>(c->nq),
                          c->keys, c->key_stride, idx->num_sms, idx->stream));
     idx->stats.kernel_launches += 1;
     idx->stats.scan_bytes += static_cast<uint64_t>(ceil_div<int64_t>(c->nq, 8)) * n * chunks_per_set(idx) * 16;
+    idx->stats.scan_macs += static_cast<uint64_t>(c->nq) * n * idx->m;
   }
   cudaEventRecord(idx->ev[3], idx->stream);
   BVSS_TRY(alloc_select_state(idx, c));
@@ -523,7 +538,9 @@ int select_sampled(bvss_index* idx, bvss_search_ctx* c, bool* ok) {
   BVSS_TRY(launch_scan_tc(idx->sketch, scan_operand(idx, false), idx->mass, n, n, idx->m, c->qsk, c->qmass, nq, c->qx, c->qpad, nullptr,
                           0, wc, idx->num_sms, idx->stream, c->sel.prefix, cnt, bid, bkey, static_cast<int>(cap),
                           c->id_base, false));
-  idx->stats.scan_bytes += static_cast<uint64_t>(ceil_div<int64_t>(c->nq, 256)) * (n + ns) * chunks_per_set(idx) * 16;
+  idx->stats.scan_bytes += scan_tc_db_bytes(idx->sketch, idx->m, n, nq, idx->num_sms) +
+                           scan_tc_db_bytes(idx->sketch, idx->m, ns, nq, idx->num_sms);
+  idx->stats.scan_macs += static_cast<uint64_t>(nq) * (n + ns) * idx->m;
   cudaEventRecord(idx->ev[3], idx->stream);
   // 4. exact top-teff from the buffers
   BVSS_TRY(c->alloc(static_cast<size_t>(nq) * c->T * sizeof(int32_t), reinterpret_cast<void**>(&c->cand)));
@@ -611,7 +628,8 @@ int refine_topk(bvss_index* idx, bvss_search_ctx* c, int64_t* out_ids_dev, float
   const int nq = static_cast<int>(c->nq);
   int exact_all = 0;
   if (idx->terms != 0 && c->max_mq <= 128) {  // tensor path: query rows fit the M=128 tile
-    BVSS_TRY(c->alloc(static_cast<size_t>(nq) * c->T * sizeof(float), reinterpret_cast<void**>(&c->approx)));
+    if (!c->approx)  // once per context (brute force calls this per chunk)
+      BVSS_TRY(c->alloc(static_cast<size_t>(nq) * c->T * sizeof(float), reinterpret_cast<void**>(&c->approx)));
     int* counter;
     BVSS_TRY(idx->ws.get("work_counter", sizeof(int), reinterpret_cast<void**>(&counter)));
     unsigned long long* rows;
@@ -979,6 +997,54 @@ int bvss_filter(bvss_index* idx, const float* queries, const int64_t* query_offs
                               nullptr, idx->stream));
   BVSS_TRY(from_device(idx, out_cand, cand, static_cast<size_t>(nq) * T * 4, dev));
   if (out_score) BVSS_TRY(from_device(idx, out_score, score, static_cast<size_t>(nq) * T * 4, dev));
+  BVSS_CUDA(cudaStreamSynchronize(idx->stream));
+  return BVSS_OK;
+}
+
+// K8 brute force ("precise calculations according to Definition 4"): the exact top-k over the first
+// set_limit sets, as chunks of the refine path (tensor-core Hausdorff + exact fix-up window, which is exact)
+// merged by K7.
+int bvss_bruteforce(bvss_index* idx, const float* queries, const int64_t* query_offsets, int64_t nq,
+                    int64_t set_limit, int32_t k, int64_t* out_ids, float* out_dist, uint32_t flags) {
+  BVSS_TRY(validate_search(idx, queries, query_offsets, nq, k, k));
+  if (!out_ids || !out_dist) BVSS_FAIL(BVSS_EINVAL, "null output");
+  DeviceGuard g(idx->device);
+  const bool dev = (flags & BVSS_DEVICE_PTRS) != 0;
+  std::vector<int64_t> qo;
+  BVSS_TRY(host_offsets(idx, query_offsets, nq, dev, qo));
+  const int64_t lim = (set_limit <= 0 || set_limit > idx->n) ? idx->n : set_limit;
+  std::unique_ptr<bvss_search_ctx> c(new bvss_search_ctx());
+  c->idx = idx;
+  c->k = k;
+  const int chunk = static_cast<int>(lim < 8192 ? (lim < k ? k : lim) : 8192);
+  c->T = chunk;
+  BVSS_TRY(prepare_queries(idx, c.get(), queries, qo, dev, (flags & BVSS_VALIDATE_FINITE) != 0));
+  BVSS_TRY(c->alloc(static_cast<size_t>(nq) * chunk * 4, reinterpret_cast<void**>(&c->cand)));
+  BVSS_TRY(c->alloc(nq * 4, reinterpret_cast<void**>(&c->count)));
+  int64_t *ids[3];
+  float* dd[3];
+  for (int b = 0; b < 3; ++b) {  // [0] running, [1] chunk (contiguous after [0] for the 2-way merge), [2] merged
+    BVSS_TRY(c->alloc(static_cast<size_t>(nq) * k * 8 * (b == 0 ? 2 : 1), reinterpret_cast<void**>(&ids[b])));
+    BVSS_TRY(c->alloc(static_cast<size_t>(nq) * k * 4 * (b == 0 ? 2 : 1), reinterpret_cast<void**>(&dd[b])));
+  }
+  int64_t* run_i = ids[0];
+  float* run_d = dd[0];
+  int64_t* chk_i = ids[0] + static_cast<int64_t>(nq) * k;
+  float* chk_d = dd[0] + static_cast<int64_t>(nq) * k;
+  for (int64_t c0 = 0; c0 < lim; c0 += chunk) {
+    const int cnt = static_cast<int>(c0 + chunk <= lim ? chunk : lim - c0);
+    fill_range_kernel<<<idx->num_sms * 4, 256, 0, idx->stream>>>(c->cand, c->count, static_cast<int>(nq), chunk, c0,
+                                                                  cnt);
+    BVSS_TRY(post_launch("fill_range_kernel", idx->stream));
+    BVSS_TRY(refine_topk(idx, c.get(), c0 == 0 ? run_i : chk_i, c0 == 0 ? run_d : chk_d));
+    if (c0 > 0) {
+      BVSS_TRY(launch_merge_topk(run_i, run_d, 2, nq, k, ids[1], dd[1], idx->stream));
+      BVSS_CUDA(cudaMemcpyAsync(run_i, ids[1], static_cast<size_t>(nq) * k * 8, cudaMemcpyDeviceToDevice, idx->stream));
+      BVSS_CUDA(cudaMemcpyAsync(run_d, dd[1], static_cast<size_t>(nq) * k * 4, cudaMemcpyDeviceToDevice, idx->stream));
+    }
+  }
+  BVSS_TRY(from_device(idx, out_ids, run_i, static_cast<size_t>(nq) * k * 8, dev));
+  BVSS_TRY(from_device(idx, out_dist, run_d, static_cast<size_t>(nq) * k * 4, dev));
   BVSS_CUDA(cudaStreamSynchronize(idx->stream));
   return BVSS_OK;
 }

@@ -1,6 +1,6 @@
 // encode.cu — K1: FlyHash projection + winner-take-all (Def 7, PAPER.md P:317-320;
 // Alg 1 lines 4-7), fused with the refine-operand preparation (K9:
-// fp32 squared norm and the bf16 hi/lo split of every vector).
+// fp32 squared norm and the scaled fp16 hi/lo split of every vector).
 //
 // One warp per vector.  The vector is staged in shared memory; lane l computes
 // the activations of rows j = l + 32 t (t < m/32) as a left-to-right fp32 sum

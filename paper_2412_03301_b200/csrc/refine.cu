@@ -83,6 +83,7 @@ struct RefineArgs {
   int* work_counter;
   unsigned long long* rows_counter;  // candidate rows gathered (stats)
   unsigned long long* prof;          // developer per-role cycle counters (env BVSS_REFINE_PROF) or null
+  int prefetch;                      // developer switch: L2 prefetch of the next tile's rows (env BVSS_REFINE_PREFETCH=1)
 };
 
 struct ItemTable {
@@ -136,6 +137,9 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+}
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
@@ -346,6 +350,17 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(RefineArgs
       const uint32_t qbytes = static_cast<uint32_t>((mq + 7) & ~7) / 8u * KCS * 1024u;
       for (int tile = 0; tile < ntiles; ++tile) {
         const int e0 = t.tile_first[tile], e1 = t.tile_first[tile + 1];
+        if (a.prefetch && tile + 1 < ntiles) {  // warm L2 with the next tile's rows (all K super-chunks)
+          const int f0 = t.tile_first[tile + 1], f1 = t.tile_first[tile + 2];
+          for (int e = f0 + lane; e < f1; e += 32) {
+            const uint32_t nb = static_cast<uint32_t>((t.ent_m[e] + 7) & ~7) / 8u * KCS * 1024u;
+            for (int ks = 0; ks < KS; ++ks) {
+              const size_t src = ((static_cast<size_t>(ks) * a.pgroups + (t.ent_pbase[e] >> 3)) * KCS) * 8 * kKChunk;
+              prefetch_l2(a.hs + src, nb);
+              if (three) prefetch_l2(a.ls + src, nb);
+            }
+          }
+        }
         uint32_t bytes = 0;  // B bytes of one piece of one stage
         for (int e = e0 + lane; e < e1; e += 32) bytes += static_cast<uint32_t>((t.ent_m[e] + 7) & ~7) / 8u * KCS * 1024u;
         bytes = static_cast<uint32_t>(warp_sum(static_cast<int>(bytes)));
@@ -532,7 +547,14 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(RefineArgs
   }
 }
 
-int refine_kcs(int dpad) { return (dpad / kKChunk) % 2 == 0 ? 2 : 1; }
+int refine_kcs(int dpad) {
+  static const int forced = [] {  // developer switch: K-chunks per stage (1, 2 or 3; must divide dpad/64)
+    const char* e = getenv("BVSS_REFINE_KCS");
+    return e ? atoi(e) : 0;
+  }();
+  if (forced > 0 && (dpad / kKChunk) % forced == 0) return forced;
+  return (dpad / kKChunk) % 2 == 0 ? 2 : 1;
+}
 
 size_t refine_smem_bytes(int terms, int KCS, int& stages, uint32_t& stage_bytes) {
   const uint32_t a_bytes = 128u * KCS * 128u, b_bytes = kTileRows * KCS * 128u;
@@ -572,6 +594,10 @@ int launch_refine_tc(const __half* hs, const __half* ls, const float* vscale, in
   a.total_items = a.items_per_query * nq;
   a.work_counter = work_counter;
   a.rows_counter = rows_counter;
+  {
+    const char* e = getenv("BVSS_REFINE_PREFETCH");
+    a.prefetch = e ? atoi(e) : 0;
+  }
   static unsigned long long* prof = nullptr;
   a.prof = nullptr;
   if (getenv("BVSS_REFINE_PROF")) {

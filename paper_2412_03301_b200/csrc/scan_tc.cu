@@ -567,6 +567,37 @@ static int launch_mode(const ScanArgs& a, int mode, int ks, size_t smem, int gri
   return launch_ks<FP4, EMIT, MODE_STREAM>(a, ks, smem, grid, st);
 }
 
+// Operand residency: the database tile stationary (query tiles streamed from L2) when it fits, else the
+// query tile, else both streamed; the stage ring takes the rest of the shared-memory budget.
+int scan_tc_mode(int kind, int m) {
+  const bool fp4 = kind == BVSS_SKETCH_BINARY;
+  const int U = scan_tc_units(kind, m), N = fp4 ? 240 : 256;
+  const size_t a_tile = static_cast<size_t>(kScanM) * U * 16, b_tile = static_cast<size_t>(N) * U * 16;
+  const size_t a_stage = static_cast<size_t>(kScanM) * kScanStageB, b_stage = static_cast<size_t>(N) * kScanStageB;
+  int mode = MODE_STREAM;
+  if (b_tile + 4 * a_stage <= static_cast<size_t>(kScanSmemBudget)) mode = MODE_BRES;
+  else if (a_tile + 4 * b_stage <= static_cast<size_t>(kScanSmemBudget)) mode = MODE_ARES;
+  if (const char* e = getenv("BVSS_SCAN_MODE")) {  // developer switch (0 = query tile resident, 1 = streamed)
+    const int want = atoi(e);
+    if (want == MODE_STREAM || (want == MODE_ARES && a_tile + 4 * b_stage <= static_cast<size_t>(kScanSmemBudget)))
+      mode = want;
+  }
+  return mode;
+}
+// Bytes of the database operand one scan launch streams from memory (the algorithmic traffic of K3):
+// once per run of a CTA when the database tile is stationary, once per query tile otherwise.
+uint64_t scan_tc_db_bytes(int kind, int m, int64_t n, int nq, int num_sms) {
+  const int U = scan_tc_units(kind, m), N = kind == BVSS_SKETCH_BINARY ? 240 : 256;
+  const int64_t nt = ceil_div<int64_t>(n, N), qt = ceil_div(nq, kScanM);
+  const uint64_t row = static_cast<uint64_t>(U) * 16;
+  if (scan_tc_mode(kind, m) == MODE_BRES) {
+    const int64_t work = nt * qt, grid = work < num_sms ? work : num_sms;
+    const int64_t runs = nt + (grid < qt * nt ? grid : 0);  // each database tile once, plus CTA-boundary splits
+    return static_cast<uint64_t>(runs < 2 * nt ? runs : 2 * nt) * N * row;
+  }
+  return static_cast<uint64_t>(qt) * n * row;
+}
+
 // keys mode: keys != null; emit mode: tau != null (cnt must be zeroed by the caller).
 // S: the DB operand [U][n_stride][16 B]; SQ: query sketches (row-major chunks) expanded into Qx
 // ([U][qpad][16 B], qpad >= ceil(nq/128)*128) unless expand == false (Qx already holds them).
@@ -607,18 +638,10 @@ int launch_scan_tc(int kind, const void* S, const int32_t* mass, int64_t n, int6
   a.buf_key = buf_key;
   a.cap = cap;
   a.id_base = id_base;
-  // operand residency: the database tile stationary (A streamed from L2) when it fits, else the query
-  // tile, else both streamed; the stage ring takes the rest of the shared-memory budget
   const size_t a_tile = static_cast<size_t>(kScanM) * U * 16, b_tile = static_cast<size_t>(N) * U * 16;
   const size_t a_stage = static_cast<size_t>(kScanM) * kScanStageB, b_stage = static_cast<size_t>(N) * kScanStageB;
   const size_t budget = kScanSmemBudget;
-  int mode = MODE_STREAM;
-  if (b_tile + 4 * a_stage <= budget) mode = MODE_BRES;
-  else if (a_tile + 4 * b_stage <= budget) mode = MODE_ARES;
-  if (const char* e = getenv("BVSS_SCAN_MODE")) {  // developer switch (0 = query tile resident, 1 = streamed)
-    const int want = atoi(e);
-    if (want == MODE_STREAM || (want == MODE_ARES && a_tile + 4 * b_stage <= budget)) mode = want;
-  }
+  const int mode = scan_tc_mode(kind, m);
   const size_t fixed = mode == MODE_BRES ? b_tile : (mode == MODE_ARES ? a_tile : 0);
   const size_t stage = (mode == MODE_BRES ? 0 : b_stage) + (mode == MODE_ARES ? 0 : a_stage);
   int ks = static_cast<int>((budget - fixed) / stage);

@@ -316,3 +316,23 @@ def test_filter_many_query_tiles(name, ov):
             base = (ids, dist)
         else:
             assert np.array_equal(ids, base[0]) and np.array_equal(dist, base[1])
+
+
+@pytest.mark.parametrize("name,ov,limit", [("cfg1", dict(n=600, nq=5), 0), ("cfg3", dict(n=9000, nq=4), 8500),
+                                           ("cfg4", dict(n=700, nq=3), 5)])
+def test_bruteforce_matches_oracle(name, ov, limit):
+    """K8: exact top-k over the first set_limit sets (several 8192-set chunks merged; limit < k pads)."""
+    _need_gpu()
+    cfg = synth.get_config(name, **ov)
+    data = synth.to_numpy(synth.generate(cfg, device="cpu"))
+    idx = B.Index(data["vectors"], data["offsets"], m=cfg.m, s=cfg.s, L=cfg.L, sketch=cfg.sketch, seed=cfg.seed)
+    ids, dist = idx.bruteforce(data["queries"], data["q_offsets"], cfg.k, set_limit=limit)
+    idx.close()
+    V, off = data["vectors"], data["offsets"]
+    n_lim = cfg.n if limit <= 0 else min(limit, cfg.n)
+    for qi in range(ids.shape[0]):
+        Q = data["queries"][data["q_offsets"][qi]:data["q_offsets"][qi + 1]]
+        r_ids, r_d = O.bruteforce_topk(Q, V, off, cfg.k, ids=np.arange(n_lim, dtype=np.int64))
+        check_topk(ids[qi], dist[qi], r_ids, r_d, lambda i: O.hausdorff(Q, V[off[i]:off[i + 1]]))
+        if n_lim < cfg.k:
+            assert np.all(ids[qi][n_lim:] == -1) and np.all(np.isinf(dist[qi][n_lim:]))
