@@ -34,6 +34,9 @@
 // warps 2-5 epilogue.  Accumulators (128 lanes x 256 columns) are
 // double-buffered in TMEM (512 columns); item tables and tile infos are handed
 // over with mbarriers, so the persistent loop has no CTA-wide barrier.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <cstdio>
 #include <cstdlib>
 
@@ -83,6 +86,11 @@ struct RefineArgs {
   int* work_counter;
   unsigned long long* rows_counter;  // candidate rows gathered (stats)
   unsigned long long* prof;          // developer per-role cycle counters (env BVSS_REFINE_PROF) or null
+  // TMA maps over the pre-swizzled operand viewed as [KS][P/8][KCS][8 rows][64 halves] with box
+  // (64 halves x h rows) of one K-chunk of one 8-row group, h = 1..8: the last, partial group of a set
+  // is fetched without its padding rows
+  CUtensorMap tm_hi[8], tm_lo[8];
+  int tma;                           // developer switch BVSS_REFINE_TMA=1: partial groups by TMA (measured slower)
   int prefetch;                      // developer switch: L2 prefetch of the next tile's rows (env BVSS_REFINE_PREFETCH=1)
 };
 
@@ -141,6 +149,14 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 __device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
+// one box of a 5D tensor map into shared memory, completion on an mbarrier (transaction bytes)
+__device__ __forceinline__ void tma_5d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, int c3, int c4,
+                                       uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
@@ -162,7 +178,7 @@ __device__ __forceinline__ void tmem_ld16f(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-__global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(RefineArgs a) {
+__global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __grid_constant__ RefineArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ RefineCtl S;
   uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -362,7 +378,9 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(RefineArgs
           }
         }
         uint32_t bytes = 0;  // B bytes of one piece of one stage
-        for (int e = e0 + lane; e < e1; e += 32) bytes += static_cast<uint32_t>((t.ent_m[e] + 7) & ~7) / 8u * KCS * 1024u;
+        for (int e = e0 + lane; e < e1; e += 32)
+          bytes += a.tma ? static_cast<uint32_t>(t.ent_m[e]) * KCS * 128u
+                         : static_cast<uint32_t>((t.ent_m[e] + 7) & ~7) / 8u * KCS * 1024u;
         bytes = static_cast<uint32_t>(warp_sum(static_cast<int>(bytes)));
         const uint32_t stage_tx = (three ? 2u : 1u) * (bytes + static_cast<uint32_t>(reps) * qbytes);
         for (int ks = 0; ks < KS; ++ks, ++stage_ctr) {
@@ -374,12 +392,23 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(RefineArgs
           if (lane == 0) mbar_arrive_expect_tx(&S.full[st], stage_tx);
           __syncwarp();
           for (int e = e0 + lane; e < e1; e += 32) {
-            const int mp = (t.ent_m[e] + 7) & ~7;
-            const size_t src = ((static_cast<size_t>(ks) * a.pgroups + (t.ent_pbase[e] >> 3)) * KCS) * 8 * kKChunk;
-            const uint32_t nb = static_cast<uint32_t>(mp) / 8u * KCS * 1024u;
+            const int m = t.ent_m[e];
+            const int full = a.tma ? (m >> 3) : ((m + 7) >> 3), rem = a.tma ? (m & 7) : 0;
+            const int64_t g0 = t.ent_pbase[e] >> 3;
+            const size_t src = ((static_cast<size_t>(ks) * a.pgroups + g0) * KCS) * 8 * kKChunk;
             const uint32_t o = static_cast<uint32_t>(t.ent_col[e]) / 8u * KCS * 1024u;
-            bulk_g2s(b_hi + o, a.hs + src, nb, &S.full[st]);
-            if (three) bulk_g2s(b_lo + o, a.ls + src, nb, &S.full[st]);
+            if (full) {  // whole 8-row groups: one contiguous run of full * KCS KB
+              const uint32_t nb = static_cast<uint32_t>(full) * KCS * 1024u;
+              bulk_g2s(b_hi + o, a.hs + src, nb, &S.full[st]);
+              if (three) bulk_g2s(b_lo + o, a.ls + src, nb, &S.full[st]);
+            }
+            if (rem) {  // the last group's rem real rows, one K-chunk at a time (no padding rows read)
+              for (int kc = 0; kc < KCS; ++kc) {
+                const uint32_t dst = o + (static_cast<uint32_t>(full) * KCS + kc) * 1024u;
+                tma_5d(b_hi + dst, &a.tm_hi[rem - 1], 0, 0, kc, static_cast<int>(g0 + full), ks, &S.full[st]);
+                if (three) tma_5d(b_lo + dst, &a.tm_lo[rem - 1], 0, 0, kc, static_cast<int>(g0 + full), ks, &S.full[st]);
+              }
+            }
           }
           if (lane >= 32 - reps) {  // query replicas: replica r at A rows r * rep_rows
             const int r = lane - (32 - reps);
@@ -604,6 +633,35 @@ int launch_refine_tc(const __half* hs, const __half* ls, const float* vscale, in
     if (!prof) cudaMalloc(&prof, 16 * sizeof(unsigned long long));
     cudaMemsetAsync(prof, 0, 16 * sizeof(unsigned long long), st);
     a.prof = prof;
+  }
+  {  // TMA maps for the partial last group of every set (h = 1..8 rows)
+    const char* e = getenv("BVSS_REFINE_TMA");  // developer switch: 0 = copy whole padded groups
+    a.tma = e ? atoi(e) : 0;
+  }
+  if (a.tma) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+      cudaDriverEntryPointQueryResult q;
+      void* fn = nullptr;
+      BVSS_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+      if (!fn || q != cudaDriverEntryPointSuccess) BVSS_FAIL(BVSS_ECUDA, "cuTensorMapEncodeTiled unavailable");
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t dims[5] = {64, 8, static_cast<cuuint64_t>(a.KCS), static_cast<cuuint64_t>(a.pgroups),
+                                static_cast<cuuint64_t>(a.KC / a.KCS)};
+    const cuuint64_t strides[4] = {128, 1024, static_cast<cuuint64_t>(a.KCS) * 1024,
+                                   static_cast<cuuint64_t>(a.pgroups) * a.KCS * 1024};
+    const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    for (int h = 1; h <= 8; ++h) {
+      const cuuint32_t box[5] = {64, static_cast<cuuint32_t>(h), 1, 1, 1};
+      for (int piece = 0; piece < (a.terms == 3 ? 2 : 1); ++piece) {
+        CUresult r = encode(piece ? &a.tm_lo[h - 1] : &a.tm_hi[h - 1], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 5,
+                            const_cast<__half*>(piece ? ls : hs), dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) BVSS_FAIL(BVSS_ECUDA, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+      }
+    }
   }
   BVSS_CUDA(cudaMemsetAsync(work_counter, 0, sizeof(int), st));
   BVSS_CUDA(cudaFuncSetAttribute(refine_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
