@@ -71,6 +71,7 @@ int launch_select_buf(const int32_t* cnt, const uint32_t* bkey, const int32_t* b
 int launch_expand_db_fp4(const void* S, int64_t n, int64_t n_stride, int m, void* X, int num_sms, cudaStream_t st);
 int scan_tc_units(int kind, int m);
 uint64_t scan_tc_db_bytes(int kind, int m, int64_t n, int nq, int num_sms);
+bool select_buf_sorted(int teff);
 int launch_gather_sample(const void* sk, const int32_t* mass, int64_t n, int cps, int64_t ns, void* out,
                          int32_t* out_mass, int num_sms, cudaStream_t s);
 struct SelectState {
@@ -95,7 +96,8 @@ int launch_refine_tc(const __half* hs, const __half* ls, const float* vscale, in
                      const float* vnorm, const int64_t* off, int dpad, const __half* qhs, const __half* qls,
                      const float* qscale, int64_t qrows, const int64_t* qrow, const float* qnorm, const int64_t* qoff, int max_mq, const int32_t* cand,
                      const int32_t* count, int T, int nq, int64_t id_base, float* out_h2, int terms, int* work_counter,
-                     unsigned long long* rows_counter, int num_sms, cudaStream_t st);
+                     unsigned long long* rows_counter, int num_sms, int64_t n_local, int32_t* bounds, cudaStream_t st);
+int64_t refine_range_sets(int64_t n_local, int64_t prows, int dpad, int T);
 int launch_topk_fixup(const float* approx, const int32_t* cand, const int32_t* count, int T, int k, const float* V,
                       const int64_t* off, int64_t id_base, int d, const float* Qv, const int64_t* qoff,
                       const float* qnorm, float vmax2, float c1, float c2, int exact_all, int64_t* out_ids,
@@ -273,6 +275,7 @@ struct bvss_search_ctx {
   int32_t* local_hist = nullptr;
   int32_t* cand = nullptr;
   int32_t* count = nullptr;
+  bool cand_sorted = true;    // candidate lists in ascending id order (the refine may then run range-major)
   float* approx = nullptr;
   void* qsk = nullptr;        // query sketches, row-major padded to whole chunks
   int32_t* qmass = nullptr;   // query sketch masses
@@ -550,6 +553,7 @@ int select_sampled(bvss_index* idx, bvss_search_ctx* c, bool* ok) {
   BVSS_CUDA(cudaMemsetAsync(fail, 0, sizeof(int), idx->stream));
   BVSS_TRY(launch_select_buf(cnt, bkey, bid, static_cast<int>(cap), static_cast<int>(c->teff), c->key_bits, c->T, nq,
                              c->cand, c->count, fail, idx->stream));
+  c->cand_sorted = select_buf_sorted(static_cast<int>(c->teff));
   cudaEventRecord(idx->ev[4], idx->stream);
   idx->stats.kernel_launches += 4 + 2 * c->rounds;
   int hf = 0;
@@ -620,6 +624,7 @@ int fallback_full(bvss_index* idx, bvss_search_ctx* c) {
     idx->stats.kernel_launches += 4 + 2 * c->rounds;
   }
   cudaEventRecord(idx->ev[4], idx->stream);
+  c->cand_sorted = true;  // order-preserving emission
   return BVSS_OK;
 }
 
@@ -634,10 +639,20 @@ int refine_topk(bvss_index* idx, bvss_search_ctx* c, int64_t* out_ids_dev, float
     BVSS_TRY(idx->ws.get("work_counter", sizeof(int), reinterpret_cast<void**>(&counter)));
     unsigned long long* rows;
     BVSS_TRY(idx->ws.get("rows_counter", sizeof(unsigned long long), reinterpret_cast<void**>(&rows)));
+    int32_t* bounds = nullptr;  // range bounds of the range-major refine (refine.cu)
+    {
+      const int64_t rs = refine_range_sets(idx->n, idx->prows, idx->dpad, c->T);
+      if (rs > 0 && c->cand_sorted) {
+        const int64_t nr = (idx->n + rs - 1) / rs;
+        const size_t bb = ((static_cast<size_t>(nq) * (nr + 1) * 4) + 15) & ~size_t(15);
+        BVSS_TRY(idx->ws.get("refine_bounds", bb + static_cast<size_t>(nq) * (16 + 32 * 8),
+                             reinterpret_cast<void**>(&bounds)));
+      }
+    }
     BVSS_TRY(launch_refine_tc(idx->hi, idx->lo, idx->vscale, idx->prows, idx->pbase, idx->vnorm, idx->off, idx->dpad, c->qhi,
                               c->qlo, c->qscale, c->qrows,
                               c->qrow, c->qnorm, c->qoff, c->max_mq, c->cand, c->count, c->T, nq, c->id_base,
-                              c->approx, idx->terms, counter, rows, idx->num_sms, idx->stream));
+                              c->approx, idx->terms, counter, rows, idx->num_sms, c->cand_sorted ? idx->n : 0, bounds, idx->stream));
     idx->stats.kernel_launches += 1;
   } else {
     exact_all = 1;
@@ -1080,7 +1095,8 @@ int bvss_refine(bvss_index* idx, const float* queries, const int64_t* query_offs
     BVSS_TRY(launch_refine_tc(idx->hi, idx->lo, idx->vscale, idx->prows, idx->pbase, idx->vnorm, idx->off, idx->dpad, c->qhi,
                               c->qlo, c->qscale, c->qrows,
                               c->qrow, c->qnorm, c->qoff, c->max_mq, c->cand, c->count, T, static_cast<int>(nq), 0,
-                              c->approx, idx->terms, counter, nullptr, idx->num_sms, idx->stream));
+                              c->approx, idx->terms, counter, nullptr, idx->num_sms,
+                              0 /* caller lists: any order */, nullptr, idx->stream));
   } else {
     exact_all = 1;
   }

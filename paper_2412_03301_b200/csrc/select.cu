@@ -404,6 +404,13 @@ __device__ uint32_t buf_select(const uint32_t* vals, const uint32_t* keys, bool 
   return prefix;
 }
 
+// power-of-two length of the in-smem id sort of select_buf_kernel (0: too long, not sorted)
+__host__ __device__ __forceinline__ int sorted_len(int teff) {
+  int p = 1;
+  while (p < teff) p <<= 1;
+  return p <= 16384 ? p : 0;
+}
+
 __global__ void __launch_bounds__(kBufThreads) select_buf_kernel(const int32_t* __restrict__ cnt,
                                                                  const uint32_t* __restrict__ bkey,
                                                                  const int32_t* __restrict__ bid, int cap, int teff,
@@ -431,12 +438,36 @@ __global__ void __launch_bounds__(kBufThreads) select_buf_kernel(const int32_t* 
   const uint32_t theta = buf_select(ids, keys, true, tau, c, 31, quota, hist, &s_dig, &s_before, &dummy);
   if (threadIdx.x == 0) s_pos = 0u;
   __syncthreads();
+  // the selected ids, then a bitonic sort so the list comes out in ascending id order (as the full-key path
+  // and bvss_filter); lists longer than the smem sort stay in emission order (the refine then runs query-major)
+  extern __shared__ uint32_t sort_buf[];
+  const int P = sorted_len(teff);
+  uint32_t* dst = P ? sort_buf : reinterpret_cast<uint32_t*>(crow);
   for (int e = threadIdx.x; e < c; e += blockDim.x) {
     const uint32_t k = keys[e];
     if (k < tau || (k == tau && ids[e] <= theta)) {
       const uint32_t pos = atomicAdd(&s_pos, 1u);
-      crow[pos] = static_cast<int32_t>(ids[e]);
+      dst[pos] = ids[e];
     }
+  }
+  if (P) {
+    for (int i = teff + threadIdx.x; i < P; i += blockDim.x) sort_buf[i] = 0xFFFFFFFFu;
+    __syncthreads();
+    for (int size = 2; size <= P; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = threadIdx.x; i < P / 2; i += blockDim.x) {
+          const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+          const bool up = (lo & size) == 0;
+          const uint32_t x = sort_buf[lo], y = sort_buf[hi];
+          if ((x > y) == up) {
+            sort_buf[lo] = y;
+            sort_buf[hi] = x;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (int i = threadIdx.x; i < teff; i += blockDim.x) crow[i] = static_cast<int32_t>(sort_buf[i]);
   }
   for (int i = teff + threadIdx.x; i < T; i += blockDim.x) crow[i] = -1;
   if (threadIdx.x == 0) count[q] = teff;
@@ -455,9 +486,13 @@ __global__ void gather_sample_kernel(const uint4* __restrict__ sk, const int32_t
   }
 }
 
+bool select_buf_sorted(int teff) { return sorted_len(teff) != 0; }
+
 int launch_select_buf(const int32_t* cnt, const uint32_t* bkey, const int32_t* bid, int cap, int teff, int key_bits,
                       int T, int nq, int32_t* cand, int32_t* count, int* fail, cudaStream_t s) {
-  select_buf_kernel<<<nq, kBufThreads, 0, s>>>(cnt, bkey, bid, cap, teff, key_bits, T, cand, count, fail);
+  const size_t smem = static_cast<size_t>(sorted_len(teff)) * 4;
+  BVSS_CUDA(cudaFuncSetAttribute(select_buf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  select_buf_kernel<<<nq, kBufThreads, smem, s>>>(cnt, bkey, bid, cap, teff, key_bits, T, cand, count, fail);
   BVSS_TRY(post_launch(__func__, s));
   return BVSS_OK;
 }

@@ -336,3 +336,32 @@ def test_bruteforce_matches_oracle(name, ov, limit):
         check_topk(ids[qi], dist[qi], r_ids, r_d, lambda i: O.hausdorff(Q, V[off[i]:off[i + 1]]))
         if n_lim < cfg.k:
             assert np.all(ids[qi][n_lim:] == -1) and np.all(np.isinf(dist[qi][n_lim:]))
+
+
+@pytest.mark.parametrize("rng_sets", ["0", "1500"])
+def test_search_range_major_refine(monkeypatch, rng_sets):
+    """The refine's range-major group mode (developer switch BVSS_REFINE_GROUP=1: 4 queries per tile,
+    candidate lists cut by database range) against the query-major mode and the oracle pipeline, on the
+    sampled-threshold search path (n >= 65536, candidate lists sorted by select_buf)."""
+    _need_gpu()
+    cfg = synth.get_config("cfg3", n=70000, nq=24, T=300)
+    data = synth.to_numpy(synth.generate(cfg, device="cpu"))
+    idx = B.Index(data["vectors"], data["offsets"], m=cfg.m, s=cfg.s, L=cfg.L, sketch=cfg.sketch, seed=cfg.seed)
+    if rng_sets != "0":
+        monkeypatch.setenv("BVSS_REFINE_RANGE", rng_sets)
+    out = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("BVSS_REFINE_GROUP", mode)
+        ids, dist = idx.search(data["queries"], data["q_offsets"], cfg.k, cfg.T)
+        out[mode] = (ids, dist, idx.stats())
+    idx.close()
+    assert out["1"][2]["select_batches"] >= 1
+    assert np.array_equal(out["0"][0], out["1"][0]) and np.array_equal(out["0"][1], out["1"][1])
+    assert out["0"][2]["fixup_sets"] == out["1"][2]["fixup_sets"]  # identical tensor-core values
+    oi = O.OracleIndex(data["vectors"], data["offsets"], cfg.m, cfg.s, cfg.L, cfg.seed, sketch=cfg.sketch)
+    V, off = data["vectors"], data["offsets"]
+    ids, dist = out["1"][0], out["1"][1]
+    for qi in range(0, cfg.nq, 6):
+        Q = data["queries"][data["q_offsets"][qi]:data["q_offsets"][qi + 1]]
+        r_ids, r_d = oi.search(Q, cfg.k, cfg.T)
+        check_topk(ids[qi], dist[qi], r_ids, r_d, lambda i: O.hausdorff(Q, V[off[i]:off[i + 1]]))

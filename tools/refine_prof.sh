@@ -1,7 +1,7 @@
 #!/bin/bash
 # per-role wait breakdown of the refine kernel (developer tool)
 A="--n ${N:-200000} --nq 2048 --steps 1 --warmup 0 --no-cpu-baseline --recall-queries 0 --no-e2e"
-for e in ${EXPS:-0 4}; do
-  echo "== experiment $e"
-  BVSS_REFINE_PROF=1 BVSS_REFINE_EXPERIMENT=$e python bench.py $A 2>&1 | grep "refine prof" | tail -1
+for g in ${GROUPS_:-0 1}; do
+  echo "== group $g"
+  BVSS_REFINE_PROF=1 BVSS_REFINE_GROUP=$g python bench.py $A 2>&1 | grep "refine prof" | tail -1
 done
