@@ -58,6 +58,7 @@ constexpr int kScanEpiCols = 96;  // columns per epilogue warp (three per TMEM l
 constexpr int kScanSmemBudget = 220 * 1024;
 constexpr int kScanMaxStages = 8;
 constexpr uint32_t kScaleOne = 0x7F7F7F7Fu;  // four ue8m0 scale factors = 2^0
+constexpr int kMassSlots = 4;  // mass slots: the producer runs up to 4 tiles ahead of the epilogue
 
 struct ScanArgs {
   const uint4* S;              // DB operand [U][n_stride][16 B] (FP4 expansion or u8 counters)
@@ -86,9 +87,9 @@ struct ScanCtl {
   uint64_t tfull[2];
   uint64_t tempty[2];
   uint64_t afull, aempty;
-  uint64_t mfull[2], mempty[2];  // database masses of a tile (producer -> epilogue)
+  uint64_t mfull[kMassSlots], mempty[kMassSlots];  // database masses of a tile (producer -> epilogue)
   uint32_t tmem_base;
-  __align__(16) uint32_t mass[2][256];  // FP4: float bits; i8: int
+  __align__(16) uint32_t mass[kMassSlots][256];  // FP4: float bits; i8: int
   uint32_t emit_mask[kScanEpiWarps][kScanEpiCols / 32][32];  // emit pass-1 bits [warp][chunk][lane]
 };
 
@@ -208,6 +209,8 @@ __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&S.tfull[b], 1);
       tc::mbar_init(&S.tempty[b], kScanEpiWarps);
+    }
+    for (int b = 0; b < kMassSlots; ++b) {
       tc::mbar_init(&S.mfull[b], 32);
       tc::mbar_init(&S.mempty[b], kScanEpiWarps);
     }
@@ -255,9 +258,9 @@ __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
         }
         ++rc;
       }
-      {  // masses of the tile's sets -> smem slot tc_ & 1 (columns past n get a huge mass: never selected)
-        const uint32_t slot = tc_ & 1u;
-        tc::mbar_wait(&S.mempty[slot], ((tc_ >> 1) & 1u) ^ 1u);
+      {  // masses of the tile's sets -> smem slot tc_ % 4 (columns past n get a huge mass: never selected)
+        const uint32_t slot = tc_ % kMassSlots;
+        tc::mbar_wait(&S.mempty[slot], ((tc_ / kMassSlots) & 1u) ^ 1u);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int c = lane * 8 + j;
@@ -357,13 +360,14 @@ __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
       {
         const uint32_t acc = tc_ & 1u;
         const int64_t i0 = static_cast<int64_t>(t) * N;
-        tc::mbar_wait(&S.mfull[acc], (tc_ >> 1) & 1u);
+        const uint32_t ms = tc_ % kMassSlots;  // mass slot of this tile
+        tc::mbar_wait(&S.mfull[ms], (tc_ / kMassSlots) & 1u);
         tc::mbar_wait(&S.tfull[acc], (tc_ >> 1) & 1u);
         tc::fence_after_sync();
         const uint32_t tbase = tmem + acc * kAcc + (static_cast<uint32_t>(quarter * 32) << 16);
         // masses: float (FP4: the accumulator is an exact integer-valued f32) or int (i8: s32 accumulator)
         auto load_mass = [&](int c0, uint32_t (&pi)[32]) {
-          const uint4* mp = reinterpret_cast<const uint4*>(&S.mass[acc][c0]);  // warp-uniform: broadcast
+          const uint4* mp = reinterpret_cast<const uint4*>(&S.mass[ms][c0]);  // warp-uniform: broadcast
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const uint4 t4 = mp[j];
@@ -397,7 +401,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
           __syncwarp();
           if (lane == 0) {
             tc::mbar_arrive(&S.tempty[acc]);
-            tc::mbar_arrive(&S.mempty[acc]);
+            tc::mbar_arrive(&S.mempty[ms]);
           }
         };
         if (EMIT) {
@@ -450,7 +454,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
                   if (pos < a.cap) {
                     const int64_t o = static_cast<int64_t>(q) * a.cap + pos;
                     a.buf_id[o] = static_cast<int32_t>(a.id_base + i0 + c0 + j);
-                    a.buf_key[o] = key_of(S.mass[acc][c0 + j], vb[b]);
+                    a.buf_key[o] = key_of(S.mass[ms][c0 + j], vb[b]);
                   }
                   ++pos;
                 }

@@ -251,7 +251,11 @@ __global__ void __launch_bounds__(kTopkThreads) topk_fixup_kernel(
 //   3. the k smallest exact distances by (distance, id).
 constexpr int kTxThreads = 256;
 
+constexpr int kTxCache = 256;  // window candidates whose row ranges are cached in smem
+
 struct TxSmem {
+  int64_t jv0[kTxCache];  // first row and row count of window candidate w
+  int jmi[kTxCache];
   uint32_t hist[256];
   uint32_t rowmin[256];   // min_v D^2 of each query row (kMaxMq)
   uint32_t colmin[32];    // min_q D^2 of each set row of the current block
@@ -387,11 +391,26 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
   for (int i = tid; i < mq; i += blockDim.x) S.rowmin[i] = 0x7f800000u;
   if (tid < 32) S.colmin[tid] = 0x7f800000u;
   if (tid == 0) S.hv = 0.0f;
-  // job sequence: (window entry w, set-row block vb); the next job's rows are staged while this one computes
-  auto job_rows = [&](int w, int vb, const float** src, int* rows) {
-    const int64_t cid = static_cast<int64_t>(cq[win[w]]) - id_base;
+  // the window candidates' row ranges, gathered in parallel once (smem for the first kTxCache entries)
+  for (int x = tid; x < min(nw, kTxCache); x += blockDim.x) {
+    const int64_t cid = static_cast<int64_t>(cq[win[x]]) - id_base;
     const int64_t v0 = off[cid];
-    const int mi = static_cast<int>(off[cid + 1] - v0);
+    S.jv0[x] = v0;
+    S.jmi[x] = static_cast<int>(off[cid + 1] - v0);
+  }
+  __syncthreads();
+  // job sequence: (window entry w, set-row block vb)
+  auto job_rows = [&](int w, int vb, const float** src, int* rows) {
+    int64_t v0;
+    int mi;
+    if (w < kTxCache) {
+      v0 = S.jv0[w];
+      mi = S.jmi[w];
+    } else {
+      const int64_t cid = static_cast<int64_t>(cq[win[w]]) - id_base;
+      v0 = off[cid];
+      mi = static_cast<int>(off[cid + 1] - v0);
+    }
     *src = V + (v0 + static_cast<int64_t>(vb) * RB) * d;
     *rows = min(RB, mi - vb * RB);
     return mi;
@@ -433,6 +452,7 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
         const float4* va = reinterpret_cast<const float4*>(Vb) + j0 * stride4;
         const float4* vb4 = reinterpret_cast<const float4*>(Vb) + j1 * stride4;
         const int kb = split * d4 / dsplit, ke = (split + 1) * d4 / dsplit;
+#pragma unroll 4
         for (int c = kb; c < ke; ++c) {
           const float4 x0 = qa[c], x1 = qb4[c], y0 = va[c], y1 = vb4[c];
 #define BVSS_DD(A, X, Y)                                  \
