@@ -137,7 +137,8 @@ BVSS_API void bvss_free_index(bvss_index* idx);
 BVSS_API const char* bvss_last_error(void);
 BVSS_API int bvss_get_info(const bvss_index* idx, bvss_info* out);
 BVSS_API int bvss_get_stats(const bvss_index* idx, bvss_stats* out);
-/* Issue all work of this index on `stream` (a cudaStream_t; NULL = the index's own stream). */
+/* Issue all work of this index on `stream` (a cudaStream_t; NULL = the index's own non-blocking
+ * stream, which is NOT ordered with the legacy default stream: pass cudaStreamLegacy to use that). */
 BVSS_API int bvss_set_stream(bvss_index* idx, void* stream);
 /* Number of sm_100-class devices visible (0 if none); never fails. */
 BVSS_API int bvss_device_count(void);

@@ -166,7 +166,10 @@ class Index:
         if any(_is_cuda(t) for t in tensors if t is not None):
             import torch
             st = torch.cuda.current_stream(self.device).cuda_stream
-            _check(lib.bvss_set_stream(self._h, C.c_void_p(st)))
+            # torch reports the legacy default stream as 0; the C ABI reads NULL as "the index's own
+            # stream", so name the legacy stream explicitly (cudaStreamLegacy == 0x1) to stay ordered
+            # with torch's work on it
+            _check(lib.bvss_set_stream(self._h, C.c_void_p(st if st else 1)))
             return DEVICE_PTRS
         _check(lib.bvss_set_stream(self._h, None))
         return 0

@@ -82,6 +82,33 @@ class LibShardOps:
             self.ctx = None
 
 
+def _host_collectives(group) -> bool:
+    """gloo moves host tensors; NCCL moves device tensors in place."""
+    return dist.get_backend(group) == "gloo"
+
+
+def _all_reduce_sum(t, group):
+    if _host_collectives(group) and t.is_cuda:
+        h = t.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return t
+
+
+def _all_gather(t, world, group):
+    """[world * rows, ...] concatenation of every rank's t (rank order)."""
+    if _host_collectives(group) and t.is_cuda:
+        h = t.cpu().contiguous()
+        out = torch.empty((world * h.shape[0],) + tuple(h.shape[1:]), dtype=h.dtype)
+        dist.all_gather_into_tensor(out, h, group=group)
+        return out.to(t.device)
+    out = torch.empty((world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+    dist.all_gather_into_tensor(out, t, group=group)
+    return out
+
+
 def sharded_search(ops, queries, q_offsets, k: int, T: int, n_total: int, group=None):
     """Run the exact global-T protocol for one query batch; every rank returns
     the same merged top-k (ids int64 [nq][k], dist fp32 [nq][k])."""
@@ -92,18 +119,13 @@ def sharded_search(ops, queries, q_offsets, k: int, T: int, n_total: int, group=
     try:
         for r in range(rounds):
             h = ops.hist(r)
-            dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)      # C1
+            _all_reduce_sum(h, group)                                    # C1
             ops.resolve(r, h)
         eq = ops.tie_counts()
-        # outputs are allocated flat along dim 0 ([world * rows, ...]; gloo requires it) and viewed per rank
-        all_eq = torch.empty((world * eq.shape[0],), dtype=eq.dtype, device=eq.device)
-        dist.all_gather_into_tensor(all_eq, eq, group=group)           # C2
-        all_eq = all_eq.view(world, -1)
+        all_eq = _all_gather(eq, world, group).view(world, -1)           # C2
         ids, dd = ops.finish(all_eq, world, rank)
-        all_ids = torch.empty((world * ids.shape[0], ids.shape[1]), dtype=ids.dtype, device=ids.device)
-        all_d = torch.empty((world * dd.shape[0], dd.shape[1]), dtype=dd.dtype, device=dd.device)
-        dist.all_gather_into_tensor(all_ids, ids, group=group)         # C3
-        dist.all_gather_into_tensor(all_d, dd, group=group)
+        all_ids = _all_gather(ids, world, group)                         # C3
+        all_d = _all_gather(dd, world, group)
         return ops.merge(all_ids.view(world, *ids.shape), all_d.view(world, *dd.shape), world)  # K7
     finally:
         ops.end()

@@ -1,0 +1,74 @@
+"""The sharded search through the library's real phases (bvss_dist_* + K7 merge,
+paper_2412_03301_b200/dist.py LibShardOps) on the GPU: two processes, each
+holding one contiguous shard of the database as its own index on cuda:0, the
+collectives over gloo (CUDA tensors staged through the host; only one GPU is
+available here, and the protocol has no kernel that waits on another rank).
+The merged top-k must equal the single-index search exactly (same kernels on
+every (query, set) pair; global top-T by the exact tie protocol)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, cfg_kw, out_dir):
+    import torch
+    import torch.distributed as dist
+    from gen import synth
+    from paper_2412_03301_b200 import bvss as B
+    from paper_2412_03301_b200 import dist as D
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        cfg = synth.get_config(**cfg_kw)
+        g = synth.generate(cfg, device="cuda")
+        lo, hi = D.shard_range(cfg.n, world, rank)
+        off = g["offsets"]
+        vec = g["vectors"][int(off[lo]):int(off[hi])].contiguous()
+        idx = B.Index(vec, (off[lo:hi + 1] - off[lo]).contiguous(), m=cfg.m, s=cfg.s, L=cfg.L, sketch=cfg.sketch,
+                      seed=cfg.seed)
+        ids, dd = D.sharded_search(D.LibShardOps(idx, lo), g["queries"], g["q_offsets"], cfg.k, cfg.T, cfg.n)
+        torch.cuda.synchronize()
+        np.save(os.path.join(out_dir, f"ids{rank}.npy"), ids.cpu().numpy())
+        np.save(os.path.join(out_dir, f"dist{rank}.npy"), dd.cpu().numpy())
+        idx.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,cfg_kw", [(2, dict(name="cfg3", n=6001, nq=9, T=300)),
+                                          (3, dict(name="cfg2", n=3001, nq=5, T=120, d=64)),
+                                          (2, dict(name="cfg1", n=500, nq=6, T=600))])
+def test_sharded_search_equals_single_index(tmp_path, world, cfg_kw):
+    import torch
+    import torch.multiprocessing as mp
+    from gen import synth
+    from paper_2412_03301_b200 import bvss as B
+    if B.device_count() < 1:
+        pytest.fail("no sm_100 device visible to libbvss")
+    port = _free_port()
+    mp.start_processes(_worker, args=(world, port, cfg_kw, str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    cfg = synth.get_config(**cfg_kw)
+    g = synth.generate(cfg, device="cuda")
+    idx = B.Index(g["vectors"], g["offsets"], m=cfg.m, s=cfg.s, L=cfg.L, sketch=cfg.sketch, seed=cfg.seed,
+                  select_mode=1)
+    ref_ids, ref_d = idx.search(g["queries"], g["q_offsets"], cfg.k, cfg.T)
+    idx.close()
+    ref_ids, ref_d = ref_ids.cpu().numpy(), ref_d.cpu().numpy()
+    for r in range(world):
+        ids = np.load(tmp_path / f"ids{r}.npy")
+        dd = np.load(tmp_path / f"dist{r}.npy")
+        np.testing.assert_array_equal(ids, ref_ids)
+        np.testing.assert_array_equal(dd, ref_d)
