@@ -110,6 +110,8 @@ struct ItemTable {
   int q, c0, mq, rep_rows, reps, ntiles;
   int64_t q0, qrow;
   int gq0, gqend;     // group mode: the item's queries [gq0, gqend); tile t holds queries gq0 + 4 tile_grp[t] + quarter
+  int gmq[32];        // group mode: m_q and first padded row of the item's 32 queries (0 / unused past gqend)
+  int64_t gqr[32];
   int8_t tile_grp[kItemCands + 1];
   int8_t ent_quarter[kItemCands];  // group mode: lane quarter (query) of each entry
   int32_t tile_first[kItemCands + 1];  // first table entry of each tile (entries are in tile order)
@@ -372,6 +374,13 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
         rows += static_cast<unsigned long long>(m);
       }
       cursor += nc;
+      {  // the item's queries: m_q and first padded row (one load each, lane = query)
+        const int q = q0 + lane;
+        const bool ok = q < qend;
+        const longlong2 mt = ok ? a.qmeta[q] : make_longlong2(0, 0);
+        t.gmq[lane] = static_cast<int>(mt.x);
+        t.gqr[lane] = mt.y;
+      }
       if (lane == 0) {
         t.tile_first[ntiles] = nent;
         t.nc = nc;
@@ -544,19 +553,12 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
       for (int tile = 0; tile < ntiles; ++tile) {
         const int e0 = t.tile_first[tile], e1 = t.tile_first[tile + 1];
         if (a.group) {  // the tile's 4 queries: q = gq0 + 4 grp + quarter
-          const int qg = t.gq0 + 4 * t.tile_grp[tile] + (lane & 3);
-          uint32_t gb = 0u;
-          int64_t gr = 0;
-          if (lane < 4 && qg < t.gqend) {
-            const longlong2 mt = a.qmeta[qg];
-            gb = static_cast<uint32_t>((static_cast<int>(mt.x) + 7) & ~7) / 8u * KCS * 1024u;
-            gr = mt.y;
-          }
+          const int jb = 4 * t.tile_grp[tile];  // the tile's queries: item slots jb .. jb+3 (table, no global loads)
           qbytes = 0;
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            gbytes[j] = __shfl_sync(0xffffffffu, gb, j);
-            gqrow[j] = __shfl_sync(0xffffffffu, gr, j);
+            gbytes[j] = static_cast<uint32_t>((t.gmq[jb + j] + 7) & ~7) / 8u * KCS * 1024u;
+            gqrow[j] = t.gqr[jb + j];
             qbytes += gbytes[j];
           }
         }
