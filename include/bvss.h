@@ -133,6 +133,19 @@ BVSS_API int bvss_build_index(const float* vectors, const int64_t* set_offsets, 
 BVSS_API int bvss_search(bvss_index* idx, const float* queries, const int64_t* query_offsets, int64_t nq,
                 int32_t k, int32_t T, int64_t* out_ids, float* out_dist, uint32_t flags);
 
+/* Streaming build, for databases larger than host memory (cfg5 is 98 GB): declare the
+ * totals, append sets in order in chunks (vectors [local_offsets[n_chunk]][d] fp32 and local_offsets
+ * [n_chunk+1] starting at 0, host pointers unless p->flags has BVSS_DEVICE_PTRS; the chunk buffers may
+ * be reused when append returns), then finish, which runs the build of bvss_build_index on the
+ * appended data (identical result).  Until finish every search call returns BVSS_ESTATE.
+ * Errors: BVSS_EINVAL (sizes, offsets, more data than declared, finish before all of it arrived),
+ * BVSS_ESTATE (append/finish on a finished index), plus the build errors. */
+BVSS_API int bvss_index_begin(int64_t n_total, int64_t nvec_total, int32_t d, const bvss_params* p,
+                     bvss_index** out);
+BVSS_API int bvss_index_append(bvss_index* idx, const float* vectors, const int64_t* local_offsets,
+                      int64_t n_chunk);
+BVSS_API int bvss_index_finish(bvss_index* idx);
+
 BVSS_API void bvss_free_index(bvss_index* idx);
 BVSS_API const char* bvss_last_error(void);
 BVSS_API int bvss_get_info(const bvss_index* idx, bvss_info* out);

@@ -26,7 +26,8 @@ DEVICE_PTRS, VALIDATE_FINITE, KEEP_CODES = 0x1, 0x2, 0x4
 EXPORTS = (
     "bvss_build_index", "bvss_search", "bvss_free_index", "bvss_last_error", "bvss_get_info", "bvss_get_stats",
     "bvss_set_stream", "bvss_device_count", "bvss_export_projection", "bvss_export_codes", "bvss_export_sketches",
-    "bvss_query_sketch", "bvss_filter", "bvss_refine", "bvss_bruteforce", "bvss_refine_error_bound", "bvss_dist_begin",
+    "bvss_query_sketch", "bvss_filter", "bvss_refine", "bvss_bruteforce", "bvss_index_begin", "bvss_index_append",
+    "bvss_index_finish", "bvss_refine_error_bound", "bvss_dist_begin",
     "bvss_dist_hist", "bvss_dist_resolve", "bvss_dist_tie_counts", "bvss_dist_finish", "bvss_merge_topk",
     "bvss_dist_end",
 )
@@ -84,6 +85,9 @@ def _load():
         "bvss_filter": (C.c_int, [VP, P, P, I64, I32, P, P, U32]),
         "bvss_refine": (C.c_int, [VP, P, P, I64, P, I32, I32, P, P, P, U32]),
         "bvss_bruteforce": (C.c_int, [VP, P, P, I64, I64, I32, P, P, U32]),
+        "bvss_index_begin": (C.c_int, [I64, I64, I32, P, C.POINTER(VP)]),
+        "bvss_index_append": (C.c_int, [VP, P, P, I64]),
+        "bvss_index_finish": (C.c_int, [VP]),
         "bvss_refine_error_bound": (C.c_double, [VP, C.c_double]),
         "bvss_dist_begin": (C.c_int, [VP, P, P, I64, I32, I32, I64, U32, C.POINTER(VP), C.POINTER(I32)]),
         "bvss_dist_hist": (C.c_int, [VP, I32, P]),
@@ -160,6 +164,34 @@ class Index:
             torch.cuda.current_stream(device).synchronize()
         _check(lib.bvss_build_index(vp, op, n, d, C.byref(p), C.byref(self._h)))
         self.n, self.d, self.m, self.s, self.L, self.device = n, d, m, s, L, device
+
+    @classmethod
+    def from_chunks(cls, chunks, *, n_total, nvec_total, d, m, s, L, sketch="binary", seed=0, device=0,
+                    keep_codes=False, projection=None, refine_terms=0, query_batch=0, select_mode=0):
+        """Streaming build (bvss_index_begin / append / finish): `chunks` yields host arrays
+        (vectors [v][d] fp32, local_offsets [c+1] int64 starting at 0), sets in database order."""
+        self = cls.__new__(cls)
+        proj = None if projection is None else np.ascontiguousarray(projection, dtype=np.uint16)
+        p = Params(m=m, s=s, L=L, sketch=SKETCH_BINARY if sketch == "binary" else SKETCH_COUNT_U8, seed=seed,
+                   projection=(proj.ctypes.data if proj is not None else None), device=device,
+                   flags=KEEP_CODES if keep_codes else 0, query_batch=query_batch, refine_terms=refine_terms,
+                   select_mode=select_mode)
+        self._h = C.c_void_p()
+        _check(lib.bvss_index_begin(int(n_total), int(nvec_total), int(d), C.byref(p), C.byref(self._h)))
+        try:
+            for vec, off in chunks:
+                vec = np.ascontiguousarray(vec, dtype=np.float32)
+                off = np.ascontiguousarray(off, dtype=np.int64)
+                _check(lib.bvss_index_append(self._h, C.c_void_p(vec.ctypes.data), C.c_void_p(off.ctypes.data),
+                                             int(off.shape[0]) - 1))
+            _check(lib.bvss_index_finish(self._h))
+        except Exception:
+            lib.bvss_free_index(self._h)
+            self._h = C.c_void_p()
+            raise
+        self.sketch_kind = sketch
+        self.n, self.d, self.m, self.s, self.L, self.device = int(n_total), int(d), m, s, L, device
+        return self
 
     # ------------------------------------------------------------- helpers
     def _bind_stream(self, tensors):

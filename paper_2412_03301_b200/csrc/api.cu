@@ -243,6 +243,13 @@ struct bvss_index {
   void* smp_skx = nullptr;    // the same for the sample
   int32_t* smp_mass = nullptr;
   size_t owned_bytes = 0;
+  // streaming build (bvss_index_begin / append / finish): vectors land in pend_V until finish
+  bool pending = false;
+  int64_t n_total = 0, nvec_total = 0, n_appended = 0, nvec_appended = 0;
+  std::vector<int64_t> pend_off;
+  std::vector<uint16_t> pend_proj;
+  bvss_params pend_p{};
+  float* pend_V = nullptr;
   Workspace ws;
   bvss_stats stats{};
   cudaEvent_t ev[8] = {};
@@ -706,6 +713,7 @@ int make_ctx(bvss_index* idx, const float* queries, const std::vector<int64_t>& 
 
 int validate_search(bvss_index* idx, const float* q, const int64_t* qo, int64_t nq, int k, int T) {
   if (!idx) BVSS_FAIL(BVSS_EINVAL, "null index");
+  if (idx->pending) BVSS_FAIL(BVSS_ESTATE, "streaming build not finished (bvss_index_finish)");
   if (!q || !qo) BVSS_FAIL(BVSS_EINVAL, "null query pointer");
   if (nq < 1) BVSS_FAIL(BVSS_EINVAL, "nq must be >= 1");
   if (k < 1) BVSS_FAIL(BVSS_EINVAL, "k must be >= 1");
@@ -745,11 +753,29 @@ int bvss_device_count(void) {
   return ok;
 }
 
-int bvss_build_index(const float* vectors, const int64_t* set_offsets, int64_t n, int32_t d, const bvss_params* p,
-                     bvss_index** out) {
+}  // extern "C"
+
+namespace {
+int validate_params(int64_t n, int32_t d, const bvss_params* p) {
+  if (n < 1) BVSS_FAIL(BVSS_EINVAL, "n must be >= 1");
+  if (d < 1 || d > 65535) BVSS_FAIL(BVSS_EINVAL, "d must be in [1, 65535]");
+  if (p->m < 32 || p->m % 32 || p->m > 2048) BVSS_FAIL(BVSS_EINVAL, "m must be a multiple of 32 in [32, 2048]");
+  if (p->L < 1 || p->L > p->m) BVSS_FAIL(BVSS_EINVAL, "L must be in [1, m]");
+  if (p->s < 1 || static_cast<int>(p->s) > d || p->s > 32) BVSS_FAIL(BVSS_EINVAL, "s must be in [1, min(d, 32)]");
+  if (p->sketch > 1) BVSS_FAIL(BVSS_EINVAL, "unknown sketch kind");
+  if (p->refine_terms != 0 && p->refine_terms != 1 && p->refine_terms != 3 && p->refine_terms != 255)
+    BVSS_FAIL(BVSS_EINVAL, "refine_terms must be 0 (default), 1, 3 or 255 (exact)");
+  if (p->select_mode > 2) BVSS_FAIL(BVSS_EINVAL, "select_mode must be 0 (auto), 1 (full keys) or 2 (sampled)");
+  return BVSS_OK;
+}
+
+// The build (Algs 1, 3, 5).  adopt_V: a device buffer [nvec][d] the index takes over (streaming build) instead of
+// copying `vectors`.
+int build_impl(const float* vectors, const int64_t* set_offsets, int64_t n, int32_t d, const bvss_params* p,
+               float* adopt_V, bvss_index** out) {
   if (!out) BVSS_FAIL(BVSS_EINVAL, "null out");
   *out = nullptr;
-  if (!vectors || !set_offsets || !p) BVSS_FAIL(BVSS_EINVAL, "null argument");
+  if ((!vectors && !adopt_V) || !set_offsets || !p) BVSS_FAIL(BVSS_EINVAL, "null argument");
   if (n < 1) BVSS_FAIL(BVSS_EINVAL, "n must be >= 1");
   if (d < 1 || d > 65535) BVSS_FAIL(BVSS_EINVAL, "d must be in [1, 65535]");
   if (p->m < 32 || p->m % 32 || p->m > 2048) BVSS_FAIL(BVSS_EINVAL, "m must be a multiple of 32 in [32, 2048]");
@@ -816,9 +842,14 @@ int bvss_build_index(const float* vectors, const int64_t* set_offsets, int64_t n
   BVSS_CUDA(cudaMemcpyAsync(idx->Wt, Wt.data(), Wt.size() * 2, cudaMemcpyHostToDevice, idx->stream));
   BVSS_CUDA(cudaStreamSynchronize(idx->stream));
   // data
-  BVSS_TRY(dalloc(static_cast<size_t>(nvec) * d * 4, reinterpret_cast<void**>(&idx->V)));
+  if (adopt_V) {
+    idx->V = adopt_V;
+    idx->owned_bytes += static_cast<size_t>(nvec) * d * 4;
+  } else {
+    BVSS_TRY(dalloc(static_cast<size_t>(nvec) * d * 4, reinterpret_cast<void**>(&idx->V)));
+  }
   BVSS_TRY(dalloc((n + 1) * 8, reinterpret_cast<void**>(&idx->off)));
-  BVSS_TRY(to_device(idx.get(), idx->V, vectors, static_cast<size_t>(nvec) * d * 4, dev_ptrs));
+  if (!adopt_V) BVSS_TRY(to_device(idx.get(), idx->V, vectors, static_cast<size_t>(nvec) * d * 4, dev_ptrs));
   BVSS_CUDA(cudaMemcpyAsync(idx->off, off_h.data(), (n + 1) * 8, cudaMemcpyHostToDevice, st));
   if (p->flags & BVSS_VALIDATE_FINITE) {
     int* bad;
@@ -888,6 +919,100 @@ int bvss_build_index(const float* vectors, const int64_t* set_offsets, int64_t n
   *out = idx.release();
   return BVSS_OK;
 }
+}  // namespace
+
+extern "C" {
+
+int bvss_build_index(const float* vectors, const int64_t* set_offsets, int64_t n, int32_t d, const bvss_params* p,
+                     bvss_index** out) {
+  return build_impl(vectors, set_offsets, n, d, p, nullptr, out);
+}
+
+int bvss_index_begin(int64_t n_total, int64_t nvec_total, int32_t d, const bvss_params* p, bvss_index** out) {
+  if (!out || !p) BVSS_FAIL(BVSS_EINVAL, "null argument");
+  *out = nullptr;
+  BVSS_TRY(validate_params(n_total, d, p));
+  if (nvec_total < n_total) BVSS_FAIL(BVSS_EINVAL, "nvec_total < n_total (every set has >= 1 vector)");
+  int num_sms = 0;
+  BVSS_TRY(check_device(p->device, &num_sms));
+  DeviceGuard g(p->device);
+  std::unique_ptr<bvss_index> idx(new bvss_index());
+  idx->pending = true;
+  idx->device = p->device;
+  idx->num_sms = num_sms;
+  idx->n_total = n_total;
+  idx->nvec_total = nvec_total;
+  idx->d = d;
+  idx->pend_p = *p;
+  if (p->projection) {
+    idx->pend_proj.assign(p->projection, p->projection + static_cast<size_t>(p->m) * p->s);
+    idx->pend_p.projection = idx->pend_proj.data();
+  }
+  idx->pend_off.assign(1, 0);
+  idx->pend_off.reserve(n_total + 1);
+  BVSS_CUDA(cudaStreamCreateWithFlags(&idx->own_stream, cudaStreamNonBlocking));
+  idx->stream = idx->own_stream;
+  BVSS_CUDA(cudaMalloc(reinterpret_cast<void**>(&idx->pend_V), static_cast<size_t>(nvec_total) * d * 4));
+  *out = idx.release();
+  return BVSS_OK;
+}
+
+int bvss_index_append(bvss_index* idx, const float* vectors, const int64_t* local_offsets, int64_t n_chunk) {
+  if (!idx || !vectors || !local_offsets) BVSS_FAIL(BVSS_EINVAL, "null argument");
+  if (!idx->pending) BVSS_FAIL(BVSS_ESTATE, "index is not in a streaming build");
+  if (n_chunk < 1) BVSS_FAIL(BVSS_EINVAL, "n_chunk must be >= 1");
+  DeviceGuard g(idx->device);
+  const bool dev = (idx->pend_p.flags & BVSS_DEVICE_PTRS) != 0;
+  std::vector<int64_t> lo(n_chunk + 1);
+  if (dev) {
+    BVSS_CUDA(cudaMemcpy(lo.data(), local_offsets, (n_chunk + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  } else {
+    std::memcpy(lo.data(), local_offsets, (n_chunk + 1) * sizeof(int64_t));
+  }
+  BVSS_TRY(check_offsets(lo.data(), n_chunk, "chunk"));
+  if (idx->n_appended + n_chunk > idx->n_total || idx->nvec_appended + lo[n_chunk] > idx->nvec_total)
+    BVSS_FAIL(BVSS_EINVAL, "chunk exceeds the sizes declared at bvss_index_begin");
+  BVSS_CUDA(cudaMemcpyAsync(idx->pend_V + idx->nvec_appended * idx->d, vectors,
+                            static_cast<size_t>(lo[n_chunk]) * idx->d * 4,
+                            dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, idx->stream));
+  BVSS_CUDA(cudaStreamSynchronize(idx->stream));  // the caller may reuse its chunk buffers on return
+  for (int64_t i = 1; i <= n_chunk; ++i) idx->pend_off.push_back(idx->nvec_appended + lo[i]);
+  idx->n_appended += n_chunk;
+  idx->nvec_appended += lo[n_chunk];
+  return BVSS_OK;
+}
+
+int bvss_index_finish(bvss_index* idx) {
+  if (!idx) BVSS_FAIL(BVSS_EINVAL, "null index");
+  if (!idx->pending) BVSS_FAIL(BVSS_ESTATE, "index is not in a streaming build");
+  if (idx->n_appended != idx->n_total || idx->nvec_appended != idx->nvec_total)
+    BVSS_FAIL(BVSS_EINVAL, "appended %lld sets / %lld vectors, declared %lld / %lld",
+              static_cast<long long>(idx->n_appended), static_cast<long long>(idx->nvec_appended),
+              static_cast<long long>(idx->n_total), static_cast<long long>(idx->nvec_total));
+  DeviceGuard g(idx->device);
+  bvss_params p = idx->pend_p;
+  p.flags &= ~BVSS_DEVICE_PTRS;  // offsets are host-side now; vectors are adopted
+  bvss_index* built = nullptr;
+  BVSS_TRY(build_impl(nullptr, idx->pend_off.data(), idx->n_total, idx->d, &p, idx->pend_V, &built));
+  idx->pend_V = nullptr;  // owned by `built` now
+  // move the built state into the caller's handle
+  cudaStream_t old_stream = idx->own_stream;
+  *idx = std::move(*built);
+  built->own_stream = nullptr;
+  built->V = nullptr;
+  built->off = nullptr;
+  built->Wt = nullptr;
+  built->hi = built->lo = nullptr;
+  built->vscale = built->vnorm = nullptr;
+  built->pbase = nullptr;
+  built->codes = nullptr;
+  built->sk = built->smp_sk = built->skx = built->smp_skx = nullptr;
+  built->mass = built->smp_mass = nullptr;
+  for (auto& e : built->ev) e = nullptr;
+  delete built;
+  if (old_stream) cudaStreamDestroy(old_stream);
+  return BVSS_OK;
+}
 
 void bvss_free_index(bvss_index* idx) {
   if (!idx) return;
@@ -898,6 +1023,7 @@ void bvss_free_index(bvss_index* idx) {
                   idx->skx,   idx->smp_skx};
   for (void* p : ptrs)
     if (p) cudaFree(p);
+  if (idx->pend_V) cudaFree(idx->pend_V);
   idx->ws.release();
   for (auto& e : idx->ev)
     if (e) cudaEventDestroy(e);

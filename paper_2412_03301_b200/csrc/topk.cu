@@ -326,10 +326,12 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
       S.hist[tid] = 0u;
       __syncthreads();
 #pragma unroll
-      for (int e = 0; e < kReg; ++e) {
+      for (int e = 0; e < kReg; ++e) {  // warp-aggregated: the values cluster in a few bins
         const uint32_t u = ur[e];
-        if (tid + e * kTxThreads < cnt && (rnd == 0 || (u >> (shift + 8)) == pre))
-          atomicAdd(&S.hist[(u >> shift) & 255u], 1u);
+        const bool in = tid + e * kTxThreads < cnt && (rnd == 0 || (u >> (shift + 8)) == pre);
+        const uint32_t bin = in ? ((u >> shift) & 255u) : 256u;
+        const unsigned peers = __match_any_sync(0xffffffffu, bin);
+        if (in && lane == __ffs(peers) - 1) atomicAdd(&S.hist[bin], static_cast<uint32_t>(__popc(peers)));
       }
       for (int i = tid + kReg * kTxThreads; i < cnt; i += blockDim.x) {
         const uint32_t u = __float_as_uint(ap[i]);

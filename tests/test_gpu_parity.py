@@ -365,3 +365,30 @@ def test_search_range_major_refine(monkeypatch, rng_sets):
         Q = data["queries"][data["q_offsets"][qi]:data["q_offsets"][qi + 1]]
         r_ids, r_d = oi.search(Q, cfg.k, cfg.T)
         check_topk(ids[qi], dist[qi], r_ids, r_d, lambda i: O.hausdorff(Q, V[off[i]:off[i + 1]]))
+
+
+def test_streaming_build_equals_build():
+    """bvss_index_begin / append (uneven chunks) / finish builds the same index as bvss_build_index:
+    identical codes, sketches and search results; search before finish and over-long appends fail."""
+    _need_gpu()
+    cfg = synth.get_config("cfg3", n=3001, nq=5, T=200)
+    data = synth.to_numpy(synth.generate(cfg, device="cpu"))
+    V, off = data["vectors"], data["offsets"]
+    kw = dict(m=cfg.m, s=cfg.s, L=cfg.L, sketch=cfg.sketch, seed=cfg.seed, keep_codes=True)
+    ref = B.Index(V, off, **kw)
+    cuts = [0, 1, 700, 2999, cfg.n]
+
+    def chunks():
+        for a, b in zip(cuts, cuts[1:]):
+            yield V[off[a]:off[b]], off[a:b + 1] - off[a]
+    idx = B.Index.from_chunks(chunks(), n_total=cfg.n, nvec_total=int(off[-1]), d=cfg.d, **kw)
+    assert np.array_equal(idx.export_codes(), ref.export_codes())
+    assert np.array_equal(idx.export_sketches(), ref.export_sketches())
+    r1 = ref.search(data["queries"], data["q_offsets"], cfg.k, cfg.T)
+    r2 = idx.search(data["queries"], data["q_offsets"], cfg.k, cfg.T)
+    assert np.array_equal(r1[0], r2[0]) and np.array_equal(r1[1], r2[1])
+    ref.close()
+    idx.close()
+    with pytest.raises(B.BvssError) as e:  # more data than declared
+        B.Index.from_chunks(chunks(), n_total=cfg.n - 1, nvec_total=int(off[-1]), d=cfg.d, **kw)
+    assert e.value.code == B.EINVAL
