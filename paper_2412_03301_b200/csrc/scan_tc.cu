@@ -64,7 +64,7 @@ struct ScanArgs {
   const uint4* S;              // DB operand [U][n_stride][16 B] (FP4 expansion or u8 counters)
   const int32_t* massS;        // [n]
   int64_t n, n_stride;
-  const uint4* Qx;             // query operand [U][qpad][16 B]
+  const uint4* Qx;             // query operand [qpad/128][U][128 rows][16 B] (query-tile-major)
   const int32_t* massQ;        // [nq]
   int nq, qpad;
   int U;                       // 16-byte K units per row
@@ -241,7 +241,6 @@ __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
     int qt, t;
     bool first, last;
     while (seq.next(qt, t, first, last)) {
-      const int q0 = qt * kScanM;
       const int64_t i0 = static_cast<int64_t>(t) * N;
       const int rows = static_cast<int>(a.n - i0 < N ? a.n - i0 : N);
       if (first && !(MODE == MODE_STREAM)) {  // the stationary tile of this run: U units of [rows][16 B]
@@ -249,10 +248,12 @@ __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
         const uint32_t rrows = ARES ? kScanM : N;
         if (lane == 0) arrive_expect_tx(&S.afull, (ARES ? kScanM : rows) * a.U * 16u);
         __syncwarp();
-        for (int uu = lane; uu < a.U; uu += 32) {
-          if (ARES)
-            bulk_copy(res + uu * (rrows * 16u), a.Qx + static_cast<int64_t>(uu) * a.qpad + q0, kScanM * 16u, &S.afull);
-          else
+        if (ARES) {  // the query tile is one contiguous run of U x 2 KB (query-tile-major Qx)
+          if (lane == 0)
+            bulk_copy(res, a.Qx + static_cast<int64_t>(qt) * a.U * kScanM, static_cast<uint32_t>(a.U) * kScanM * 16u,
+                      &S.afull);
+        } else {
+          for (int uu = lane; uu < a.U; uu += 32)
             bulk_copy(res + uu * (rrows * 16u), a.S + static_cast<int64_t>(uu) * a.n_stride + i0,
                       static_cast<uint32_t>(rows) * 16u, &S.afull);
         }
@@ -279,10 +280,8 @@ __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
           const int uu = 8 * kc + lane;
           bulk_copy(sb + lane * (N * 16u), a.S + static_cast<int64_t>(uu) * a.n_stride + i0,
                     static_cast<uint32_t>(rows) * 16u, &S.full[st]);
-        } else if (!ARES && lane >= 8 && lane < 16) {  // streamed A units
-          const int uu = 8 * kc + (lane - 8);
-          bulk_copy(sa + (lane - 8) * (kScanM * 16u), a.Qx + static_cast<int64_t>(uu) * a.qpad + q0, kScanM * 16u,
-                    &S.full[st]);
+        } else if (!ARES && lane == 8) {  // streamed A: units 8kc .. 8kc+7 of the query tile, one 16 KB run
+          bulk_copy(sa, a.Qx + (static_cast<int64_t>(qt) * a.U + 8 * kc) * kScanM, 8u * kScanM * 16u, &S.full[st]);
         }
       }
       ++tc_;
@@ -500,13 +499,16 @@ __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
   }
 }
 
-// queries -> [U][qpad][16 B]: binary -> FP4 nibbles (32 bits per unit), count -> the uint8 counters (16 per unit)
+// queries -> [qpad/128][U][128][16 B]: binary -> FP4 nibbles (32 bits per unit), count -> the uint8 counters
 __global__ void expand_queries_kernel(int kind, const uint4* __restrict__ SQ /*[nq][cps] row-major chunks*/, int cps,
                                       int nq, int qpad, int U, uint4* __restrict__ Qx) {
+  // query-tile-major [qpad/128][U][128][16 B]: a tile's K units are contiguous (one bulk copy per stage)
   const int64_t total = static_cast<int64_t>(U) * qpad;
   for (int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; t < total;
        t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int q = static_cast<int>(t % qpad), u = static_cast<int>(t / qpad);
+    const int64_t qt = t / (static_cast<int64_t>(U) * 128);
+    const int rem = static_cast<int>(t - qt * U * 128);
+    const int u = rem >> 7, q = static_cast<int>(qt * 128 + (rem & 127));
     uint4 out = make_uint4(0, 0, 0, 0);
     if (q < nq) {
       if (kind == BVSS_SKETCH_BINARY) {
