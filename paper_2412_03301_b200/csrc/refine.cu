@@ -395,6 +395,7 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
         t.gqend = qend;
         t.ntiles = ntiles;
         if (a.rows_counter) atomicAdd(a.rows_counter, rows);
+        if (a.prof) atomicAdd(&a.prof[16], static_cast<unsigned long long>(ntiles));  // developer: tiles
       }
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&S.tab_full[tb]);
@@ -486,6 +487,7 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
         t.qrow = qr;
         t.ntiles = ntiles;
         if (a.rows_counter) atomicAdd(a.rows_counter, rows);
+        if (a.prof) atomicAdd(&a.prof[16], static_cast<unsigned long long>(ntiles));  // developer: tiles
       }
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&S.tab_full[tb]);  // release: the warp's table writes are visible
@@ -901,8 +903,8 @@ int launch_refine_tc(const __half* hs, const __half* ls, const float* vscale, in
   static unsigned long long* prof = nullptr;
   a.prof = nullptr;
   if (getenv("BVSS_REFINE_PROF")) {
-    if (!prof) cudaMalloc(&prof, 16 * sizeof(unsigned long long));
-    cudaMemsetAsync(prof, 0, 16 * sizeof(unsigned long long), st);
+    if (!prof) cudaMalloc(&prof, 17 * sizeof(unsigned long long));
+    cudaMemsetAsync(prof, 0, 17 * sizeof(unsigned long long), st);
     a.prof = prof;
   }
   a.bounds = nullptr;
@@ -980,7 +982,7 @@ int launch_refine_tc(const __half* hs, const __half* ls, const float* vscale, in
   refine_tc_kernel<<<grid, kRefineThreads, smem, st>>>(a);
   BVSS_TRY(post_launch(__func__, st));
   if (a.prof) {  // developer instrumentation: per-CTA average Mcycles per role
-    unsigned long long h[16];
+    unsigned long long h[17];
     cudaMemcpyAsync(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
     const double g = grid;
@@ -990,6 +992,7 @@ int launch_refine_tc(const __half* hs, const __half* ls, const float* vscale, in
             "tfull %.2f, info %.2f)\n",
             h[12] / g / 1e6, h[7] / g / 1e6, h[1] / g / 1e6, h[15] / g / 1e6, h[0] / g / 1e6, h[11] / g / 1e6, h[3] / g / 1e6, h[2] / g / 1e6, h[13] / g / 1e6, h[4] / g / 1e6, h[5] / g / 1e6,
             h[6] / g / 1e6, h[14] / g / 1e6, h[8] / g / 1e6 / kEpiWarps, h[9] / g / 1e6 / kEpiWarps, h[10] / g / 1e6 / kEpiWarps);
+    fprintf(stderr, "[refine prof] tiles %llu (group mode %d)\n", h[16], a.group);
   }
   return BVSS_OK;
 }
