@@ -499,7 +499,10 @@ bool sampled_select_eligible(const bvss_index* idx) {
   if (!use_tc_scan(idx) || idx->ns == 0) return false;
   if (idx->select_mode == 2) return true;
   if (idx->select_mode == 1) return false;
-  return idx->n >= 65536;
+  // auto: binary sketches only.  Count-sketch L2^2 keys of small sets tie massively (a singleton's key
+  // depends only on its overlap with the query), so the emission buffers overflow at the threshold and
+  // the batch would fall back anyway (measured on cfg4: every batch).
+  return idx->n >= 65536 && idx->sketch == BVSS_SKETCH_BINARY;
 }
 
 // Sampled-threshold selection (select_mode 2) for one prepared batch: the
