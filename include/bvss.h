@@ -80,8 +80,9 @@ typedef struct {
   uint32_t select_mode;  /* bvss_search candidate selection: 0 = auto, 1 = full key rows (scan writes every
                             score, radix select over them), 2 = sampled threshold (scan emits only scores <=
                             a per-query threshold estimated on a database sample; exact, with a per-batch
-                            fallback to 1 when the estimate is too low or the buffer overflows).  Auto = 2 when
-                            the tensor-core scan runs (m % 128 == 0) and n >= 65536.  Results are identical. */
+                            fallback to 1 when the estimate is too low or the buffer overflows).  Auto = 2 for
+                            binary sketches when the tensor-core scan runs and n >= 65536 (count-sketch keys
+                            tie massively at the threshold).  Results are identical. */
 } bvss_params;
 
 typedef struct bvss_index bvss_index;
