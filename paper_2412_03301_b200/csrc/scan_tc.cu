@@ -78,6 +78,7 @@ struct ScanArgs {
   uint32_t* buf_key;       // [nq][cap] keys
   int cap;
   int64_t id_base;
+  int dbg;  // developer switch (env BVSS_SCAN_DBG=1): the epilogue only releases the accumulators
 };
 
 template <int KS, int N>
@@ -403,7 +404,9 @@ __global__ void __launch_bounds__(kScanThreads, 1) scan_tc_kernel(ScanArgs a) {
             tc::mbar_arrive(&S.mempty[ms]);
           }
         };
-        if (EMIT) {
+        if (a.dbg) {
+          release();
+        } else if (EMIT) {
           // pass 1: which keys pass (one bit per column), then ONE atomic per thread per tile;
           // pass 2 re-reads only the chunks where some lane emits and writes those entries
           uint32_t(*masks)[32] = S.emit_mask[warp - 2];
@@ -644,6 +647,7 @@ int launch_scan_tc(int kind, const void* S, const int32_t* mass, int64_t n, int6
   a.buf_key = buf_key;
   a.cap = cap;
   a.id_base = id_base;
+  a.dbg = getenv("BVSS_SCAN_DBG") ? atoi(getenv("BVSS_SCAN_DBG")) : 0;
   const size_t a_tile = static_cast<size_t>(kScanM) * U * 16, b_tile = static_cast<size_t>(N) * U * 16;
   const size_t a_stage = static_cast<size_t>(kScanM) * kScanStageB, b_stage = static_cast<size_t>(N) * kScanStageB;
   const size_t budget = kScanSmemBudget;
