@@ -66,6 +66,13 @@ def load_peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "src": "fallback"}
 
 
+def workload_config(cfg, T, k):
+    """The `config` both arms report (the same workload)."""
+    return {"workload": (f"{cfg.name}: n={cfg.n} sets, d={cfg.d}, {cfg.nq} query sets, T={T}, k={k}, "
+                         f"m={cfg.m}, s={cfg.s}, L={cfg.L}, {cfg.sketch} sketch"),
+            "global_batch": cfg.nq}
+
+
 # ------------------------------------------------------------------ clocks --
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -327,11 +334,9 @@ def main_ours(args):
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": ("e2m1 FP4 tensor-core scan (exact 0/1 products), " if cfg.sketch == "binary" else "u8 tensor-core scan, ") + "fp16 tensor-core Gram + exact fp32 fix-up (refine)",
             "data": f"synthetic (gen/synth.py {cfg.name} recipe, noise_mode={args.noise}), generated on GPU",
-            "config": {"workload": (f"{cfg.name}: n={cfg.n} sets, d={cfg.d}, {cfg.nq} query sets, T={T}, k={k}, "
-                                    f"m={cfg.m}, s={cfg.s}, L={cfg.L}, {cfg.sketch} sketch"),
-                       "global_batch": cfg.nq, "parallelism": f"db-shard{world}" if world > 1 else "single-gpu",
-                       "l2": "flushed (256 MB write) before every timed step; DB 27.6 GB fp32 >> L2",
-                       "refine_terms": args.terms, "query_batch": int(idx.stats()["query_batch"])},
+            "config": dict(workload_config(cfg, T, k), parallelism=f"db-shard{world}" if world > 1 else "single-gpu",
+                           l2="flushed (256 MB write) before every timed step; DB 27.6 GB fp32 >> L2",
+                           refine_terms=args.terms, query_batch=int(idx.stats()["query_batch"])),
             "recall@10": recall["recall"] if recall else None,
             "recall": recall,
             "filter_scan_GBps": round(scan_gbs, 1),
@@ -414,8 +419,7 @@ def main_reference(args):
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 1), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64 (oracle)", "impl": "reference",
             "data": f"synthetic ({cfg.name} recipe)",
-            "config": {"workload": f"{cfg.name}: n={cfg.n} sets, d={cfg.d}, T={cfg.T}, k={cfg.k} (one query set "
-                                   f"per step, extrapolated)"},
+            "config": dict(workload_config(cfg, cfg.T, cfg.k), parallelism="cpu-oracle"),
             "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
