@@ -5,9 +5,10 @@
 // G = Q V^T is formed by tcgen05.mma with the QUERY as the A operand (M = 128:
 // the query rows replicated 128/(32*ceil(m_q/32)) times, one replica per TMEM
 // lane quarter) and 256 packed candidate rows as the B operand (N = 256), K = d.
-// Measured on B200 (tools/microbench_umma.cu) a tcgen05.mma costs ~138 cycles
-// whatever N is, so N = 256 candidate rows per instruction is what keeps the
-// tensor pipe off the critical path.  Operands are the scaled fp16 split made at
+// Measured on B200 (tools/microbench_umma.cu, 148 CTAs) a tcgen05.mma M=128 K=16
+// costs ~200-220 cycles whatever N is (64..256; A in shared memory or in TMEM), so
+// N = 256 candidate rows per instruction is what keeps the tensor pipe off the
+// critical path.  Operands are the scaled fp16 split made at
 // build time, x = s (hi + lo) + r with s a power of two >= max|x|; terms = 1
 // issues hi*hi (|error| <= ~2^-10 |x||y|), terms = 3 hi*hi + hi*lo + lo*hi.
 //
@@ -50,7 +51,7 @@ constexpr int kKChunk = 64;      // fp16 per K-chunk = 128 bytes = one SW128 row
 constexpr int kEpiWarps = 8;           // warps 2-5 and 8-11 (two per TMEM lane quarter)
 constexpr int kRefineThreads = 32 * 12;  // 0 copy, 1 MMA, 2-5 epilogue, 6 table, 7 tile info, 8-11 epilogue
 constexpr int kMaxQ = 128;       // query rows the tensor path handles (M)
-constexpr int kMaxStages = 4;
+constexpr int kMaxStages = 8;
 constexpr int kInfoSlots = 4;
 constexpr int kMaxSetsPerTile = kTileRows / 8;
 
@@ -91,6 +92,7 @@ struct RefineArgs {
   // is fetched without its padding rows
   CUtensorMap tm_hi[8], tm_lo[8];
   int tma;                           // developer switch BVSS_REFINE_TMA=1: partial groups by TMA (measured slower)
+  int tail;                          // read only the m real rows of every set (no 8-row padding): BVSS_REFINE_TAIL
   // group mode (all m_q <= 32): an item is (query block, database range, group of 4 queries); the 4
   // queries take one TMEM lane quarter each and share the B tiles of their candidates in the range, and
   // items run range-major inside a query block so the CTAs in flight gather the same range (L2 reuse)
@@ -103,6 +105,13 @@ struct RefineArgs {
   const float2* qpack;               // [nq][32] (|q_i|^2, 2 scale_i) per query row, 0 past m_q (group mode)
   const longlong2* qmeta;            // [nq] (m_q, first padded query row) (group mode)
   int prefetch;                      // developer switch: L2 prefetch of the next tile's rows (env BVSS_REFINE_PREFETCH=1)
+  // A in TMEM (terms = 1, query-major, dpad <= 512): the query is copied once per work item into TMEM
+  // columns [acol, acol + dpad/2) by tcgen05.cp, replicated over the lane quarters by the copy itself
+  // (32x128b.warpx4 / 64x128b.warpx2::02_13 / 128x128b); the stage ring then carries B only, and the
+  // two accumulators take N = ncols columns each (ncols = 160 at dpad = 384)
+  int atmem;
+  int ncols;                         // candidate rows per tile (MMA N); 256 when A is in shared memory
+  uint32_t acol;                     // first TMEM column of the resident query (atmem)
 };
 
 struct ItemTable {
@@ -445,7 +454,7 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
           vb[i] = a.off[cid];
           msz[i] = static_cast<int>(a.off[cid + 1] - vb[i]);
           pb[i] = a.pbase[cid];
-          if (msz[i] > kTileRows) a.out_h2[static_cast<int64_t>(q) * a.T + c0 + c] = 0.0f;  // exact path
+          if (msz[i] > a.ncols) a.out_h2[static_cast<int64_t>(q) * a.T + c0 + c] = 0.0f;  // exact path
         }
       }
       for (int j = lane; j < kMaxQ; j += 32) {
@@ -453,13 +462,13 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
         t.qs2[j] = (j < mq) ? 2.0f * a.qscale[qr + j] : 0.0f;
       }
       // greedy packing: sets whole inside 256-row tiles at 8-aligned columns
-      int ntiles = 0, nent = 0, pos = kTileRows;
+      int ntiles = 0, nent = 0, pos = a.ncols;
       unsigned long long rows = 0;
       for (int c = 0; c < nc; ++c) {
         const int m = __shfl_sync(0xffffffffu, msz[c >> 5], c & 31);
-        if (m > kTileRows) continue;
+        if (m > a.ncols) continue;
         const int mp = (m + 7) & ~7;
-        if (pos + ((m + 15) & ~15) > kTileRows) {  // the epilogue reads 16-column chunks from the set start
+        if (pos + ((m + 15) & ~15) > a.ncols) {  // the epilogue reads 16-column chunks from the set start
           if (lane == 0) t.tile_first[ntiles] = nent;
           ++ntiles;
           pos = 0;
@@ -510,6 +519,9 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
 #pragma unroll
         for (int k = 0; k < kTileRows / 32; ++k) {  // lane owns columns lane + 32k: locate the set, load
           const int j = lane + 32 * k;
+          vn8[k] = 0.0f;
+          vs8[k] = 0.0f;
+          if (32 * k >= a.ncols) continue;
           int lo = e0, hi = e1;  // largest e with ent_col[e] <= j
           while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
@@ -517,8 +529,6 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
             else hi = mid;
           }
           const int r = j - t.ent_col[lo];
-          vn8[k] = 0.0f;
-          vs8[k] = 0.0f;
           if (r < t.ent_m[lo]) {
             vn8[k] = a.vnorm[t.ent_vbase[lo] + r];
             vs8[k] = a.vscale[t.ent_pbase[lo] + r];
@@ -526,6 +536,7 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
         }
 #pragma unroll
         for (int k = 0; k < kTileRows / 32; ++k) {
+          if (32 * k >= a.ncols) continue;
           inf.vn[lane + 32 * k] = vn8[k];
           inf.vs[lane + 32 * k] = vs8[k];
         }
@@ -552,6 +563,18 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
       uint32_t qbytes = static_cast<uint32_t>((mq + 7) & ~7) / 8u * KCS * 1024u;
       uint32_t gbytes[4] = {0u, 0u, 0u, 0u};  // group mode: A bytes / rows of each quarter's query (per tile)
       int64_t gqrow[4] = {0, 0, 0, 0};
+      if (a.atmem) {  // the item's query, one super-chunk per stage, once (the MMA warp copies it into TMEM)
+        for (int ks = 0; ks < KS; ++ks, ++stage_ctr) {
+          const uint32_t st = stage_ctr % NST;
+          PROF_WAIT(1, tc::mbar_wait(&S.empty[st], ((stage_ctr / NST) & 1u) ^ 1u));
+          if (lane == 0) {
+            mbar_arrive_expect_tx(&S.full[st], qbytes);
+            const size_t src = ((static_cast<size_t>(ks) * a.qgroups + (qr >> 3)) * KCS) * 8 * kKChunk;
+            bulk_g2s(ring_s + st * a.stage_bytes, a.qhs + src, qbytes, &S.full[st]);
+          }
+          __syncwarp();
+        }
+      }
       for (int tile = 0; tile < ntiles; ++tile) {
         const int e0 = t.tile_first[tile], e1 = t.tile_first[tile + 1];
         if (a.group) {  // the tile's 4 queries: q = gq0 + 4 grp + quarter
@@ -577,24 +600,31 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
         }
         uint32_t bytes = 0;  // B bytes of one piece of one stage
         for (int e = e0 + lane; e < e1; e += 32)
-          bytes += a.tma ? static_cast<uint32_t>(t.ent_m[e]) * KCS * 128u
+          bytes += (a.tma || a.tail) ? static_cast<uint32_t>(t.ent_m[e]) * KCS * 128u
                          : static_cast<uint32_t>((t.ent_m[e] + 7) & ~7) / 8u * KCS * 1024u;
         bytes = static_cast<uint32_t>(warp_sum(static_cast<int>(bytes)));
-        const uint32_t stage_tx = (three ? 2u : 1u) * (bytes + (a.group ? qbytes : static_cast<uint32_t>(reps) * qbytes));
+        const uint32_t stage_tx = a.atmem ? bytes
+                                          : (three ? 2u : 1u) * (bytes + (a.group ? qbytes : static_cast<uint32_t>(reps) * qbytes));
         for (int ks = 0; ks < KS; ++ks, ++stage_ctr) {
           const uint32_t st = stage_ctr % NST;
           PROF_WAIT(1, tc::mbar_wait(&S.empty[st], ((stage_ctr / NST) & 1u) ^ 1u));
           const uint32_t sbase = ring_s + st * a.stage_bytes;
           const uint32_t a_hi = sbase, a_lo = sbase + a.a_bytes;
-          const uint32_t b_hi = sbase + (three ? 2u : 1u) * a.a_bytes, b_lo = b_hi + a.b_bytes;
+          const uint32_t b_hi = a.atmem ? sbase : sbase + (three ? 2u : 1u) * a.a_bytes, b_lo = b_hi + a.b_bytes;
           if (lane == 0) mbar_arrive_expect_tx(&S.full[st], stage_tx);
           __syncwarp();
           for (int e = e0 + lane; e < e1; e += 32) {
             const int m = t.ent_m[e];
-            const int full = a.tma ? (m >> 3) : ((m + 7) >> 3), rem = a.tma ? (m & 7) : 0;
             const int64_t g0 = t.ent_pbase[e] >> 3;
             const size_t src = ((static_cast<size_t>(ks) * a.pgroups + g0) * KCS) * 8 * kKChunk;
             const uint32_t o = static_cast<uint32_t>(t.ent_col[e]) / 8u * KCS * 1024u;
+            if (a.tail && KCS == 1) {  // one K-chunk per stage: the set's m rows are one contiguous run
+              bulk_g2s(b_hi + o, a.hs + src, static_cast<uint32_t>(m) * 128u, &S.full[st]);
+              if (three) bulk_g2s(b_lo + o, a.ls + src, static_cast<uint32_t>(m) * 128u, &S.full[st]);
+              continue;
+            }
+            const bool part = a.tma || a.tail;
+            const int full = part ? (m >> 3) : ((m + 7) >> 3), rem = part ? (m & 7) : 0;
             if (full) {  // whole 8-row groups: one contiguous run of full * KCS KB
               const uint32_t nb = static_cast<uint32_t>(full) * KCS * 1024u;
               bulk_g2s(b_hi + o, a.hs + src, nb, &S.full[st]);
@@ -603,12 +633,19 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
             if (rem) {  // the last group's rem real rows, one K-chunk at a time (no padding rows read)
               for (int kc = 0; kc < KCS; ++kc) {
                 const uint32_t dst = o + (static_cast<uint32_t>(full) * KCS + kc) * 1024u;
+                if (a.tail) {  // plain bulk copies of the rem pre-swizzled rows of each K-chunk
+                  const size_t so = src + (static_cast<size_t>(full) * KCS + kc) * 8 * kKChunk;
+                  bulk_g2s(b_hi + dst, a.hs + so, static_cast<uint32_t>(rem) * 128u, &S.full[st]);
+                  if (three) bulk_g2s(b_lo + dst, a.ls + so, static_cast<uint32_t>(rem) * 128u, &S.full[st]);
+                  continue;
+                }
                 tma_5d(b_hi + dst, &a.tm_hi[rem - 1], 0, 0, kc, static_cast<int>(g0 + full), ks, &S.full[st]);
                 if (three) tma_5d(b_lo + dst, &a.tm_lo[rem - 1], 0, 0, kc, static_cast<int>(g0 + full), ks, &S.full[st]);
               }
             }
           }
-          if (a.group) {  // group mode: quarter j holds query j's rows (A rows 32j ..)
+          if (a.atmem) {
+          } else if (a.group) {  // group mode: quarter j holds query j's rows (A rows 32j ..)
             if (lane >= 28 && gbytes[lane - 28] > 0) {
               const int j = lane - 28;
               const size_t src = ((static_cast<size_t>(ks) * a.qgroups + (gqrow[j] >> 3)) * KCS) * 8 * kKChunk;
@@ -631,21 +668,47 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
   } else if (warp == 1) {
     // =========================== MMA issuer (one thread) ===========================
     uint32_t stage_ctr = 0, tile_ctr = 0;
-    const uint32_t idesc = tc::idesc_f16_f32(128, kTileRows);
+    const uint32_t idesc = tc::idesc_f16_f32(128, a.ncols);
     for (uint32_t it = 0;; ++it) {
       const int tb = it & 1;
       const ItemTable& t = S.tab[tb];
       PROF_WAIT(4, tc::mbar_wait(&S.tab_full[tb], (it >> 1) & 1u));
       const int nc = t.nc;
       if (nc < 0) break;
-      const int ntiles = t.ntiles;
+      const int ntiles = t.ntiles, rep_rows = t.rep_rows;
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&S.tab_empty[tb]);  // the MMA warp needs nothing else from the table
+      if (a.atmem) {  // the query into TMEM (the tcgen05 pipe keeps issue order: the previous item's MMAs
+                      // have read the old query before these copies overwrite it)
+        for (int ks = 0; ks < KS; ++ks, ++stage_ctr) {
+          const uint32_t st = stage_ctr % NST;
+          PROF_WAIT(6, tc::mbar_wait(&S.full[st], (stage_ctr / NST) & 1u));
+          tc::fence_after_sync();
+          if (lane == 0) {
+            const uint32_t sbase = ring_s + st * a.stage_bytes;
+            for (int kc = 0; kc < KCS; ++kc) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {  // 16-byte K slices: 4 TMEM columns each
+                const uint32_t col = tmem + a.acol + static_cast<uint32_t>((ks * KCS + kc) * 32 + j * 4);
+                const uint64_t d = sw128_desc_sbo(sbase + kc * 1024u + j * 16u, sbo);
+                if (rep_rows == 32)
+                  asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(col), "l"(d) : "memory");
+                else if (rep_rows == 64)
+                  asm volatile("tcgen05.cp.cta_group::1.64x128b.warpx2::02_13 [%0], %1;" ::"r"(col), "l"(d) : "memory");
+                else
+                  asm volatile("tcgen05.cp.cta_group::1.128x128b [%0], %1;" ::"r"(col), "l"(d) : "memory");
+              }
+            }
+            tc::umma_commit(&S.empty[st]);
+          }
+          __syncwarp();
+        }
+      }
       for (int tile = 0; tile < ntiles; ++tile, ++tile_ctr) {
         const uint32_t acc = tile_ctr & 1u;
         PROF_WAIT(5, tc::mbar_wait(&S.tempty[acc], ((tile_ctr >> 1) & 1u) ^ 1u));
         tc::fence_after_sync();
-        const uint32_t d_tmem = tmem + acc * kTileRows;
+        const uint32_t d_tmem = tmem + acc * a.ncols;
         for (int ks = 0; ks < KS; ++ks, ++stage_ctr) {
           const uint32_t st = stage_ctr % NST;
           PROF_WAIT(6, tc::mbar_wait(&S.full[st], (stage_ctr / NST) & 1u));
@@ -653,12 +716,21 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
           if (lane == 0) {
             const uint32_t sbase = ring_s + st * a.stage_bytes;
             const uint32_t a_hi = sbase, a_lo = sbase + a.a_bytes;
-            const uint32_t b_hi = sbase + (three ? 2u : 1u) * a.a_bytes, b_lo = b_hi + a.b_bytes;
+            const uint32_t b_hi = a.atmem ? sbase : sbase + (three ? 2u : 1u) * a.a_bytes, b_lo = b_hi + a.b_bytes;
             for (int kc = 0; kc < KCS; ++kc) {
 #pragma unroll
               for (int kk = 0; kk < kKChunk / 16; ++kk) {
                 const uint32_t koff = kc * 1024u + kk * 32u;
                 const uint32_t accum = (ks | kc | kk) ? 1u : 0u;
+                if (a.atmem) {
+                  const uint32_t acol = tmem + a.acol + static_cast<uint32_t>((ks * KCS + kc) * 32 + kk * 8);
+                  asm volatile(
+                      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+                      "r"(acol), "l"(sw128_desc_sbo(b_hi + koff, sbo)), "r"(idesc), "r"(accum)
+                      : "memory");
+                  continue;
+                }
                 tc::umma_bf16(d_tmem, sw128_desc_sbo(a_hi + koff, sbo), sw128_desc_sbo(b_hi + koff, sbo), idesc,
                               accum);
                 if (three) {
@@ -702,7 +774,7 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
         PROF_WAIT(9, tc::mbar_wait(&S.tfull[acc], (tile_ctr >> 1) & 1u));
         PROF_WAIT(10, tc::mbar_wait(&S.info_full[slot], (tile_ctr / kInfoSlots) & 1u));
         tc::fence_after_sync();
-        const uint32_t tbase = tmem + acc * kTileRows + (static_cast<uint32_t>(ew * 32) << 16);
+        const uint32_t tbase = tmem + acc * a.ncols + (static_cast<uint32_t>(ew * 32) << 16);
         const int e0 = inf.first, ne = inf.count;
         if (a.group && t.tile_grp[tile] != gcur) {  // this quarter's query for the tile's group
           gcur = t.tile_grp[tile];
@@ -858,9 +930,9 @@ int refine_kcs(int dpad) {
   return (dpad / kKChunk) % 2 == 0 ? 2 : 1;
 }
 
-size_t refine_smem_bytes(int terms, int KCS, int& stages, uint32_t& stage_bytes) {
-  const uint32_t a_bytes = 128u * KCS * 128u, b_bytes = kTileRows * KCS * 128u;
-  stage_bytes = (terms == 3 ? 2u : 1u) * (a_bytes + b_bytes);
+size_t refine_smem_bytes(int terms, int KCS, int atmem, int ncols, int& stages, uint32_t& stage_bytes) {
+  const uint32_t a_bytes = 128u * KCS * 128u, b_bytes = static_cast<uint32_t>(ncols) * KCS * 128u;
+  stage_bytes = atmem ? b_bytes : (terms == 3 ? 2u : 1u) * (a_bytes + b_bytes);
   const size_t ctrl = (sizeof(RefineCtl) + 127) & ~size_t(127);  // static __shared__
   const size_t budget = 227 * 1024 - 1024 - ctrl;
   stages = static_cast<int>(budget / stage_bytes);
@@ -884,14 +956,6 @@ int launch_refine_tc(const __half* hs, const __half* ls, const float* vscale, in
   a.qhs = qhs; a.qls = qls; a.qscale = qscale; a.qgroups = qrows / 8; a.qrow = qrow; a.qnorm = qnorm; a.qoff = qoff;
   a.cand = cand; a.count = count; a.T = T; a.nq = nq; a.id_base = id_base; a.out_h2 = out_h2;
   a.terms = terms == 3 ? 3 : 1;
-  int stages;
-  uint32_t stage_bytes;
-  const size_t smem = refine_smem_bytes(a.terms, a.KCS, stages, stage_bytes);
-  if (stages < 1) BVSS_FAIL(BVSS_EUNSUPPORTED, "refine stage does not fit shared memory");
-  a.stages = stages;
-  a.stage_bytes = stage_bytes;
-  a.a_bytes = 128u * a.KCS * 128u;
-  a.b_bytes = kTileRows * a.KCS * 128u;
   a.items_per_query = ceil_div(T, kItemCands);
   a.total_items = a.items_per_query * nq;
   a.work_counter = work_counter;
@@ -950,6 +1014,9 @@ int launch_refine_tc(const __half* hs, const __half* ls, const float* vscale, in
   {  // TMA maps for the partial last group of every set (h = 1..8 rows)
     const char* e = getenv("BVSS_REFINE_TMA");  // developer switch: 0 = copy whole padded groups
     a.tma = e ? atoi(e) : 0;
+    const char* f = getenv("BVSS_REFINE_TAIL");
+    a.tail = f ? atoi(f) : 0;
+    if (a.tail) a.tma = 0;
   }
   if (a.tma) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
@@ -976,6 +1043,37 @@ int launch_refine_tc(const __half* hs, const __half* ls, const float* vscale, in
       }
     }
   }
+  // A in TMEM: one term, query-major, and TMEM room for the query (dpad/2 columns)
+  // next to two accumulators of at least 128 columns
+  a.atmem = 0;
+  a.ncols = kTileRows;
+  a.acol = 0;
+  {
+    // developer switch BVSS_REFINE_ATMEM=1, off by default: measured slower (67.6 vs 53.9 ms at cfg3,
+    // tools/ab_env.py): a tcgen05.mma costs ~200 cycles whatever N (tools/microbench_umma.cu), so the
+    // narrower N = 160 tiles the TMEM budget leaves cost 1.6x the MMA time per candidate row
+    const char* e = getenv("BVSS_REFINE_ATMEM");
+    const int want = e ? atoi(e) : 0;
+    const int ncols = ((512 - dpad / 2) / 2) & ~15;
+    if (want && a.terms == 1 && !a.group && !a.tma && !a.tail && ncols >= 128) {
+      a.atmem = 1;
+      a.ncols = ncols < kTileRows ? ncols : kTileRows;
+      a.acol = static_cast<uint32_t>(2 * a.ncols);
+    }
+    if (const char* f = getenv("BVSS_REFINE_NCOLS")) {  // developer switch: tile width (multiple of 16)
+      const int nf = atoi(f);
+      if (nf >= 32 && nf % 16 == 0 && nf <= a.ncols) a.ncols = nf;
+      if (a.atmem) a.acol = 512u - static_cast<uint32_t>(dpad / 2);
+    }
+  }
+  int stages;
+  uint32_t stage_bytes;
+  const size_t smem = refine_smem_bytes(a.terms, a.KCS, a.atmem, a.ncols, stages, stage_bytes);
+  if (stages < 1) BVSS_FAIL(BVSS_EUNSUPPORTED, "refine stage does not fit shared memory");
+  a.stages = stages;
+  a.stage_bytes = stage_bytes;
+  a.a_bytes = 128u * a.KCS * 128u;
+  a.b_bytes = static_cast<uint32_t>(a.ncols) * a.KCS * 128u;
   BVSS_CUDA(cudaMemsetAsync(work_counter, 0, sizeof(int), st));
   BVSS_CUDA(cudaFuncSetAttribute(refine_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const int grid = a.total_items < num_sms ? a.total_items : num_sms;
