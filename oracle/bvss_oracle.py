@@ -263,7 +263,7 @@ def hausdorff(Q: np.ndarray, V: np.ndarray) -> float:
 
 def meanmin_from_dist(Dm: np.ndarray) -> float:
     """MeanMin distance d_mean-min(A, B) = 1/|A| sum_{a in A} min_b d(a, b)
-    (P:196), on Dm[a][b].  Used only as a §3.2 pin."""
+    (P:196), on Dm[a][b]."""
     Dm = np.asarray(Dm, dtype=np.float64)
     return float(Dm.min(axis=1).mean())
 
@@ -271,6 +271,24 @@ def meanmin_from_dist(Dm: np.ndarray) -> float:
 def min_from_dist(Dm: np.ndarray) -> float:
     """Min distance d_min(A, B) = min_{a,b} d(a, b)."""
     return float(np.min(Dm))
+
+
+METRICS = ("hausdorff", "meanmin", "min")
+
+
+def set_distance(Q: np.ndarray, V: np.ndarray, metric: str = "hausdorff") -> float:
+    """The rerank distance between the query set Q and a database set V, fp64
+    direct differences: Hausdorff (Def 4; the paper's metric), or
+    the §3.2 alternatives: MeanMin d_mean-min(Q, V)
+    (A = the query set, reading R23) and Min d_min(Q, V)."""
+    Dm = pairwise_dist(Q, V)
+    if metric == "hausdorff":
+        return hausdorff_from_dist(Dm)
+    if metric == "meanmin":
+        return meanmin_from_dist(Dm)
+    if metric == "min":
+        return min_from_dist(Dm)
+    raise ValueError(metric)
 
 
 def hausdorff_gram(Q: np.ndarray, V: np.ndarray) -> float:
@@ -283,13 +301,15 @@ def hausdorff_gram(Q: np.ndarray, V: np.ndarray) -> float:
     return hausdorff_from_dist(np.sqrt(np.maximum(d2, 0.0)))
 
 
-def refine(Q: np.ndarray, cand: np.ndarray, vectors: np.ndarray, offsets: np.ndarray) -> np.ndarray:
+def refine(Q: np.ndarray, cand: np.ndarray, vectors: np.ndarray, offsets: np.ndarray,
+           metric: str = "hausdorff") -> np.ndarray:
     """Alg 6 lines 19-22 (iterating F2 per reading R5): exact
-    Haus(Q, V_i) for every candidate i.  Returns fp64 ``[len(cand)]``."""
+    Haus(Q, V_i) (or the MeanMin / Min alternative, ``set_distance``) for every
+    candidate i.  Returns fp64 ``[len(cand)]``."""
     o = np.asarray(offsets, dtype=np.int64)
     out = np.empty(len(cand), dtype=np.float64)
     for t, i in enumerate(np.asarray(cand, dtype=np.int64)):
-        out[t] = hausdorff(Q, vectors[o[i]:o[i + 1]])
+        out[t] = set_distance(Q, vectors[o[i]:o[i + 1]], metric)
     return out
 
 
@@ -361,21 +381,21 @@ class OracleIndex:
     def set_vectors(self, i: int) -> np.ndarray:
         return self.vectors[self.offsets[i]:self.offsets[i + 1]]
 
-    def search(self, Q, k: int, T: int):
+    def search(self, Q, k: int, T: int, metric: str = "hausdorff"):
         """Alg 6 with F1 = D: filter to T candidates, exact
-        Hausdorff rerank, top-k by (distance, id)."""
+        Hausdorff (or MeanMin / Min) rerank, top-k by (distance, id)."""
         if T < k:
             raise ValueError("T < k (reading R16)")
         cand = self.filter(Q, T)
-        dist = refine(Q, cand, self.vectors, self.offsets)
+        dist = refine(Q, cand, self.vectors, self.offsets, metric)
         return top_k(cand, dist, k)
 
-    def bruteforce(self, Q, k: int, limit: int | None = None):
+    def bruteforce(self, Q, k: int, limit: int | None = None, metric: str = "hausdorff"):
         """Exact top-k over all sets ("precise calculations according to
         Definition 4")."""
         n = self.n if limit is None else min(limit, self.n)
         ids = np.arange(n, dtype=np.int64)
-        dist = refine(Q, ids, self.vectors, self.offsets)
+        dist = refine(Q, ids, self.vectors, self.offsets, metric)
         return top_k(ids, dist, k)
 
 

@@ -317,6 +317,46 @@ def test_hausdorff_singletons_closed_form():
 
 # ----------------------------------------------------------------- top-k and the whole path
 
+def test_set_distance_point_sets_hand_computed():
+    """MeanMin / Min / Hausdorff on 1-D point sets whose distance matrix is
+    worked out by hand: Q = {0, 10}, A = {1, 7} -> d(Q,A) = [[1, 7], [9, 3]]:
+    MeanMin(Q, A) = (1 + 3) / 2 = 2 (P:196), Min = 1 (P:193), Haus = 3 (Def 4);
+    MeanMin(A, Q) = (1 + 3) / 2 = 2.  Q = {0, 10}, B = {1, 9, 30}:
+    d = [[1, 9, 30], [9, 1, 20]] -> MeanMin(Q, B) = 1, MeanMin(B, Q) = (1 + 1 + 20) / 3,
+    Min = 1, Haus = 20 (the asymmetry of §3.2)."""
+    Q = np.array([[0.0], [10.0]])
+    A = np.array([[1.0], [7.0]])
+    B = np.array([[1.0], [9.0], [30.0]])
+    assert O.set_distance(Q, A, "meanmin") == 2.0
+    assert O.set_distance(A, Q, "meanmin") == 2.0
+    assert O.set_distance(Q, A, "min") == 1.0
+    assert O.set_distance(Q, A, "hausdorff") == 3.0
+    assert O.set_distance(Q, B, "meanmin") == 1.0
+    assert O.set_distance(B, Q, "meanmin") == pytest.approx(22.0 / 3.0)
+    assert O.set_distance(Q, B, "min") == O.set_distance(B, Q, "min") == 1.0
+    assert O.set_distance(Q, B, "hausdorff") == O.set_distance(B, Q, "hausdorff") == 20.0
+
+
+def test_set_distance_singletons_order_and_brute_force():
+    """Singletons: all three metrics reduce to ||q - v|| (Def 4).
+    Random sets: Min <= MeanMin <= max_q min_v <= Haus, and MeanMin equals a
+    pure-Python double loop."""
+    rng = np.random.default_rng(11)
+    q, v = rng.normal(size=(1, 5)), rng.normal(size=(1, 5))
+    e = float(np.sqrt(((q - v) ** 2).sum()))
+    for mt in O.METRICS:
+        assert O.set_distance(q, v, mt) == pytest.approx(e, rel=1e-15)
+    for _ in range(20):
+        Q = rng.normal(size=(rng.integers(1, 6), 3))
+        V = rng.normal(size=(rng.integers(1, 6), 3))
+        mn, mm, h = (O.set_distance(Q, V, mt) for mt in ("min", "meanmin", "hausdorff"))
+        assert mn <= mm + 1e-12 and mm <= h + 1e-12
+        loop = 0.0
+        for a in Q:
+            loop += min(sum((float(a[t]) - float(b[t])) ** 2 for t in range(3)) ** 0.5 for b in V)
+        assert mm == pytest.approx(loop / len(Q), rel=1e-12)
+
+
 def test_top_k_order_and_padding():
     ids, d = O.top_k(np.array([7, 3, 5]), np.array([0.5, 0.5, 0.1]), 5)
     assert ids.tolist() == [5, 3, 7, -1, -1]
