@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--terms", type=int, default=0, choices=[0, 1, 3, 255])
     ap.add_argument("--noise", default="per_coord", choices=["per_coord", "total"])
+    ap.add_argument("--metric", default="hausdorff", choices=["hausdorff", "meanmin", "min"],
+                    help="rerank distance (default: the paper's Hausdorff; MeanMin / Min are the §3.2 alternatives)")
     ap.add_argument("--recall-queries", type=int, default=100)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -122,7 +124,7 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------- cpu baseline --
-def oracle_sample(cfg, T, k, n_sample=10000, q_sample=3, seed_shift=0):
+def oracle_sample(cfg, T, k, n_sample=10000, q_sample=3, seed_shift=0, metric="hausdorff"):
     """The oracle (as it stands, single-threaded numpy) on a bounded sample of
     the workload: a DB of n_sample sets drawn by the same generator recipe, and
     q_sample query sets.  Per query it times the query encode+sketch (a-4), the
@@ -146,7 +148,7 @@ def oracle_sample(cfg, T, k, n_sample=10000, q_sample=3, seed_shift=0):
         scores = O.hamming_scores(sq, oi.sketches) if cfg.sketch == "binary" else O.count_l2_scores(sq, oi.sketches)
         cand = O.select_top_T(scores, Tr)
         t2 = time.perf_counter()
-        dist = O.refine(Q, cand, oi.vectors, oi.offsets)
+        dist = O.refine(Q, cand, oi.vectors, oi.offsets, metric)
         O.top_k(cand, dist, k)
         t3 = time.perf_counter()
         t_enc += t1 - t0
@@ -207,7 +209,7 @@ def main_ours(args):
     b1 = torch.cuda.Event(enable_timing=True)
     b0.record()
     idx = B.Index(vec, off, m=cfg.m, s=cfg.s, L=cfg.L, sketch=cfg.sketch, seed=cfg.seed, device=local,
-                  refine_terms=args.terms)
+                  refine_terms=args.terms, metric=args.metric)
     b1.record()
     torch.cuda.synchronize()
     build_ms = b0.elapsed_time(b1)
@@ -324,7 +326,7 @@ def main_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        qps, sample, secs = oracle_sample(cfg, T, k)
+        qps, sample, secs = oracle_sample(cfg, T, k, metric=args.metric)
         cpu = {"value": round(qps, 4), "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
                "cpu_seconds": round(secs, 1)}
 
@@ -336,7 +338,8 @@ def main_ours(args):
             "data": f"synthetic (gen/synth.py {cfg.name} recipe, noise_mode={args.noise}), generated on GPU",
             "config": dict(workload_config(cfg, T, k), parallelism=f"db-shard{world}" if world > 1 else "single-gpu",
                            l2="flushed (256 MB write) before every timed step; DB 27.6 GB fp32 >> L2",
-                           refine_terms=args.terms, query_batch=int(idx.stats()["query_batch"])),
+                           refine_terms=args.terms, query_batch=int(idx.stats()["query_batch"]),
+                           **({} if args.metric == "hausdorff" else {"metric": args.metric})),
             "recall@10": recall["recall"] if recall else None,
             "recall": recall,
             "filter_scan_GBps": round(scan_gbs, 1),
@@ -406,11 +409,12 @@ def main_reference(args):
         over["T"] = args.T
     cfg = synth.get_config(args.config, **over)
     for w in range(args.warmup):
-        oracle_sample(cfg, cfg.T, cfg.k, n_sample=2000, q_sample=1, seed_shift=100 + w)
+        oracle_sample(cfg, cfg.T, cfg.k, n_sample=2000, q_sample=1, seed_shift=100 + w, metric=args.metric)
     vals, secs = [], 0.0
     sample = ""
     for s in range(args.steps):
-        qps, sample, sec = oracle_sample(cfg, cfg.T, cfg.k, n_sample=5000, q_sample=1, seed_shift=s)
+        qps, sample, sec = oracle_sample(cfg, cfg.T, cfg.k, n_sample=5000, q_sample=1, seed_shift=s,
+                                         metric=args.metric)
         vals.append(1.0 / qps)
         secs += sec
     ms_per_step = statistics.mean(vals) * 1000.0
@@ -419,7 +423,8 @@ def main_reference(args):
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 1), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64 (oracle)", "impl": "reference",
             "data": f"synthetic ({cfg.name} recipe)",
-            "config": dict(workload_config(cfg, cfg.T, cfg.k), parallelism="cpu-oracle"),
+            "config": dict(workload_config(cfg, cfg.T, cfg.k), parallelism="cpu-oracle",
+                           **({} if args.metric == "hausdorff" else {"metric": args.metric})),
             "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
             "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)

@@ -83,7 +83,13 @@ typedef struct {
                             fallback to 1 when the estimate is too low or the buffer overflows).  Auto = 2 for
                             binary sketches when the tensor-core scan runs and n >= 65536 (count-sketch keys
                             tie massively at the threshold).  Results are identical. */
+  uint32_t metric;       /* rerank distance (bvss_metric): 0 = Hausdorff (Def 4; the paper's
+                            metric), 1 = MeanMin d_mean-min(Q, V) = 1/|Q| sum_q min_v ||q - v|| (the
+                            query set first, reading R23), 2 = Min d_min(Q, V) = min ||q - v||.
+                            The §3.2 alternatives; the filter is unchanged. */
 } bvss_params;
+
+typedef enum { BVSS_METRIC_HAUSDORFF = 0, BVSS_METRIC_MEANMIN = 1, BVSS_METRIC_MIN = 2 } bvss_metric;
 
 typedef struct bvss_index bvss_index;
 
@@ -180,7 +186,8 @@ BVSS_API int bvss_filter(bvss_index* idx, const float* queries, const int64_t* q
 /* Refine (a-7 + a-8: Alg 6 lines 19-23): given candidate lists (as from
  * bvss_filter, -1 padded), compute the tensor-core Hausdorff of every candidate
  * and the exact top-k.  out_approx [nq][T] fp32 receives the tensor-core
- * squared Hausdorff per candidate (NaN where cand == -1; may be NULL). */
+ * value per candidate (NaN where cand == -1; may be NULL): the squared
+ * distance for Hausdorff and Min, the distance for MeanMin (bvss_params.metric). */
 BVSS_API int bvss_refine(bvss_index* idx, const float* queries, const int64_t* query_offsets, int64_t nq,
                 const int32_t* cand, int32_t T, int32_t k, int64_t* out_ids, float* out_dist,
                 float* out_approx, uint32_t flags);

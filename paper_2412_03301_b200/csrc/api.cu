@@ -96,12 +96,14 @@ int launch_refine_tc(const __half* hs, const __half* ls, const float* vscale, in
                      const float* vnorm, const int64_t* off, int dpad, const __half* qhs, const __half* qls,
                      const float* qscale, int64_t qrows, const int64_t* qrow, const float* qnorm, const int64_t* qoff, int max_mq, const int32_t* cand,
                      const int32_t* count, int T, int nq, int64_t id_base, float* out_h2, int terms, int* work_counter,
-                     unsigned long long* rows_counter, int num_sms, int64_t n_local, int32_t* bounds, cudaStream_t st);
+                     unsigned long long* rows_counter, int num_sms, int64_t n_local, int32_t* bounds, int metric,
+                     float* out_err, float c1, float c2, float vmax2, cudaStream_t st);
 int64_t refine_range_sets(int64_t n_local, int64_t prows, int dpad, int T);
 int launch_topk_fixup(const float* approx, const int32_t* cand, const int32_t* count, int T, int k, const float* V,
                       const int64_t* off, int64_t id_base, int d, const float* Qv, const int64_t* qoff,
                       const float* qnorm, float vmax2, float c1, float c2, int exact_all, int64_t* out_ids,
-                      float* out_dist, int nq, int64_t* fixup_counter, void* scratch, cudaStream_t st);
+                      float* out_dist, int nq, int64_t* fixup_counter, void* scratch, int metric,
+                      const float* approx_err, cudaStream_t st);
 int launch_merge_topk(const int64_t* ids, const float* dist, int P, int64_t nq, int k, int64_t* out_ids,
                       float* out_dist, cudaStream_t st);
 
@@ -237,6 +239,7 @@ struct bvss_index {
   void* sk = nullptr;         // chunk-major sketches
   int32_t* mass = nullptr;
   uint32_t select_mode = 0;   // 0 auto, 1 full keys, 2 sampled threshold
+  int metric = 0;             // rerank metric: 0 Hausdorff, 1 MeanMin, 2 Min (bvss_params.metric)
   int64_t ns = 0;             // database sample for the threshold estimate (select_mode 2)
   void* smp_sk = nullptr;     // chunk-major sketches of the sample
   void* skx = nullptr;        // binary: tensor-core scan operand, FP4 expansion [m/32][n][16 B] (scan_tc.cu)
@@ -284,6 +287,7 @@ struct bvss_search_ctx {
   int32_t* count = nullptr;
   bool cand_sorted = true;    // candidate lists in ascending id order (the refine may then run range-major)
   float* approx = nullptr;
+  float* approx_err = nullptr; // MeanMin: per-candidate bound on |approx - exact| (refine.cu)
   void* qsk = nullptr;        // query sketches, row-major padded to whole chunks
   int32_t* qmass = nullptr;   // query sketch masses
   uint32_t* qcodes = nullptr; // query codes
@@ -642,9 +646,13 @@ int fallback_full(bvss_index* idx, bvss_search_ctx* c) {
 int refine_topk(bvss_index* idx, bvss_search_ctx* c, int64_t* out_ids_dev, float* out_dist_dev) {
   const int nq = static_cast<int>(c->nq);
   int exact_all = 0;
+  float c1, c2;
+  error_consts(idx, &c1, &c2);
   if (idx->terms != 0 && c->max_mq <= 128) {  // tensor path: query rows fit the M=128 tile
     if (!c->approx)  // once per context (brute force calls this per chunk)
       BVSS_TRY(c->alloc(static_cast<size_t>(nq) * c->T * sizeof(float), reinterpret_cast<void**>(&c->approx)));
+    if (idx->metric == 1 && !c->approx_err)
+      BVSS_TRY(c->alloc(static_cast<size_t>(nq) * c->T * sizeof(float), reinterpret_cast<void**>(&c->approx_err)));
     int* counter;
     BVSS_TRY(idx->ws.get("work_counter", sizeof(int), reinterpret_cast<void**>(&counter)));
     unsigned long long* rows;
@@ -662,14 +670,13 @@ int refine_topk(bvss_index* idx, bvss_search_ctx* c, int64_t* out_ids_dev, float
     BVSS_TRY(launch_refine_tc(idx->hi, idx->lo, idx->vscale, idx->prows, idx->pbase, idx->vnorm, idx->off, idx->dpad, c->qhi,
                               c->qlo, c->qscale, c->qrows,
                               c->qrow, c->qnorm, c->qoff, c->max_mq, c->cand, c->count, c->T, nq, c->id_base,
-                              c->approx, idx->terms, counter, rows, idx->num_sms, c->cand_sorted ? idx->n : 0, bounds, idx->stream));
+                              c->approx, idx->terms, counter, rows, idx->num_sms, c->cand_sorted ? idx->n : 0, bounds,
+                              idx->metric, c->approx_err, c1, c2, idx->vmax2, idx->stream));
     idx->stats.kernel_launches += 1;
   } else {
     exact_all = 1;
   }
   cudaEventRecord(idx->ev[5], idx->stream);
-  float c1, c2;
-  error_consts(idx, &c1, &c2);
   int64_t* fix;
   BVSS_TRY(idx->ws.get("fixup_counter", sizeof(int64_t), reinterpret_cast<void**>(&fix)));
   BVSS_CUDA(cudaMemsetAsync(fix, 0, sizeof(int64_t), idx->stream));
@@ -677,7 +684,7 @@ int refine_topk(bvss_index* idx, bvss_search_ctx* c, int64_t* out_ids_dev, float
   BVSS_TRY(idx->ws.get("topk_scratch", static_cast<size_t>(nq) * c->T * 8, &scratch));
   BVSS_TRY(launch_topk_fixup(c->approx, c->cand, c->count, c->T, c->k, idx->V, idx->off, c->id_base, idx->d, c->qv,
                              c->qoff, c->qnorm, idx->vmax2, c1, c2, exact_all, out_ids_dev, out_dist_dev, nq, fix,
-                             scratch, idx->stream));
+                             scratch, idx->metric, c->approx_err, idx->stream));
   cudaEventRecord(idx->ev[6], idx->stream);
   idx->stats.kernel_launches += 1;
   return BVSS_OK;
@@ -769,6 +776,7 @@ int validate_params(int64_t n, int32_t d, const bvss_params* p) {
   if (p->refine_terms != 0 && p->refine_terms != 1 && p->refine_terms != 3 && p->refine_terms != 255)
     BVSS_FAIL(BVSS_EINVAL, "refine_terms must be 0 (default), 1, 3 or 255 (exact)");
   if (p->select_mode > 2) BVSS_FAIL(BVSS_EINVAL, "select_mode must be 0 (auto), 1 (full keys) or 2 (sampled)");
+  if (p->metric > 2) BVSS_FAIL(BVSS_EINVAL, "metric must be 0 (Hausdorff), 1 (MeanMin) or 2 (Min)");
   return BVSS_OK;
 }
 
@@ -788,6 +796,7 @@ int build_impl(const float* vectors, const int64_t* set_offsets, int64_t n, int3
   if (p->refine_terms != 0 && p->refine_terms != 1 && p->refine_terms != 3 && p->refine_terms != 255)
     BVSS_FAIL(BVSS_EINVAL, "refine_terms must be 0 (default), 1, 3 or 255 (exact)");
   if (p->select_mode > 2) BVSS_FAIL(BVSS_EINVAL, "select_mode must be 0 (auto), 1 (full keys) or 2 (sampled)");
+  if (p->metric > 2) BVSS_FAIL(BVSS_EINVAL, "metric must be 0 (Hausdorff), 1 (MeanMin) or 2 (Min)");
   int num_sms = 0;
   BVSS_TRY(check_device(p->device, &num_sms));
   DeviceGuard g(p->device);
@@ -815,6 +824,7 @@ int build_impl(const float* vectors, const int64_t* set_offsets, int64_t n, int3
   idx->terms = p->refine_terms == 0 ? 1 : (p->refine_terms == 255 ? 0 : static_cast<int>(p->refine_terms));
   idx->query_batch = p->query_batch;
   idx->select_mode = p->select_mode;
+  idx->metric = static_cast<int>(p->metric);
   BVSS_CUDA(cudaStreamCreateWithFlags(&idx->own_stream, cudaStreamNonBlocking));
   idx->stream = idx->own_stream;
   for (auto& e : idx->ev) BVSS_CUDA(cudaEventCreate(&e));
@@ -1216,26 +1226,29 @@ int bvss_refine(bvss_index* idx, const float* queries, const int64_t* query_offs
   BVSS_TRY(c->alloc(static_cast<size_t>(nq) * k * 8, reinterpret_cast<void**>(&oid)));
   BVSS_TRY(c->alloc(static_cast<size_t>(nq) * k * 4, reinterpret_cast<void**>(&odist)));
   int exact_all = 0;
+  float c1, c2;
+  error_consts(idx, &c1, &c2);
   if (idx->terms != 0 && c->max_mq <= 128) {  // tensor path: query rows fit the M=128 tile
     BVSS_TRY(c->alloc(static_cast<size_t>(nq) * T * 4, reinterpret_cast<void**>(&c->approx)));
     BVSS_CUDA(cudaMemsetAsync(c->approx, 0xFF, static_cast<size_t>(nq) * T * 4, idx->stream));  // NaN where unused
+    if (idx->metric == 1)
+      BVSS_TRY(c->alloc(static_cast<size_t>(nq) * T * 4, reinterpret_cast<void**>(&c->approx_err)));
     int* counter;
     BVSS_TRY(idx->ws.get("work_counter", sizeof(int), reinterpret_cast<void**>(&counter)));
     BVSS_TRY(launch_refine_tc(idx->hi, idx->lo, idx->vscale, idx->prows, idx->pbase, idx->vnorm, idx->off, idx->dpad, c->qhi,
                               c->qlo, c->qscale, c->qrows,
                               c->qrow, c->qnorm, c->qoff, c->max_mq, c->cand, c->count, T, static_cast<int>(nq), 0,
                               c->approx, idx->terms, counter, nullptr, idx->num_sms,
-                              0 /* caller lists: any order */, nullptr, idx->stream));
+                              0 /* caller lists: any order */, nullptr, idx->metric, c->approx_err, c1, c2,
+                              idx->vmax2, idx->stream));
   } else {
     exact_all = 1;
   }
-  float c1, c2;
-  error_consts(idx, &c1, &c2);
   void* scratch;
   BVSS_TRY(idx->ws.get("topk_scratch", static_cast<size_t>(nq) * T * 8, &scratch));
   BVSS_TRY(launch_topk_fixup(c->approx, c->cand, c->count, T, k, idx->V, idx->off, 0, idx->d, c->qv, c->qoff, c->qnorm,
                              idx->vmax2, c1, c2, exact_all, oid, odist, static_cast<int>(nq), nullptr, scratch,
-                             idx->stream));
+                             idx->metric, c->approx_err, idx->stream));
   BVSS_TRY(from_device(idx, out_ids, oid, static_cast<size_t>(nq) * k * 8, dev));
   BVSS_TRY(from_device(idx, out_dist, odist, static_cast<size_t>(nq) * k * 4, dev));
   if (out_approx && c->approx) BVSS_TRY(from_device(idx, out_approx, c->approx, static_cast<size_t>(nq) * T * 4, dev));

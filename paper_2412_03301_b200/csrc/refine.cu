@@ -110,6 +110,9 @@ struct RefineArgs {
   // (32x128b.warpx4 / 64x128b.warpx2::02_13 / 128x128b); the stage ring then carries B only, and the
   // two accumulators take N = ncols columns each (ncols = 160 at dpad = 384)
   int atmem;
+  int metric;                        // 0 Hausdorff (H^2), 1 MeanMin (mean_q sqrt(min_v D^2)), 2 Min (min D^2)
+  float* out_err;                    // MeanMin: [nq][T] bound on |approx - exact| per candidate (topk.cu window)
+  float c1, c2, vmax2;               // the squared-distance error bound E = c1 |q||v| + c2 (|q|^2 + |v|^2)
   int ncols;                         // candidate rows per tile (MMA N); 256 when A is in shared memory
   uint32_t acol;                     // first TMEM column of the resident query (atmem)
 };
@@ -131,6 +134,7 @@ struct ItemTable {
   int64_t ent_pbase[kItemCands];       // first padded row
   float qn[kMaxQ];                     // |q_i|^2
   float qs2[kMaxQ];                    // 2 * scale of query row i
+  float E;                             // squared-distance error bound of the item's query (MeanMin)
 };
 
 struct TileInfo {
@@ -203,7 +207,14 @@ __device__ __forceinline__ void tmem_ld16f(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// METRIC: 0 Hausdorff, 1 MeanMin, 2 Min; EXPER: the developer switches (A in TMEM, padding-free tails, TMA
+// tails, range-major group items, L2 prefetch, narrower tiles) -- compiled out of the default instantiation,
+// whose hot loops they measurably slow down (tools/ab_lib.sh)
+template <int METRIC, bool EXPER>
 __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __grid_constant__ RefineArgs a) {
+  const bool x_atmem = EXPER && a.atmem, x_tail = EXPER && a.tail, x_tma = EXPER && a.tma, x_group = EXPER && a.group,
+             x_prefetch = EXPER && a.prefetch;
+  const int x_ncols = EXPER ? a.ncols : kTileRows;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ RefineCtl S;
   uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -228,7 +239,7 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
     }
     tc::fence_mbar_init();
   }
-  for (int i = tid; i < kEpiWarps * kTileRows; i += blockDim.x) (&S.cm[0][0])[i] = 0x7f800000u;
+  for (int i = tid; i < kEpiWarps * kTileRows; i += blockDim.x) (&S.cm[0][0])[i] = METRIC == 1 ? 0u : 0x7f800000u;
   for (int i = tid; i < kEpiWarps * kMaxSetsPerTile; i += blockDim.x) (&S.hq[0][0])[i] = 0u;
   if (warp == 1) tc::tmem_alloc(&S.tmem_base, 512);
   tc::fence_before_sync();
@@ -236,11 +247,11 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
   tc::fence_after_sync();
   const uint32_t tmem = S.tmem_base;
   const int KCS = a.KCS, KS = a.KC / a.KCS;
-  const bool three = a.terms == 3;
+  const bool three = EXPER && a.terms == 3;  // the 3-term Gram runs in the EXPER instantiation
   const uint32_t sbo = static_cast<uint32_t>(KCS) * 1024u;
   const long long t_role0 = clock64();
 
-  if (warp == 6 && a.group) {
+  if (warp == 6 && x_group) {
     // ====== item tables, group mode: (query block, range, 32 queries); tiles hold 4 queries (one per lane quarter) ======
     int q0 = 0, qend = 0;
     int pl = 0, cntq = 0, incl = 0;  // this lane's query: first position of its slice, slice length, inclusive prefix
@@ -454,21 +465,25 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
           vb[i] = a.off[cid];
           msz[i] = static_cast<int>(a.off[cid + 1] - vb[i]);
           pb[i] = a.pbase[cid];
-          if (msz[i] > a.ncols) a.out_h2[static_cast<int64_t>(q) * a.T + c0 + c] = 0.0f;  // exact path
+          if (msz[i] > x_ncols) a.out_h2[static_cast<int64_t>(q) * a.T + c0 + c] = 0.0f;  // exact path
         }
       }
+      float mq2 = 0.0f;
       for (int j = lane; j < kMaxQ; j += 32) {
         t.qn[j] = (j < mq) ? a.qnorm[q0 + j] : 0.0f;
         t.qs2[j] = (j < mq) ? 2.0f * a.qscale[qr + j] : 0.0f;
+        mq2 = fmaxf(mq2, t.qn[j]);
       }
+      mq2 = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(mq2)));
+      if (lane == 0) t.E = a.c1 * sqrtf(mq2) * sqrtf(a.vmax2) + a.c2 * (mq2 + a.vmax2);
       // greedy packing: sets whole inside 256-row tiles at 8-aligned columns
-      int ntiles = 0, nent = 0, pos = a.ncols;
+      int ntiles = 0, nent = 0, pos = x_ncols;
       unsigned long long rows = 0;
       for (int c = 0; c < nc; ++c) {
         const int m = __shfl_sync(0xffffffffu, msz[c >> 5], c & 31);
-        if (m > a.ncols) continue;
+        if (m > x_ncols) continue;
         const int mp = (m + 7) & ~7;
-        if (pos + ((m + 15) & ~15) > a.ncols) {  // the epilogue reads 16-column chunks from the set start
+        if (pos + ((m + 15) & ~15) > x_ncols) {  // the epilogue reads 16-column chunks from the set start
           if (lane == 0) t.tile_first[ntiles] = nent;
           ++ntiles;
           pos = 0;
@@ -521,7 +536,7 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
           const int j = lane + 32 * k;
           vn8[k] = 0.0f;
           vs8[k] = 0.0f;
-          if (32 * k >= a.ncols) continue;
+          if (32 * k >= x_ncols) continue;
           int lo = e0, hi = e1;  // largest e with ent_col[e] <= j
           while (hi - lo > 1) {
             const int mid = (lo + hi) >> 1;
@@ -536,7 +551,7 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
         }
 #pragma unroll
         for (int k = 0; k < kTileRows / 32; ++k) {
-          if (32 * k >= a.ncols) continue;
+          if (32 * k >= x_ncols) continue;
           inf.vn[lane + 32 * k] = vn8[k];
           inf.vs[lane + 32 * k] = vs8[k];
         }
@@ -563,7 +578,7 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
       uint32_t qbytes = static_cast<uint32_t>((mq + 7) & ~7) / 8u * KCS * 1024u;
       uint32_t gbytes[4] = {0u, 0u, 0u, 0u};  // group mode: A bytes / rows of each quarter's query (per tile)
       int64_t gqrow[4] = {0, 0, 0, 0};
-      if (a.atmem) {  // the item's query, one super-chunk per stage, once (the MMA warp copies it into TMEM)
+      if (x_atmem) {  // the item's query, one super-chunk per stage, once (the MMA warp copies it into TMEM)
         for (int ks = 0; ks < KS; ++ks, ++stage_ctr) {
           const uint32_t st = stage_ctr % NST;
           PROF_WAIT(1, tc::mbar_wait(&S.empty[st], ((stage_ctr / NST) & 1u) ^ 1u));
@@ -577,7 +592,7 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
       }
       for (int tile = 0; tile < ntiles; ++tile) {
         const int e0 = t.tile_first[tile], e1 = t.tile_first[tile + 1];
-        if (a.group) {  // the tile's 4 queries: q = gq0 + 4 grp + quarter
+        if (x_group) {  // the tile's 4 queries: q = gq0 + 4 grp + quarter
           const int jb = 4 * t.tile_grp[tile];  // the tile's queries: item slots jb .. jb+3 (table, no global loads)
           qbytes = 0;
 #pragma unroll
@@ -587,7 +602,7 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
             qbytes += gbytes[j];
           }
         }
-        if (a.prefetch && tile + 1 < ntiles) {  // warm L2 with the next tile's rows (all K super-chunks)
+        if (x_prefetch && tile + 1 < ntiles) {  // warm L2 with the next tile's rows (all K super-chunks)
           const int f0 = t.tile_first[tile + 1], f1 = t.tile_first[tile + 2];
           for (int e = f0 + lane; e < f1; e += 32) {
             const uint32_t nb = static_cast<uint32_t>((t.ent_m[e] + 7) & ~7) / 8u * KCS * 1024u;
@@ -600,17 +615,17 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
         }
         uint32_t bytes = 0;  // B bytes of one piece of one stage
         for (int e = e0 + lane; e < e1; e += 32)
-          bytes += (a.tma || a.tail) ? static_cast<uint32_t>(t.ent_m[e]) * KCS * 128u
+          bytes += (x_tma || x_tail) ? static_cast<uint32_t>(t.ent_m[e]) * KCS * 128u
                          : static_cast<uint32_t>((t.ent_m[e] + 7) & ~7) / 8u * KCS * 1024u;
         bytes = static_cast<uint32_t>(warp_sum(static_cast<int>(bytes)));
-        const uint32_t stage_tx = a.atmem ? bytes
-                                          : (three ? 2u : 1u) * (bytes + (a.group ? qbytes : static_cast<uint32_t>(reps) * qbytes));
+        const uint32_t stage_tx = x_atmem ? bytes
+                                          : (three ? 2u : 1u) * (bytes + (x_group ? qbytes : static_cast<uint32_t>(reps) * qbytes));
         for (int ks = 0; ks < KS; ++ks, ++stage_ctr) {
           const uint32_t st = stage_ctr % NST;
           PROF_WAIT(1, tc::mbar_wait(&S.empty[st], ((stage_ctr / NST) & 1u) ^ 1u));
           const uint32_t sbase = ring_s + st * a.stage_bytes;
           const uint32_t a_hi = sbase, a_lo = sbase + a.a_bytes;
-          const uint32_t b_hi = a.atmem ? sbase : sbase + (three ? 2u : 1u) * a.a_bytes, b_lo = b_hi + a.b_bytes;
+          const uint32_t b_hi = x_atmem ? sbase : sbase + (three ? 2u : 1u) * a.a_bytes, b_lo = b_hi + a.b_bytes;
           if (lane == 0) mbar_arrive_expect_tx(&S.full[st], stage_tx);
           __syncwarp();
           for (int e = e0 + lane; e < e1; e += 32) {
@@ -618,12 +633,12 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
             const int64_t g0 = t.ent_pbase[e] >> 3;
             const size_t src = ((static_cast<size_t>(ks) * a.pgroups + g0) * KCS) * 8 * kKChunk;
             const uint32_t o = static_cast<uint32_t>(t.ent_col[e]) / 8u * KCS * 1024u;
-            if (a.tail && KCS == 1) {  // one K-chunk per stage: the set's m rows are one contiguous run
+            if (x_tail && KCS == 1) {  // one K-chunk per stage: the set's m rows are one contiguous run
               bulk_g2s(b_hi + o, a.hs + src, static_cast<uint32_t>(m) * 128u, &S.full[st]);
               if (three) bulk_g2s(b_lo + o, a.ls + src, static_cast<uint32_t>(m) * 128u, &S.full[st]);
               continue;
             }
-            const bool part = a.tma || a.tail;
+            const bool part = x_tma || x_tail;
             const int full = part ? (m >> 3) : ((m + 7) >> 3), rem = part ? (m & 7) : 0;
             if (full) {  // whole 8-row groups: one contiguous run of full * KCS KB
               const uint32_t nb = static_cast<uint32_t>(full) * KCS * 1024u;
@@ -633,7 +648,7 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
             if (rem) {  // the last group's rem real rows, one K-chunk at a time (no padding rows read)
               for (int kc = 0; kc < KCS; ++kc) {
                 const uint32_t dst = o + (static_cast<uint32_t>(full) * KCS + kc) * 1024u;
-                if (a.tail) {  // plain bulk copies of the rem pre-swizzled rows of each K-chunk
+                if (x_tail) {  // plain bulk copies of the rem pre-swizzled rows of each K-chunk
                   const size_t so = src + (static_cast<size_t>(full) * KCS + kc) * 8 * kKChunk;
                   bulk_g2s(b_hi + dst, a.hs + so, static_cast<uint32_t>(rem) * 128u, &S.full[st]);
                   if (three) bulk_g2s(b_lo + dst, a.ls + so, static_cast<uint32_t>(rem) * 128u, &S.full[st]);
@@ -644,8 +659,8 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
               }
             }
           }
-          if (a.atmem) {
-          } else if (a.group) {  // group mode: quarter j holds query j's rows (A rows 32j ..)
+          if (x_atmem) {
+          } else if (x_group) {  // group mode: quarter j holds query j's rows (A rows 32j ..)
             if (lane >= 28 && gbytes[lane - 28] > 0) {
               const int j = lane - 28;
               const size_t src = ((static_cast<size_t>(ks) * a.qgroups + (gqrow[j] >> 3)) * KCS) * 8 * kKChunk;
@@ -668,7 +683,7 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
   } else if (warp == 1) {
     // =========================== MMA issuer (one thread) ===========================
     uint32_t stage_ctr = 0, tile_ctr = 0;
-    const uint32_t idesc = tc::idesc_f16_f32(128, a.ncols);
+    const uint32_t idesc = tc::idesc_f16_f32(128, x_ncols);
     for (uint32_t it = 0;; ++it) {
       const int tb = it & 1;
       const ItemTable& t = S.tab[tb];
@@ -678,7 +693,7 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
       const int ntiles = t.ntiles, rep_rows = t.rep_rows;
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&S.tab_empty[tb]);  // the MMA warp needs nothing else from the table
-      if (a.atmem) {  // the query into TMEM (the tcgen05 pipe keeps issue order: the previous item's MMAs
+      if (x_atmem) {  // the query into TMEM (the tcgen05 pipe keeps issue order: the previous item's MMAs
                       // have read the old query before these copies overwrite it)
         for (int ks = 0; ks < KS; ++ks, ++stage_ctr) {
           const uint32_t st = stage_ctr % NST;
@@ -708,7 +723,7 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
         const uint32_t acc = tile_ctr & 1u;
         PROF_WAIT(5, tc::mbar_wait(&S.tempty[acc], ((tile_ctr >> 1) & 1u) ^ 1u));
         tc::fence_after_sync();
-        const uint32_t d_tmem = tmem + acc * a.ncols;
+        const uint32_t d_tmem = tmem + acc * x_ncols;
         for (int ks = 0; ks < KS; ++ks, ++stage_ctr) {
           const uint32_t st = stage_ctr % NST;
           PROF_WAIT(6, tc::mbar_wait(&S.full[st], (stage_ctr / NST) & 1u));
@@ -716,13 +731,13 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
           if (lane == 0) {
             const uint32_t sbase = ring_s + st * a.stage_bytes;
             const uint32_t a_hi = sbase, a_lo = sbase + a.a_bytes;
-            const uint32_t b_hi = a.atmem ? sbase : sbase + (three ? 2u : 1u) * a.a_bytes, b_lo = b_hi + a.b_bytes;
+            const uint32_t b_hi = x_atmem ? sbase : sbase + (three ? 2u : 1u) * a.a_bytes, b_lo = b_hi + a.b_bytes;
             for (int kc = 0; kc < KCS; ++kc) {
 #pragma unroll
               for (int kk = 0; kk < kKChunk / 16; ++kk) {
                 const uint32_t koff = kc * 1024u + kk * 32u;
                 const uint32_t accum = (ks | kc | kk) ? 1u : 0u;
-                if (a.atmem) {
+                if (x_atmem) {
                   const uint32_t acol = tmem + a.acol + static_cast<uint32_t>((ks * KCS + kc) * 32 + kk * 8);
                   asm volatile(
                       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -766,6 +781,8 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
       bool qvalid = qi < mq;
       float qn = qvalid ? t.qn[qi] : 0.0f, qs2 = qvalid ? t.qs2[qi] : 0.0f;
       float* out = a.out_h2 + static_cast<int64_t>(t.q) * a.T + t.c0;
+      float* oerr = a.out_err ? a.out_err + static_cast<int64_t>(t.q) * a.T + t.c0 : nullptr;
+      const float Eq = t.E, sqE = sqrtf(t.E);
       int gcur = -1;  // group mode: the tile group whose query this warp has loaded
       for (int tile = 0; tile < ntiles; ++tile, ++tile_ctr) {
         const uint32_t acc = tile_ctr & 1u;
@@ -774,9 +791,9 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
         PROF_WAIT(9, tc::mbar_wait(&S.tfull[acc], (tile_ctr >> 1) & 1u));
         PROF_WAIT(10, tc::mbar_wait(&S.info_full[slot], (tile_ctr / kInfoSlots) & 1u));
         tc::fence_after_sync();
-        const uint32_t tbase = tmem + acc * a.ncols + (static_cast<uint32_t>(ew * 32) << 16);
+        const uint32_t tbase = tmem + acc * x_ncols + (static_cast<uint32_t>(ew * 32) << 16);
         const int e0 = inf.first, ne = inf.count;
-        if (a.group && t.tile_grp[tile] != gcur) {  // this quarter's query for the tile's group
+        if (x_group && t.tile_grp[tile] != gcur) {  // this quarter's query for the tile's group
           gcur = t.tile_grp[tile];
           const int q = t.gq0 + 4 * gcur + ew;
           mq = 0;
@@ -794,15 +811,16 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
         // sets of this tile: replica rep takes sets rep + nrep*k, its two warps (sub) alternate;
         // group mode: quarter ew takes the sets of its query, its two warps alternate
         int gk = 0;
-        for (int s = a.group ? 0 : rep + nrep * sub; s < ne; s += a.group ? 1 : 2 * nrep) {
+        for (int s = x_group ? 0 : rep + nrep * sub; s < ne; s += x_group ? 1 : 2 * nrep) {
           const int e = e0 + s;
-          if (a.group) {
+          if (x_group) {
             if (t.ent_quarter[e] != ew) continue;
             if ((gk++ & 1) != sub) continue;
           }
           const int col0 = t.ent_col[e], m = t.ent_m[e];
           float rmin = __int_as_float(0x7f800000);  // per lane (query row): min over the set's columns
           float hv = 0.0f;                          // max over columns of (min over rows)
+          float mv = __int_as_float(0x7f800000);    // min over columns of (min over rows): Min metric
           for (int j0 = 0; j0 < m; j0 += 32) {
             uint32_t g[32];
             tc::tmem_ld16(tbase + col0 + j0, *reinterpret_cast<uint32_t(*)[16]>(&g[0]));
@@ -822,18 +840,46 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
                     if (qvalid) d2 = fmaxf(qn + vn[jj] - (qs2 * vs[jj]) * __uint_as_float(g[j]), 0.0f);
                     rmin = fminf(rmin, d2);
                     const uint32_t cmin = __reduce_min_sync(0xffffffffu, __float_as_uint(d2));
-                    if (wpr == 1) hv = fmaxf(hv, __uint_as_float(cmin));
-                    else if (lane == 0) atomicMin(&S.cm[rep][col0 + j0 + j], cmin);
+                    if (wpr == 1) {
+                      hv = fmaxf(hv, __uint_as_float(cmin));
+                      mv = fminf(mv, __uint_as_float(cmin));
+                    } else if (lane == 0 && METRIC != 1) {
+                      atomicMin(&S.cm[rep][col0 + j0 + j], cmin);
+                    }
                   }
                 }
               }
             }
           }
-          const uint32_t hq = __reduce_max_sync(0xffffffffu, qvalid ? __float_as_uint(rmin) : 0u);
-          if (wpr == 1) {
-            if (lane == 0) out[t.ent_cand[e]] = fmaxf(__uint_as_float(hq), hv);
-          } else if (lane == 0) {
-            atomicMax(&S.hq[rep][s % kMaxSetsPerTile], hq);
+          if (METRIC == 1) {  // MeanMin: this warp's rows' sum of sqrt(min_v D^2) (fixed butterfly order)
+            // and of the per-row error bound: the row minimum a is within E of the exact one b, so
+            // |sqrt a - sqrt b| <= min(sqrt E, E / (sqrt a + sqrt max(0, a - E))) (+ the sqrt rounding)
+            const float ra = fmaxf(rmin, 0.0f), sa = sqrtf(ra);
+            float sq = qvalid ? sa : 0.0f;
+            float er = qvalid ? fminf(sqE, Eq / (sa + sqrtf(fmaxf(ra - Eq, 0.0f)))) + 1e-7f * sa : 0.0f;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              sq += __shfl_xor_sync(0xffffffffu, sq, o);
+              er += __shfl_xor_sync(0xffffffffu, er, o);
+            }
+            if (wpr == 1) {
+              if (lane == 0) {
+                out[t.ent_cand[e]] = sq / static_cast<float>(mq);
+                oerr[t.ent_cand[e]] = er / static_cast<float>(mq);
+              }
+            } else if (lane == 0) {
+              atomicAdd(reinterpret_cast<float*>(&S.hq[rep][s % kMaxSetsPerTile]), sq);
+              atomicAdd(reinterpret_cast<float*>(&S.cm[rep][s % kMaxSetsPerTile]), er);  // (no column minima)
+            }
+          } else if (METRIC == 2) {  // Min: min over every (query row, set row) of D^2
+            if (wpr == 1 && lane == 0) out[t.ent_cand[e]] = mv;
+          } else {
+            const uint32_t hq = __reduce_max_sync(0xffffffffu, qvalid ? __float_as_uint(rmin) : 0u);
+            if (wpr == 1) {
+              if (lane == 0) out[t.ent_cand[e]] = fmaxf(__uint_as_float(hq), hv);
+            } else if (lane == 0) {
+              atomicMax(&S.hq[rep][s % kMaxSetsPerTile], hq);
+            }
           }
         }
         // TMEM reads of this tile are done
@@ -846,14 +892,29 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
             for (int s = rep + nrep * sub; s < ne; s += 2 * nrep) {
               const int e = e0 + s;
               const int col0 = t.ent_col[e], m = t.ent_m[e];
-              float hv = 0.0f;
+              if (METRIC == 1) {  // MeanMin: the replica's row sums (value, error bound)
+                if (lane == 0) {
+                  const int sl = s % kMaxSetsPerTile;
+                  out[t.ent_cand[e]] = __uint_as_float(S.hq[rep][sl]) / static_cast<float>(mq);
+                  oerr[t.ent_cand[e]] = __uint_as_float(S.cm[rep][sl]) / static_cast<float>(mq);
+                  S.hq[rep][sl] = 0u;
+                  S.cm[rep][sl] = 0u;
+                }
+                continue;
+              }
+              float hv = 0.0f, mv = __int_as_float(0x7f800000);
               for (int j = lane; j < m; j += 32) {
                 hv = fmaxf(hv, __uint_as_float(S.cm[rep][col0 + j]));
+                mv = fminf(mv, __uint_as_float(S.cm[rep][col0 + j]));
                 S.cm[rep][col0 + j] = 0x7f800000u;
               }
               hv = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(hv)));
+              mv = __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(mv)));
               if (lane == 0) {
-                out[t.ent_cand[e]] = fmaxf(__uint_as_float(S.hq[rep][s % kMaxSetsPerTile]), hv);
+                const uint32_t acc_hq = S.hq[rep][s % kMaxSetsPerTile];
+                out[t.ent_cand[e]] = METRIC == 1   ? __uint_as_float(acc_hq) / static_cast<float>(mq)
+                                     : METRIC == 2 ? mv
+                                                     : fmaxf(__uint_as_float(acc_hq), hv);
                 S.hq[rep][s % kMaxSetsPerTile] = 0u;
               }
             }
@@ -945,7 +1006,8 @@ int launch_refine_tc(const __half* hs, const __half* ls, const float* vscale, in
                      const float* qscale, int64_t qrows, const int64_t* qrow, const float* qnorm, const int64_t* qoff,
                      int max_mq, const int32_t* cand, const int32_t* count, int T, int nq, int64_t id_base,
                      float* out_h2, int terms, int* work_counter, unsigned long long* rows_counter, int num_sms,
-                     int64_t n_local, int32_t* bounds, cudaStream_t st) {
+                     int64_t n_local, int32_t* bounds, int metric, float* out_err, float c1, float c2, float vmax2,
+                     cudaStream_t st) {
   if (nq <= 0 || T <= 0) return BVSS_OK;
   if (max_mq > kMaxQ) BVSS_FAIL(BVSS_EUNSUPPORTED, "query set with %d vectors exceeds the %d-row tensor tile", max_mq, kMaxQ);
   if (dpad % kKChunk) BVSS_FAIL(BVSS_EINVAL, "dpad must be a multiple of 64");
@@ -956,6 +1018,12 @@ int launch_refine_tc(const __half* hs, const __half* ls, const float* vscale, in
   a.qhs = qhs; a.qls = qls; a.qscale = qscale; a.qgroups = qrows / 8; a.qrow = qrow; a.qnorm = qnorm; a.qoff = qoff;
   a.cand = cand; a.count = count; a.T = T; a.nq = nq; a.id_base = id_base; a.out_h2 = out_h2;
   a.terms = terms == 3 ? 3 : 1;
+  a.metric = metric;
+  a.out_err = out_err;
+  a.c1 = c1;
+  a.c2 = c2;
+  a.vmax2 = vmax2;
+  if (metric == 1 && !out_err) BVSS_FAIL(BVSS_EINVAL, "MeanMin refine needs the error-bound output");
   a.items_per_query = ceil_div(T, kItemCands);
   a.total_items = a.items_per_query * nq;
   a.work_counter = work_counter;
@@ -980,7 +1048,7 @@ int launch_refine_tc(const __half* hs, const __half* ls, const float* vscale, in
     const char* e = getenv("BVSS_REFINE_GROUP");  // developer switch: 1 = range-major group items
     const int want = e ? atoi(e) : 0;
     const int64_t rs = refine_range_sets(n_local, prows, dpad, T);
-    if (want && max_mq <= 32 && nq >= 16 && rs > 0 && bounds) {
+    if (want && metric == 0 && max_mq <= 32 && nq >= 16 && rs > 0 && bounds) {
       const double qbytes = 32.0 * dpad * 2.0;                    // A rows of one query (upper bound)
       int qb = static_cast<int>(60.0 * (1 << 20) / qbytes);      // query rows of a block stay in L2
       if (const char* b = getenv("BVSS_REFINE_QBLOCK")) qb = atoi(b);
@@ -1075,9 +1143,12 @@ int launch_refine_tc(const __half* hs, const __half* ls, const float* vscale, in
   a.a_bytes = 128u * a.KCS * 128u;
   a.b_bytes = static_cast<uint32_t>(a.ncols) * a.KCS * 128u;
   BVSS_CUDA(cudaMemsetAsync(work_counter, 0, sizeof(int), st));
-  BVSS_CUDA(cudaFuncSetAttribute(refine_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const int grid = a.total_items < num_sms ? a.total_items : num_sms;
-  refine_tc_kernel<<<grid, kRefineThreads, smem, st>>>(a);
+  const bool exper = a.atmem || a.tail || a.tma || a.group || a.prefetch || a.ncols != kTileRows || a.terms == 3;
+  auto kfn = exper ? (metric == 1 ? refine_tc_kernel<1, true> : metric == 2 ? refine_tc_kernel<2, true> : refine_tc_kernel<0, true>)
+                   : (metric == 1 ? refine_tc_kernel<1, false> : metric == 2 ? refine_tc_kernel<2, false> : refine_tc_kernel<0, false>);
+  BVSS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  kfn<<<grid, kRefineThreads, smem, st>>>(a);
   BVSS_TRY(post_launch(__func__, st));
   if (a.prof) {  // developer instrumentation: per-CTA average Mcycles per role
     unsigned long long h[17];

@@ -43,6 +43,20 @@ __device__ __forceinline__ float block_max_f(float v, float* red) {
   return r;
 }
 
+// block-wide sum in a fixed order (butterfly within warps, warps in index order): deterministic
+__device__ __forceinline__ float block_sum_f(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float r = red[0];
+  for (int i = 1; i < (blockDim.x >> 5); ++i) r += red[i];
+  __syncthreads();
+  return r;
+}
+
 template <bool VEC>
 __device__ __forceinline__ void load_chunk(const float* __restrict__ p, int kb, int d, bool ok, float (&x)[kKB]) {
   if (VEC) {
@@ -288,7 +302,8 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
     const float* __restrict__ V, const int64_t* __restrict__ off, int64_t id_base, int d, int d4, int stride4, int RB,
     const float* __restrict__ Qv, const int64_t* __restrict__ qoff, const float* __restrict__ qnorm, float vmax2,
     float c1, float c2, int exact_all, int32_t* __restrict__ win_g, float* __restrict__ ex_g,
-    int64_t* __restrict__ out_ids, float* __restrict__ out_dist, int64_t* __restrict__ fixup_counter) {
+    int64_t* __restrict__ out_ids, float* __restrict__ out_dist, int64_t* __restrict__ fixup_counter, int metric,
+    const float* __restrict__ approx_err) {
   extern __shared__ __align__(16) float txs[];
   float* Qs = txs;                                          // [RB][stride4*4]
   float* Vs0 = Qs + static_cast<int64_t>(RB) * stride4 * 4;   // [RB][stride4*4]
@@ -302,6 +317,8 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
   const int mq = static_cast<int>(qoff[q + 1] - q0);
   const int kk = min(k, cnt);
   const float* ap = approx ? approx + static_cast<int64_t>(q) * T : nullptr;
+  // MeanMin with per-candidate error bounds e: select on the upper bounds a + e, test the lower bounds a - e
+  const float* aerr = (metric == 1 && approx_err) ? approx_err + static_cast<int64_t>(q) * T : nullptr;
   const int32_t* cq = cand + static_cast<int64_t>(q) * T;
   int32_t* win = win_g + static_cast<int64_t>(q) * T;
   float* ex = ex_g + static_cast<int64_t>(q) * T;
@@ -319,7 +336,7 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
 #pragma unroll
     for (int e = 0; e < kReg; ++e) {
       const int i = tid + e * kTxThreads;
-      ur[e] = i < cnt ? __float_as_uint(ap[i]) : 0xFFFFFFFFu;
+      ur[e] = i < cnt ? __float_as_uint(aerr ? ap[i] + aerr[i] : ap[i]) : 0xFFFFFFFFu;
     }
     for (int rnd = 0; rnd < 4; ++rnd) {  // radix select of the kk-th smallest (uint order of floats >= 0)
       const int shift = 24 - 8 * rnd;
@@ -334,7 +351,7 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
         if (in && lane == __ffs(peers) - 1) atomicAdd(&S.hist[bin], static_cast<uint32_t>(__popc(peers)));
       }
       for (int i = tid + kReg * kTxThreads; i < cnt; i += blockDim.x) {
-        const uint32_t u = __float_as_uint(ap[i]);
+        const uint32_t u = __float_as_uint(aerr ? ap[i] + aerr[i] : ap[i]);
         if (rnd == 0 || (u >> (shift + 8)) == pre) atomicAdd(&S.hist[(u >> shift) & 255u], 1u);
       }
       __syncthreads();
@@ -373,7 +390,12 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
       pre = S.prefix;
       need = S.need;
     }
-    W = (__uint_as_float(pre) + 2.0f * E) * (1.0f + 1e-6f);
+    // Hausdorff / Min: values are squared distances, each within E of the exact one; MeanMin: values are
+    // distances (the mean of sqrt(min_v D^2)), each row term within sqrt(E) since |sqrt a - sqrt b| <=
+    // sqrt|a - b|, and the fp32 sums add a few ulps per term (the 2e-5 slack)
+    W = aerr ? __uint_as_float(pre) * (1.0f + 2e-5f) + 1e-30f  // the k-th smallest upper bound
+        : metric == 1 ? (__uint_as_float(pre) + 2.0f * sqrtf(E)) * (1.0f + 2e-5f) + 1e-30f
+                      : (__uint_as_float(pre) + 2.0f * E) * (1.0f + 1e-6f);
   }
   __syncthreads();
   if (exact_all) {
@@ -381,7 +403,7 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
     if (tid == 0) S.wcount = cnt;
   } else {
     for (int i = tid; i < cnt; i += blockDim.x)
-      if (ap[i] <= W) win[atomicAdd(&S.wcount, 1u)] = i;
+      if ((aerr ? ap[i] - aerr[i] : ap[i]) <= W) win[atomicAdd(&S.wcount, 1u)] = i;
   }
   __syncthreads();
   const int nw = static_cast<int>(S.wcount);
@@ -507,16 +529,22 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
       S.colmin[lane] = 0x7f800000u;
       if (lane == 0) S.hv = fmaxf(S.hv, cm);
     }
-    if (nw_ != w) {  // candidate done: H^2 = max(max_q min_v D^2, max_v min_q D^2)
+    if (nw_ != w) {  // candidate done: H^2 = max(max_q min_v D^2, max_v min_q D^2) (or MeanMin / Min)
       __syncthreads();
-      float hq = 0.0f;
+      float hq = 0.0f, sq = 0.0f, mn = __int_as_float(0x7f800000);
       for (int i = tid; i < mq; i += blockDim.x) {
-        hq = fmaxf(hq, __uint_as_float(S.rowmin[i]));
+        const float r = __uint_as_float(S.rowmin[i]);
+        hq = fmaxf(hq, r);
+        sq += sqrtf(r);
+        mn = fminf(mn, r);
         S.rowmin[i] = 0x7f800000u;
       }
-      hq = block_max_f(hq, bred);
+      float val;
+      if (metric == 1) val = block_sum_f(sq, bred) / static_cast<float>(mq);  // MeanMin (a distance)
+      else if (metric == 2) val = -block_max_f(-mn, bred);                     // Min (squared)
+      else val = fmaxf(block_max_f(hq, bred), S.hv);                          // Hausdorff (squared)
       if (tid == 0) {
-        ex[w] = fmaxf(hq, S.hv);
+        ex[w] = val;
         S.hv = 0.0f;
       }
     }
@@ -553,7 +581,8 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
         od[r] = __int_as_float(0x7f800000);
       } else {
         oi[r] = static_cast<int64_t>(static_cast<uint32_t>(b & 0xffffffffull));
-        od[r] = sqrtf(__uint_as_float(static_cast<uint32_t>(b >> 32)));
+        const float e = __uint_as_float(static_cast<uint32_t>(b >> 32));
+        od[r] = metric == 1 ? e : sqrtf(e);
       }
     }
     if (b != ~0ull) {  // mark the winner as taken
@@ -575,7 +604,8 @@ static size_t tx_smem(int stride4, int RB) {
 int launch_topk_fixup(const float* approx, const int32_t* cand, const int32_t* count, int T, int k, const float* V,
                       const int64_t* off, int64_t id_base, int d, const float* Qv, const int64_t* qoff,
                       const float* qnorm, float vmax2, float c1, float c2, int exact_all, int64_t* out_ids,
-                      float* out_dist, int nq, int64_t* fixup_counter, void* scratch /*[nq][T] x 8 B*/, cudaStream_t st) {
+                      float* out_dist, int nq, int64_t* fixup_counter, void* scratch /*[nq][T] x 8 B*/, int metric,
+                      const float* approx_err, cudaStream_t st) {
   if (nq <= 0) return BVSS_OK;
   if (k > T) BVSS_FAIL(BVSS_EINVAL, "k > T");
   const int d4 = (d + 3) / 4;
@@ -589,11 +619,12 @@ int launch_topk_fixup(const float* approx, const int32_t* cand, const int32_t* c
     BVSS_CUDA(cudaFuncSetAttribute(topk_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     topk_exact_kernel<<<nq, kTxThreads, smem, st>>>(approx, cand, count, T, k, V, off, id_base, d, d4, stride4, RB, Qv,
                                                     qoff, qnorm, vmax2, c1, c2, exact_all, win, ex, out_ids, out_dist,
-                                                    fixup_counter);
+                                                    fixup_counter, metric, approx_err);
     BVSS_TRY(post_launch("topk_exact_kernel", st));
     return BVSS_OK;
   }
-  // very wide vectors: the warp-per-candidate kernel (global-memory operands)
+  // very wide vectors: the warp-per-candidate kernel (global-memory operands; Hausdorff only)
+  if (metric != 0) BVSS_FAIL(BVSS_EUNSUPPORTED, "MeanMin / Min rerank needs d <= ~3500 (CTA fix-up kernel)");
   const size_t smem = topk_smem_bytes(T);
   if (smem > 190 * 1024) BVSS_FAIL(BVSS_EUNSUPPORTED, "T=%d exceeds the top-k kernel limit (16384)", T);
   if (d % 4 == 0) {
