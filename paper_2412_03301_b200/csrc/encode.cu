@@ -13,7 +13,7 @@
 
 namespace bvss {
 
-template <int RM>  // RM = capacity in 32-row groups (m/32 <= RM)
+template <int RM, int SS>  // RM = capacity in 32-row groups (m/32 <= RM); SS = s when fixed at compile time, else 0
 __global__ void __launch_bounds__(256) flyhash_wta_kernel(
     const float* __restrict__ V, int64_t nvec, int d, const uint16_t* __restrict__ Wt /*[s][m]*/, int m,
     int s, int L, uint32_t* __restrict__ codes /*[nvec][m/32] or null*/, float* __restrict__ norms /*[nvec] or null*/,
@@ -79,7 +79,15 @@ __global__ void __launch_bounds__(256) flyhash_wta_kernel(
         if (t < R) {
           const int j = t * 32 + lane;
           float acc = 0.0f;
-          for (int u = 0; u < s; ++u) acc = __fadd_rn(acc, myv[sW[u * m + j]]);
+          if (SS > 0) {  // all s index loads and gathers issue together; only the adds are chained
+            float g[SS > 0 ? SS : 1];
+#pragma unroll
+            for (int u = 0; u < SS; ++u) g[u] = myv[sW[u * m + j]];
+#pragma unroll
+            for (int u = 0; u < SS; ++u) acc = __fadd_rn(acc, g[u]);
+          } else {
+            for (int u = 0; u < s; ++u) acc = __fadd_rn(acc, myv[sW[u * m + j]]);
+          }
           key[t] = float_order_key(acc);
         }
       }
@@ -144,7 +152,8 @@ int launch_encode(const float* V, int64_t nvec, int d, const uint16_t* Wt, int m
   const int grid = static_cast<int>(want < int64_t(num_sms) * 8 ? want : int64_t(num_sms) * 8);
 #define BVSS_ENC(RMv)                                                                                     \
   do {                                                                                                    \
-    auto kfn = flyhash_wta_kernel<RMv>;                                                                   \
+    auto kfn = s == 8 ? flyhash_wta_kernel<RMv, 8> : s == 6 ? flyhash_wta_kernel<RMv, 6>                  \
+             : s == 12 ? flyhash_wta_kernel<RMv, 12> : flyhash_wta_kernel<RMv, 0>;                        \
     BVSS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem))); \
     kfn<<<grid, 256, smem, st>>>(V, nvec, d, Wt, m, s, L, codes, norms, hs, ls, scale, dpad, rows, dst_row, kcs); \
   } while (0)

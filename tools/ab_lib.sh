@@ -7,6 +7,6 @@ for r in $(seq ${ROUNDS:-2}); do
   for L in $LIBS; do
     if [ $L = new ]; then P=""; else P=$PWD/$L; fi
     BVSS_LIB=$P python bench.py $A 2>&1 | tail -1 | python -c "
-import json,sys; j=json.loads(sys.stdin.read()); print('$L', round(j['stages_ms']['ms_refine'], 2), j['stages_ms'], j['clocks']['sm_mhz'])"
+import json,sys; j=json.loads(sys.stdin.read()); print('$L', round(j['stages_ms']['ms_refine'], 2), j['stages_ms'], j['clocks']['sm_mhz'], j.get('build', {}).get('ms'))"
   done
 done
