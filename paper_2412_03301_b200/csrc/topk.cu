@@ -563,6 +563,29 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
   }
   __syncthreads();
   // ---- 3. the k smallest by (exact H^2, id)
+  if (nw <= kTxCache) {  // one pass: every window entry's rank among the (distance, id) keys (unique ids)
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(S.jv0);  // row ranges are done with
+    for (int x = tid; x < nw; x += blockDim.x)
+      keys[x] = (static_cast<unsigned long long>(__float_as_uint(ex[x])) << 32) | static_cast<uint32_t>(cq[win[x]]);
+    __syncthreads();
+    int64_t* oi = out_ids + static_cast<int64_t>(q) * k;
+    float* od = out_dist + static_cast<int64_t>(q) * k;
+    for (int x = tid; x < nw; x += blockDim.x) {
+      const unsigned long long kx = keys[x];
+      int rank = 0;
+      for (int y = 0; y < nw; ++y) rank += keys[y] < kx ? 1 : 0;
+      if (rank < k) {
+        const float e = __uint_as_float(static_cast<uint32_t>(kx >> 32));
+        oi[rank] = static_cast<int64_t>(static_cast<uint32_t>(kx & 0xffffffffull));
+        od[rank] = metric == 1 ? e : sqrtf(e);
+      }
+    }
+    for (int r = nw + tid; r < k; r += blockDim.x) {
+      oi[r] = -1;
+      od[r] = __int_as_float(0x7f800000);
+    }
+    return;
+  }
   for (int r = 0; r < k; ++r) {
     unsigned long long best = ~0ull;
     for (int x = tid; x < nw; x += blockDim.x) {
