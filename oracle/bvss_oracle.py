@@ -218,6 +218,19 @@ def count_l2_scores(CQ: np.ndarray, C: np.ndarray) -> np.ndarray:
     return (diff * diff).sum(axis=1)
 
 
+def overlap_scores(SQ: np.ndarray, S: np.ndarray, kind: str = "binary") -> np.ndarray:
+    """The OVERLAP filter score (reading R24, SURVEY A1 flag): the shared-bit
+    count popc(S_Q AND S^(i)) the north_star's scan computes ("ANDs and
+    popcounts"), or for count sketches the counter dot product
+    sum_j C_Q[j] C_i[j] (Theorem 2's collision count).  Higher is
+    closer; returns int64 ``[n]``."""
+    if kind == "binary":
+        a = np.bitwise_and(np.asarray(S, dtype=np.uint32), np.asarray(SQ, dtype=np.uint32)[None, :])
+        return popcount_rows(a)
+    C = np.asarray(S, dtype=np.int64)
+    return (C * np.asarray(SQ, dtype=np.int64)[None, :]).sum(axis=1)
+
+
 # ---------------------------------------------------------------------------
 # a-6: top-T candidate selection  (Alg 6 lines 10-18 P:795-806; readings R3, R4)
 # ---------------------------------------------------------------------------
@@ -340,7 +353,7 @@ class OracleIndex:
     """Index state of Algs 1, 3, 5 for one database (P:323-343, P:665-682,
     P:738-757): W, per-vector codes D^H, per-set sketches."""
 
-    def __init__(self, vectors, offsets, m, s, L, seed, sketch="binary", W=None):
+    def __init__(self, vectors, offsets, m, s, L, seed, sketch="binary", W=None, score="default"):
         self.vectors = np.ascontiguousarray(vectors, dtype=np.float32)
         self.offsets = _check_offsets(offsets)
         if self.offsets[-1] != self.vectors.shape[0]:
@@ -348,6 +361,7 @@ class OracleIndex:
         self.d = self.vectors.shape[1]
         self.m, self.s, self.L, self.seed = m, s, L, seed
         self.kind = sketch
+        self.score = score  # "default" (Hamming / L2^2, ascending) or "overlap" (descending, R24)
         self.W = projection(seed, m, s, self.d) if W is None else np.asarray(W, dtype=np.uint16)
         self.codes = encode(self.vectors, self.W, L)
         if sketch == "binary":
@@ -370,7 +384,10 @@ class OracleIndex:
         return sketch_count(codes, off, self.m)[0]
 
     def scores(self, Q) -> np.ndarray:
+        """Filter scores, smaller = closer (the order select_top_T ranks by)."""
         sq = self.query_sketch(Q)
+        if self.score == "overlap":
+            return -overlap_scores(sq, self.sketches, self.kind)
         if self.kind == "binary":
             return hamming_scores(sq, self.sketches)
         return count_l2_scores(sq, self.sketches)

@@ -236,6 +236,33 @@ def test_count_l2_reduces_to_hamming_on_binary_counters():
 
 # ----------------------------------------------------------------- top-T
 
+def test_overlap_scores_bit_loop_and_identities():
+    """OVERLAP (R24): popc(S_Q AND S_i) by a per-bit Python loop; Hamming =
+    p_Q + p_i - 2 overlap against the independent XOR form; count sketches:
+    the dot product by a loop and L2^2 = |C_Q|^2 + |C_i|^2 - 2 dot; the
+    ranking is by descending overlap, ties by id."""
+    rng = np.random.default_rng(21)
+    m = 96
+    S = rng.integers(0, 2**32, size=(40, m // 32), dtype=np.uint64).astype(np.uint32)
+    SQ = rng.integers(0, 2**32, size=(m // 32,), dtype=np.uint64).astype(np.uint32)
+    ov = O.overlap_scores(SQ, S)
+    for i in range(S.shape[0]):
+        loop = sum(((int(S[i, w]) >> b) & (int(SQ[w]) >> b) & 1) for w in range(m // 32) for b in range(32))
+        assert ov[i] == loop
+    pq = O.popcount_rows(SQ[None, :])[0]
+    assert np.array_equal(O.hamming_scores(SQ, S), pq + O.popcount_rows(S) - 2 * ov)
+    C = rng.integers(0, 6, size=(30, 20)).astype(np.uint8)
+    CQ = rng.integers(0, 6, size=(20,)).astype(np.uint8)
+    dot = O.overlap_scores(CQ, C, "count")
+    for i in range(C.shape[0]):
+        assert dot[i] == sum(int(C[i, j]) * int(CQ[j]) for j in range(20))
+    n2 = lambda x: (x.astype(np.int64) ** 2).sum(-1)
+    assert np.array_equal(O.count_l2_scores(CQ, C), n2(CQ) + n2(C) - 2 * dot)
+    # descending overlap, ties by id: a set equal to the query's sketch and a superset come first
+    S2 = np.array([[0x0F], [0xFF], [0x0F], [0x01]], dtype=np.uint32)
+    assert O.select_top_T(-O.overlap_scores(np.array([0x0F], dtype=np.uint32), S2), 4).tolist() == [0, 1, 2, 3]
+
+
 def test_select_top_T_ties_by_id_and_nesting():
     sc = np.array([5, 1, 3, 1, 3, 3, 0, 9], dtype=np.int64)
     assert O.select_top_T(sc, 4).tolist() == [6, 1, 3, 2]
