@@ -87,7 +87,14 @@ typedef struct {
                             metric), 1 = MeanMin d_mean-min(Q, V) = 1/|Q| sum_q min_v ||q - v|| (the
                             query set first, reading R23), 2 = Min d_min(Q, V) = min ||q - v||.
                             The §3.2 alternatives; the filter is unchanged. */
+  uint32_t score;        /* filter score (bvss_score_kind): 0 = Hamming (binary) / squared L2 (count,
+                            reading R2); 1 = OVERLAP (reading R24): rank by the shared-bit count
+                            popc(S_Q AND S_i) (count: the dot product <C_Q, C_i>) descending, ties by id;
+                            bvss_filter reports it as the ascending key 2 (m - popc) (binary) /
+                            2 (m 255^2 - dot) (count). */
 } bvss_params;
+
+typedef enum { BVSS_SCORE_DEFAULT = 0, BVSS_SCORE_OVERLAP = 1 } bvss_score_kind;
 
 typedef enum { BVSS_METRIC_HAUSDORFF = 0, BVSS_METRIC_MEANMIN = 1, BVSS_METRIC_MIN = 2 } bvss_metric;
 

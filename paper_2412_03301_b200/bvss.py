@@ -43,9 +43,10 @@ class Params(C.Structure):
     _fields_ = [("m", C.c_uint32), ("s", C.c_uint32), ("L", C.c_uint32), ("sketch", C.c_uint32),
                 ("seed", C.c_uint64), ("projection", C.c_void_p), ("device", C.c_int32), ("flags", C.c_uint32),
                 ("query_batch", C.c_uint32), ("refine_terms", C.c_uint32),
-                ("select_mode", C.c_uint32), ("metric", C.c_uint32)]
+                ("select_mode", C.c_uint32), ("metric", C.c_uint32), ("score", C.c_uint32)]
 
 METRICS = {"hausdorff": 0, "meanmin": 1, "min": 2}  # bvss_metric (rerank distance)
+SCORES = {"default": 0, "overlap": 1}  # bvss_score_kind (filter score)
 
 
 class Info(C.Structure):
@@ -138,7 +139,7 @@ class Index:
 
     def __init__(self, vectors, offsets, *, m, s, L, sketch="binary", seed=0, device=0, keep_codes=False,
                  validate=False, projection=None, refine_terms=0, query_batch=0, select_mode=0,
-                 metric="hausdorff"):
+                 metric="hausdorff", score="default"):
         dev = _is_cuda(vectors)
         if dev != _is_cuda(offsets):
             raise ValueError("vectors and offsets must both be host arrays or both CUDA tensors")
@@ -158,7 +159,7 @@ class Index:
                    projection=(proj.ctypes.data if proj is not None else None), device=device,
                    flags=(DEVICE_PTRS if dev else 0) | (KEEP_CODES if keep_codes else 0) |
                    (VALIDATE_FINITE if validate else 0), query_batch=query_batch, refine_terms=refine_terms,
-                   select_mode=select_mode, metric=METRICS[metric])
+                   select_mode=select_mode, metric=METRICS[metric], score=SCORES[score])
         self._h = C.c_void_p()
         vp, _k1 = _ptr(vectors)
         op, _k2 = _ptr(offsets)
@@ -171,7 +172,7 @@ class Index:
     @classmethod
     def from_chunks(cls, chunks, *, n_total, nvec_total, d, m, s, L, sketch="binary", seed=0, device=0,
                     keep_codes=False, projection=None, refine_terms=0, query_batch=0, select_mode=0,
-                    metric="hausdorff"):
+                    metric="hausdorff", score="default"):
         """Streaming build (bvss_index_begin / append / finish): `chunks` yields host arrays
         (vectors [v][d] fp32, local_offsets [c+1] int64 starting at 0), sets in database order."""
         self = cls.__new__(cls)
@@ -179,7 +180,7 @@ class Index:
         p = Params(m=m, s=s, L=L, sketch=SKETCH_BINARY if sketch == "binary" else SKETCH_COUNT_U8, seed=seed,
                    projection=(proj.ctypes.data if proj is not None else None), device=device,
                    flags=KEEP_CODES if keep_codes else 0, query_batch=query_batch, refine_terms=refine_terms,
-                   select_mode=select_mode, metric=METRICS[metric])
+                   select_mode=select_mode, metric=METRICS[metric], score=SCORES[score])
         self._h = C.c_void_p()
         _check(lib.bvss_index_begin(int(n_total), int(nvec_total), int(d), C.byref(p), C.byref(self._h)))
         try:

@@ -108,6 +108,10 @@ int launch_merge_topk(const int64_t* ids, const float* dist, int P, int64_t nq, 
                       float* out_dist, cudaStream_t st);
 
 // ------------------------------------------------------- small kernels --
+__global__ void fill_i32_kernel(int32_t* __restrict__ x, int64_t n, int32_t v) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) x[i] = v;
+}
 __global__ void max_float_kernel(const float* __restrict__ x, int64_t n, unsigned int* __restrict__ out) {
   float m = 0.0f;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
@@ -240,6 +244,7 @@ struct bvss_index {
   int32_t* mass = nullptr;
   uint32_t select_mode = 0;   // 0 auto, 1 full keys, 2 sampled threshold
   int metric = 0;             // rerank metric: 0 Hausdorff, 1 MeanMin, 2 Min (bvss_params.metric)
+  int score = 0;              // filter score: 0 Hamming / L2^2, 1 OVERLAP (bvss_params.score, reading R24)
   int64_t ns = 0;             // database sample for the threshold estimate (select_mode 2)
   void* smp_sk = nullptr;     // chunk-major sketches of the sample
   void* skx = nullptr;        // binary: tensor-core scan operand, FP4 expansion [m/32][n][16 B] (scan_tc.cu)
@@ -345,6 +350,11 @@ struct DeviceGuard {
   }
 };
 
+// OVERLAP (R24) key offset: K0 - 2 <S_Q, S_i> >= 0 for every pair (binary: <.,.> <= m; count: <= m 255^2)
+int64_t overlap_k0(const bvss_index* idx) {
+  return idx->sketch == BVSS_SKETCH_BINARY ? 2ll * idx->m : 2ll * idx->m * 255 * 255;
+}
+
 int chunks_per_set(const bvss_index* idx) {
   return idx->sketch == BVSS_SKETCH_BINARY ? static_cast<int>(((idx->m / 32) + 3) / 4) : static_cast<int>(idx->m / 16);
 }
@@ -434,6 +444,12 @@ int prepare_queries(bvss_index* idx, bvss_search_ctx* c, const float* queries, c
   BVSS_TRY(c->alloc(nq * sizeof(int32_t), reinterpret_cast<void**>(&c->qmass)));
   BVSS_TRY(launch_sketch(c->qcodes, idx->m, c->qoff, nq, idx->sketch, c->qsk, c->qmass, 1, cps, idx->num_sms,
                          idx->stream));
+  if (idx->score == 1) {  // OVERLAP (R24): key = K0 + 0 - 2 <S_Q, S_i> with zero database masses (build)
+    fill_i32_kernel<<<static_cast<int>((nq + 255) / 256), 256, 0, idx->stream>>>(c->qmass, nq,
+                                                                              static_cast<int32_t>(overlap_k0(idx)));
+    idx->stats.kernel_launches += 1;
+    BVSS_TRY(post_launch("fill_i32_kernel", idx->stream));
+  }
   cudaEventRecord(idx->ev[2], idx->stream);
   idx->stats.kernel_launches += 2;
   return BVSS_OK;
@@ -465,6 +481,10 @@ int alloc_select_state(bvss_index* idx, bvss_search_ctx* c) {
   BVSS_TRY(c->alloc(nq * sizeof(int32_t), reinterpret_cast<void**>(&c->sel.digit)));
   BVSS_TRY(c->alloc(static_cast<size_t>(nq) * kHistBins * sizeof(int32_t), reinterpret_cast<void**>(&c->local_hist)));
   c->key_bits = key_bits_for(idx->sketch, idx->m);
+  if (idx->score == 1) {  // OVERLAP keys span [0, K0]
+    c->key_bits = 1;
+    while ((overlap_k0(idx) >> c->key_bits) != 0) ++c->key_bits;
+  }
   c->rounds = rounds_for(c->key_bits);
   c->next_round = 0;
   return BVSS_OK;
@@ -777,6 +797,7 @@ int validate_params(int64_t n, int32_t d, const bvss_params* p) {
     BVSS_FAIL(BVSS_EINVAL, "refine_terms must be 0 (default), 1, 3 or 255 (exact)");
   if (p->select_mode > 2) BVSS_FAIL(BVSS_EINVAL, "select_mode must be 0 (auto), 1 (full keys) or 2 (sampled)");
   if (p->metric > 2) BVSS_FAIL(BVSS_EINVAL, "metric must be 0 (Hausdorff), 1 (MeanMin) or 2 (Min)");
+  if (p->score > 1) BVSS_FAIL(BVSS_EINVAL, "score must be 0 (Hamming / L2^2) or 1 (OVERLAP)");
   return BVSS_OK;
 }
 
@@ -797,6 +818,7 @@ int build_impl(const float* vectors, const int64_t* set_offsets, int64_t n, int3
     BVSS_FAIL(BVSS_EINVAL, "refine_terms must be 0 (default), 1, 3 or 255 (exact)");
   if (p->select_mode > 2) BVSS_FAIL(BVSS_EINVAL, "select_mode must be 0 (auto), 1 (full keys) or 2 (sampled)");
   if (p->metric > 2) BVSS_FAIL(BVSS_EINVAL, "metric must be 0 (Hausdorff), 1 (MeanMin) or 2 (Min)");
+  if (p->score > 1) BVSS_FAIL(BVSS_EINVAL, "score must be 0 (Hamming / L2^2) or 1 (OVERLAP)");
   int num_sms = 0;
   BVSS_TRY(check_device(p->device, &num_sms));
   DeviceGuard g(p->device);
@@ -825,6 +847,7 @@ int build_impl(const float* vectors, const int64_t* set_offsets, int64_t n, int3
   idx->query_batch = p->query_batch;
   idx->select_mode = p->select_mode;
   idx->metric = static_cast<int>(p->metric);
+  idx->score = static_cast<int>(p->score);
   BVSS_CUDA(cudaStreamCreateWithFlags(&idx->own_stream, cudaStreamNonBlocking));
   idx->stream = idx->own_stream;
   for (auto& e : idx->ev) BVSS_CUDA(cudaEventCreate(&e));
@@ -906,6 +929,7 @@ int build_impl(const float* vectors, const int64_t* set_offsets, int64_t n, int3
   BVSS_TRY(dalloc(static_cast<size_t>(n) * cps * 16, &idx->sk));
   BVSS_TRY(dalloc(static_cast<size_t>(n) * 4, reinterpret_cast<void**>(&idx->mass)));
   BVSS_TRY(launch_sketch(codes, p->m, idx->off, n, p->sketch, idx->sk, idx->mass, n, 1, num_sms, st));
+  if (idx->score == 1) BVSS_CUDA(cudaMemsetAsync(idx->mass, 0, static_cast<size_t>(n) * 4, st));  // OVERLAP (R24)
   if (use_tc_scan(idx.get())) {
     // strided database sample for the sampled-threshold select
     idx->ns = n < 16384 ? n : 16384;
