@@ -91,10 +91,13 @@ typedef struct {
                             reading R2); 1 = OVERLAP (reading R24): rank by the shared-bit count
                             popc(S_Q AND S_i) (count: the dot product <C_Q, C_i>) descending, ties by id;
                             bvss_filter reports it as the ascending key 2 (m - popc) (binary) /
-                            2 (m 255^2 - dot) (count). */
+                            2 (m 255^2 - dot) (count); 2 = BINARIZED (reading R25): Hamming between
+                            the binarised counters (C_Q > 0) and (C_i > 0), which equal the OR-fold
+                            binary sketches, so a count index scored BINARIZED is built as a binary
+                            index (bvss_get_info / bvss_export_sketches then report binary sketches). */
 } bvss_params;
 
-typedef enum { BVSS_SCORE_DEFAULT = 0, BVSS_SCORE_OVERLAP = 1 } bvss_score_kind;
+typedef enum { BVSS_SCORE_DEFAULT = 0, BVSS_SCORE_OVERLAP = 1, BVSS_SCORE_BINARIZED = 2 } bvss_score_kind;
 
 typedef enum { BVSS_METRIC_HAUSDORFF = 0, BVSS_METRIC_MEANMIN = 1, BVSS_METRIC_MIN = 2 } bvss_metric;
 

@@ -361,7 +361,7 @@ class OracleIndex:
         self.d = self.vectors.shape[1]
         self.m, self.s, self.L, self.seed = m, s, L, seed
         self.kind = sketch
-        self.score = score  # "default" (Hamming / L2^2, ascending) or "overlap" (descending, R24)
+        self.score = score  # "default" (Hamming / L2^2), "overlap" (descending, R24), "binarized" (R25)
         self.W = projection(seed, m, s, self.d) if W is None else np.asarray(W, dtype=np.uint16)
         self.codes = encode(self.vectors, self.W, L)
         if sketch == "binary":
@@ -388,6 +388,8 @@ class OracleIndex:
         sq = self.query_sketch(Q)
         if self.score == "overlap":
             return -overlap_scores(sq, self.sketches, self.kind)
+        if self.score == "binarized" and self.kind == "count":  # R25: Hamming between (C_Q > 0), (C_i > 0)
+            return hamming_scores(pack_bits(sq[None, :] > 0)[0], pack_bits(self.sketches > 0))
         if self.kind == "binary":
             return hamming_scores(sq, self.sketches)
         return count_l2_scores(sq, self.sketches)

@@ -46,7 +46,7 @@ class Params(C.Structure):
                 ("select_mode", C.c_uint32), ("metric", C.c_uint32), ("score", C.c_uint32)]
 
 METRICS = {"hausdorff": 0, "meanmin": 1, "min": 2}  # bvss_metric (rerank distance)
-SCORES = {"default": 0, "overlap": 1}  # bvss_score_kind (filter score)
+SCORES = {"default": 0, "overlap": 1, "binarized": 2}  # bvss_score_kind (filter score)
 
 
 class Info(C.Structure):
@@ -153,7 +153,7 @@ class Index:
             offsets = np.ascontiguousarray(offsets, dtype=np.int64)
         n = int(offsets.shape[0]) - 1
         d = int(vectors.shape[1])
-        self.sketch_kind = sketch
+        self.sketch_kind = "binary" if score == "binarized" else sketch  # BINARIZED: a binary index (R25)
         proj = None if projection is None else np.ascontiguousarray(projection, dtype=np.uint16)
         p = Params(m=m, s=s, L=L, sketch=SKETCH_BINARY if sketch == "binary" else SKETCH_COUNT_U8, seed=seed,
                    projection=(proj.ctypes.data if proj is not None else None), device=device,
@@ -194,7 +194,7 @@ class Index:
             lib.bvss_free_index(self._h)
             self._h = C.c_void_p()
             raise
-        self.sketch_kind = sketch
+        self.sketch_kind = "binary" if score == "binarized" else sketch  # BINARIZED: a binary index (R25)
         self.n, self.d, self.m, self.s, self.L, self.device = int(n_total), int(d), m, s, L, device
         return self
 

@@ -797,7 +797,7 @@ int validate_params(int64_t n, int32_t d, const bvss_params* p) {
     BVSS_FAIL(BVSS_EINVAL, "refine_terms must be 0 (default), 1, 3 or 255 (exact)");
   if (p->select_mode > 2) BVSS_FAIL(BVSS_EINVAL, "select_mode must be 0 (auto), 1 (full keys) or 2 (sampled)");
   if (p->metric > 2) BVSS_FAIL(BVSS_EINVAL, "metric must be 0 (Hausdorff), 1 (MeanMin) or 2 (Min)");
-  if (p->score > 1) BVSS_FAIL(BVSS_EINVAL, "score must be 0 (Hamming / L2^2) or 1 (OVERLAP)");
+  if (p->score > 2) BVSS_FAIL(BVSS_EINVAL, "score must be 0 (Hamming / L2^2), 1 (OVERLAP) or 2 (BINARIZED)");
   return BVSS_OK;
 }
 
@@ -818,7 +818,7 @@ int build_impl(const float* vectors, const int64_t* set_offsets, int64_t n, int3
     BVSS_FAIL(BVSS_EINVAL, "refine_terms must be 0 (default), 1, 3 or 255 (exact)");
   if (p->select_mode > 2) BVSS_FAIL(BVSS_EINVAL, "select_mode must be 0 (auto), 1 (full keys) or 2 (sampled)");
   if (p->metric > 2) BVSS_FAIL(BVSS_EINVAL, "metric must be 0 (Hausdorff), 1 (MeanMin) or 2 (Min)");
-  if (p->score > 1) BVSS_FAIL(BVSS_EINVAL, "score must be 0 (Hamming / L2^2) or 1 (OVERLAP)");
+  if (p->score > 2) BVSS_FAIL(BVSS_EINVAL, "score must be 0 (Hamming / L2^2), 1 (OVERLAP) or 2 (BINARIZED)");
   int num_sms = 0;
   BVSS_TRY(check_device(p->device, &num_sms));
   DeviceGuard g(p->device);
@@ -840,7 +840,9 @@ int build_impl(const float* vectors, const int64_t* set_offsets, int64_t n, int3
   idx->m = p->m;
   idx->s = p->s;
   idx->L = p->L;
-  idx->sketch = p->sketch;
+  // BINARIZED (R25): Hamming on (C > 0) is Hamming on the OR-fold, so a count-sketch index scored
+  // BINARIZED is built and scanned as a binary-sketch index
+  idx->sketch = (p->sketch == BVSS_SKETCH_COUNT_U8 && p->score == 2) ? static_cast<uint32_t>(BVSS_SKETCH_BINARY) : p->sketch;
   idx->seed = p->seed;
   // 0 = default (1-term fp16 tensor-core pass + exact window), 1, 3, 255 = exact SIMT for every candidate
   idx->terms = p->refine_terms == 0 ? 1 : (p->refine_terms == 255 ? 0 : static_cast<int>(p->refine_terms));
@@ -928,7 +930,7 @@ int build_impl(const float* vectors, const int64_t* set_offsets, int64_t n, int3
   const int cps = chunks_per_set(idx.get());
   BVSS_TRY(dalloc(static_cast<size_t>(n) * cps * 16, &idx->sk));
   BVSS_TRY(dalloc(static_cast<size_t>(n) * 4, reinterpret_cast<void**>(&idx->mass)));
-  BVSS_TRY(launch_sketch(codes, p->m, idx->off, n, p->sketch, idx->sk, idx->mass, n, 1, num_sms, st));
+  BVSS_TRY(launch_sketch(codes, p->m, idx->off, n, idx->sketch, idx->sk, idx->mass, n, 1, num_sms, st));
   if (idx->score == 1) BVSS_CUDA(cudaMemsetAsync(idx->mass, 0, static_cast<size_t>(n) * 4, st));  // OVERLAP (R24)
   if (use_tc_scan(idx.get())) {
     // strided database sample for the sampled-threshold select
@@ -936,7 +938,7 @@ int build_impl(const float* vectors, const int64_t* set_offsets, int64_t n, int3
     BVSS_TRY(dalloc(static_cast<size_t>(idx->ns) * cps * 16, &idx->smp_sk));
     BVSS_TRY(dalloc(static_cast<size_t>(idx->ns) * 4, reinterpret_cast<void**>(&idx->smp_mass)));
     BVSS_TRY(launch_gather_sample(idx->sk, idx->mass, n, cps, idx->ns, idx->smp_sk, idx->smp_mass, num_sms, st));
-    if (p->sketch == BVSS_SKETCH_BINARY) {  // FP4 tensor-core operands (m/2 bytes per set)
+    if (idx->sketch == BVSS_SKETCH_BINARY) {  // FP4 tensor-core operands (m/2 bytes per set)
       BVSS_TRY(dalloc(static_cast<size_t>(n) * p->m / 2, &idx->skx));
       BVSS_TRY(dalloc(static_cast<size_t>(idx->ns) * p->m / 2, &idx->smp_skx));
       BVSS_TRY(launch_expand_db_fp4(idx->sk, n, n, p->m, idx->skx, num_sms, st));

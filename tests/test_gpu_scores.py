@@ -68,3 +68,29 @@ def test_overlap_search_matches_oracle(scase):
         Q = d["queries"][d["q_offsets"][qi]:d["q_offsets"][qi + 1]]
         r_ids, r_d = oi.search(Q, cfg.k, cfg.T)
         check_topk(ids[qi], dist[qi], r_ids, r_d, lambda i: O.hausdorff(Q, V[off[i]:off[i + 1]]))
+
+
+def test_binarized_count_index_matches_oracle():
+    """BINARIZED (R25) on a count-sketch config: the index is a binary one (FP4 scan); its candidates equal
+    the oracle's Hamming between binarised count sketches, and the search matches the oracle pipeline."""
+    _need_gpu()
+    cfg = synth.get_config("cfg2", n=2500, nq=5, T=150)
+    d = synth.to_numpy(synth.generate(cfg, device="cpu"))
+    idx = B.Index(d["vectors"], d["offsets"], m=cfg.m, s=cfg.s, L=cfg.L, sketch="count", seed=cfg.seed,
+                  score="binarized")
+    oi = O.OracleIndex(d["vectors"], d["offsets"], cfg.m, cfg.s, cfg.L, cfg.seed, sketch="count", score="binarized")
+    db = idx.export_sketches()
+    qsk = idx.query_sketch(d["queries"], d["q_offsets"])
+    cand, score = idx.filter(d["queries"], d["q_offsets"], cfg.T)
+    for qi in range(cand.shape[0]):
+        sc = O.hamming_scores(qsk[qi], db)
+        got = cand[qi][cand[qi] >= 0]
+        assert np.array_equal(np.sort(O.select_top_T(sc, cfg.T)), got)
+        assert np.array_equal(score[qi][: got.shape[0]].astype(np.int64), sc[got])
+    ids, dist = idx.search(d["queries"], d["q_offsets"], cfg.k, cfg.T)
+    idx.close()
+    V, off = d["vectors"], d["offsets"]
+    for qi in range(ids.shape[0]):
+        Q = d["queries"][d["q_offsets"][qi]:d["q_offsets"][qi + 1]]
+        r_ids, r_d = oi.search(Q, cfg.k, cfg.T)
+        check_topk(ids[qi], dist[qi], r_ids, r_d, lambda i: O.hausdorff(Q, V[off[i]:off[i + 1]]))

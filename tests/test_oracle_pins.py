@@ -263,6 +263,22 @@ def test_overlap_scores_bit_loop_and_identities():
     assert O.select_top_T(-O.overlap_scores(np.array([0x0F], dtype=np.uint32), S2), 4).tolist() == [0, 1, 2, 3]
 
 
+def test_binarized_count_score_equals_binary_sketch_hamming():
+    """BINARIZED (R25): Hamming between the binarised count sketches equals the
+    Hamming of the OR-fold binary sketches of the same codes (Def 8 vs Def 10:
+    S = (C > 0)), for every query, through two different oracle paths."""
+    rng = np.random.default_rng(4)
+    sizes = rng.integers(1, 7, size=60)
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    V = rng.normal(size=(off[-1], 24)).astype(np.float32)
+    cnt = O.OracleIndex(V, off, 64, 3, 5, 9, sketch="count", score="binarized")
+    bin_ = O.OracleIndex(V, off, 64, 3, 5, 9, sketch="binary")
+    for q in range(4):
+        Q = rng.normal(size=(int(rng.integers(1, 5)), 24)).astype(np.float32)
+        assert np.array_equal(cnt.scores(Q), bin_.scores(Q))
+        assert np.array_equal(cnt.filter(Q, 10), bin_.filter(Q, 10))
+
+
 def test_select_top_T_ties_by_id_and_nesting():
     sc = np.array([5, 1, 3, 1, 3, 3, 0, 9], dtype=np.int64)
     assert O.select_top_T(sc, 4).tolist() == [6, 1, 3, 2]
