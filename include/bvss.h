@@ -94,10 +94,12 @@ typedef struct {
                             2 (m 255^2 - dot) (count); 2 = BINARIZED (reading R25): Hamming between
                             the binarised counters (C_Q > 0) and (C_i > 0), which equal the OR-fold
                             binary sketches, so a count index scored BINARIZED is built as a binary
-                            index (bvss_get_info / bvss_export_sketches then report binary sketches). */
+                            index (bvss_get_info / bvss_export_sketches then report binary sketches);
+                            3 = L1 (reading R26): sum_j |C_Q[j] - C_i[j]| for count sketches (SIMT
+                            vabsdiffu4 / dp4a scan, full-key select); on binary sketches L1 = Hamming. */
 } bvss_params;
 
-typedef enum { BVSS_SCORE_DEFAULT = 0, BVSS_SCORE_OVERLAP = 1, BVSS_SCORE_BINARIZED = 2 } bvss_score_kind;
+typedef enum { BVSS_SCORE_DEFAULT = 0, BVSS_SCORE_OVERLAP = 1, BVSS_SCORE_BINARIZED = 2, BVSS_SCORE_L1 = 3 } bvss_score_kind;
 
 typedef enum { BVSS_METRIC_HAUSDORFF = 0, BVSS_METRIC_MEANMIN = 1, BVSS_METRIC_MIN = 2 } bvss_metric;
 

@@ -231,6 +231,13 @@ def overlap_scores(SQ: np.ndarray, S: np.ndarray, kind: str = "binary") -> np.nd
     return (C * np.asarray(SQ, dtype=np.int64)[None, :]).sum(axis=1)
 
 
+def count_l1_scores(CQ: np.ndarray, C: np.ndarray) -> np.ndarray:
+    """Reading R26 (SURVEY A2's L1 flag): L1 distance between counter vectors,
+    sum_j |C_Q[j] - C_i[j]|, exact int64.  Returns int64 ``[n]``."""
+    diff = np.asarray(C, dtype=np.int64) - np.asarray(CQ, dtype=np.int64)[None, :]
+    return np.abs(diff).sum(axis=1)
+
+
 # ---------------------------------------------------------------------------
 # a-6: top-T candidate selection  (Alg 6 lines 10-18 P:795-806; readings R3, R4)
 # ---------------------------------------------------------------------------
@@ -388,6 +395,8 @@ class OracleIndex:
         sq = self.query_sketch(Q)
         if self.score == "overlap":
             return -overlap_scores(sq, self.sketches, self.kind)
+        if self.score == "l1" and self.kind == "count":  # R26
+            return count_l1_scores(sq, self.sketches)
         if self.score == "binarized" and self.kind == "count":  # R25: Hamming between (C_Q > 0), (C_i > 0)
             return hamming_scores(pack_bits(sq[None, :] > 0)[0], pack_bits(self.sketches > 0))
         if self.kind == "binary":

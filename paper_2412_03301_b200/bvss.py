@@ -46,7 +46,7 @@ class Params(C.Structure):
                 ("select_mode", C.c_uint32), ("metric", C.c_uint32), ("score", C.c_uint32)]
 
 METRICS = {"hausdorff": 0, "meanmin": 1, "min": 2}  # bvss_metric (rerank distance)
-SCORES = {"default": 0, "overlap": 1, "binarized": 2}  # bvss_score_kind (filter score)
+SCORES = {"default": 0, "overlap": 1, "binarized": 2, "l1": 3}  # bvss_score_kind (filter score)
 
 
 class Info(C.Structure):

@@ -457,7 +457,12 @@ int prepare_queries(bvss_index* idx, bvss_search_ctx* c, const float* queries, c
 
 bool use_tc_scan(const bvss_index* idx) {
   static const bool simt = getenv("BVSS_SCAN_SIMT") != nullptr;  // developer switch: SIMT popc/dp4a scan
+  if (idx->score == 3 && idx->sketch == BVSS_SKETCH_COUNT_U8) return false;  // L1 (R26): no GEMM form
   return idx->m % (idx->sketch == BVSS_SKETCH_BINARY ? 256 : 128) == 0 && !simt;
+}
+// the SIMT scan's kind: the sketch kind, or 2 = count sketches scored L1 (R26)
+int scan_kind(const bvss_index* idx) {
+  return (idx->score == 3 && idx->sketch == BVSS_SKETCH_COUNT_U8) ? 2 : static_cast<int>(idx->sketch);
 }
 // database operand of the tensor-core scan (binary: FP4 expansion; count: the counters themselves)
 const void* scan_operand(const bvss_index* idx, bool sample) {
@@ -507,7 +512,7 @@ int scan_batch(bvss_index* idx, bvss_search_ctx* c) {
     idx->stats.scan_bytes += scan_tc_db_bytes(idx->sketch, idx->m, n, static_cast<int>(c->nq), idx->num_sms);
     idx->stats.scan_macs += static_cast<uint64_t>(c->nq) * n * idx->m;
   } else {
-    BVSS_TRY(launch_scan(idx->sketch, idx->sk, idx->mass, n, n, idx->m, c->qsk, c->qmass, static_cast<int>(c->nq),
+    BVSS_TRY(launch_scan(scan_kind(idx), idx->sk, idx->mass, n, n, idx->m, c->qsk, c->qmass, static_cast<int>(c->nq),
                          c->keys, c->key_stride, idx->num_sms, idx->stream));
     idx->stats.kernel_launches += 1;
     idx->stats.scan_bytes += static_cast<uint64_t>(ceil_div<int64_t>(c->nq, 8)) * n * chunks_per_set(idx) * 16;
@@ -638,7 +643,7 @@ int fallback_full(bvss_index* idx, bvss_search_ctx* c) {
                               c->qx, c->qpad, keys, key_stride, wc, idx->num_sms, idx->stream, nullptr, nullptr,
                               nullptr, nullptr, 0, 0, true));
     } else {
-      BVSS_TRY(launch_scan(idx->sketch, idx->sk, idx->mass, n, n, idx->m, sq, c->qmass + q0, ns, keys, key_stride,
+      BVSS_TRY(launch_scan(scan_kind(idx), idx->sk, idx->mass, n, n, idx->m, sq, c->qmass + q0, ns, keys, key_stride,
                            idx->num_sms, idx->stream));
     }
     SelectState s2 = c->sel;
@@ -797,7 +802,7 @@ int validate_params(int64_t n, int32_t d, const bvss_params* p) {
     BVSS_FAIL(BVSS_EINVAL, "refine_terms must be 0 (default), 1, 3 or 255 (exact)");
   if (p->select_mode > 2) BVSS_FAIL(BVSS_EINVAL, "select_mode must be 0 (auto), 1 (full keys) or 2 (sampled)");
   if (p->metric > 2) BVSS_FAIL(BVSS_EINVAL, "metric must be 0 (Hausdorff), 1 (MeanMin) or 2 (Min)");
-  if (p->score > 2) BVSS_FAIL(BVSS_EINVAL, "score must be 0 (Hamming / L2^2), 1 (OVERLAP) or 2 (BINARIZED)");
+  if (p->score > 3) BVSS_FAIL(BVSS_EINVAL, "score must be 0 (Hamming / L2^2), 1 (OVERLAP), 2 (BINARIZED) or 3 (L1)");
   return BVSS_OK;
 }
 
@@ -818,7 +823,7 @@ int build_impl(const float* vectors, const int64_t* set_offsets, int64_t n, int3
     BVSS_FAIL(BVSS_EINVAL, "refine_terms must be 0 (default), 1, 3 or 255 (exact)");
   if (p->select_mode > 2) BVSS_FAIL(BVSS_EINVAL, "select_mode must be 0 (auto), 1 (full keys) or 2 (sampled)");
   if (p->metric > 2) BVSS_FAIL(BVSS_EINVAL, "metric must be 0 (Hausdorff), 1 (MeanMin) or 2 (Min)");
-  if (p->score > 2) BVSS_FAIL(BVSS_EINVAL, "score must be 0 (Hamming / L2^2), 1 (OVERLAP) or 2 (BINARIZED)");
+  if (p->score > 3) BVSS_FAIL(BVSS_EINVAL, "score must be 0 (Hamming / L2^2), 1 (OVERLAP), 2 (BINARIZED) or 3 (L1)");
   int num_sms = 0;
   BVSS_TRY(check_device(p->device, &num_sms));
   DeviceGuard g(p->device);

@@ -53,7 +53,9 @@ __global__ void __launch_bounds__(256) scan_binary_kernel(const uint4* __restric
   }
 }
 
-template <int QT>
+// L1 = false: squared L2 |C_Q|^2 + |C_i|^2 - 2 <C_Q, C_i> (R2); L1 = true: sum_j |C_Q[j] - C_i[j]| (R26),
+// per byte |a - b| by vabsdiffu4 and the byte sum by dp4a with ones
+template <int QT, bool L1>
 __global__ void __launch_bounds__(256) scan_count_kernel(const uint4* __restrict__ C, const int32_t* __restrict__ nC,
                                                          int64_t n, int64_t n_stride, int chunks,
                                                          const uint4* __restrict__ CQ /*[nq][chunks]*/,
@@ -79,16 +81,23 @@ __global__ void __launch_bounds__(256) scan_count_kernel(const uint4* __restrict
 #pragma unroll
       for (int q = 0; q < QT; ++q) {
         const uint4 b = sqc[q * chunks + c];
-        acc[q] = __dp4a(a.x, b.x, acc[q]);
-        acc[q] = __dp4a(a.y, b.y, acc[q]);
-        acc[q] = __dp4a(a.z, b.z, acc[q]);
-        acc[q] = __dp4a(a.w, b.w, acc[q]);
+        if (L1) {
+          acc[q] = __dp4a(__vabsdiffu4(a.x, b.x), 0x01010101u, acc[q]);
+          acc[q] = __dp4a(__vabsdiffu4(a.y, b.y), 0x01010101u, acc[q]);
+          acc[q] = __dp4a(__vabsdiffu4(a.z, b.z), 0x01010101u, acc[q]);
+          acc[q] = __dp4a(__vabsdiffu4(a.w, b.w), 0x01010101u, acc[q]);
+        } else {
+          acc[q] = __dp4a(a.x, b.x, acc[q]);
+          acc[q] = __dp4a(a.y, b.y, acc[q]);
+          acc[q] = __dp4a(a.z, b.z, acc[q]);
+          acc[q] = __dp4a(a.w, b.w, acc[q]);
+        }
       }
     }
     const uint32_t ni = static_cast<uint32_t>(nC[i]);
 #pragma unroll
     for (int q = 0; q < QT; ++q)
-      if (qg + q < nq) keys[static_cast<int64_t>(qg + q) * key_stride + i] = snq[q] + ni - 2u * acc[q];
+      if (qg + q < nq) keys[static_cast<int64_t>(qg + q) * key_stride + i] = L1 ? acc[q] : snq[q] + ni - 2u * acc[q];
   }
 }
 
@@ -126,7 +135,7 @@ int launch_scan(int kind, const void* S, const int32_t* mass, int64_t n, int64_t
     const int cap = ceil_div(num_sms * 8 * 4, gy);
     if (gx > cap) gx = cap < 1 ? 1 : cap;
     const size_t smem = static_cast<size_t>(QT) * chunks * 16;
-    auto kfn = scan_count_kernel<QT>;
+    auto kfn = kind == 2 ? scan_count_kernel<QT, true> : scan_count_kernel<QT, false>;  // kind 2: count, L1
     BVSS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     kfn<<<dim3(gx, gy), 256, smem, st>>>(static_cast<const uint4*>(S), mass, n, n_stride, chunks,
                                          static_cast<const uint4*>(SQ), massQ, nq, static_cast<uint32_t*>(keys),

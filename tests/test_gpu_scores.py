@@ -94,3 +94,31 @@ def test_binarized_count_index_matches_oracle():
         Q = d["queries"][d["q_offsets"][qi]:d["q_offsets"][qi + 1]]
         r_ids, r_d = oi.search(Q, cfg.k, cfg.T)
         check_topk(ids[qi], dist[qi], r_ids, r_d, lambda i: O.hausdorff(Q, V[off[i]:off[i + 1]]))
+
+
+@pytest.mark.parametrize("ov", [dict(n=3001, nq=5, T=200), dict(n=20011, nq=3, T=500, d=64)])
+def test_l1_count_score_matches_oracle(ov):
+    """L1 (R26) on count sketches: SIMT vabsdiffu4/dp4a scan + full-key select, candidates and keys bit-exact
+    given the GPU sketches, and the search against the oracle pipeline."""
+    _need_gpu()
+    cfg = synth.get_config("cfg2", **ov)
+    d = synth.to_numpy(synth.generate(cfg, device="cpu"))
+    idx = B.Index(d["vectors"], d["offsets"], m=cfg.m, s=cfg.s, L=cfg.L, sketch="count", seed=cfg.seed, score="l1")
+    db = idx.export_sketches()
+    qsk = idx.query_sketch(d["queries"], d["q_offsets"])
+    for T in (1, cfg.T, cfg.n + 2):
+        cand, score = idx.filter(d["queries"], d["q_offsets"], T)
+        for qi in range(cand.shape[0]):
+            sc = O.count_l1_scores(qsk[qi], db)
+            got = cand[qi][cand[qi] >= 0]
+            assert got.shape[0] == min(T, cfg.n)
+            assert np.array_equal(np.sort(O.select_top_T(sc, T)), got)
+            assert np.array_equal(score[qi][: got.shape[0]].astype(np.int64), sc[got])
+    ids, dist = idx.search(d["queries"], d["q_offsets"], cfg.k, cfg.T)
+    idx.close()
+    oi = O.OracleIndex(d["vectors"], d["offsets"], cfg.m, cfg.s, cfg.L, cfg.seed, sketch="count", score="l1")
+    V, off = d["vectors"], d["offsets"]
+    for qi in range(ids.shape[0]):
+        Q = d["queries"][d["q_offsets"][qi]:d["q_offsets"][qi + 1]]
+        r_ids, r_d = oi.search(Q, cfg.k, cfg.T)
+        check_topk(ids[qi], dist[qi], r_ids, r_d, lambda i: O.hausdorff(Q, V[off[i]:off[i + 1]]))

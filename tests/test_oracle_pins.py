@@ -279,6 +279,21 @@ def test_binarized_count_score_equals_binary_sketch_hamming():
         assert np.array_equal(cnt.filter(Q, 10), bin_.filter(Q, 10))
 
 
+def test_count_l1_scores_loop_and_binary_reduction():
+    """L1 (R26): a per-counter loop; on 0/1 counters L1 = L2^2 = Hamming."""
+    rng = np.random.default_rng(5)
+    C = rng.integers(0, 255, size=(25, 16)).astype(np.uint8)
+    CQ = rng.integers(0, 255, size=(16,)).astype(np.uint8)
+    l1 = O.count_l1_scores(CQ, C)
+    for i in range(C.shape[0]):
+        assert l1[i] == sum(abs(int(C[i, j]) - int(CQ[j])) for j in range(16))
+    B01 = rng.integers(0, 2, size=(25, 64)).astype(np.uint8)
+    BQ = rng.integers(0, 2, size=(64,)).astype(np.uint8)
+    ham = O.hamming_scores(O.pack_bits(BQ[None, :] > 0)[0], O.pack_bits(B01 > 0))
+    assert np.array_equal(O.count_l1_scores(BQ, B01), ham)
+    assert np.array_equal(O.count_l2_scores(BQ, B01), ham)
+
+
 def test_select_top_T_ties_by_id_and_nesting():
     sc = np.array([5, 1, 3, 1, 3, 3, 0, 9], dtype=np.int64)
     assert O.select_top_T(sc, 4).tolist() == [6, 1, 3, 2]
