@@ -37,3 +37,24 @@ def test_no_cpu_fallback(libpath):
     with pytest.raises(bvss.BvssError) as e:
         bvss.Index(np.zeros((4, 8), np.float32), np.array([0, 4]), m=32, s=2, L=4)
     assert e.value.code in (bvss.EUNSUPPORTED, bvss.ECUDA)
+
+
+@pytest.mark.parametrize("struct,pyname", [("bvss_params", "Params"), ("bvss_info", "Info"), ("bvss_stats", "Stats")])
+def test_struct_layouts_match_header(tmp_path, struct, pyname):
+    """The ctypes mirrors of the ABI structs have the header's size and field offsets (compiled with gcc)."""
+    import shutil
+    import subprocess
+    from paper_2412_03301_b200 import bvss
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    py = getattr(bvss, pyname)
+    fields = [f for f, _ in py._fields_]
+    src = tmp_path / "layout.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "bvss.h"\nint main(void) {\n'
+                   f'  printf("%zu\\n", sizeof({struct}));\n' +
+                   "".join(f'  printf("%zu\\n", offsetof({struct}, {f}));\n' for f in fields) + "  return 0;\n}\n")
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)], check=True)
+    out = [int(x) for x in subprocess.run([str(exe)], check=True, capture_output=True, text=True).stdout.split()]
+    assert out[0] == ctypes.sizeof(py), (struct, out[0], ctypes.sizeof(py))
+    assert out[1:] == [getattr(py, f).offset for f in fields]
