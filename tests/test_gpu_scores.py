@@ -39,6 +39,19 @@ def scase(request):
     idx.close()
 
 
+_ORACLES = {}
+
+
+def _oracle_index(cfg, d, score):
+    """One oracle index per workload (its encode dominates the test time); the filter score is a view."""
+    key = (cfg.name, cfg.n, cfg.nq, cfg.d, cfg.T)
+    if key not in _ORACLES:
+        _ORACLES[key] = O.OracleIndex(d["vectors"], d["offsets"], cfg.m, cfg.s, cfg.L, cfg.seed, sketch=cfg.sketch)
+    oi = _ORACLES[key]
+    oi.score = score
+    return oi
+
+
 def _k0(cfg):
     return 2 * cfg.m if cfg.sketch == "binary" else 2 * cfg.m * 255 * 255
 
@@ -62,7 +75,7 @@ def test_overlap_filter_given_gpu_sketches(scase):
 def test_overlap_search_matches_oracle(scase):
     cfg, d, idx = scase["cfg"], scase["data"], scase["idx"]
     ids, dist = idx.search(d["queries"], d["q_offsets"], cfg.k, cfg.T)
-    oi = O.OracleIndex(d["vectors"], d["offsets"], cfg.m, cfg.s, cfg.L, cfg.seed, sketch=cfg.sketch, score="overlap")
+    oi = _oracle_index(cfg, d, "overlap")
     V, off = d["vectors"], d["offsets"]
     for qi in range(ids.shape[0]):
         Q = d["queries"][d["q_offsets"][qi]:d["q_offsets"][qi + 1]]
