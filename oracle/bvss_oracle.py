@@ -360,7 +360,10 @@ class OracleIndex:
     """Index state of Algs 1, 3, 5 for one database (P:323-343, P:665-682,
     P:738-757): W, per-vector codes D^H, per-set sketches."""
 
-    def __init__(self, vectors, offsets, m, s, L, seed, sketch="binary", W=None, score="default"):
+    def __init__(self, vectors, offsets, m, s, L, seed, sketch="binary", W=None, score="default", sketches=None):
+        """``sketches``: database sketches handed in from the stage under test
+        (stage-wise parity: each stage is fed the previous stage's
+        output), skipping the database encode; queries are still encoded here."""
         self.vectors = np.ascontiguousarray(vectors, dtype=np.float32)
         self.offsets = _check_offsets(offsets)
         if self.offsets[-1] != self.vectors.shape[0]:
@@ -370,6 +373,12 @@ class OracleIndex:
         self.kind = sketch
         self.score = score  # "default" (Hamming / L2^2), "overlap" (descending, R24), "binarized" (R25)
         self.W = projection(seed, m, s, self.d) if W is None else np.asarray(W, dtype=np.uint16)
+        if sketches is not None:
+            self.codes = None
+            self.sketches = np.asarray(sketches)
+            if self.sketches.shape[0] != self.n or sketch not in ("binary", "count"):
+                raise ValueError("sketches must hold one row per set")
+            return
         self.codes = encode(self.vectors, self.W, L)
         if sketch == "binary":
             self.sketches = sketch_binary(self.codes, self.offsets)

@@ -59,3 +59,16 @@ def codes_match_modulo_near_ties(gpu_codes, ora_codes, V, W, L, m):
 
 def offsets_from_sizes(sizes):
     return np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+
+
+_ORACLES = {}
+
+
+def oracle_from_gpu_sketches(cfg, data, gpu_idx, score="default"):
+    """An oracle index over the GPU's exported database sketches (stage-wise parity: the sketches are
+    checked bit-exact elsewhere), cached per workload -- the database encode dominates the oracle time."""
+    key = (cfg.name, cfg.n, cfg.nq, cfg.d, cfg.seed, cfg.sketch, score)
+    if key not in _ORACLES:
+        _ORACLES[key] = O.OracleIndex(data["vectors"], data["offsets"], cfg.m, cfg.s, cfg.L, cfg.seed,
+                                      sketch=cfg.sketch, score=score, sketches=gpu_idx.export_sketches())
+    return _ORACLES[key]

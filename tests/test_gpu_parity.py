@@ -14,7 +14,8 @@ import pytest
 
 from gen import synth
 from oracle import bvss_oracle as O
-from tests._common import check_topk, codes_match_modulo_near_ties, dist_close, offsets_from_sizes
+from tests._common import (check_topk, codes_match_modulo_near_ties, dist_close, offsets_from_sizes,
+                           oracle_from_gpu_sketches)
 
 pytestmark = pytest.mark.gpu
 
@@ -250,6 +251,8 @@ def _modes_agree(cfg, data, Ts, env_cap=None, monkeypatch=None):
             ids, dist = idx.search(data["queries"], data["q_offsets"], cfg.k, T)
             res.append((ids, dist, idx.stats()))
         out[mode] = res
+        if mode == 1:
+            out["oracle"] = oracle_from_gpu_sketches(cfg, data, idx)
         idx.close()
     for (i1, d1, s1), (i2, d2, s2) in zip(out[1], out[2]):
         assert s1["select_batches"] == 0
@@ -268,7 +271,7 @@ def test_sampled_select_equals_full_select(name, ov):
     data = synth.to_numpy(synth.generate(cfg, device="cpu"))
     out = _modes_agree(cfg, data, (cfg.k, cfg.T, 4 * cfg.T))
     ids, dist, st = out[2][1]
-    oi = O.OracleIndex(data["vectors"], data["offsets"], cfg.m, cfg.s, cfg.L, cfg.seed, sketch=cfg.sketch)
+    oi = out["oracle"]
     V, off = data["vectors"], data["offsets"]
     for qi in range(3):
         Q = data["queries"][data["q_offsets"][qi]:data["q_offsets"][qi + 1]]
@@ -354,11 +357,11 @@ def test_search_range_major_refine(monkeypatch, rng_sets):
         monkeypatch.setenv("BVSS_REFINE_GROUP", mode)
         ids, dist = idx.search(data["queries"], data["q_offsets"], cfg.k, cfg.T)
         out[mode] = (ids, dist, idx.stats())
+    oi = oracle_from_gpu_sketches(cfg, data, idx)
     idx.close()
     assert out["1"][2]["select_batches"] >= 1
     assert np.array_equal(out["0"][0], out["1"][0]) and np.array_equal(out["0"][1], out["1"][1])
     assert out["0"][2]["fixup_sets"] == out["1"][2]["fixup_sets"]  # identical tensor-core values
-    oi = O.OracleIndex(data["vectors"], data["offsets"], cfg.m, cfg.s, cfg.L, cfg.seed, sketch=cfg.sketch)
     V, off = data["vectors"], data["offsets"]
     ids, dist = out["1"][0], out["1"][1]
     for qi in range(0, cfg.nq, 6):

@@ -8,7 +8,7 @@ import pytest
 
 from gen import synth
 from oracle import bvss_oracle as O
-from tests._common import check_topk
+from tests._common import check_topk, oracle_from_gpu_sketches
 
 pytestmark = pytest.mark.gpu
 
@@ -39,19 +39,6 @@ def scase(request):
     idx.close()
 
 
-_ORACLES = {}
-
-
-def _oracle_index(cfg, d, score):
-    """One oracle index per workload (its encode dominates the test time); the filter score is a view."""
-    key = (cfg.name, cfg.n, cfg.nq, cfg.d, cfg.T)
-    if key not in _ORACLES:
-        _ORACLES[key] = O.OracleIndex(d["vectors"], d["offsets"], cfg.m, cfg.s, cfg.L, cfg.seed, sketch=cfg.sketch)
-    oi = _ORACLES[key]
-    oi.score = score
-    return oi
-
-
 def _k0(cfg):
     return 2 * cfg.m if cfg.sketch == "binary" else 2 * cfg.m * 255 * 255
 
@@ -75,7 +62,7 @@ def test_overlap_filter_given_gpu_sketches(scase):
 def test_overlap_search_matches_oracle(scase):
     cfg, d, idx = scase["cfg"], scase["data"], scase["idx"]
     ids, dist = idx.search(d["queries"], d["q_offsets"], cfg.k, cfg.T)
-    oi = _oracle_index(cfg, d, "overlap")
+    oi = oracle_from_gpu_sketches(cfg, d, idx, score="overlap")
     V, off = d["vectors"], d["offsets"]
     for qi in range(ids.shape[0]):
         Q = d["queries"][d["q_offsets"][qi]:d["q_offsets"][qi + 1]]
@@ -128,8 +115,8 @@ def test_l1_count_score_matches_oracle(ov):
             assert np.array_equal(np.sort(O.select_top_T(sc, T)), got)
             assert np.array_equal(score[qi][: got.shape[0]].astype(np.int64), sc[got])
     ids, dist = idx.search(d["queries"], d["q_offsets"], cfg.k, cfg.T)
+    oi = oracle_from_gpu_sketches(cfg, d, idx, score="l1")
     idx.close()
-    oi = O.OracleIndex(d["vectors"], d["offsets"], cfg.m, cfg.s, cfg.L, cfg.seed, sketch="count", score="l1")
     V, off = d["vectors"], d["offsets"]
     for qi in range(ids.shape[0]):
         Q = d["queries"][d["q_offsets"][qi]:d["q_offsets"][qi + 1]]
