@@ -49,7 +49,8 @@ constexpr int kTileRows = 256;   // candidate rows per tile (MMA N)
 constexpr int kItemCands = 128;  // candidates per work item
 constexpr int kKChunk = 64;      // fp16 per K-chunk = 128 bytes = one SW128 row
 constexpr int kEpiWarps = 8;           // warps 2-5 and 8-11 (two per TMEM lane quarter)
-constexpr int kRefineThreads = 32 * 13;  // 0 copy, 1 MMA, 2-5 epilogue, 6 table, 7 tile info, 8-11 epilogue,
+constexpr int kProducers = 2;  // copy-producer warps: 0, 12 (measured: 3 is no faster)
+constexpr int kRefineThreads = 32 * (11 + kProducers);  // 0 copy, 1 MMA, 2-5 epilogue, 6 table, 7 tile info, 8-11 epilogue,
                                           // 12 second copy producer (the copies of a stage are split in two)
 constexpr int kMaxQ = 128;       // query rows the tensor path handles (M)
 constexpr int kMaxStages = 8;
@@ -232,7 +233,7 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
       tc::mbar_init(&S.tfull[b], 1);
       tc::mbar_init(&S.tempty[b], kEpiWarps);
       tc::mbar_init(&S.tab_full[b], 1);
-      tc::mbar_init(&S.tab_empty[b], 5);  // 2 copy producers + MMA warp + epilogue + tile-info warp
+      tc::mbar_init(&S.tab_empty[b], kProducers + 3);  // copy producers + MMA warp + epilogue + tile-info warp
     }
     for (int s = 0; s < kInfoSlots; ++s) {
       tc::mbar_init(&S.info_full[s], 1);
@@ -566,11 +567,11 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&S.tab_empty[tb]);
     }
-  } else if (warp == 0 || warp == 12) {
+  } else if (warp == 0 || warp >= 12) {
     // =========================== producers: bulk copies ===========================
     // warp 0 arms each stage's barrier and copies the even entries of the tile, warp 12 the odd entries
     // and the query replicas (a bulk copy is issued once per active lane: two warps halve the issue chain)
-    const int pw = warp == 0 ? 0 : 1;
+    const int pw = warp == 0 ? 0 : warp - 11;
     uint32_t stage_ctr = 0;
     for (uint32_t it = 0;; ++it) {
       const int tb = it & 1;
@@ -632,7 +633,7 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
           const uint32_t b_hi = x_atmem ? sbase : sbase + (three ? 2u : 1u) * a.a_bytes, b_lo = b_hi + a.b_bytes;
           if (lane == 0 && pw == 0) mbar_arrive_expect_tx(&S.full[st], stage_tx);  // (the other warp's copies
           __syncwarp();                                                           // may land first: tx < 0 is legal)
-          for (int e = e0 + 2 * lane + pw; e < e1; e += 64) {
+          for (int e = e0 + kProducers * lane + pw; e < e1; e += 32 * kProducers) {
             const int m = t.ent_m[e];
             const int64_t g0 = t.ent_pbase[e] >> 3;
             const size_t src = ((static_cast<size_t>(ks) * a.pgroups + g0) * KCS) * 8 * kKChunk;
@@ -663,7 +664,7 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
               }
             }
           }
-          if (x_atmem || pw == 0) {
+          if (x_atmem || pw != kProducers - 1) {
           } else if (x_group) {  // group mode: quarter j holds query j's rows (A rows 32j ..)
             if (lane >= 28 && gbytes[lane - 28] > 0) {
               const int j = lane - 28;
