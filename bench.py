@@ -77,39 +77,60 @@ def workload_config(cfg, T, k):
 
 # ------------------------------------------------------------------ clocks --
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """nvidia-smi clock / throttle-reason samples every 100 ms.  The sampler is started before the warm-up
+    (nvidia-smi's own start-up stalls the driver for milliseconds) and only the samples whose timestamp falls
+    inside the timed region (`mark()` .. `stop()`) are reported."""
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, gpu_index):
         self.gpu = gpu_index
         self.proc = None
         self.path = None
+        self.t0 = None
+        self.t1 = None
+
+    def mark(self):
+        """Start of the timed region."""
+        self.t0 = time.time()
 
     def start(self):
         fd, self.path = tempfile.mkstemp(suffix=".csv")
         os.close(fd)
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200",
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
                  "-i", str(self.gpu)], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
 
     def stop(self):
+        self.t1 = time.time()
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)  # let the sample that covers the end of the timed region land
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
+        import datetime
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        rows = []
         with open(self.path) as f:
             for line in f:
                 parts = [p.strip() for p in line.split(",")]
-                if len(parts) < 6:
+                if len(parts) < 7:
                     continue
+                try:
+                    ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                except ValueError:
+                    ts = None
+                rows.append((ts, parts[1:]))
+        inside = [r for ts, r in rows if ts is not None and self.t0 is not None and self.t0 - 0.1 <= ts <= self.t1 + 0.1]
+        for parts in (inside or [r for _, r in rows]):
                 try:
                     sm.append(float(parts[0]))
                     mx.append(float(parts[1]))
@@ -224,6 +245,8 @@ def main_ours(args):
         return D.sharded_search(D.LibShardOps(idx, lo), qv, qo, k, T, cfg.n)
 
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+    clk = ClockSampler(local)
+    clk.start()  # before the warm-up: nvidia-smi's start-up must not fall into the timed region
     for _ in range(args.warmup):
         flush.zero_()
         step()
@@ -231,8 +254,7 @@ def main_ours(args):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clk = ClockSampler(local)
-    clk.start()
+    clk.mark()
     st_sum, launches = {}, 0
     times = []
     for _ in range(args.steps):
