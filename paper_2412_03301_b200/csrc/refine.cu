@@ -30,11 +30,16 @@
 // reach ~7 TB/s on B200, 2.5 KB copies only ~4 TB/s.)  Queries use the same
 // layout with 8-aligned rows.
 //
-// CTA = 6 warps: warp 0 producer (work items, item tables, tile infos, bulk
-// copies through a stage ring), warp 1 TMEM owner + MMA issuer (one thread),
-// warps 2-5 epilogue.  Accumulators (128 lanes x 256 columns) are
-// double-buffered in TMEM (512 columns); item tables and tile infos are handed
-// over with mbarriers, so the persistent loop has no CTA-wide barrier.
+// CTA = 13 warps: warp 6 builds the item tables (work items, set sizes, tile
+// packing), warp 7 the tile infos (|v|^2 and scale of every column), warps 0
+// and 12 issue the bulk copies of a stage (even / odd entries; one cp.async.bulk
+// issues per active lane), warp 1 owns TMEM and issues the MMAs (one thread),
+// warps 2-5 and 8-11 run the epilogue (two per TMEM lane quarter).
+// Accumulators (128 lanes x 256 columns) are double-buffered in TMEM (512
+// columns); item tables, tile infos and stages are handed over with mbarriers,
+// so the persistent loop has no CTA-wide barrier.  The kernel is a template on
+// the rerank metric (Hausdorff / MeanMin / Min) and on the developer switches
+// (EXPER), which stay out of the default instantiation's hot loops.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
