@@ -115,11 +115,19 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
+        out = self.parse(self.path, self.t0, self.t1)
+        os.unlink(self.path)
+        return out
+
+    @staticmethod
+    def parse(path, t0, t1):
+        """Median SM clock, max clock and the active throttle reasons of the samples in [t0, t1] (+-0.1 s);
+        all samples if none carries a usable timestamp."""
         import datetime
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         rows = []
-        with open(self.path) as f:
+        with open(path) as f:
             for line in f:
                 parts = [p.strip() for p in line.split(",")]
                 if len(parts) < 7:
@@ -129,17 +137,16 @@ class ClockSampler:
                 except ValueError:
                     ts = None
                 rows.append((ts, parts[1:]))
-        inside = [r for ts, r in rows if ts is not None and self.t0 is not None and self.t0 - 0.1 <= ts <= self.t1 + 0.1]
+        inside = [r for ts, r in rows if ts is not None and t0 is not None and t0 - 0.1 <= ts <= t1 + 0.1]
         for parts in (inside or [r for _, r in rows]):
-                try:
-                    sm.append(float(parts[0]))
-                    mx.append(float(parts[1]))
-                except ValueError:
-                    continue
-                for nm, v in zip(names, parts[2:6]):
-                    if v.lower().startswith("active"):
-                        reasons.add(nm)
-        os.unlink(self.path)
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": sorted(reasons), "samples": len(sm)}
 
