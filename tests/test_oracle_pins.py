@@ -27,7 +27,31 @@ def gold(name):
 def test_splitmix64_known_answer():
     g = gold("splitmix64.json")
     it = O.splitmix64_stream(g["state"])
-    assert [next(it) for _ in range(3)] == [int(h, 16) for h in g["outputs_hex"]]
+    assert [next(it) for _ in range(8)] == [int(h, 16) for h in g["outputs_hex"]]
+
+
+def test_projection_row0_from_published_draws():
+    """Row 0 seeds its SplitMix64 state with seed ^ (0 * C) = seed, so at seed 0
+    its draws are the published state-0 outputs (tests/golden/splitmix64.json).
+    d = 64: 2^64 mod 64 = 0, no rejection, dims = u mod 64 = the low 6 bits:
+    0xaf & 63 = 47, 0xf4 & 63 = 52, 0x4f & 63 = 15, 0xec & 63 = 44,
+    0x9b & 63 = 27, 0xea & 63 = 42 (all distinct) -> sorted [15 27 42 44 47 52]
+    (BJ cfg1 shape: s = 6 ones per row, d = 64; reading R7)."""
+    W = O.projection(0, 4, 6, 64)
+    assert W[0].tolist() == [15, 27, 42, 44, 47, 52]
+    # d = 384 (not a power of two; 2^64 mod 384 = 256 != 0, but no published draw lies in the
+    # rejected tail [2^64 - 256, 2^64)): dims = u mod 384 of the first 8 draws, first 8 distinct kept
+    g = gold("splitmix64.json")
+    draws = [int(h, 16) for h in g["outputs_hex"]]
+    assert (1 << 64) % 384 == 256 and all(u < (1 << 64) - 256 for u in draws)
+    want = []
+    for u in draws:
+        if u % 384 not in want:
+            want.append(u % 384)
+    assert len(want) == 8
+    assert O.projection(0, 2, 8, 384)[0].tolist() == sorted(want)
+    # row 1 does NOT reuse the state-0 stream (per-row seed mixing seed ^ (j * 0xD1B54A32D192ED03))
+    assert O.projection(0, 2, 6, 64)[1].tolist() != [15, 27, 42, 44, 47, 52]
 
 
 @pytest.mark.parametrize("m,s,d", [(512, 6, 64), (64, 8, 384), (32, 12, 768), (40, 3, 3)])
@@ -50,6 +74,35 @@ def test_projection_uniform_over_dims():
     assert chi2 < 140.0  # dof 63: p ~ 1e-7 threshold
     # rows are not all identical and all C(d,s) patterns are possible in principle
     assert len({tuple(r) for r in W.tolist()}) > m - 5
+
+
+# ----------------------------------------------------------------- near-tie rows
+
+def test_near_tie_rows_hand_built():
+    """The code-parity exemption (BJ north_star: rows whose activation is within
+    1e-5 relative of the L-th largest).  Hand-built activations, identity-like W
+    (s = 3 dims per row, the unused dims are exact zeros):
+      row 0: x0 + x1 + x2 = 1e4 + 1e-3 - 1e4 -> fp64 1e-3, but fp32 left to right 9.765625e-4
+      row 1: x1 = 1e-3 exactly (the L-th largest for L = 2)
+      row 2: 5.0 (largest), row 3: -5.0, row 4: 0.0
+      rows 5/6: 1e-3 (1 - 0.5e-5) (inside the band) / 1e-3 (1 - 2e-5) (outside)
+    Pins: the band is rel * |a_(L)| with rel = 1e-5; a_(L) is the L-th (not the
+    (L+1)-th or (L-1)-th) largest; the activation is taken in fp64 (in fp32 row 0
+    would sit 2.3 % below a_(L) and not be flagged)."""
+    x = np.zeros(12)
+    x[0], x[1], x[2] = 1e4, 1e-3, -1e4
+    x[5], x[6] = 5.0, -5.0
+    x[8] = 1e-3 * (1 - 0.5e-5)
+    x[9] = 1e-3 * (1 - 2e-5)
+    W = np.array([[0, 1, 2], [1, 3, 4], [3, 4, 5], [3, 4, 6], [3, 4, 7], [3, 4, 8], [3, 4, 9]], dtype=np.uint16)
+    a32 = O.activations(x[None, :].astype(np.float32), W)[0]
+    assert a32[0] == np.float32(9.765625e-4)  # the fp32 order really loses the 1e-3 (precondition)
+    got = O.near_tie_rows(x[None, :], W, 2)[0]
+    assert got.tolist() == [True, True, False, False, False, True, False]
+    # L = 1: a_(1) = 5.0 -> only row 2
+    assert O.near_tie_rows(x[None, :], W, 1)[0].tolist() == [False, False, True, False, False, False, False]
+    # a wider band (rel = 3e-5) also takes row 6
+    assert O.near_tie_rows(x[None, :], W, 2, rel=3e-5)[0].tolist() == [True, True, False, False, False, True, True]
 
 
 # ----------------------------------------------------------------- activations
