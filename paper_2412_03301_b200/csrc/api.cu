@@ -623,7 +623,9 @@ int fallback_full(bvss_index* idx, bvss_search_ctx* c) {
   const int64_t n = idx->n;
   const int key_size = idx->sketch == BVSS_SKETCH_BINARY ? 2 : 4;
   const int64_t key_stride = (n + 7) & ~int64_t(7);
-  int64_t sub = static_cast<int64_t>((4.0 * (1ull << 30)) / (static_cast<double>(key_stride) * key_size));
+  double sub_bytes = 4.0 * (1ull << 30);
+  if (const char* e = getenv("BVSS_DEBUG_SUBBATCH_BYTES")) sub_bytes = atof(e);  // test switch: many sub-batches
+  int64_t sub = static_cast<int64_t>(sub_bytes / (static_cast<double>(key_stride) * key_size));
   if (sub < 1) sub = 1;
   if (sub > nq) sub = nq;
   void* keys;
@@ -673,7 +675,7 @@ int refine_topk(bvss_index* idx, bvss_search_ctx* c, int64_t* out_ids_dev, float
   int exact_all = 0;
   float c1, c2;
   error_consts(idx, &c1, &c2);
-  if (idx->terms != 0 && c->max_mq <= 128) {  // tensor path: query rows fit the M=128 tile
+  if (idx->terms != 0) {  // tensor path (query sets > 128 rows: per query on the exact path, refine.cu)
     if (!c->approx)  // once per context (brute force calls this per chunk)
       BVSS_TRY(c->alloc(static_cast<size_t>(nq) * c->T * sizeof(float), reinterpret_cast<void**>(&c->approx)));
     if (idx->metric == 1 && !c->approx_err)
@@ -1259,7 +1261,7 @@ int bvss_refine(bvss_index* idx, const float* queries, const int64_t* query_offs
   int exact_all = 0;
   float c1, c2;
   error_consts(idx, &c1, &c2);
-  if (idx->terms != 0 && c->max_mq <= 128) {  // tensor path: query rows fit the M=128 tile
+  if (idx->terms != 0) {  // tensor path (query sets > 128 rows: per query on the exact path, refine.cu)
     BVSS_TRY(c->alloc(static_cast<size_t>(nq) * T * 4, reinterpret_cast<void**>(&c->approx)));
     BVSS_CUDA(cudaMemsetAsync(c->approx, 0xFF, static_cast<size_t>(nq) * T * 4, idx->stream));  // NaN where unused
     if (idx->metric == 1)

@@ -57,7 +57,11 @@ constexpr int kEpiWarps = 8;           // warps 2-5 and 8-11 (two per TMEM lane 
 constexpr int kProducers = 2;  // copy-producer warps: 0, 12 (measured: 3 is no faster)
 constexpr int kRefineThreads = 32 * (11 + kProducers);  // 0 copy, 1 MMA, 2-5 epilogue, 6 table, 7 tile info, 8-11 epilogue,
                                           // 12 second copy producer (the copies of a stage are split in two)
-constexpr int kMaxQ = 128;       // query rows the tensor path handles (M)
+constexpr int kMaxQ = 128;       // query rows the tensor path handles (M); larger query sets take the exact path
+// tensor-core value of a candidate the tensor path does not take (a database set > 256 rows, a query set >
+// 128 rows): negative, so that K6 (topk.cu) keeps it out of the k-th-smallest select (as uint32 bits it orders
+// after every finite non-negative value) and always inside the exact window (-1 <= W)
+constexpr float kExactSentinel = -1.0f;
 constexpr int kMaxStages = 8;
 constexpr int kInfoSlots = 4;
 constexpr int kMaxSetsPerTile = kTileRows / 8;
@@ -368,7 +372,10 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
           vb[i] = a.off[cid];
           msz[i] = static_cast<int>(a.off[cid + 1] - vb[i]);
           pb[i] = a.pbase[cid];
-          if (msz[i] > kTileRows) a.out_h2[static_cast<int64_t>(q) * a.T + cpos[i]] = 0.0f;  // exact path
+          if (msz[i] > kTileRows) {  // exact path: the sentinel (< 0) keeps the set out of K6's k-th select
+            a.out_h2[static_cast<int64_t>(q) * a.T + cpos[i]] = kExactSentinel;  // and inside its window
+            if (a.out_err) a.out_err[static_cast<int64_t>(q) * a.T + cpos[i]] = 0.0f;
+          }
         }
       }
       // tiles: 256 rows, sets whole at 8-aligned columns, and one group of 4 queries (q0 + 4g ..) per tile
@@ -446,6 +453,13 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
         c0 = (item % a.items_per_query) * kItemCands;
         const int cnt = a.count ? a.count[q] : a.T;
         nc = min(kItemCands, cnt - c0);
+        if (nc > 0 && a.qoff[q + 1] - a.qoff[q] > kMaxQ) {  // query rows exceed the M = 128 tile: every
+          for (int c = lane; c < nc; c += 32) {                // candidate of this item takes the exact path
+            a.out_h2[static_cast<int64_t>(q) * a.T + c0 + c] = kExactSentinel;
+            if (a.out_err) a.out_err[static_cast<int64_t>(q) * a.T + c0 + c] = 0.0f;
+          }
+          continue;
+        }
         if (nc > 0) break;
       }
       if (nc < 0) {
@@ -472,7 +486,10 @@ __global__ void __launch_bounds__(kRefineThreads, 1) refine_tc_kernel(const __gr
           vb[i] = a.off[cid];
           msz[i] = static_cast<int>(a.off[cid + 1] - vb[i]);
           pb[i] = a.pbase[cid];
-          if (msz[i] > x_ncols) a.out_h2[static_cast<int64_t>(q) * a.T + c0 + c] = 0.0f;  // exact path
+          if (msz[i] > x_ncols) {  // exact path: the sentinel (< 0) keeps the set out of K6's k-th select
+            a.out_h2[static_cast<int64_t>(q) * a.T + c0 + c] = kExactSentinel;  // and inside its window
+            if (a.out_err) a.out_err[static_cast<int64_t>(q) * a.T + c0 + c] = 0.0f;
+          }
         }
       }
       float mq2 = 0.0f;
@@ -1019,7 +1036,7 @@ int launch_refine_tc(const __half* hs, const __half* ls, const float* vscale, in
                      int64_t n_local, int32_t* bounds, int metric, float* out_err, float c1, float c2, float vmax2,
                      cudaStream_t st) {
   if (nq <= 0 || T <= 0) return BVSS_OK;
-  if (max_mq > kMaxQ) BVSS_FAIL(BVSS_EUNSUPPORTED, "query set with %d vectors exceeds the %d-row tensor tile", max_mq, kMaxQ);
+  // query sets > kMaxQ rows are routed per query to the exact path (item table warp)
   if (dpad % kKChunk) BVSS_FAIL(BVSS_EINVAL, "dpad must be a multiple of 64");
   RefineArgs a;
   a.hs = hs; a.ls = ls; a.vscale = vscale; a.pgroups = prows / 8; a.pbase = pbase; a.vnorm = vnorm; a.off = off;

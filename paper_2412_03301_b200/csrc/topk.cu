@@ -192,6 +192,7 @@ __global__ void __launch_bounds__(kTopkThreads) topk_fixup_kernel(
       __syncthreads();
     }
     W = (__uint_as_float(S.prefix) + 2.0f * E) * (1.0f + 1e-6f);
+    if (S.prefix & 0x80000000u) W = __int_as_float(0x7f800000);  // k-th key is a refine sentinel: all in
   }
   __syncthreads();
   for (int i = threadIdx.x; i < cnt; i += blockDim.x)
@@ -396,6 +397,9 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
     W = aerr ? __uint_as_float(pre) * (1.0f + 2e-5f) + 1e-30f  // the k-th smallest upper bound
         : metric == 1 ? (__uint_as_float(pre) + 2.0f * sqrtf(E)) * (1.0f + 2e-5f) + 1e-30f
                       : (__uint_as_float(pre) + 2.0f * E) * (1.0f + 1e-6f);
+    // the k-th smallest key is a refine sentinel (< 0: a candidate the tensor path did not take): fewer than
+    // k candidates have a tensor-core value, so every candidate is in the window
+    if (pre & 0x80000000u) W = __int_as_float(0x7f800000);
   }
   __syncthreads();
   if (exact_all) {

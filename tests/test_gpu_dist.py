@@ -72,3 +72,30 @@ def test_sharded_search_equals_single_index(tmp_path, world, cfg_kw):
         dd = np.load(tmp_path / f"dist{r}.npy")
         np.testing.assert_array_equal(ids, ref_ids)
         np.testing.assert_array_equal(dd, ref_d)
+
+
+def test_sharded_search_matches_oracle(tmp_path):
+    """The merged sharded result against the oracle pipeline (not only against the single-index GPU path):
+    world size 2, a query subset checked by the tie-tolerant rule (Def 4, Alg 6)."""
+    import torch.multiprocessing as mp
+    from gen import synth
+    from oracle import bvss_oracle as O
+    from paper_2412_03301_b200 import bvss as B
+    from tests._common import check_topk
+    if B.device_count() < 1:
+        pytest.fail("no sm_100 device visible to libbvss")
+    cfg_kw = dict(name="cfg3", n=4001, nq=6, T=250)
+    world = 2
+    port = _free_port()
+    mp.start_processes(_worker, args=(world, port, cfg_kw, str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    cfg = synth.get_config(**cfg_kw)
+    h = synth.to_numpy(synth.generate(cfg, device="cuda"))  # the workers' exact data (CUDA generator)
+    oi = O.OracleIndex(h["vectors"], h["offsets"], cfg.m, cfg.s, cfg.L, cfg.seed, sketch=cfg.sketch)
+    ids = np.load(tmp_path / "ids0.npy")
+    dd = np.load(tmp_path / "dist0.npy")
+    V, off = h["vectors"], h["offsets"]
+    for qi in range(cfg.nq):
+        Q = h["queries"][h["q_offsets"][qi]:h["q_offsets"][qi + 1]]
+        r_ids, r_d = oi.search(Q, cfg.k, cfg.T)
+        check_topk(ids[qi], dd[qi], r_ids, r_d, lambda i: O.hausdorff(Q, V[off[i]:off[i + 1]]))
