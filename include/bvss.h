@@ -126,6 +126,11 @@ typedef struct {
   uint64_t select_batches;   /* query batches selected on the sampled-threshold path */
   uint64_t select_fallbacks; /* of those, batches redone on the full-key path */
   uint64_t scan_macs;        /* (query sketch bit, database sketch bit) products of the scan (nq x n x m) */
+  /* candidate-major (dense) refine: batches it ran, (query set, database set) pairs that
+     survived the lower-bound prune, candidates it emitted to the exact top-k, (query vector, database vector)
+     pairs and tensor-core flop (2 x M x N x K of every MMA tile, padding included) */
+  uint64_t dense_batches, dense_survivors, dense_emitted, dense_pairs;
+  double dense_flop;
 } bvss_stats;
 
 /* ---------------------------------------------------------------- core -- */

@@ -60,7 +60,9 @@ class Stats(C.Structure):
                 ("ms_refine", C.c_float), ("ms_topk", C.c_float), ("ms_d2h", C.c_float), ("ms_total", C.c_float),
                 ("scan_bytes", C.c_uint64), ("gather_bytes", C.c_uint64), ("cand_rows", C.c_uint64),
                 ("fixup_sets", C.c_uint64), ("kernel_launches", C.c_int32), ("query_batch", C.c_int32),
-                ("select_batches", C.c_uint64), ("select_fallbacks", C.c_uint64), ("scan_macs", C.c_uint64)]
+                ("select_batches", C.c_uint64), ("select_fallbacks", C.c_uint64), ("scan_macs", C.c_uint64),
+                ("dense_batches", C.c_uint64), ("dense_survivors", C.c_uint64), ("dense_emitted", C.c_uint64),
+                ("dense_pairs", C.c_uint64), ("dense_flop", C.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

@@ -106,11 +106,36 @@ int launch_topk_fixup(const float* approx, const int32_t* cand, const int32_t* c
                       const float* approx_err, cudaStream_t st);
 int launch_merge_topk(const int64_t* ids, const float* dist, int P, int64_t nq, int k, int64_t* out_ids,
                       float* out_dist, cudaStream_t st);
+int launch_select_bitmap(int key_size, const void* keys, int64_t key_stride, int64_t n, int nq, SelectState st,
+                         int T, uint32_t* bitmap, int64_t words, cudaStream_t s);
+int dense_max_dpad();
+int launch_dense_db_operand(const float* V, int64_t nvec, int d, int dpad, float inv_s, __half* hd, int num_sms,
+                            cudaStream_t st);
+int launch_dense_query_operand(const float* Qv, const float* qnorm, const int32_t* rowmap, const int32_t* rowq,
+                               int64_t rows, int d, int dpad, float inv_s, __half* qd, int32_t* lane_qid,
+                               float* lane_qn, int num_sms, cudaStream_t st);
+int launch_dense_prep(const int64_t* qoff, const float* qnorm, int nq, float c1, float c2, float vmax2, float* qE,
+                      float* lists, int64_t nlist, int32_t* cnt, const int32_t* huge, int nhuge, const uint32_t* mask,
+                      int64_t mask_stride, int64_t id_base, int32_t* ids, float* vals, int cap, int num_sms,
+                      cudaStream_t st);
+int launch_dense_hausdorff(const __half* qd, int ntq, const __half* hd, int64_t nvec, int dpad, int ntiles,
+                           const int32_t* tile_s0, const int32_t* tile_s1, const int64_t* off, const float* vn,
+                           const int32_t* lane_qid, const float* lane_qn, const float* qE, const float* tau0,
+                           float cneg, int k, int R, float* lists, int32_t* cnt, int32_t* ids, float* vals, int cap,
+                           const uint32_t* mask, int64_t mask_stride, int64_t id_base, unsigned long long* stat,
+                           int num_sms, cudaStream_t st);
 
 // ------------------------------------------------------- small kernels --
 __global__ void fill_i32_kernel(int32_t* __restrict__ x, int64_t n, int32_t v) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i < n) x[i] = v;
+}
+__global__ void fill_f32_kernel(float* __restrict__ x, int64_t n, float v) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) x[i] = v;
+}
+void fill_f32_inf(float* x, int64_t n, cudaStream_t st) {
+  if (n > 0) fill_f32_kernel<<<static_cast<int>((n + 255) / 256), 256, 0, st>>>(x, n, INFINITY);
 }
 __global__ void max_float_kernel(const float* __restrict__ x, int64_t n, unsigned int* __restrict__ out) {
   float m = 0.0f;
@@ -258,6 +283,17 @@ struct bvss_index {
   std::vector<uint16_t> pend_proj;
   bvss_params pend_p{};
   float* pend_V = nullptr;
+  // dense (candidate-major) refine, dense.cu: built on first use
+  std::vector<int64_t> off_h;   // host copy of the set offsets
+  __half* hd = nullptr;         // [nvec][dpad] fp16 = x / dense_s
+  float dense_s = 1.0f;         // power of two >= max|x|
+  int32_t* dtile_s0 = nullptr;  // [dntiles] first set of each dense tile (whole sets, <= 256 rows)
+  int32_t* dtile_s1 = nullptr;
+  int dntiles = 0;
+  std::vector<int32_t> dtile_s0_h;
+  int32_t* dhuge = nullptr;     // sets of more than 256 rows (exact path)
+  int dnhuge = 0;
+  unsigned long long dense_stat[2] = {0, 0};  // survivors / emitted of the last dense call
   Workspace ws;
   bvss_stats stats{};
   cudaEvent_t ev[8] = {};
@@ -717,6 +753,266 @@ int refine_topk(bvss_index* idx, bvss_search_ctx* c, int64_t* out_ids_dev, float
   return BVSS_OK;
 }
 
+// ------------------------------------------------ dense (candidate-major) refine, dense.cu --
+// The database operand of the dense kernel (fp16 x / S, S a power of two >= max|x|) and its tile plan (runs
+// of whole consecutive sets of <= 256 rows; larger sets go to the exact path), built on first use.
+int ensure_dense(bvss_index* idx) {
+  if (idx->hd) return BVSS_OK;
+  if (idx->dpad > dense_max_dpad()) BVSS_FAIL(BVSS_EUNSUPPORTED, "dense refine needs d <= %d", dense_max_dpad());
+  const float mx = std::sqrt(idx->vmax2);  // max |x_i| <= max |x|
+  int ex = 0;
+  if (mx > 0.0f) std::frexp(mx, &ex);      // mx = f 2^ex, f in [0.5, 1): 2^ex > mx
+  idx->dense_s = std::ldexp(1.0f, ex);
+  const size_t hb = static_cast<size_t>(idx->nvec) * idx->dpad * 2;
+  BVSS_CUDA(cudaMalloc(reinterpret_cast<void**>(&idx->hd), hb));
+  idx->owned_bytes += hb;
+  BVSS_TRY(launch_dense_db_operand(idx->V, idx->nvec, idx->d, idx->dpad, 1.0f / idx->dense_s, idx->hd, idx->num_sms,
+                                   idx->stream));
+  std::vector<int32_t> s0, s1, huge;
+  const std::vector<int64_t>& o = idx->off_h;
+  for (int64_t i = 0; i < idx->n;) {
+    if (o[i + 1] - o[i] > 256) {
+      huge.push_back(static_cast<int32_t>(i));
+      ++i;
+      continue;
+    }
+    const int64_t start = i;
+    while (i < idx->n && o[i + 1] - o[i] <= 256 && o[i + 1] - o[start] <= 256) ++i;
+    s0.push_back(static_cast<int32_t>(start));
+    s1.push_back(static_cast<int32_t>(i));
+  }
+  idx->dntiles = static_cast<int>(s0.size());
+  idx->dnhuge = static_cast<int>(huge.size());
+  const size_t tb = std::max<size_t>(s0.size(), 1) * 4;
+  BVSS_CUDA(cudaMalloc(reinterpret_cast<void**>(&idx->dtile_s0), tb));
+  BVSS_CUDA(cudaMalloc(reinterpret_cast<void**>(&idx->dtile_s1), tb));
+  BVSS_CUDA(cudaMalloc(reinterpret_cast<void**>(&idx->dhuge), std::max<size_t>(huge.size(), 1) * 4));
+  idx->owned_bytes += 2 * tb;
+  if (!s0.empty()) {
+    BVSS_CUDA(cudaMemcpyAsync(idx->dtile_s0, s0.data(), s0.size() * 4, cudaMemcpyHostToDevice, idx->stream));
+    BVSS_CUDA(cudaMemcpyAsync(idx->dtile_s1, s1.data(), s1.size() * 4, cudaMemcpyHostToDevice, idx->stream));
+  }
+  if (!huge.empty())
+    BVSS_CUDA(cudaMemcpyAsync(idx->dhuge, huge.data(), huge.size() * 4, cudaMemcpyHostToDevice, idx->stream));
+  BVSS_CUDA(cudaStreamSynchronize(idx->stream));  // host vectors go out of scope
+  idx->dtile_s0_h = s0;
+  return BVSS_OK;
+}
+
+// the dense path takes a batch when every query set fits one 32-lane warp of the query tile, the metric is
+// Hausdorff and d fits the resident query tile
+bool dense_supported(const bvss_index* idx, const bvss_search_ctx* c) {
+  return idx->metric == 0 && idx->terms != 0 && idx->dpad <= dense_max_dpad() && c->max_mq <= 32;
+}
+
+// BVSS_DENSE: 0 = never, 1 = whenever supported, unset = auto (the candidate budget is a large fraction of
+// the database: gathering T candidates per query then costs more than one dense pass)
+bool dense_wanted(const bvss_index* idx, int64_t teff) {
+  static const int env = [] {
+    const char* e = getenv("BVSS_DENSE");
+    return e ? atoi(e) : -1;
+  }();
+  if (env == 0 || idx->metric != 0 || idx->terms == 0 || idx->dpad > dense_max_dpad()) return false;
+  if (env == 1) return true;
+  return teff * 8 >= idx->n;
+}
+
+// Exact top-k of a prepared batch by the dense kernel: every (query, set) Gram on the tensor cores, the
+// branch-and-bound prune, the emitted candidate lists, then K6 (topk_exact_kernel) on those lists.
+// mask: optional candidate bitmap (row q at mask + q * mask_stride); ntiles_use: dense tiles to scan (a
+// prefix; brute force over the first set_limit sets).  *done = false when the batch is not supported or a
+// candidate list overflowed (the caller then runs the query-major path; the result is the same).
+int dense_refine_topk(bvss_index* idx, bvss_search_ctx* c, const uint32_t* mask, int64_t mask_stride, int ntiles_use,
+                      int64_t* out_ids_dev, float* out_dist_dev, bool* done) {
+  *done = false;
+  if (!dense_supported(idx, c)) return BVSS_OK;
+  BVSS_TRY(ensure_dense(idx));
+  const int nq = static_cast<int>(c->nq), k = c->k;
+  // query packing: best fit (decreasing sizes) into 32-row warp bins, 4 bins per 128-row tile
+  std::vector<int> order(nq);
+  for (int q = 0; q < nq; ++q) order[q] = q;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    return c->qoff_host[a + 1] - c->qoff_host[a] > c->qoff_host[b + 1] - c->qoff_host[b];
+  });
+  std::vector<std::vector<int>> by_space(33);
+  std::vector<int> fill;
+  std::vector<std::vector<int>> bins;
+  for (int q : order) {
+    const int m = static_cast<int>(c->qoff_host[q + 1] - c->qoff_host[q]);
+    int b = -1;
+    for (int sp = m; sp <= 32 && b < 0; ++sp)
+      if (!by_space[sp].empty()) {
+        b = by_space[sp].back();
+        by_space[sp].pop_back();
+      }
+    if (b < 0) {
+      b = static_cast<int>(bins.size());
+      bins.emplace_back();
+      fill.push_back(0);
+    }
+    bins[b].push_back(q);
+    fill[b] += m;
+    by_space[32 - fill[b]].push_back(b);
+  }
+  const int ntq = static_cast<int>((bins.size() + 3) / 4);
+  const int64_t rows = static_cast<int64_t>(ntq) * 128;
+  std::vector<int32_t> rowmap(rows, -1), rowq(rows, -1);
+  for (size_t b = 0; b < bins.size(); ++b) {
+    int64_t r = static_cast<int64_t>(b) * 32;  // tile b/4, lane quarter b%4
+    for (int q : bins[b])
+      for (int64_t v = c->qoff_host[q]; v < c->qoff_host[q + 1]; ++v, ++r) {
+        rowmap[r] = static_cast<int32_t>(v);
+        rowq[r] = q;
+      }
+  }
+  const int ntiles = ntiles_use;
+  int R = static_cast<int>(ceil_div<int64_t>(2 * idx->num_sms, ntq));
+  if (R < 4) R = 4;
+  if (R > ntiles) R = ntiles < 1 ? 1 : ntiles;
+  const double spl = std::max(1.0, static_cast<double>(idx->n) / (2.0 * R * k));
+  int64_t cap = static_cast<int64_t>(2.0 * R * k * (2.0 + std::log(spl)) * 2.0) + idx->dnhuge + 1024;
+  if (const char* e = getenv("BVSS_DEBUG_DENSE_CAP")) cap = atoll(e);  // test switch: force overflows
+  cap = (cap + 255) & ~int64_t(255);
+  // query max norm -> S_q
+  unsigned int* vmax;
+  BVSS_TRY(idx->ws.get("vmax", sizeof(unsigned int), reinterpret_cast<void**>(&vmax)));
+  BVSS_CUDA(cudaMemsetAsync(vmax, 0, sizeof(unsigned int), idx->stream));
+  max_float_kernel<<<idx->num_sms, 256, 0, idx->stream>>>(c->qnorm, c->nqvec, vmax);
+  BVSS_TRY(post_launch("max_float_kernel", idx->stream));
+  unsigned int hv = 0;
+  BVSS_CUDA(cudaMemcpyAsync(&hv, vmax, sizeof(hv), cudaMemcpyDeviceToHost, idx->stream));
+  BVSS_CUDA(cudaStreamSynchronize(idx->stream));
+  float qmax2;
+  std::memcpy(&qmax2, &hv, 4);
+  int ex = 0;
+  if (qmax2 > 0.0f) std::frexp(std::sqrt(qmax2), &ex);
+  const float sq = std::ldexp(1.0f, ex);
+  // buffers
+  __half* qd;
+  int32_t *d_rowmap, *d_rowq, *lane_qid, *cnt, *ids;
+  float *lane_qn, *qE, *tau0, *lists, *vals;
+  unsigned long long* stat;
+  const int64_t nlist = static_cast<int64_t>(nq) * R * 2 * k;
+  BVSS_TRY(c->alloc(rows * idx->dpad * 2, reinterpret_cast<void**>(&qd)));
+  BVSS_TRY(c->alloc(rows * 4, reinterpret_cast<void**>(&d_rowmap)));
+  BVSS_TRY(c->alloc(rows * 4, reinterpret_cast<void**>(&d_rowq)));
+  BVSS_TRY(c->alloc(rows * 4, reinterpret_cast<void**>(&lane_qid)));
+  BVSS_TRY(c->alloc(rows * 4, reinterpret_cast<void**>(&lane_qn)));
+  BVSS_TRY(c->alloc(nq * 4, reinterpret_cast<void**>(&qE)));
+  BVSS_TRY(c->alloc(nq * 4, reinterpret_cast<void**>(&tau0)));
+  BVSS_TRY(c->alloc(nlist * 4, reinterpret_cast<void**>(&lists)));
+  BVSS_TRY(c->alloc(nq * 4, reinterpret_cast<void**>(&cnt)));
+  BVSS_TRY(c->alloc(static_cast<size_t>(nq) * cap * 4, reinterpret_cast<void**>(&ids)));
+  BVSS_TRY(c->alloc(static_cast<size_t>(nq) * cap * 4, reinterpret_cast<void**>(&vals)));
+  BVSS_TRY(c->alloc(2 * sizeof(unsigned long long), reinterpret_cast<void**>(&stat)));
+  BVSS_CUDA(cudaMemcpyAsync(d_rowmap, rowmap.data(), rows * 4, cudaMemcpyHostToDevice, idx->stream));
+  BVSS_CUDA(cudaMemcpyAsync(d_rowq, rowq.data(), rows * 4, cudaMemcpyHostToDevice, idx->stream));
+  BVSS_CUDA(cudaMemsetAsync(stat, 0, 2 * sizeof(unsigned long long), idx->stream));
+  BVSS_TRY(launch_dense_query_operand(c->qv, c->qnorm, d_rowmap, d_rowq, rows, idx->d, idx->dpad, 1.0f / sq, qd,
+                                      lane_qid, lane_qn, idx->num_sms, idx->stream));
+  float c1, c2;
+  error_consts(idx, &c1, &c2);
+  fill_f32_inf(tau0, nq, idx->stream);
+  BVSS_TRY(launch_dense_prep(c->qoff, c->qnorm, nq, c1, c2, idx->vmax2, qE, lists, nlist, cnt, idx->dhuge,
+                             idx->dnhuge, mask, mask_stride, c->id_base, ids, vals, static_cast<int>(cap),
+                             idx->num_sms, idx->stream));
+  cudaEventRecord(idx->ev[4], idx->stream);
+  BVSS_TRY(launch_dense_hausdorff(qd, ntq, idx->hd, idx->nvec, idx->dpad, ntiles, idx->dtile_s0, idx->dtile_s1,
+                                  idx->off, idx->vnorm, lane_qid, lane_qn, qE, tau0, -2.0f * sq * idx->dense_s, k, R,
+                                  lists, cnt, ids, vals, static_cast<int>(cap), mask, mask_stride, c->id_base, stat,
+                                  idx->num_sms, idx->stream));
+  cudaEventRecord(idx->ev[5], idx->stream);
+  idx->stats.kernel_launches += 6;
+  // overflow check
+  std::vector<int32_t> hc(nq);
+  BVSS_CUDA(cudaMemcpyAsync(hc.data(), cnt, nq * 4, cudaMemcpyDeviceToHost, idx->stream));
+  BVSS_CUDA(cudaMemcpyAsync(idx->dense_stat, stat, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                            idx->stream));
+  BVSS_CUDA(cudaStreamSynchronize(idx->stream));
+  for (int q = 0; q < nq; ++q)
+    if (hc[q] > cap) {
+      idx->stats.select_fallbacks += 1;  // (reported as a fallback of the dense path)
+      return BVSS_OK;                    // *done stays false: the caller takes the query-major path
+    }
+  int64_t* fix;
+  BVSS_TRY(idx->ws.get("fixup_counter", sizeof(int64_t), reinterpret_cast<void**>(&fix)));
+  BVSS_CUDA(cudaMemsetAsync(fix, 0, sizeof(int64_t), idx->stream));
+  void* scratch;
+  BVSS_TRY(idx->ws.get("topk_scratch", static_cast<size_t>(nq) * cap * 8, &scratch));
+  BVSS_TRY(launch_topk_fixup(vals, ids, cnt, static_cast<int>(cap), k, idx->V, idx->off, c->id_base, idx->d, c->qv,
+                             c->qoff, c->qnorm, idx->vmax2, c1, c2, 0, out_ids_dev, out_dist_dev, nq, fix, scratch, 0,
+                             nullptr, idx->stream));
+  cudaEventRecord(idx->ev[6], idx->stream);
+  idx->stats.kernel_launches += 1;
+  idx->stats.dense_batches += 1;
+  idx->stats.dense_survivors += idx->dense_stat[0];
+  idx->stats.dense_emitted += idx->dense_stat[1];
+  idx->stats.dense_pairs += static_cast<uint64_t>(c->nqvec) * static_cast<uint64_t>(
+      ntiles_use >= idx->dntiles ? idx->nvec : idx->off_h[idx->dtile_s0_h[ntiles_use]]);
+  idx->stats.dense_flop += 2.0 * static_cast<double>(rows) * idx->dpad *
+                           static_cast<double>(ntiles_use) * 256.0;
+  *done = true;
+  return BVSS_OK;
+}
+
+// candidate bitmap of a prepared batch (bit i of row q = set i is in the query's top-T): full-key scans and
+// radix selects in sub-batches whose key rows fit 4 GB, written by select_bitmap_kernel
+int dense_mask(bvss_index* idx, bvss_search_ctx* c, uint32_t** mask, int64_t* stride) {
+  const int nq = static_cast<int>(c->nq);
+  const int64_t n = idx->n;
+  const int key_size = idx->sketch == BVSS_SKETCH_BINARY ? 2 : 4;
+  const int64_t key_stride = (n + 7) & ~int64_t(7);
+  double sub_bytes = 4.0 * (1ull << 30);
+  if (const char* e = getenv("BVSS_DEBUG_SUBBATCH_BYTES")) sub_bytes = atof(e);
+  int64_t sub = static_cast<int64_t>(sub_bytes / (static_cast<double>(key_stride) * key_size));
+  if (sub < 1) sub = 1;
+  if (sub > nq) sub = nq;
+  const int64_t words = (n + 31) / 32;
+  BVSS_TRY(c->alloc(static_cast<size_t>(nq) * words * 4, reinterpret_cast<void**>(mask)));
+  BVSS_CUDA(cudaMemsetAsync(*mask, 0, static_cast<size_t>(nq) * words * 4, idx->stream));
+  *stride = words;
+  void* keys;
+  BVSS_TRY(idx->ws.get("keys", static_cast<size_t>(sub) * key_stride * key_size, &keys));
+  BVSS_TRY(alloc_select_state(idx, c));
+  const bool tcs = use_tc_scan(idx);
+  int* wc = nullptr;
+  if (tcs) {
+    BVSS_TRY(expand_alloc(idx, c));
+    BVSS_TRY(idx->ws.get("scan_counter", sizeof(int), reinterpret_cast<void**>(&wc)));
+  }
+  const int cps = chunks_per_set(idx);
+  for (int q0 = 0; q0 < nq; q0 += static_cast<int>(sub)) {
+    const int ns = static_cast<int>(q0 + sub <= nq ? sub : nq - q0);
+    const void* sq = static_cast<const uint8_t*>(c->qsk) + static_cast<size_t>(q0) * cps * 16;
+    if (tcs) {
+      BVSS_TRY(launch_scan_tc(idx->sketch, scan_operand(idx, false), idx->mass, n, n, idx->m, sq, c->qmass + q0, ns,
+                              c->qx, c->qpad, keys, key_stride, wc, idx->num_sms, idx->stream, nullptr, nullptr,
+                              nullptr, nullptr, 0, 0, true));
+      idx->stats.scan_bytes += scan_tc_db_bytes(idx->sketch, idx->m, n, ns, idx->num_sms);
+    } else {
+      BVSS_TRY(launch_scan(scan_kind(idx), idx->sk, idx->mass, n, n, idx->m, sq, c->qmass + q0, ns, keys, key_stride,
+                           idx->num_sms, idx->stream));
+    }
+    idx->stats.scan_macs += static_cast<uint64_t>(ns) * n * idx->m;
+    SelectState s2 = c->sel;
+    s2.prefix += q0;
+    s2.below += q0;
+    s2.teff += q0;
+    s2.eq += q0;
+    s2.quota += q0;
+    s2.digit += q0;
+    BVSS_TRY(launch_select_init(s2, ns, c->teff, idx->stream));
+    for (int r = 0; r < c->rounds; ++r) {
+      BVSS_TRY(launch_select_hist(key_size, keys, key_stride, n, ns, s2, c->key_bits, r, c->local_hist, idx->stream));
+      BVSS_TRY(launch_select_resolve(c->local_hist, s2, ns, c->key_bits, r, idx->stream));
+    }
+    BVSS_TRY(launch_select_bitmap(key_size, keys, key_stride, n, ns, s2, c->T, *mask + static_cast<int64_t>(q0) * words,
+                                  words, idx->stream));
+    idx->stats.kernel_launches += 3 + 2 * c->rounds;
+  }
+  return BVSS_OK;
+}
+
 float ev_ms(bvss_index* idx, int a, int b) {
   float ms = 0.0f;
   if (cudaEventElapsedTime(&ms, idx->ev[a], idx->ev[b]) != cudaSuccess) return 0.0f;
@@ -911,14 +1207,16 @@ int build_impl(const float* vectors, const int64_t* set_offsets, int64_t n, int3
   pb[0] = 0;
   for (int64_t i = 0; i < n; ++i) pb[i + 1] = pb[i] + ((off_h[i + 1] - off_h[i] + 7) & ~int64_t(7));
   idx->prows = pb[n];
+  idx->off_h = off_h;
   BVSS_TRY(dalloc((n + 1) * 8, reinterpret_cast<void**>(&idx->pbase)));
   BVSS_CUDA(cudaMemcpyAsync(idx->pbase, pb.data(), (n + 1) * 8, cudaMemcpyHostToDevice, st));
   BVSS_TRY(dalloc(static_cast<size_t>(idx->prows) * idx->dpad * 2, reinterpret_cast<void**>(&idx->hi)));
-  BVSS_TRY(dalloc(static_cast<size_t>(idx->prows) * idx->dpad * 2, reinterpret_cast<void**>(&idx->lo)));
+  if (idx->terms == 3)  // the lo piece of the fp16 split is read only by the 3-term Gram
+    BVSS_TRY(dalloc(static_cast<size_t>(idx->prows) * idx->dpad * 2, reinterpret_cast<void**>(&idx->lo)));
   BVSS_TRY(dalloc(static_cast<size_t>(idx->prows) * 4, reinterpret_cast<void**>(&idx->vscale)));
   BVSS_CUDA(cudaMemsetAsync(idx->vscale, 0, static_cast<size_t>(idx->prows) * 4, st));
   BVSS_CUDA(cudaMemsetAsync(idx->hi, 0, static_cast<size_t>(idx->prows) * idx->dpad * 2, st));
-  BVSS_CUDA(cudaMemsetAsync(idx->lo, 0, static_cast<size_t>(idx->prows) * idx->dpad * 2, st));
+  if (idx->lo) BVSS_CUDA(cudaMemsetAsync(idx->lo, 0, static_cast<size_t>(idx->prows) * idx->dpad * 2, st));
   int64_t* dst_row;
   BVSS_TRY(idx->ws.get("dst_row", static_cast<size_t>(nvec) * 8, reinterpret_cast<void**>(&dst_row)));
   pad_rows_kernel<<<num_sms * 8, 256, 0, st>>>(idx->off, idx->pbase, n, dst_row);
@@ -1054,6 +1352,8 @@ int bvss_index_finish(bvss_index* idx) {
   built->codes = nullptr;
   built->sk = built->smp_sk = built->skx = built->smp_skx = nullptr;
   built->mass = built->smp_mass = nullptr;
+  built->hd = nullptr;
+  built->dtile_s0 = built->dtile_s1 = built->dhuge = nullptr;
   for (auto& e : built->ev) e = nullptr;
   delete built;
   if (old_stream) cudaStreamDestroy(old_stream);
@@ -1066,7 +1366,7 @@ void bvss_free_index(bvss_index* idx) {
   if (idx->stream) cudaStreamSynchronize(idx->stream);
   void* ptrs[] = {idx->Wt,    idx->V,     idx->off,   idx->hi,   idx->lo,     idx->vscale, idx->pbase,
                   idx->vnorm, idx->codes, idx->sk,    idx->mass, idx->smp_sk, idx->smp_mass,
-                  idx->skx,   idx->smp_skx};
+                  idx->skx,   idx->smp_skx, idx->hd, idx->dtile_s0, idx->dtile_s1, idx->dhuge};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (idx->pend_V) cudaFree(idx->pend_V);
@@ -1200,6 +1500,43 @@ int bvss_bruteforce(bvss_index* idx, const float* queries, const int64_t* query_
   std::vector<int64_t> qo;
   BVSS_TRY(host_offsets(idx, query_offsets, nq, dev, qo));
   const int64_t lim = (set_limit <= 0 || set_limit > idx->n) ? idx->n : set_limit;
+  if (dense_wanted(idx, idx->n)) {  // K8 on the dense kernel (dense.cu): one pass over the first lim sets
+    std::unique_ptr<bvss_search_ctx> c(new bvss_search_ctx());
+    c->idx = idx;
+    c->k = k;
+    c->T = static_cast<int>(lim < (1ll << 30) ? lim : (1ll << 30));
+    idx->stats = bvss_stats{};
+    BVSS_TRY(prepare_queries(idx, c.get(), queries, qo, dev, (flags & BVSS_VALIDATE_FINITE) != 0));
+    if (dense_supported(idx, c.get())) {
+      BVSS_TRY(ensure_dense(idx));
+      int nt = idx->dntiles;
+      uint32_t* mask = nullptr;
+      if (lim < idx->n) {  // tiles up to the one holding set lim - 1, and a shared bitmap of the sets < lim
+        nt = static_cast<int>(std::upper_bound(idx->dtile_s0_h.begin(), idx->dtile_s0_h.end(),
+                                               static_cast<int32_t>(lim - 1)) - idx->dtile_s0_h.begin());
+        const int64_t words = (idx->n + 31) / 32;
+        std::vector<uint32_t> row(words, 0u);
+        for (int64_t i = 0; i < lim; ++i) row[i >> 5] |= 1u << (i & 31);
+        BVSS_TRY(c->alloc(words * 4, reinterpret_cast<void**>(&mask)));
+        BVSS_CUDA(cudaMemcpyAsync(mask, row.data(), words * 4, cudaMemcpyHostToDevice, idx->stream));
+        BVSS_CUDA(cudaStreamSynchronize(idx->stream));
+      }
+      int64_t* oi;
+      float* od;
+      BVSS_TRY(c->alloc(static_cast<size_t>(nq) * k * 8, reinterpret_cast<void**>(&oi)));
+      BVSS_TRY(c->alloc(static_cast<size_t>(nq) * k * 4, reinterpret_cast<void**>(&od)));
+      bool done = false;
+      BVSS_TRY(dense_refine_topk(idx, c.get(), mask, 0, nt, oi, od, &done));
+      if (done) {
+        BVSS_TRY(from_device(idx, out_ids, oi, static_cast<size_t>(nq) * k * 8, dev));
+        BVSS_TRY(from_device(idx, out_dist, od, static_cast<size_t>(nq) * k * 4, dev));
+        BVSS_CUDA(cudaStreamSynchronize(idx->stream));
+        idx->stats.ms_refine = ev_ms(idx, 4, 5);
+        idx->stats.ms_topk = ev_ms(idx, 5, 6);
+        return BVSS_OK;
+      }
+    }
+  }
   std::unique_ptr<bvss_search_ctx> c(new bvss_search_ctx());
   c->idx = idx;
   c->k = k;
@@ -1325,19 +1662,37 @@ int bvss_search(bvss_index* idx, const float* queries, const int64_t* query_offs
     for (int64_t i = 0; i <= nb; ++i) sub[i] = qo[b0 + i] - qo[b0];
     std::unique_ptr<bvss_search_ctx> c;
     const bool sampled = sampled_select_eligible(idx);
-    BVSS_TRY(make_ctx(idx, queries + qo[b0] * idx->d, sub, k, T, idx->n, flags, c, !sampled));
-    bool ok = false;
-    if (sampled) BVSS_TRY(select_sampled(idx, c.get(), &ok));
-    if (!ok) {
-      if (sampled) {
-        BVSS_TRY(fallback_full(idx, c.get()));
-      } else {
-        BVSS_TRY(run_select_single(idx, c.get()));
-        BVSS_TRY(emit_candidates(idx, c.get()));
-      }
+    const int64_t teff = T < idx->n ? T : idx->n;
+    const bool try_dense = dense_wanted(idx, teff);
+    BVSS_TRY(make_ctx(idx, queries + qo[b0] * idx->d, sub, k, T, idx->n, flags, c, !sampled && !try_dense));
+    bool done = false;
+    double t_sel = 0.0;
+    if (try_dense && dense_supported(idx, c.get())) {
+      // candidate-major refine (dense.cu): the candidate set as a bitmap (none when T >= n), one dense pass
+      uint32_t* mask = nullptr;
+      int64_t mstride = 0;
+      if (teff < idx->n) BVSS_TRY(dense_mask(idx, c.get(), &mask, &mstride));
+      cudaEventRecord(idx->ev[3], idx->stream);
+      t_sel = now_us();
+      BVSS_TRY(dense_refine_topk(idx, c.get(), mask, mstride, idx->dntiles, oid, odist, &done));
+      if (!done && !sampled) BVSS_TRY(scan_batch(idx, c.get()));  // overflow: the query-major path below
+    } else if (try_dense && !sampled) {
+      BVSS_TRY(scan_batch(idx, c.get()));
     }
-    const double t_sel = now_us();
-    BVSS_TRY(refine_topk(idx, c.get(), oid, odist));
+    if (!done) {
+      bool ok = false;
+      if (sampled) BVSS_TRY(select_sampled(idx, c.get(), &ok));
+      if (!ok) {
+        if (sampled) {
+          BVSS_TRY(fallback_full(idx, c.get()));
+        } else {
+          BVSS_TRY(run_select_single(idx, c.get()));
+          BVSS_TRY(emit_candidates(idx, c.get()));
+        }
+      }
+      t_sel = now_us();
+      BVSS_TRY(refine_topk(idx, c.get(), oid, odist));
+    }
     const double t_ref = now_us();
     BVSS_TRY(from_device(idx, out_ids + b0 * k, oid, static_cast<size_t>(nb) * k * 8, dev));
     BVSS_TRY(from_device(idx, out_dist + b0 * k, odist, static_cast<size_t>(nb) * k * 4, dev));

@@ -1,0 +1,516 @@
+// dense.cu — K8d: candidate-major (dense) Hausdorff top-k on the 5th-generation
+// tensor cores, with a rigorous branch-and-bound prune (Def 4; Alg 6
+// lines 19-23 P:809-814; "precise calculations" for the brute force).
+//
+// When the candidate budget T is a large fraction of n (the recall@10 >= 0.9
+// operating point of the synthetic workloads) or T = n (K8, the
+// recall ground truth), gathering each query's candidates (K5, query-major)
+// moves T x (set rows) x d x 2 bytes per query.  This kernel instead streams the
+// database ONCE per 128-row query tile: the query tile is the stationary A
+// operand (M = 128 packed query rows, resident in shared memory), the database
+// rows stream through a TMA ring as the B operand (N = 256 rows per tile, K = d
+// in 64-element SW128 chunks), and tcgen05.mma accumulates the Gram tile in TMEM
+// (two 256-column accumulators, double-buffered against the epilogue).
+//
+// Layouts (built once per index / per batch):
+//   database  hd [nvec][dpad] fp16 = x / S_db, one global power-of-two scale
+//             S_db >= max|x| (row-major; tiles are runs of whole consecutive sets
+//             of <= 256 rows, any start row: TMA swizzles on the fly);
+//   queries   qd [ntq*128][dpad] fp16 = x / S_q, query sets packed into 32-row
+//             warp bins (a set never straddles a warp), 4 bins per tile.
+// D^2(q, v) = |q|^2 + |v|^2 - 2 S_q S_db g(q, v), g the fp16 Gram.
+//
+// Epilogue (8 warps, two per TMEM lane quarter; lane = query row, column =
+// database row; sets of a tile alternate between the two warps of a quarter):
+//   per database set V and lane q:   r_q = max(0, min_v D^2(q, v))  (lane-local)
+//   A(Q, V) = max_{q in Q} r_q  is a lower bound of H^2(Q, V) = max(A, B).
+// Branch and bound per query: tau_Q = the k-th smallest upper bound (H2c + E)
+// among the sets seen so far (a list of k per (query, range, warp) in global
+// memory; any k distinct sets' upper bounds bound the true k-th H^2 from above).
+// A set is pruned when some lane of Q has r_q > tau_Q + E (so A - E > tau_Q:
+// its exact H^2 exceeds the exact k-th, the set cannot be in the top-k).  A set
+// that survives gets B(Q, V) = max_v min_q D^2 by one redux.sync.min per column
+// (TMEM re-read; survivors are rare once tau has settled), H2c = max(A, B), and
+// is emitted to the query's candidate list when H2c - E <= tau_Q.  K6
+// (topk_exact_kernel) then recomputes the final window exactly in fp32: the
+// emitted lists contain every set whose H2c - E <= the final U_k, which is the
+// K6 window rule, so the result is exact (E from error_consts()).
+//
+// CTA = 10 warps: 0 TMA producer, 1 TMEM owner + MMA issuer (one thread), 2-9
+// epilogue.  Persistent: unit u = blockIdx.x + i * gridDim.x is (query tile
+// u / R, database range u % R); consecutive units run the same ranges at the
+// same time on all SMs, so each database tile is read from HBM about once per
+// wave and served from L2 to the other CTAs.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "tc.cuh"
+
+namespace bvss {
+
+constexpr int kDenseN = 256;      // database rows per tile (MMA N)
+constexpr int kDenseM = 128;      // packed query rows per tile (MMA M)
+constexpr int kDenseThreads = 320;
+constexpr int kDenseMaxStages = 8;
+constexpr uint32_t kAChunkBytes = kDenseM * 128;  // one 64-element K chunk of the query tile (16 KB)
+constexpr uint32_t kBChunkBytes = kDenseN * 128;  // one K chunk of a database tile (32 KB)
+
+struct DenseArgs {
+  CUtensorMap tmA;              // qd [ntq*128][dpad] fp16, box {64, 128}, SWIZZLE_128B
+  CUtensorMap tmB;              // hd [nvec][dpad] fp16, box {64, 256}, SWIZZLE_128B
+  int KC;                       // dpad / 64
+  int stages;
+  int ntq;                      // query tiles
+  int R;                        // database ranges
+  int ntiles;                   // database tiles
+  const int32_t* tile_s0;       // [ntiles] first set of each tile
+  const int32_t* tile_s1;       // [ntiles] one past the last set
+  const int64_t* off;           // [n+1]
+  const float* vn;              // [nvec] squared norms
+  const int32_t* lane_qid;      // [ntq*128] query of each packed row, -1 = padding
+  const float* lane_qn;         // [ntq*128] squared norm of each packed row
+  const float* qE;              // [nq] squared-distance error bound of each query
+  const float* tau0;            // [nq] initial tau (an upper bound on the k-th H^2; +inf if none)
+  float cneg;                   // -2 S_q S_db
+  int k;
+  float* lists;                 // [nq][R][2][k] sorted upper bounds, +inf-initialised
+  int32_t* cnt;                 // [nq] emitted candidates (may exceed cap: overflow)
+  int32_t* ids;                 // [nq][cap]
+  float* vals;                  // [nq][cap] tensor-core H^2
+  int cap;
+  const uint32_t* mask;         // optional candidate bitmap, row q at mask + q * mask_stride (bit i = set i)
+  int64_t mask_stride;          // words per query row (0: one row shared by every query)
+  int64_t id_base;
+  unsigned long long* stat;     // [2]: survivors, emitted (may be null)
+};
+
+struct DenseCtl {
+  uint64_t full[kDenseMaxStages];
+  uint64_t empty[kDenseMaxStages];
+  uint64_t a_full, a_empty;
+  uint64_t tfull[2], tempty[2];
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// 32 lanes x 32 bit, 32 consecutive columns -> 32 registers per thread
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr)
+      : "memory");
+}
+
+__device__ __forceinline__ float vload_volatile(const float* p) {
+  float v;
+  asm volatile("ld.volatile.global.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void range_tiles(int r, int R, int ntiles, int* t0, int* t1) {
+  *t0 = static_cast<int>((static_cast<int64_t>(ntiles) * r) / R);
+  *t1 = static_cast<int>((static_cast<int64_t>(ntiles) * (r + 1)) / R);
+}
+
+__global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const __grid_constant__ DenseArgs a) {
+  extern __shared__ __align__(1024) uint8_t dsm_raw[];
+  __shared__ DenseCtl S;
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t a_s = smem_u32(base);                                  // KC x 16 KB query tile
+  const uint32_t ring_s = a_s + static_cast<uint32_t>(a.KC) * kAChunkBytes;  // stages x 32 KB
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int NST = a.stages;
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) {
+      tc::mbar_init(&S.full[s], 1);
+      tc::mbar_init(&S.empty[s], 1);
+    }
+    tc::mbar_init(&S.a_full, 1);
+    tc::mbar_init(&S.a_empty, 1);
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&S.tfull[b], 1);
+      tc::mbar_init(&S.tempty[b], 8);
+    }
+    tc::fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc(&S.tmem_base, 512);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = S.tmem_base;
+  const int units = a.ntq * a.R;
+
+  if (warp == 0) {
+    // =========================== TMA producer ===========================
+    uint32_t stage_ctr = 0, ua = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
+      const int qt = u / a.R, r = u % a.R;
+      tc::mbar_wait(&S.a_empty, (ua & 1u) ^ 1u);
+      if (lane == 0) {
+        expect_tx(&S.a_full, static_cast<uint32_t>(a.KC) * kAChunkBytes);
+        for (int kc = 0; kc < a.KC; ++kc) tma_2d(a_s + kc * kAChunkBytes, &a.tmA, kc * 64, qt * kDenseM, &S.a_full);
+      }
+      int t0, t1;
+      range_tiles(r, a.R, a.ntiles, &t0, &t1);
+      for (int t = t0; t < t1; ++t) {
+        const int row0 = static_cast<int>(a.off[a.tile_s0[t]]);
+        for (int kc = 0; kc < a.KC; ++kc, ++stage_ctr) {
+          const uint32_t st = stage_ctr % NST;
+          tc::mbar_wait(&S.empty[st], ((stage_ctr / NST) & 1u) ^ 1u);
+          if (lane == 0) {
+            expect_tx(&S.full[st], kBChunkBytes);
+            tma_2d(ring_s + st * kBChunkBytes, &a.tmB, kc * 64, row0, &S.full[st]);
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // =========================== MMA issuer ===========================
+    uint32_t stage_ctr = 0, tile_ctr = 0, ua = 0;
+    const uint32_t idesc = tc::idesc_f16_f32(kDenseM, kDenseN);
+    for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
+      const int r = u % a.R;
+      tc::mbar_wait(&S.a_full, ua & 1u);
+      tc::fence_after_sync();
+      int t0, t1;
+      range_tiles(r, a.R, a.ntiles, &t0, &t1);
+      for (int t = t0; t < t1; ++t, ++tile_ctr) {
+        const uint32_t acc = tile_ctr & 1u;
+        tc::mbar_wait(&S.tempty[acc], ((tile_ctr >> 1) & 1u) ^ 1u);
+        tc::fence_after_sync();
+        const uint32_t d_tmem = tmem + acc * kDenseN;
+        for (int kc = 0; kc < a.KC; ++kc, ++stage_ctr) {
+          const uint32_t st = stage_ctr % NST;
+          tc::mbar_wait(&S.full[st], (stage_ctr / NST) & 1u);
+          tc::fence_after_sync();
+          if (lane == 0) {
+            const uint32_t as = a_s + kc * kAChunkBytes, bs = ring_s + st * kBChunkBytes;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              tc::umma_bf16(d_tmem, tc::sw128_desc(as + kk * 32u), tc::sw128_desc(bs + kk * 32u), idesc,
+                            (kc | kk) ? 1u : 0u);
+            tc::umma_commit(&S.empty[st]);
+            if (kc == a.KC - 1) tc::umma_commit(&S.tfull[acc]);
+          }
+          __syncwarp();
+        }
+      }
+      if (lane == 0) tc::umma_commit(&S.a_empty);  // the query tile may be overwritten once these MMAs are done
+      __syncwarp();
+    }
+  } else {
+    // =========================== epilogue (warps 2..9) ===========================
+    const int quarter = warp & 3;
+    const int sub = (warp - 2) >> 2;
+    const float INF = __int_as_float(0x7f800000);
+    uint32_t tile_ctr = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int qt = u / a.R, r = u % a.R;
+      const int prow = qt * kDenseM + quarter * 32 + lane;
+      const int qid = a.lane_qid[prow];
+      const bool valid = qid >= 0;
+      const float qn = valid ? a.lane_qn[prow] : 0.0f;
+      const unsigned segmask = __match_any_sync(0xffffffffu, qid);
+      const float E = valid ? a.qE[qid] : 0.0f;
+      float* own = valid ? a.lists + ((static_cast<int64_t>(qid) * a.R + r) * 2 + sub) * a.k : nullptr;
+      const float* other = valid ? a.lists + ((static_cast<int64_t>(qid) * a.R + r) * 2 + (sub ^ 1)) * a.k : nullptr;
+      float tau = valid ? a.tau0[qid] : INF;
+      int t0, t1;
+      range_tiles(r, a.R, a.ntiles, &t0, &t1);
+      for (int t = t0; t < t1; ++t, ++tile_ctr) {
+        const uint32_t acc = tile_ctr & 1u;
+        if (valid) tau = fminf(tau, vload_volatile(other + a.k - 1));  // the other warp's k-th bound
+        float thr = tau + E;
+        tc::mbar_wait(&S.tfull[acc], (tile_ctr >> 1) & 1u);
+        tc::fence_after_sync();
+        const int s0 = a.tile_s0[t], s1 = a.tile_s1[t];
+        const int64_t row0 = a.off[s0];
+        const uint32_t tb = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * kDenseN;
+        for (int i = s0 + sub; i < s1; i += 2) {
+          const int64_t v0 = a.off[i];
+          const int col0 = static_cast<int>(v0 - row0);
+          const int mv = static_cast<int>(a.off[i + 1] - v0);
+          float run = INF;
+          for (int j0 = 0; j0 < mv; j0 += 32) {
+            const float vnl = (j0 + lane < mv) ? __ldg(a.vn + v0 + j0 + lane) : 0.0f;
+            uint32_t g[32];
+            tmem_ld32(tb + static_cast<uint32_t>(col0 + j0), g);
+            tc::tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              if (j0 + j >= mv) break;
+              const float vnj = __shfl_sync(0xffffffffu, vnl, j);
+              run = fminf(run, fmaf(__uint_as_float(g[j]), a.cneg, vnj));
+            }
+          }
+          const float rq = fmaxf(run + qn, 0.0f);
+          const unsigned pass = __ballot_sync(0xffffffffu, !valid || rq <= thr);
+          unsigned sb = __ballot_sync(0xffffffffu, valid && (pass & segmask) == segmask);
+          while (sb) {  // warp-uniform: one surviving query segment at a time
+            const int leader = __ffs(sb) - 1;
+            const unsigned smask = __shfl_sync(0xffffffffu, segmask, leader);
+            sb &= ~smask;
+            const int q = __shfl_sync(0xffffffffu, qid, leader);
+            if (a.mask) {  // candidate restriction (top-T of the filter): bit i of the query's row
+              const int64_t li = i;
+              const uint32_t w = __ldg(a.mask + static_cast<int64_t>(q) * a.mask_stride + (li >> 5));
+              if (((w >> (li & 31)) & 1u) == 0u) continue;
+            }
+            const bool inseg = (smask >> lane) & 1u;
+            const float A = __uint_as_float(__reduce_max_sync(0xffffffffu, inseg ? __float_as_uint(rq) : 0u));
+            float B = 0.0f;
+            for (int j0 = 0; j0 < mv; j0 += 32) {
+              const float vnl = (j0 + lane < mv) ? __ldg(a.vn + v0 + j0 + lane) : 0.0f;
+              uint32_t g[32];
+              tmem_ld32(tb + static_cast<uint32_t>(col0 + j0), g);
+              tc::tmem_ld_wait();
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                if (j0 + j >= mv) break;
+                const float vnj = __shfl_sync(0xffffffffu, vnl, j);
+                const float d2 = fmaxf(fmaf(__uint_as_float(g[j]), a.cneg, vnj) + qn, 0.0f);
+                const uint32_t cm = __reduce_min_sync(0xffffffffu, inseg ? __float_as_uint(d2) : 0xffffffffu);
+                B = fmaxf(B, __uint_as_float(cm));
+              }
+            }
+            const float h = fmaxf(A, B);
+            float newtau = tau;  // (uniform over the segment; taken from the leader below)
+            if (lane == leader) {
+              const float ub = h + E;
+              if (ub < tau) {  // insert into this warp's sorted list of k upper bounds
+                int p = a.k - 1;
+                while (p > 0 && own[p - 1] > ub) {
+                  own[p] = own[p - 1];
+                  --p;
+                }
+                own[p] = ub;
+                newtau = fminf(own[a.k - 1], vload_volatile(other + a.k - 1));
+              }
+              if (h - E <= newtau) {
+                const int slot = atomicAdd(a.cnt + q, 1);
+                if (slot < a.cap) {
+                  a.ids[static_cast<int64_t>(q) * a.cap + slot] = static_cast<int32_t>(a.id_base + i);
+                  a.vals[static_cast<int64_t>(q) * a.cap + slot] = h;
+                }
+                if (a.stat) atomicAdd(a.stat + 1, 1ull);
+              }
+              if (a.stat) atomicAdd(a.stat, 1ull);
+            }
+            newtau = __shfl_sync(0xffffffffu, newtau, leader);
+            if (inseg) {
+              tau = newtau;
+              thr = tau + E;
+            }
+          }
+        }
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&S.tempty[acc]);
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc(tmem, 512);
+  }
+}
+
+// ------------------------------------------------------------ helper kernels --
+// fp16 copy of the database, x / S (S a power of two >= max|x|), zero-padded to dpad columns
+__global__ void dense_db_operand_kernel(const float* __restrict__ V, int64_t nvec, int d, int dpad, float inv_s,
+                                        __half* __restrict__ hd) {
+  const int64_t total = nvec * dpad;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t v = e / dpad;
+    const int c = static_cast<int>(e - v * dpad);
+    hd[e] = __float2half_rn(c < d ? V[v * d + c] * inv_s : 0.0f);
+  }
+}
+
+// packed query rows: qd[row] = fp16(q / S_q) (zero rows for padding), lane meta
+__global__ void dense_query_operand_kernel(const float* __restrict__ Qv, const float* __restrict__ qnorm,
+                                           const int32_t* __restrict__ rowmap /*[rows]: query vector or -1*/,
+                                           const int32_t* __restrict__ rowq /*[rows]: query or -1*/, int64_t rows,
+                                           int d, int dpad, float inv_s, __half* __restrict__ qd,
+                                           int32_t* __restrict__ lane_qid, float* __restrict__ lane_qn) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t r = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5; r < rows;
+       r += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+    const int32_t v = rowmap[r];
+    for (int c = lane; c < dpad; c += 32)
+      qd[r * dpad + c] = __float2half_rn((v >= 0 && c < d) ? Qv[static_cast<int64_t>(v) * d + c] * inv_s : 0.0f);
+    if (lane == 0) {
+      lane_qid[r] = v >= 0 ? rowq[r] : -1;
+      lane_qn[r] = v >= 0 ? qnorm[v] : 0.0f;
+    }
+  }
+}
+
+// per-query error bound E = c1 Mq Mv + c2 (Mq^2 + Mv^2), Mq^2 = max squared norm of the query's vectors
+__global__ void dense_query_bound_kernel(const int64_t* __restrict__ qoff, const float* __restrict__ qnorm, int nq,
+                                         float c1, float c2, float vmax2, float* __restrict__ qE) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  float m2 = 0.0f;
+  for (int64_t v = qoff[q]; v < qoff[q + 1]; ++v) m2 = fmaxf(m2, qnorm[v]);
+  qE[q] = c1 * sqrtf(m2) * sqrtf(vmax2) + c2 * (m2 + vmax2);
+}
+
+__global__ void dense_fill_kernel(float* __restrict__ x, int64_t n, float v) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    x[i] = v;
+}
+
+// sets the tiles cannot hold (> 256 rows): appended to every query's list with the K6 exact sentinel
+// (every one is recomputed exactly), honouring the candidate bitmap
+__global__ void dense_append_huge_kernel(const int32_t* __restrict__ huge, int nhuge, const uint32_t* __restrict__ mask,
+                                         int64_t mask_stride, int nq, int64_t id_base, int32_t* __restrict__ cnt,
+                                         int32_t* __restrict__ ids, float* __restrict__ vals, int cap) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  int c = 0;
+  for (int h = 0; h < nhuge; ++h) {
+    const int i = huge[h];
+    if (mask && ((mask[static_cast<int64_t>(q) * mask_stride + (i >> 5)] >> (i & 31)) & 1u) == 0u) continue;
+    if (c < cap) {
+      ids[static_cast<int64_t>(q) * cap + c] = static_cast<int32_t>(id_base + i);
+      vals[static_cast<int64_t>(q) * cap + c] = -1.0f;  // refine.cu kExactSentinel
+    }
+    ++c;
+  }
+  cnt[q] = c;
+}
+
+// ------------------------------------------------------------------ host --
+static int encode_map(CUtensorMap* map, const void* base, int64_t rows, int dpad, int box_rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    BVSS_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) BVSS_FAIL(BVSS_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(dpad), static_cast<cuuint64_t>(rows)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(dpad) * 2};
+  const cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) BVSS_FAIL(BVSS_ECUDA, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
+  return BVSS_OK;
+}
+
+int dense_max_dpad() { return 512; }
+
+// stages that fit next to a query tile of KC chunks
+static int dense_stages(int KC, size_t* smem) {
+  const size_t budget = 227 * 1024 - sizeof(DenseCtl) - 64;
+  const size_t fixed = 1024 + static_cast<size_t>(KC) * kAChunkBytes;
+  if (fixed + 2 * kBChunkBytes > budget) return 0;
+  int st = static_cast<int>((budget - fixed) / kBChunkBytes);
+  if (st > kDenseMaxStages) st = kDenseMaxStages;
+  *smem = fixed + static_cast<size_t>(st) * kBChunkBytes;
+  return st;
+}
+
+int launch_dense_db_operand(const float* V, int64_t nvec, int d, int dpad, float inv_s, __half* hd, int num_sms,
+                            cudaStream_t st) {
+  if (nvec <= 0) return BVSS_OK;
+  dense_db_operand_kernel<<<num_sms * 16, 256, 0, st>>>(V, nvec, d, dpad, inv_s, hd);
+  return post_launch("dense_db_operand_kernel", st);
+}
+
+int launch_dense_query_operand(const float* Qv, const float* qnorm, const int32_t* rowmap, const int32_t* rowq,
+                               int64_t rows, int d, int dpad, float inv_s, __half* qd, int32_t* lane_qid,
+                               float* lane_qn, int num_sms, cudaStream_t st) {
+  if (rows <= 0) return BVSS_OK;
+  dense_query_operand_kernel<<<num_sms * 4, 256, 0, st>>>(Qv, qnorm, rowmap, rowq, rows, d, dpad, inv_s, qd, lane_qid,
+                                                          lane_qn);
+  return post_launch("dense_query_operand_kernel", st);
+}
+
+int launch_dense_prep(const int64_t* qoff, const float* qnorm, int nq, float c1, float c2, float vmax2, float* qE,
+                      float* lists, int64_t nlist, int32_t* cnt, const int32_t* huge, int nhuge, const uint32_t* mask,
+                      int64_t mask_stride, int64_t id_base, int32_t* ids, float* vals, int cap, int num_sms,
+                      cudaStream_t st) {
+  dense_query_bound_kernel<<<ceil_div(nq, 128), 128, 0, st>>>(qoff, qnorm, nq, c1, c2, vmax2, qE);
+  BVSS_TRY(post_launch("dense_query_bound_kernel", st));
+  dense_fill_kernel<<<num_sms * 4, 256, 0, st>>>(lists, nlist, INFINITY);
+  BVSS_TRY(post_launch("dense_fill_kernel", st));
+  dense_append_huge_kernel<<<ceil_div(nq, 128), 128, 0, st>>>(huge, nhuge, mask, mask_stride, nq, id_base, cnt, ids,
+                                                              vals, cap);
+  return post_launch("dense_append_huge_kernel", st);
+}
+
+int launch_dense_hausdorff(const __half* qd, int ntq, const __half* hd, int64_t nvec, int dpad, int ntiles,
+                           const int32_t* tile_s0, const int32_t* tile_s1, const int64_t* off, const float* vn,
+                           const int32_t* lane_qid, const float* lane_qn, const float* qE, const float* tau0,
+                           float cneg, int k, int R, float* lists, int32_t* cnt, int32_t* ids, float* vals, int cap,
+                           const uint32_t* mask, int64_t mask_stride, int64_t id_base, unsigned long long* stat,
+                           int num_sms, cudaStream_t st) {
+  if (ntq <= 0 || ntiles <= 0) return BVSS_OK;
+  if (dpad % 64 || dpad > dense_max_dpad()) BVSS_FAIL(BVSS_EUNSUPPORTED, "dense path needs dpad <= 512");
+  DenseArgs a;
+  std::memset(&a, 0, sizeof(a));
+  BVSS_TRY(encode_map(&a.tmA, qd, static_cast<int64_t>(ntq) * kDenseM, dpad, kDenseM));
+  BVSS_TRY(encode_map(&a.tmB, hd, nvec, dpad, kDenseN));
+  a.KC = dpad / 64;
+  size_t smem = 0;
+  a.stages = dense_stages(a.KC, &smem);
+  if (a.stages < 2) BVSS_FAIL(BVSS_EUNSUPPORTED, "dense path: no room for two stages");
+  a.ntq = ntq;
+  a.R = R;
+  a.ntiles = ntiles;
+  a.tile_s0 = tile_s0;
+  a.tile_s1 = tile_s1;
+  a.off = off;
+  a.vn = vn;
+  a.lane_qid = lane_qid;
+  a.lane_qn = lane_qn;
+  a.qE = qE;
+  a.tau0 = tau0;
+  a.cneg = cneg;
+  a.k = k;
+  a.lists = lists;
+  a.cnt = cnt;
+  a.ids = ids;
+  a.vals = vals;
+  a.cap = cap;
+  a.mask = mask;
+  a.mask_stride = mask_stride;
+  a.id_base = id_base;
+  a.stat = stat;
+  const int units = ntq * R;
+  const int grid = units < num_sms ? units : num_sms;
+  BVSS_CUDA(cudaFuncSetAttribute(dense_hausdorff_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+  dense_hausdorff_kernel<<<grid, kDenseThreads, smem, st>>>(a);
+  return post_launch("dense_hausdorff_kernel", st);
+}
+
+}  // namespace bvss

@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(256) flyhash_wta_kernel(
         const int64_t o = ((((static_cast<int64_t>(ks) * groups + (row >> 3)) * kcs + kq) * 8 + (row & 7)) << 6) +
                           ((u ^ static_cast<int>(row & 7)) << 3) + e;
         hs[o] = h;
-        ls[o] = l;
+        if (ls != nullptr) ls[o] = l;  // the lo piece only for the 3-term Gram (refine_terms = 3)
       }
     }
     if (norms != nullptr) {

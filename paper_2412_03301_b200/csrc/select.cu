@@ -240,6 +240,63 @@ __global__ void __launch_bounds__(256) select_emit_kernel(const K* __restrict__ 
   if (threadIdx.x == 0 && count) count[q] = static_cast<int32_t>(taken);
 }
 
+// The same selection as select_emit_kernel, written as a bitmap (bit i of word i/32 of the query's row =
+// set i is one of its top-T candidates): the candidate restriction of the dense refine (dense.cu) at large T,
+// where [nq][T] id lists would not fit.  The bitmap must be zero on entry.
+template <typename K>
+__global__ void __launch_bounds__(256) select_bitmap_kernel(const K* __restrict__ keys, int64_t key_stride, int64_t n,
+                                                            SelectState st, int T, uint32_t* __restrict__ bitmap,
+                                                            int64_t words) {
+  __shared__ uint32_t sw[8];
+  const int q = blockIdx.x;
+  const int lane = threadIdx.x & 31;
+  const uint32_t tau = st.prefix[q];
+  const int64_t quota = st.quota[q];
+  const K* row = keys + static_cast<int64_t>(q) * key_stride;
+  uint32_t* brow = bitmap + static_cast<int64_t>(q) * words;
+  int64_t taken = 0, eq_seen = 0;
+  for (int64_t tile = 0; tile < n && taken < T; tile += static_cast<int64_t>(blockDim.x) * 8) {
+    const int64_t base = tile + static_cast<int64_t>(threadIdx.x) * 8;
+    K k[8];
+    uint32_t nlt = 0, neq = 0;
+    if (base < n) {
+      load_keys<K>(row, base, n, k);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t kk = static_cast<uint32_t>(k[i]);
+        const bool valid = base + i < n;
+        nlt += (valid && kk < tau) ? 1u : 0u;
+        neq += (valid && kk == tau) ? 1u : 0u;
+      }
+    }
+    uint32_t total;
+    const uint32_t ex = block_exclusive_scan(nlt | (neq << 16), sw, total);
+    const int64_t eq_pre = ex >> 16;
+    int64_t eq_room = quota - eq_seen;
+    if (eq_room < 0) eq_room = 0;
+    int64_t my_eq = eq_seen + eq_pre;
+    uint32_t bits = 0;
+    if (base < n) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const uint32_t kk = static_cast<uint32_t>(k[i]);
+        if (base + i >= n) break;
+        bool take = false;
+        if (kk < tau) take = true;
+        else if (kk == tau) { take = my_eq < quota; ++my_eq; }
+        if (take) bits |= 1u << i;
+      }
+    }
+    uint32_t w = bits << (8 * (lane & 3));  // 4 threads x 8 ids = one 32-id word
+    w |= __shfl_xor_sync(0xffffffffu, w, 1);
+    w |= __shfl_xor_sync(0xffffffffu, w, 2);
+    if ((lane & 3) == 0 && base < n) brow[base >> 5] = w;
+    const int64_t tlt = total & 0xFFFFu, teq = total >> 16;
+    taken += tlt + (teq < eq_room ? teq : eq_room);
+    eq_seen += teq;
+  }
+}
+
 // --------------------------------------------------------------- drivers --
 __global__ void select_init_kernel(SelectState st, int nq, int64_t teff) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
@@ -308,6 +365,18 @@ int launch_select_quota(SelectState st, const int64_t* all_eq, int nq, int world
 
 int launch_select_tiecount(const int32_t* local_hist, SelectState st, int nq, int64_t* eq_out, cudaStream_t s) {
   select_tiecount_kernel<<<ceil_div(nq, 256), 256, 0, s>>>(local_hist, st, nq, eq_out);
+  BVSS_TRY(post_launch(__func__, s));
+  return BVSS_OK;
+}
+
+int launch_select_bitmap(int key_size, const void* keys, int64_t key_stride, int64_t n, int nq, SelectState st,
+                         int T, uint32_t* bitmap, int64_t words, cudaStream_t s) {
+  if (key_size == 2)
+    select_bitmap_kernel<uint16_t><<<nq, 256, 0, s>>>(static_cast<const uint16_t*>(keys), key_stride, n, st, T, bitmap,
+                                                      words);
+  else
+    select_bitmap_kernel<uint32_t><<<nq, 256, 0, s>>>(static_cast<const uint32_t*>(keys), key_stride, n, st, T, bitmap,
+                                                      words);
   BVSS_TRY(post_launch(__func__, s));
   return BVSS_OK;
 }
