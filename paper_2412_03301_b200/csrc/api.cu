@@ -755,7 +755,7 @@ int refine_topk(bvss_index* idx, bvss_search_ctx* c, int64_t* out_ids_dev, float
 
 // ------------------------------------------------ dense (candidate-major) refine, dense.cu --
 // The database operand of the dense kernel (fp16 x / S, S a power of two >= max|x|) and its tile plan (runs
-// of whole consecutive sets of <= 256 rows; larger sets go to the exact path), built on first use.
+// of whole consecutive sets of <= 240 rows; larger sets go to the exact path), built on first use.
 int ensure_dense(bvss_index* idx) {
   if (idx->hd) return BVSS_OK;
   if (idx->dpad > dense_max_dpad()) BVSS_FAIL(BVSS_EUNSUPPORTED, "dense refine needs d <= %d", dense_max_dpad());
@@ -770,14 +770,15 @@ int ensure_dense(bvss_index* idx) {
                                    idx->stream));
   std::vector<int32_t> s0, s1, huge;
   const std::vector<int64_t>& o = idx->off_h;
+  const int64_t cap_rows = 240;  // dense.cu kDenseN
   for (int64_t i = 0; i < idx->n;) {
-    if (o[i + 1] - o[i] > 256) {
+    if (o[i + 1] - o[i] > cap_rows) {
       huge.push_back(static_cast<int32_t>(i));
       ++i;
       continue;
     }
     const int64_t start = i;
-    while (i < idx->n && o[i + 1] - o[i] <= 256 && o[i + 1] - o[start] <= 256) ++i;
+    while (i < idx->n && o[i + 1] - o[i] <= cap_rows && o[i + 1] - o[start] <= cap_rows) ++i;
     s0.push_back(static_cast<int32_t>(start));
     s1.push_back(static_cast<int32_t>(i));
   }
@@ -950,7 +951,7 @@ int dense_refine_topk(bvss_index* idx, bvss_search_ctx* c, const uint32_t* mask,
   idx->stats.dense_pairs += static_cast<uint64_t>(c->nqvec) * static_cast<uint64_t>(
       ntiles_use >= idx->dntiles ? idx->nvec : idx->off_h[idx->dtile_s0_h[ntiles_use]]);
   idx->stats.dense_flop += 2.0 * static_cast<double>(rows) * idx->dpad *
-                           static_cast<double>(ntiles_use) * 256.0;
+                           static_cast<double>(ntiles_use) * 240.0;
   *done = true;
   return BVSS_OK;
 }

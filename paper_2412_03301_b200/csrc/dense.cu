@@ -8,14 +8,14 @@
 // moves T x (set rows) x d x 2 bytes per query.  This kernel instead streams the
 // database ONCE per 128-row query tile: the query tile is the stationary A
 // operand (M = 128 packed query rows, resident in shared memory), the database
-// rows stream through a TMA ring as the B operand (N = 256 rows per tile, K = d
+// rows stream through a TMA ring as the B operand (N = 240 rows per tile, K = d
 // in 64-element SW128 chunks), and tcgen05.mma accumulates the Gram tile in TMEM
-// (two 256-column accumulators, double-buffered against the epilogue).
+// (two 240-column accumulators, double-buffered against the epilogue).
 //
 // Layouts (built once per index / per batch):
 //   database  hd [nvec][dpad] fp16 = x / S_db, one global power-of-two scale
 //             S_db >= max|x| (row-major; tiles are runs of whole consecutive sets
-//             of <= 256 rows, any start row: TMA swizzles on the fly);
+//             of <= 240 rows, any start row: TMA swizzles on the fly);
 //   queries   qd [ntq*128][dpad] fp16 = x / S_q, query sets packed into 32-row
 //             warp bins (a set never straddles a warp), 4 bins per tile.
 // D^2(q, v) = |q|^2 + |v|^2 - 2 S_q S_db g(q, v), g the fp16 Gram.
@@ -54,16 +54,19 @@
 
 namespace bvss {
 
-constexpr int kDenseN = 256;      // database rows per tile (MMA N)
+// database rows per tile (MMA N): two 240-column accumulators leave 32 spare TMEM columns, so a 32-column
+// tcgen05.ld that starts at any set inside the second accumulator stays inside the 512-column allocation
+// (a load past it faults: tools/test_tmem_ld.cu); sets start at any column (unaligned loads are legal)
+constexpr int kDenseN = 240;
 constexpr int kDenseM = 128;      // packed query rows per tile (MMA M)
 constexpr int kDenseThreads = 320;
 constexpr int kDenseMaxStages = 8;
 constexpr uint32_t kAChunkBytes = kDenseM * 128;  // one 64-element K chunk of the query tile (16 KB)
-constexpr uint32_t kBChunkBytes = kDenseN * 128;  // one K chunk of a database tile (32 KB)
+constexpr uint32_t kBChunkBytes = kDenseN * 128;  // one K chunk of a database tile (30 KB, 1024-aligned)
 
 struct DenseArgs {
   CUtensorMap tmA;              // qd [ntq*128][dpad] fp16, box {64, 128}, SWIZZLE_128B
-  CUtensorMap tmB;              // hd [nvec][dpad] fp16, box {64, 256}, SWIZZLE_128B
+  CUtensorMap tmB;              // hd [nvec][dpad] fp16, box {64, 240}, SWIZZLE_128B
   int KC;                       // dpad / 64
   int stages;
   int ntq;                      // query tiles
@@ -384,7 +387,7 @@ __global__ void dense_fill_kernel(float* __restrict__ x, int64_t n, float v) {
     x[i] = v;
 }
 
-// sets the tiles cannot hold (> 256 rows): appended to every query's list with the K6 exact sentinel
+// sets the tiles cannot hold (> 240 rows): appended to every query's list with the K6 exact sentinel
 // (every one is recomputed exactly), honouring the candidate bitmap
 __global__ void dense_append_huge_kernel(const int32_t* __restrict__ huge, int nhuge, const uint32_t* __restrict__ mask,
                                          int64_t mask_stride, int nq, int64_t id_base, int32_t* __restrict__ cnt,
