@@ -821,13 +821,14 @@ bool dense_wanted(const bvss_index* idx, int64_t teff) {
 // Exact top-k of a prepared batch by the dense kernel: every (query, set) Gram on the tensor cores, the
 // branch-and-bound prune, the emitted candidate lists, then K6 (topk_exact_kernel) on those lists.
 // mask: optional candidate bitmap (row q at mask + q * mask_stride); ntiles_use: dense tiles to scan (a
-// prefix; brute force over the first set_limit sets).  *done = false when the batch is not supported or a
+// prefix, for brute force over the first set_limit sets; -1 = all).  *done = false when the batch is not supported or a
 // candidate list overflowed (the caller then runs the query-major path; the result is the same).
 int dense_refine_topk(bvss_index* idx, bvss_search_ctx* c, const uint32_t* mask, int64_t mask_stride, int ntiles_use,
                       int64_t* out_ids_dev, float* out_dist_dev, bool* done) {
   *done = false;
   if (!dense_supported(idx, c)) return BVSS_OK;
   BVSS_TRY(ensure_dense(idx));
+  if (ntiles_use < 0 || ntiles_use > idx->dntiles) ntiles_use = idx->dntiles;  // (-1: every tile)
   const int nq = static_cast<int>(c->nq), k = c->k;
   // query packing: best fit (decreasing sizes) into 32-row warp bins, 4 bins per 128-row tile
   std::vector<int> order(nq);
@@ -1675,7 +1676,7 @@ int bvss_search(bvss_index* idx, const float* queries, const int64_t* query_offs
       if (teff < idx->n) BVSS_TRY(dense_mask(idx, c.get(), &mask, &mstride));
       cudaEventRecord(idx->ev[3], idx->stream);
       t_sel = now_us();
-      BVSS_TRY(dense_refine_topk(idx, c.get(), mask, mstride, idx->dntiles, oid, odist, &done));
+      BVSS_TRY(dense_refine_topk(idx, c.get(), mask, mstride, -1, oid, odist, &done));
       if (!done && !sampled) BVSS_TRY(scan_batch(idx, c.get()));  // overflow: the query-major path below
     } else if (try_dense && !sampled) {
       BVSS_TRY(scan_batch(idx, c.get()));

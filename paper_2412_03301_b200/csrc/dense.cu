@@ -59,7 +59,8 @@ namespace bvss {
 // (a load past it faults: tools/test_tmem_ld.cu); sets start at any column (unaligned loads are legal)
 constexpr int kDenseN = 240;
 constexpr int kDenseM = 128;      // packed query rows per tile (MMA M)
-constexpr int kDenseThreads = 320;
+constexpr int kDenseThreads = 352;  // 11 warps: producer, MMA, 8 epilogue, tile info
+constexpr int kInfoSlotsD = 4;
 constexpr int kDenseMaxStages = 8;
 constexpr uint32_t kAChunkBytes = kDenseM * 128;  // one 64-element K chunk of the query tile (16 KB)
 constexpr uint32_t kBChunkBytes = kDenseN * 128;  // one K chunk of a database tile (30 KB, 1024-aligned)
@@ -93,7 +94,18 @@ struct DenseArgs {
   unsigned long long* stat;     // [2]: survivors, emitted (may be null)
 };
 
+// per-tile metadata the info warp stages for the epilogue (shared memory): the database sets of the tile
+// (first set id, count, column and size of each) and the squared norm of every column
+struct DenseInfo {
+  int s0, nsets, pad0, pad1;
+  float vn[kDenseN];
+  int16_t col0[kDenseN];
+  int16_t mv[kDenseN];
+};
+
 struct DenseCtl {
+  DenseInfo info[kInfoSlotsD];
+  uint64_t info_full[kInfoSlotsD], info_empty[kInfoSlotsD];
   uint64_t full[kDenseMaxStages];
   uint64_t empty[kDenseMaxStages];
   uint64_t a_full, a_empty;
@@ -152,6 +164,10 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&S.tfull[b], 1);
       tc::mbar_init(&S.tempty[b], 8);
+    }
+    for (int b = 0; b < kInfoSlotsD; ++b) {
+      tc::mbar_init(&S.info_full[b], 1);
+      tc::mbar_init(&S.info_empty[b], 8);
     }
     tc::fence_mbar_init();
   }
@@ -221,6 +237,55 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
       if (lane == 0) tc::umma_commit(&S.a_empty);  // the query tile may be overwritten once these MMAs are done
       __syncwarp();
     }
+  } else if (warp == 10) {
+    // =========================== tile info (sets, columns, norms) ===========================
+    uint32_t tile_ctr = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int r = u % a.R;
+      int t0, t1;
+      range_tiles(r, a.R, a.ntiles, &t0, &t1);
+      for (int t = t0; t < t1; ++t, ++tile_ctr) {
+        const int slot = tile_ctr % kInfoSlotsD;
+        DenseInfo& inf = S.info[slot];
+        const int s0 = a.tile_s0[t], s1 = a.tile_s1[t];
+        const int64_t row0 = a.off[s0];
+        const int64_t rows = a.off[s1] - row0;
+        float vn[(kDenseN + 31) / 32];
+#pragma unroll
+        for (int c = 0; c < (kDenseN + 31) / 32; ++c) {
+          const int j = lane + 32 * c;
+          vn[c] = (j < rows) ? __ldg(a.vn + row0 + j) : 0.0f;
+        }
+        int16_t cl[(kDenseN + 31) / 32], ml[(kDenseN + 31) / 32];
+#pragma unroll
+        for (int c = 0; c < (kDenseN + 31) / 32; ++c) {
+          const int j = lane + 32 * c;
+          cl[c] = 0;
+          ml[c] = 0;
+          if (j < s1 - s0) {
+            const int64_t v0 = a.off[s0 + j];
+            cl[c] = static_cast<int16_t>(v0 - row0);
+            ml[c] = static_cast<int16_t>(a.off[s0 + j + 1] - v0);
+          }
+        }
+        tc::mbar_wait(&S.info_empty[slot], ((tile_ctr / kInfoSlotsD) & 1u) ^ 1u);
+#pragma unroll
+        for (int c = 0; c < (kDenseN + 31) / 32; ++c) {
+          const int j = lane + 32 * c;
+          if (j < kDenseN) {
+            inf.vn[j] = vn[c];
+            inf.col0[j] = cl[c];
+            inf.mv[j] = ml[c];
+          }
+        }
+        if (lane == 0) {
+          inf.s0 = s0;
+          inf.nsets = s1 - s0;
+        }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&S.info_full[slot]);
+      }
+    }
   } else {
     // =========================== epilogue (warps 2..9) ===========================
     const int quarter = warp & 3;
@@ -238,24 +303,28 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
       float* own = valid ? a.lists + ((static_cast<int64_t>(qid) * a.R + r) * 2 + sub) * a.k : nullptr;
       const float* other = valid ? a.lists + ((static_cast<int64_t>(qid) * a.R + r) * 2 + (sub ^ 1)) * a.k : nullptr;
       float tau = valid ? a.tau0[qid] : INF;
+      float other_k = INF;  // the other warp's k-th bound, loaded one tile ahead (its latency stays hidden)
       int t0, t1;
       range_tiles(r, a.R, a.ntiles, &t0, &t1);
       for (int t = t0; t < t1; ++t, ++tile_ctr) {
         const uint32_t acc = tile_ctr & 1u;
-        if (valid) tau = fminf(tau, vload_volatile(other + a.k - 1));  // the other warp's k-th bound
+        const int slot = tile_ctr % kInfoSlotsD;
+        tau = fminf(tau, other_k);
+        if (valid) other_k = vload_volatile(other + a.k - 1);
         float thr = tau + E;
+        tc::mbar_wait(&S.info_full[slot], (tile_ctr / kInfoSlotsD) & 1u);
+        const DenseInfo& inf = S.info[slot];
         tc::mbar_wait(&S.tfull[acc], (tile_ctr >> 1) & 1u);
         tc::fence_after_sync();
-        const int s0 = a.tile_s0[t], s1 = a.tile_s1[t];
-        const int64_t row0 = a.off[s0];
+        const int s0 = inf.s0, nsets = inf.nsets;
         const uint32_t tb = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * kDenseN;
-        for (int i = s0 + sub; i < s1; i += 2) {
-          const int64_t v0 = a.off[i];
-          const int col0 = static_cast<int>(v0 - row0);
-          const int mv = static_cast<int>(a.off[i + 1] - v0);
+        for (int js = sub; js < nsets; js += 2) {
+          const int i = s0 + js;
+          const int col0 = inf.col0[js];
+          const int mv = inf.mv[js];
           float run = INF;
           for (int j0 = 0; j0 < mv; j0 += 32) {
-            const float vnl = (j0 + lane < mv) ? __ldg(a.vn + v0 + j0 + lane) : 0.0f;
+            const float vnl = (j0 + lane < mv) ? inf.vn[col0 + j0 + lane] : 0.0f;
             uint32_t g[32];
             tmem_ld32(tb + static_cast<uint32_t>(col0 + j0), g);
             tc::tmem_ld_wait();
@@ -283,7 +352,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
             const float A = __uint_as_float(__reduce_max_sync(0xffffffffu, inseg ? __float_as_uint(rq) : 0u));
             float B = 0.0f;
             for (int j0 = 0; j0 < mv; j0 += 32) {
-              const float vnl = (j0 + lane < mv) ? __ldg(a.vn + v0 + j0 + lane) : 0.0f;
+              const float vnl = (j0 + lane < mv) ? inf.vn[col0 + j0 + lane] : 0.0f;
               uint32_t g[32];
               tmem_ld32(tb + static_cast<uint32_t>(col0 + j0), g);
               tc::tmem_ld_wait();
@@ -328,7 +397,10 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
         }
         tc::fence_before_sync();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&S.tempty[acc]);
+        if (lane == 0) {
+          tc::mbar_arrive(&S.tempty[acc]);
+          tc::mbar_arrive(&S.info_empty[slot]);
+        }
       }
     }
   }
@@ -432,7 +504,7 @@ int dense_max_dpad() { return 512; }
 
 // stages that fit next to a query tile of KC chunks
 static int dense_stages(int KC, size_t* smem) {
-  const size_t budget = 227 * 1024 - sizeof(DenseCtl) - 64;
+  const size_t budget = 227 * 1024 - sizeof(DenseCtl) - 1024;  // static shared memory (DenseCtl, 1 KB aligned)
   const size_t fixed = 1024 + static_cast<size_t>(KC) * kAChunkBytes;
   if (fixed + 2 * kBChunkBytes > budget) return 0;
   int st = static_cast<int>((budget - fixed) / kBChunkBytes);
