@@ -109,6 +109,7 @@ int launch_merge_topk(const int64_t* ids, const float* dist, int P, int64_t nq, 
 int launch_select_bitmap(int key_size, const void* keys, int64_t key_stride, int64_t n, int nq, SelectState st,
                          int T, uint32_t* bitmap, int64_t words, cudaStream_t s);
 int dense_max_dpad();
+int dense_epi_sub();
 int launch_dense_db_operand(const float* V, int64_t nvec, int d, int dpad, float inv_s, __half* hd, int num_sms,
                             cudaStream_t st);
 int launch_dense_query_operand(const float* Qv, const float* qnorm, const int32_t* rowmap, const int32_t* rowq,
@@ -871,8 +872,9 @@ int dense_refine_topk(bvss_index* idx, bvss_search_ctx* c, const uint32_t* mask,
   int R = static_cast<int>(ceil_div<int64_t>(2 * idx->num_sms, ntq));
   if (R < 4) R = 4;
   if (R > ntiles) R = ntiles < 1 ? 1 : ntiles;
-  const double spl = std::max(1.0, static_cast<double>(idx->n) / (2.0 * R * k));
-  int64_t cap = static_cast<int64_t>(2.0 * R * k * (2.0 + std::log(spl)) * 2.0) + idx->dnhuge + 1024;
+  const double spl = std::max(1.0, static_cast<double>(idx->n) / (static_cast<double>(R) * dense_epi_sub() * k));
+  const double lists_pq = static_cast<double>(R) * dense_epi_sub();  // bound lists per query
+  int64_t cap = static_cast<int64_t>(lists_pq * k * (2.0 + std::log(spl)) * 2.0) + idx->dnhuge + 1024;
   if (const char* e = getenv("BVSS_DEBUG_DENSE_CAP")) cap = atoll(e);  // test switch: force overflows
   cap = (cap + 255) & ~int64_t(255);
   // query max norm -> S_q
@@ -894,7 +896,7 @@ int dense_refine_topk(bvss_index* idx, bvss_search_ctx* c, const uint32_t* mask,
   int32_t *d_rowmap, *d_rowq, *lane_qid, *cnt, *ids;
   float *lane_qn, *qE, *tau0, *lists, *vals;
   unsigned long long* stat;
-  const int64_t nlist = static_cast<int64_t>(nq) * R * 2 * k;
+  const int64_t nlist = static_cast<int64_t>(nq) * R * dense_epi_sub() * k;
   BVSS_TRY(c->alloc(rows * idx->dpad * 2, reinterpret_cast<void**>(&qd)));
   BVSS_TRY(c->alloc(rows * 4, reinterpret_cast<void**>(&d_rowmap)));
   BVSS_TRY(c->alloc(rows * 4, reinterpret_cast<void**>(&d_rowq)));

@@ -20,13 +20,13 @@
 //             warp bins (a set never straddles a warp), 4 bins per tile.
 // D^2(q, v) = |q|^2 + |v|^2 - 2 S_q S_db g(q, v), g the fp16 Gram.
 //
-// Epilogue (8 warps, two per TMEM lane quarter; lane = query row, column =
-// database row; sets of a tile alternate between the two warps of a quarter):
+// Epilogue (12 warps, three per TMEM lane quarter; lane = query row, column =
+// database row; sets of a tile alternate between the warps of a quarter):
 //   per database set V and lane q:   r_q = max(0, min_v D^2(q, v))  (lane-local)
 //   A(Q, V) = max_{q in Q} r_q  is a lower bound of H^2(Q, V) = max(A, B).
 // Branch and bound per query: tau_Q = the k-th smallest upper bound (H2c + E)
-// among the sets seen so far (a list of k per (query, range, warp) in global
-// memory; any k distinct sets' upper bounds bound the true k-th H^2 from above).
+// among the sets seen so far (a list of k per (query, range, epilogue warp) in
+// global memory; any k distinct sets' upper bounds bound the true k-th H^2).
 // A set is pruned when some lane of Q has r_q > tau_Q + E (so A - E > tau_Q:
 // its exact H^2 exceeds the exact k-th, the set cannot be in the top-k).  A set
 // that survives gets B(Q, V) = max_v min_q D^2 by one redux.sync.min per column
@@ -36,8 +36,8 @@
 // emitted lists contain every set whose H2c - E <= the final U_k, which is the
 // K6 window rule, so the result is exact (E from error_consts()).
 //
-// CTA = 10 warps: 0 TMA producer, 1 TMEM owner + MMA issuer (one thread), 2-9
-// epilogue.  Persistent: unit u = blockIdx.x + i * gridDim.x is (query tile
+// CTA = 15 warps: 0 TMA producer, 1 TMEM owner + MMA issuer (one thread), 2-13
+// epilogue, 14 tile info (set columns / sizes and column norms into shared memory).  Persistent: unit u = blockIdx.x + i * gridDim.x is (query tile
 // u / R, database range u % R); consecutive units run the same ranges at the
 // same time on all SMs, so each database tile is read from HBM about once per
 // wave and served from L2 to the other CTAs.
@@ -59,7 +59,10 @@ namespace bvss {
 // (a load past it faults: tools/test_tmem_ld.cu); sets start at any column (unaligned loads are legal)
 constexpr int kDenseN = 240;
 constexpr int kDenseM = 128;      // packed query rows per tile (MMA M)
-constexpr int kDenseThreads = 352;  // 11 warps: producer, MMA, 8 epilogue, tile info
+constexpr int kEpiSub = 3;                                  // epilogue warps per TMEM lane quarter
+constexpr int kEpiWarpsD = 4 * kEpiSub;
+constexpr int kInfoWarp = 2 + kEpiWarpsD;
+constexpr int kDenseThreads = 32 * (kInfoWarp + 1);        // producer, MMA, epilogue, tile info
 constexpr int kInfoSlotsD = 4;
 constexpr int kDenseMaxStages = 8;
 constexpr uint32_t kAChunkBytes = kDenseM * 128;  // one 64-element K chunk of the query tile (16 KB)
@@ -83,7 +86,7 @@ struct DenseArgs {
   const float* tau0;            // [nq] initial tau (an upper bound on the k-th H^2; +inf if none)
   float cneg;                   // -2 S_q S_db
   int k;
-  float* lists;                 // [nq][R][2][k] sorted upper bounds, +inf-initialised
+  float* lists;                 // [nq][R][kEpiSub][k] sorted upper bounds, +inf-initialised
   int32_t* cnt;                 // [nq] emitted candidates (may exceed cap: overflow)
   int32_t* ids;                 // [nq][cap]
   float* vals;                  // [nq][cap] tensor-core H^2
@@ -163,11 +166,11 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
     tc::mbar_init(&S.a_empty, 1);
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&S.tfull[b], 1);
-      tc::mbar_init(&S.tempty[b], 8);
+      tc::mbar_init(&S.tempty[b], kEpiWarpsD);
     }
     for (int b = 0; b < kInfoSlotsD; ++b) {
       tc::mbar_init(&S.info_full[b], 1);
-      tc::mbar_init(&S.info_empty[b], 8);
+      tc::mbar_init(&S.info_empty[b], kEpiWarpsD);
     }
     tc::fence_mbar_init();
   }
@@ -237,7 +240,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
       if (lane == 0) tc::umma_commit(&S.a_empty);  // the query tile may be overwritten once these MMAs are done
       __syncwarp();
     }
-  } else if (warp == 10) {
+  } else if (warp == kInfoWarp) {
     // =========================== tile info (sets, columns, norms) ===========================
     uint32_t tile_ctr = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -287,9 +290,9 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
       }
     }
   } else {
-    // =========================== epilogue (warps 2..9) ===========================
+    // =========================== epilogue (warps 2 .. 2 + kEpiWarpsD - 1) ===========================
     const int quarter = warp & 3;
-    const int sub = (warp - 2) >> 2;
+    const int sub = (warp - 2) >> 2;  // 0 .. kEpiSub-1: the quarter's warps take alternate sets
     const float INF = __int_as_float(0x7f800000);
     uint32_t tile_ctr = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -300,17 +303,21 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
       const float qn = valid ? a.lane_qn[prow] : 0.0f;
       const unsigned segmask = __match_any_sync(0xffffffffu, qid);
       const float E = valid ? a.qE[qid] : 0.0f;
-      float* own = valid ? a.lists + ((static_cast<int64_t>(qid) * a.R + r) * 2 + sub) * a.k : nullptr;
-      const float* other = valid ? a.lists + ((static_cast<int64_t>(qid) * a.R + r) * 2 + (sub ^ 1)) * a.k : nullptr;
+      const float* lq = valid ? a.lists + (static_cast<int64_t>(qid) * a.R + r) * kEpiSub * a.k : nullptr;
+      float* own = valid ? const_cast<float*>(lq) + sub * a.k : nullptr;
       float tau = valid ? a.tau0[qid] : INF;
-      float other_k = INF;  // the other warp's k-th bound, loaded one tile ahead (its latency stays hidden)
+      float other_k = INF;  // the other warps' k-th bounds, loaded one tile ahead (their latency stays hidden)
       int t0, t1;
       range_tiles(r, a.R, a.ntiles, &t0, &t1);
       for (int t = t0; t < t1; ++t, ++tile_ctr) {
         const uint32_t acc = tile_ctr & 1u;
         const int slot = tile_ctr % kInfoSlotsD;
         tau = fminf(tau, other_k);
-        if (valid) other_k = vload_volatile(other + a.k - 1);
+        if (valid) {
+          other_k = INF;
+#pragma unroll
+          for (int o = 1; o < kEpiSub; ++o) other_k = fminf(other_k, vload_volatile(lq + ((sub + o) % kEpiSub) * a.k + a.k - 1));
+        }
         float thr = tau + E;
         tc::mbar_wait(&S.info_full[slot], (tile_ctr / kInfoSlotsD) & 1u);
         const DenseInfo& inf = S.info[slot];
@@ -318,24 +325,29 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
         tc::fence_after_sync();
         const int s0 = inf.s0, nsets = inf.nsets;
         const uint32_t tb = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * kDenseN;
-        for (int js = sub; js < nsets; js += 2) {
+        for (int js = sub; js < nsets; js += kEpiSub) {
           const int i = s0 + js;
           const int col0 = inf.col0[js];
           const int mv = inf.mv[js];
-          float run = INF;
+          float run0 = INF, run1 = INF;
           for (int j0 = 0; j0 < mv; j0 += 32) {
-            const float vnl = (j0 + lane < mv) ? inf.vn[col0 + j0 + lane] : 0.0f;
+            // columns past the set get |v|^2 = +inf, so they never win the min; branches only every 8
+            // columns, so the shuffles and FMAs of a group issue back to back (two independent min chains)
+            const float vnl = (j0 + lane < mv) ? inf.vn[col0 + j0 + lane] : INF;
             uint32_t g[32];
             tmem_ld32(tb + static_cast<uint32_t>(col0 + j0), g);
             tc::tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              if (j0 + j >= mv) break;
-              const float vnj = __shfl_sync(0xffffffffu, vnl, j);
-              run = fminf(run, fmaf(__uint_as_float(g[j]), a.cneg, vnj));
+            for (int j8 = 0; j8 < 32; j8 += 8) {
+              if (j0 + j8 >= mv) break;
+#pragma unroll
+              for (int j = j8; j < j8 + 8; j += 2) {
+                run0 = fminf(run0, fmaf(__uint_as_float(g[j]), a.cneg, __shfl_sync(0xffffffffu, vnl, j)));
+                run1 = fminf(run1, fmaf(__uint_as_float(g[j + 1]), a.cneg, __shfl_sync(0xffffffffu, vnl, j + 1)));
+              }
             }
           }
-          const float rq = fmaxf(run + qn, 0.0f);
+          const float rq = fmaxf(fminf(run0, run1) + qn, 0.0f);
           const unsigned pass = __ballot_sync(0xffffffffu, !valid || rq <= thr);
           unsigned sb = __ballot_sync(0xffffffffu, valid && (pass & segmask) == segmask);
           while (sb) {  // warp-uniform: one surviving query segment at a time
@@ -352,17 +364,21 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
             const float A = __uint_as_float(__reduce_max_sync(0xffffffffu, inseg ? __float_as_uint(rq) : 0u));
             float B = 0.0f;
             for (int j0 = 0; j0 < mv; j0 += 32) {
-              const float vnl = (j0 + lane < mv) ? inf.vn[col0 + j0 + lane] : 0.0f;
+              // columns past the set: |v|^2 = -inf, D^2 clamps to 0 and never raises the max
+              const float vnl = (j0 + lane < mv) ? inf.vn[col0 + j0 + lane] : -INF;
               uint32_t g[32];
               tmem_ld32(tb + static_cast<uint32_t>(col0 + j0), g);
               tc::tmem_ld_wait();
 #pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                if (j0 + j >= mv) break;
-                const float vnj = __shfl_sync(0xffffffffu, vnl, j);
-                const float d2 = fmaxf(fmaf(__uint_as_float(g[j]), a.cneg, vnj) + qn, 0.0f);
-                const uint32_t cm = __reduce_min_sync(0xffffffffu, inseg ? __float_as_uint(d2) : 0xffffffffu);
-                B = fmaxf(B, __uint_as_float(cm));
+              for (int j8 = 0; j8 < 32; j8 += 8) {
+                if (j0 + j8 >= mv) break;
+#pragma unroll
+                for (int j = j8; j < j8 + 8; ++j) {
+                  const float vnj = __shfl_sync(0xffffffffu, vnl, j);
+                  const float d2 = fmaxf(fmaf(__uint_as_float(g[j]), a.cneg, vnj) + qn, 0.0f);
+                  const uint32_t cm = __reduce_min_sync(0xffffffffu, inseg ? __float_as_uint(d2) : 0xffffffffu);
+                  B = fmaxf(B, __uint_as_float(cm));
+                }
               }
             }
             const float h = fmaxf(A, B);
@@ -376,7 +392,10 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
                   --p;
                 }
                 own[p] = ub;
-                newtau = fminf(own[a.k - 1], vload_volatile(other + a.k - 1));
+                newtau = own[a.k - 1];
+#pragma unroll
+                for (int o = 1; o < kEpiSub; ++o)
+                  newtau = fminf(newtau, vload_volatile(lq + ((sub + o) % kEpiSub) * a.k + a.k - 1));
               }
               if (h - E <= newtau) {
                 const int slot = atomicAdd(a.cnt + q, 1);
@@ -501,6 +520,7 @@ static int encode_map(CUtensorMap* map, const void* base, int64_t rows, int dpad
 }
 
 int dense_max_dpad() { return 512; }
+int dense_epi_sub() { return kEpiSub; }
 
 // stages that fit next to a query tile of KC chunks
 static int dense_stages(int KC, size_t* smem) {
