@@ -119,10 +119,12 @@ int launch_dense_prep(const int64_t* qoff, const float* qnorm, int nq, float c1,
                       float* lists, int64_t nlist, int32_t* cnt, const int32_t* huge, int nhuge, const uint32_t* mask,
                       int64_t mask_stride, int64_t id_base, int32_t* ids, float* vals, int cap, int num_sms,
                       cudaStream_t st);
+int launch_dense_norm_operand(const float* vn, int64_t nvec, float inv_s2, __half* va, int num_sms, cudaStream_t st);
 int launch_dense_hausdorff(const __half* qd, int ntq, const __half* hd, int64_t nvec, int dpad, int ntiles,
-                           const int32_t* tile_s0, const int32_t* tile_s1, const int64_t* off, const float* vn,
-                           const int32_t* lane_qid, const float* lane_qn, const float* qE, const float* tau0,
-                           float cneg, int k, int R, float* lists, int32_t* cnt, int32_t* ids, float* vals, int cap,
+                           const int32_t* tile_s0, const int32_t* tile_s1, const int64_t* off, const __half* va,
+                           const __half* qa, const int32_t* lane_qid, const float* lane_qn, const float* qE,
+                           const float* tau0,
+                           float kappa, int k, int R, float* lists, int32_t* cnt, int32_t* ids, float* vals, int cap,
                            const uint32_t* mask, int64_t mask_stride, int64_t id_base, unsigned long long* stat,
                            int num_sms, cudaStream_t st);
 
@@ -287,6 +289,7 @@ struct bvss_index {
   // dense (candidate-major) refine, dense.cu: built on first use
   std::vector<int64_t> off_h;   // host copy of the set offsets
   __half* hd = nullptr;         // [nvec][dpad] fp16 = x / dense_s
+  __half* va = nullptr;         // [nvec][16] fp16: the split |v|^2 / dense_s^2 (the MMA's norm chunk)
   float dense_s = 1.0f;         // power of two >= max|x|
   int32_t* dtile_s0 = nullptr;  // [dntiles] first set of each dense tile (whole sets, <= 256 rows)
   int32_t* dtile_s1 = nullptr;
@@ -769,6 +772,11 @@ int ensure_dense(bvss_index* idx) {
   idx->owned_bytes += hb;
   BVSS_TRY(launch_dense_db_operand(idx->V, idx->nvec, idx->d, idx->dpad, 1.0f / idx->dense_s, idx->hd, idx->num_sms,
                                    idx->stream));
+  const size_t vb = static_cast<size_t>(idx->nvec) * 32;
+  BVSS_CUDA(cudaMalloc(reinterpret_cast<void**>(&idx->va), vb));
+  idx->owned_bytes += vb;
+  BVSS_TRY(launch_dense_norm_operand(idx->vnorm, idx->nvec, 1.0f / (idx->dense_s * idx->dense_s), idx->va,
+                                     idx->num_sms, idx->stream));
   std::vector<int32_t> s0, s1, huge;
   const std::vector<int64_t>& o = idx->off_h;
   const int64_t cap_rows = 240;  // dense.cu kDenseN
@@ -891,13 +899,21 @@ int dense_refine_topk(bvss_index* idx, bvss_search_ctx* c, const uint32_t* mask,
   int ex = 0;
   if (qmax2 > 0.0f) std::frexp(std::sqrt(qmax2), &ex);
   const float sq = std::ldexp(1.0f, ex);
+  // the norm chunk of the query tile: (alpha, alpha, 0 ...) on every row, alpha = -S_db / (2 S_q) (a power of
+  // two; it must be a normal fp16 number for the product to stay exact)
+  const float alpha = -idx->dense_s / (2.0f * sq);
+  if (std::fabs(alpha) < std::ldexp(1.0f, -14) || std::fabs(alpha) > 32768.0f) return BVSS_OK;  // (query-major)
+  std::vector<__half> qa_h(128 * 16, __float2half_rn(0.0f));
+  for (int r = 0; r < 128; ++r) qa_h[r * 16] = qa_h[r * 16 + 1] = __float2half_rn(alpha);
   // buffers
-  __half* qd;
+  __half *qd, *qa;
   int32_t *d_rowmap, *d_rowq, *lane_qid, *cnt, *ids;
   float *lane_qn, *qE, *tau0, *lists, *vals;
   unsigned long long* stat;
   const int64_t nlist = static_cast<int64_t>(nq) * R * dense_epi_sub() * k;
   BVSS_TRY(c->alloc(rows * idx->dpad * 2, reinterpret_cast<void**>(&qd)));
+  BVSS_TRY(c->alloc(128 * 16 * 2, reinterpret_cast<void**>(&qa)));
+  BVSS_CUDA(cudaMemcpyAsync(qa, qa_h.data(), 128 * 16 * 2, cudaMemcpyHostToDevice, idx->stream));
   BVSS_TRY(c->alloc(rows * 4, reinterpret_cast<void**>(&d_rowmap)));
   BVSS_TRY(c->alloc(rows * 4, reinterpret_cast<void**>(&d_rowq)));
   BVSS_TRY(c->alloc(rows * 4, reinterpret_cast<void**>(&lane_qid)));
@@ -916,13 +932,16 @@ int dense_refine_topk(bvss_index* idx, bvss_search_ctx* c, const uint32_t* mask,
                                       lane_qid, lane_qn, idx->num_sms, idx->stream));
   float c1, c2;
   error_consts(idx, &c1, &c2);
+  // the accumulator also carries alpha (h + l) ~ |v|^2 / (2 S_q S_db): its fp32 accumulation adds at most
+  // (dpad + 80) 2^-23 |v|^2 after the kappa scaling, and the (h, l) split 2^-21 |v|^2
+  c2 += static_cast<float>((idx->dpad + 80.0) * std::ldexp(1.0, -23) * 1.01 + std::ldexp(1.0, -21));
   fill_f32_inf(tau0, nq, idx->stream);
   BVSS_TRY(launch_dense_prep(c->qoff, c->qnorm, nq, c1, c2, idx->vmax2, qE, lists, nlist, cnt, idx->dhuge,
                              idx->dnhuge, mask, mask_stride, c->id_base, ids, vals, static_cast<int>(cap),
                              idx->num_sms, idx->stream));
   cudaEventRecord(idx->ev[4], idx->stream);
   BVSS_TRY(launch_dense_hausdorff(qd, ntq, idx->hd, idx->nvec, idx->dpad, ntiles, idx->dtile_s0, idx->dtile_s1,
-                                  idx->off, idx->vnorm, lane_qid, lane_qn, qE, tau0, -2.0f * sq * idx->dense_s, k, R,
+                                  idx->off, idx->va, qa, lane_qid, lane_qn, qE, tau0, -2.0f * sq * idx->dense_s, k, R,
                                   lists, cnt, ids, vals, static_cast<int>(cap), mask, mask_stride, c->id_base, stat,
                                   idx->num_sms, idx->stream));
   cudaEventRecord(idx->ev[5], idx->stream);
@@ -1356,7 +1375,7 @@ int bvss_index_finish(bvss_index* idx) {
   built->codes = nullptr;
   built->sk = built->smp_sk = built->skx = built->smp_skx = nullptr;
   built->mass = built->smp_mass = nullptr;
-  built->hd = nullptr;
+  built->hd = built->va = nullptr;
   built->dtile_s0 = built->dtile_s1 = built->dhuge = nullptr;
   for (auto& e : built->ev) e = nullptr;
   delete built;
@@ -1370,7 +1389,7 @@ void bvss_free_index(bvss_index* idx) {
   if (idx->stream) cudaStreamSynchronize(idx->stream);
   void* ptrs[] = {idx->Wt,    idx->V,     idx->off,   idx->hi,   idx->lo,     idx->vscale, idx->pbase,
                   idx->vnorm, idx->codes, idx->sk,    idx->mass, idx->smp_sk, idx->smp_mass,
-                  idx->skx,   idx->smp_skx, idx->hd, idx->dtile_s0, idx->dtile_s1, idx->dhuge};
+                  idx->skx,   idx->smp_skx, idx->hd, idx->va, idx->dtile_s0, idx->dtile_s1, idx->dhuge};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (idx->pend_V) cudaFree(idx->pend_V);

@@ -18,11 +18,17 @@
 //             of <= 240 rows, any start row: TMA swizzles on the fly);
 //   queries   qd [ntq*128][dpad] fp16 = x / S_q, query sets packed into 32-row
 //             warp bins (a set never straddles a warp), 4 bins per tile.
-// D^2(q, v) = |q|^2 + |v|^2 - 2 S_q S_db g(q, v), g the fp16 Gram.
+// The squared norm of every database row rides in the MMA as one extra K = 16
+// chunk (SWIZZLE_32B): the database row carries (h, l) = the fp16 split of
+// |v|^2 / S_db^2, the query row carries (alpha, alpha) with alpha = -S_db / (2 S_q)
+// (powers of two, exact), so the accumulator is
+//     acc(q, v) = sum_k (q_k / S_q)(v_k / S_db) + alpha (h + l)
+// and D^2(q, v) = |q|^2 + kappa acc(q, v), kappa = -2 S_q S_db < 0.  Hence
+// min_v D^2 = |q|^2 + kappa max_v acc: one FMNMX per accumulator value.
 //
 // Epilogue (12 warps, three per TMEM lane quarter; lane = query row, column =
 // database row; sets of a tile alternate between the warps of a quarter):
-//   per database set V and lane q:   r_q = max(0, min_v D^2(q, v))  (lane-local)
+//   per database set V and lane q:   r_q = max(0, |q|^2 + kappa max_v acc)  (lane-local)
 //   A(Q, V) = max_{q in Q} r_q  is a lower bound of H^2(Q, V) = max(A, B).
 // Branch and bound per query: tau_Q = the k-th smallest upper bound (H2c + E)
 // among the sets seen so far (a list of k per (query, range, epilogue warp) in
@@ -67,10 +73,25 @@ constexpr int kInfoSlotsD = 4;
 constexpr int kDenseMaxStages = 8;
 constexpr uint32_t kAChunkBytes = kDenseM * 128;  // one 64-element K chunk of the query tile (16 KB)
 constexpr uint32_t kBChunkBytes = kDenseN * 128;  // one K chunk of a database tile (30 KB, 1024-aligned)
+constexpr uint32_t kAAugBytes = kDenseM * 32;     // the query tile's norm chunk (K = 16 halves = 32 B rows)
+constexpr uint32_t kBAugBytes = kDenseN * 32;     // a database tile's norm chunk (7.5 KB)
+
+// SWIZZLE_32B K-major descriptor (8-row atoms of 8 x 32 B, SBO = 256 B; layout type 6, version 1)
+__device__ __forceinline__ uint64_t sw32_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>(1u) << 16;
+  d |= static_cast<uint64_t>(256u >> 4) << 32;
+  d |= static_cast<uint64_t>(1u) << 46;
+  d |= static_cast<uint64_t>(6u) << 61;
+  return d;
+}
 
 struct DenseArgs {
   CUtensorMap tmA;              // qd [ntq*128][dpad] fp16, box {64, 128}, SWIZZLE_128B
   CUtensorMap tmB;              // hd [nvec][dpad] fp16, box {64, 240}, SWIZZLE_128B
+  CUtensorMap tmAa;             // qa [128][16] fp16 (alpha, alpha, 0...), box {16, 128}, SWIZZLE_32B
+  CUtensorMap tmBa;             // va [nvec][16] fp16 (h, l, 0...), box {16, 240}, SWIZZLE_32B
   int KC;                       // dpad / 64
   int stages;
   int ntq;                      // query tiles
@@ -79,12 +100,11 @@ struct DenseArgs {
   const int32_t* tile_s0;       // [ntiles] first set of each tile
   const int32_t* tile_s1;       // [ntiles] one past the last set
   const int64_t* off;           // [n+1]
-  const float* vn;              // [nvec] squared norms
   const int32_t* lane_qid;      // [ntq*128] query of each packed row, -1 = padding
   const float* lane_qn;         // [ntq*128] squared norm of each packed row
   const float* qE;              // [nq] squared-distance error bound of each query
   const float* tau0;            // [nq] initial tau (an upper bound on the k-th H^2; +inf if none)
-  float cneg;                   // -2 S_q S_db
+  float kappa;                  // -2 S_q S_db
   int k;
   float* lists;                 // [nq][R][kEpiSub][k] sorted upper bounds, +inf-initialised
   int32_t* cnt;                 // [nq] emitted candidates (may exceed cap: overflow)
@@ -98,10 +118,9 @@ struct DenseArgs {
 };
 
 // per-tile metadata the info warp stages for the epilogue (shared memory): the database sets of the tile
-// (first set id, count, column and size of each) and the squared norm of every column
+// (first set id, count, column and size of each)
 struct DenseInfo {
   int s0, nsets, pad0, pad1;
-  float vn[kDenseN];
   int16_t col0[kDenseN];
   int16_t mv[kDenseN];
 };
@@ -154,7 +173,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
   __shared__ DenseCtl S;
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t a_s = smem_u32(base);                                  // KC x 16 KB query tile
-  const uint32_t ring_s = a_s + static_cast<uint32_t>(a.KC) * kAChunkBytes;  // stages x 32 KB
+  const uint32_t aa_s = a_s + static_cast<uint32_t>(a.KC) * kAChunkBytes;  // 4 KB norm chunk of the query tile
+  const uint32_t ring_s = aa_s + kAAugBytes;                               // stages x 30 KB
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int NST = a.stages;
   if (tid == 0) {
@@ -188,19 +208,25 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
       const int qt = u / a.R, r = u % a.R;
       tc::mbar_wait(&S.a_empty, (ua & 1u) ^ 1u);
       if (lane == 0) {
-        expect_tx(&S.a_full, static_cast<uint32_t>(a.KC) * kAChunkBytes);
+        expect_tx(&S.a_full, static_cast<uint32_t>(a.KC) * kAChunkBytes + kAAugBytes);
         for (int kc = 0; kc < a.KC; ++kc) tma_2d(a_s + kc * kAChunkBytes, &a.tmA, kc * 64, qt * kDenseM, &S.a_full);
+        tma_2d(aa_s, &a.tmAa, 0, 0, &S.a_full);
       }
       int t0, t1;
       range_tiles(r, a.R, a.ntiles, &t0, &t1);
       for (int t = t0; t < t1; ++t) {
         const int row0 = static_cast<int>(a.off[a.tile_s0[t]]);
-        for (int kc = 0; kc < a.KC; ++kc, ++stage_ctr) {
+        for (int kc = 0; kc <= a.KC; ++kc, ++stage_ctr) {  // kc == KC: the norm chunk
           const uint32_t st = stage_ctr % NST;
           tc::mbar_wait(&S.empty[st], ((stage_ctr / NST) & 1u) ^ 1u);
           if (lane == 0) {
-            expect_tx(&S.full[st], kBChunkBytes);
-            tma_2d(ring_s + st * kBChunkBytes, &a.tmB, kc * 64, row0, &S.full[st]);
+            if (kc < a.KC) {
+              expect_tx(&S.full[st], kBChunkBytes);
+              tma_2d(ring_s + st * kBChunkBytes, &a.tmB, kc * 64, row0, &S.full[st]);
+            } else {
+              expect_tx(&S.full[st], kBAugBytes);
+              tma_2d(ring_s + st * kBChunkBytes, &a.tmBa, 0, row0, &S.full[st]);
+            }
           }
           __syncwarp();
         }
@@ -221,18 +247,23 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
         tc::mbar_wait(&S.tempty[acc], ((tile_ctr >> 1) & 1u) ^ 1u);
         tc::fence_after_sync();
         const uint32_t d_tmem = tmem + acc * kDenseN;
-        for (int kc = 0; kc < a.KC; ++kc, ++stage_ctr) {
+        for (int kc = 0; kc <= a.KC; ++kc, ++stage_ctr) {
           const uint32_t st = stage_ctr % NST;
           tc::mbar_wait(&S.full[st], (stage_ctr / NST) & 1u);
           tc::fence_after_sync();
           if (lane == 0) {
-            const uint32_t as = a_s + kc * kAChunkBytes, bs = ring_s + st * kBChunkBytes;
+            const uint32_t bs = ring_s + st * kBChunkBytes;
+            if (kc < a.KC) {
+              const uint32_t as = a_s + kc * kAChunkBytes;
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-              tc::umma_bf16(d_tmem, tc::sw128_desc(as + kk * 32u), tc::sw128_desc(bs + kk * 32u), idesc,
-                            (kc | kk) ? 1u : 0u);
+              for (int kk = 0; kk < 4; ++kk)
+                tc::umma_bf16(d_tmem, tc::sw128_desc(as + kk * 32u), tc::sw128_desc(bs + kk * 32u), idesc,
+                              (kc | kk) ? 1u : 0u);
+            } else {  // + alpha (h + l): the database row norms
+              tc::umma_bf16(d_tmem, sw32_desc(aa_s), sw32_desc(bs), idesc, 1u);
+            }
             tc::umma_commit(&S.empty[st]);
-            if (kc == a.KC - 1) tc::umma_commit(&S.tfull[acc]);
+            if (kc == a.KC) tc::umma_commit(&S.tfull[acc]);
           }
           __syncwarp();
         }
@@ -252,13 +283,6 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
         DenseInfo& inf = S.info[slot];
         const int s0 = a.tile_s0[t], s1 = a.tile_s1[t];
         const int64_t row0 = a.off[s0];
-        const int64_t rows = a.off[s1] - row0;
-        float vn[(kDenseN + 31) / 32];
-#pragma unroll
-        for (int c = 0; c < (kDenseN + 31) / 32; ++c) {
-          const int j = lane + 32 * c;
-          vn[c] = (j < rows) ? __ldg(a.vn + row0 + j) : 0.0f;
-        }
         int16_t cl[(kDenseN + 31) / 32], ml[(kDenseN + 31) / 32];
 #pragma unroll
         for (int c = 0; c < (kDenseN + 31) / 32; ++c) {
@@ -276,7 +300,6 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
         for (int c = 0; c < (kDenseN + 31) / 32; ++c) {
           const int j = lane + 32 * c;
           if (j < kDenseN) {
-            inf.vn[j] = vn[c];
             inf.col0[j] = cl[c];
             inf.mv[j] = ml[c];
           }
@@ -329,25 +352,27 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
           const int i = s0 + js;
           const int col0 = inf.col0[js];
           const int mv = inf.mv[js];
-          float run0 = INF, run1 = INF;
+          float run0 = -INF, run1 = -INF;  // max_v acc (kappa < 0: the min over v of D^2)
           for (int j0 = 0; j0 < mv; j0 += 32) {
-            // columns past the set get |v|^2 = +inf, so they never win the min; branches only every 8
-            // columns, so the shuffles and FMAs of a group issue back to back (two independent min chains)
-            const float vnl = (j0 + lane < mv) ? inf.vn[col0 + j0 + lane] : INF;
             uint32_t g[32];
             tmem_ld32(tb + static_cast<uint32_t>(col0 + j0), g);
             tc::tmem_ld_wait();
 #pragma unroll
-            for (int j8 = 0; j8 < 32; j8 += 8) {
+            for (int j8 = 0; j8 < 32; j8 += 8) {  // whole groups of 8 columns without tests, then the tail
               if (j0 + j8 >= mv) break;
+              if (j0 + j8 + 8 <= mv) {
 #pragma unroll
-              for (int j = j8; j < j8 + 8; j += 2) {
-                run0 = fminf(run0, fmaf(__uint_as_float(g[j]), a.cneg, __shfl_sync(0xffffffffu, vnl, j)));
-                run1 = fminf(run1, fmaf(__uint_as_float(g[j + 1]), a.cneg, __shfl_sync(0xffffffffu, vnl, j + 1)));
+                for (int j = j8; j < j8 + 8; j += 2) {
+                  run0 = fmaxf(run0, __uint_as_float(g[j]));
+                  run1 = fmaxf(run1, __uint_as_float(g[j + 1]));
+                }
+              } else {
+#pragma unroll
+                for (int j = j8; j < j8 + 8; ++j) run0 = fmaxf(run0, j0 + j < mv ? __uint_as_float(g[j]) : -INF);
               }
             }
           }
-          const float rq = fmaxf(fminf(run0, run1) + qn, 0.0f);
+          const float rq = fmaxf(fmaf(a.kappa, fmaxf(run0, run1), qn), 0.0f);
           const unsigned pass = __ballot_sync(0xffffffffu, !valid || rq <= thr);
           unsigned sb = __ballot_sync(0xffffffffu, valid && (pass & segmask) == segmask);
           while (sb) {  // warp-uniform: one surviving query segment at a time
@@ -364,8 +389,6 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
             const float A = __uint_as_float(__reduce_max_sync(0xffffffffu, inseg ? __float_as_uint(rq) : 0u));
             float B = 0.0f;
             for (int j0 = 0; j0 < mv; j0 += 32) {
-              // columns past the set: |v|^2 = -inf, D^2 clamps to 0 and never raises the max
-              const float vnl = (j0 + lane < mv) ? inf.vn[col0 + j0 + lane] : -INF;
               uint32_t g[32];
               tmem_ld32(tb + static_cast<uint32_t>(col0 + j0), g);
               tc::tmem_ld_wait();
@@ -373,9 +396,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
               for (int j8 = 0; j8 < 32; j8 += 8) {
                 if (j0 + j8 >= mv) break;
 #pragma unroll
-                for (int j = j8; j < j8 + 8; ++j) {
-                  const float vnj = __shfl_sync(0xffffffffu, vnl, j);
-                  const float d2 = fmaxf(fmaf(__uint_as_float(g[j]), a.cneg, vnj) + qn, 0.0f);
+                for (int j = j8; j < j8 + 8; ++j) {  // columns past the set contribute 0 (never raise the max)
+                  const float d2 = (j0 + j < mv) ? fmaxf(fmaf(a.kappa, __uint_as_float(g[j]), qn), 0.0f) : 0.0f;
                   const uint32_t cm = __reduce_min_sync(0xffffffffu, inseg ? __float_as_uint(d2) : 0xffffffffu);
                   B = fmaxf(B, __uint_as_float(cm));
                 }
@@ -443,6 +465,21 @@ __global__ void dense_db_operand_kernel(const float* __restrict__ V, int64_t nve
   }
 }
 
+// the norm chunk of the database operand: va[v] = (h, l, 0 x 14), h + l = the fp16 split of |v|^2 / S_db^2
+__global__ void dense_norm_operand_kernel(const float* __restrict__ vn, int64_t nvec, float inv_s2,
+                                          __half* __restrict__ va) {
+  for (int64_t v = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; v < nvec;
+       v += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float x = vn[v] * inv_s2;
+    const __half h = __float2half_rn(x);
+    const __half l = __float2half_rn(x - __half2float(h));
+    __half2* row = reinterpret_cast<__half2*>(va + v * 16);
+    row[0] = __halves2half2(h, l);
+#pragma unroll
+    for (int i = 1; i < 8; ++i) row[i] = __float2half2_rn(0.0f);
+  }
+}
+
 // packed query rows: qd[row] = fp16(q / S_q) (zero rows for padding), lane meta
 __global__ void dense_query_operand_kernel(const float* __restrict__ Qv, const float* __restrict__ qnorm,
                                            const int32_t* __restrict__ rowmap /*[rows]: query vector or -1*/,
@@ -499,7 +536,8 @@ __global__ void dense_append_huge_kernel(const int32_t* __restrict__ huge, int n
 }
 
 // ------------------------------------------------------------------ host --
-static int encode_map(CUtensorMap* map, const void* base, int64_t rows, int dpad, int box_rows) {
+static int encode_map(CUtensorMap* map, const void* base, int64_t rows, int dpad, int box_rows, int box_cols = 64,
+                      CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -510,10 +548,10 @@ static int encode_map(CUtensorMap* map, const void* base, int64_t rows, int dpad
   }
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(dpad), static_cast<cuuint64_t>(rows)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(dpad) * 2};
-  const cuuint32_t box[2] = {64, static_cast<cuuint32_t>(box_rows)};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) BVSS_FAIL(BVSS_ECUDA, "cuTensorMapEncodeTiled failed (%d)", static_cast<int>(r));
   return BVSS_OK;
@@ -525,7 +563,7 @@ int dense_epi_sub() { return kEpiSub; }
 // stages that fit next to a query tile of KC chunks
 static int dense_stages(int KC, size_t* smem) {
   const size_t budget = 227 * 1024 - sizeof(DenseCtl) - 1024;  // static shared memory (DenseCtl, 1 KB aligned)
-  const size_t fixed = 1024 + static_cast<size_t>(KC) * kAChunkBytes;
+  const size_t fixed = 1024 + static_cast<size_t>(KC) * kAChunkBytes + kAAugBytes;
   if (fixed + 2 * kBChunkBytes > budget) return 0;
   int st = static_cast<int>((budget - fixed) / kBChunkBytes);
   if (st > kDenseMaxStages) st = kDenseMaxStages;
@@ -538,6 +576,12 @@ int launch_dense_db_operand(const float* V, int64_t nvec, int d, int dpad, float
   if (nvec <= 0) return BVSS_OK;
   dense_db_operand_kernel<<<num_sms * 16, 256, 0, st>>>(V, nvec, d, dpad, inv_s, hd);
   return post_launch("dense_db_operand_kernel", st);
+}
+
+int launch_dense_norm_operand(const float* vn, int64_t nvec, float inv_s2, __half* va, int num_sms, cudaStream_t st) {
+  if (nvec <= 0) return BVSS_OK;
+  dense_norm_operand_kernel<<<num_sms * 8, 256, 0, st>>>(vn, nvec, inv_s2, va);
+  return post_launch("dense_norm_operand_kernel", st);
 }
 
 int launch_dense_query_operand(const float* Qv, const float* qnorm, const int32_t* rowmap, const int32_t* rowq,
@@ -563,9 +607,10 @@ int launch_dense_prep(const int64_t* qoff, const float* qnorm, int nq, float c1,
 }
 
 int launch_dense_hausdorff(const __half* qd, int ntq, const __half* hd, int64_t nvec, int dpad, int ntiles,
-                           const int32_t* tile_s0, const int32_t* tile_s1, const int64_t* off, const float* vn,
+                           const int32_t* tile_s0, const int32_t* tile_s1, const int64_t* off, const __half* va,
+                           const __half* qa,
                            const int32_t* lane_qid, const float* lane_qn, const float* qE, const float* tau0,
-                           float cneg, int k, int R, float* lists, int32_t* cnt, int32_t* ids, float* vals, int cap,
+                           float kappa, int k, int R, float* lists, int32_t* cnt, int32_t* ids, float* vals, int cap,
                            const uint32_t* mask, int64_t mask_stride, int64_t id_base, unsigned long long* stat,
                            int num_sms, cudaStream_t st) {
   if (ntq <= 0 || ntiles <= 0) return BVSS_OK;
@@ -574,6 +619,8 @@ int launch_dense_hausdorff(const __half* qd, int ntq, const __half* hd, int64_t 
   std::memset(&a, 0, sizeof(a));
   BVSS_TRY(encode_map(&a.tmA, qd, static_cast<int64_t>(ntq) * kDenseM, dpad, kDenseM));
   BVSS_TRY(encode_map(&a.tmB, hd, nvec, dpad, kDenseN));
+  BVSS_TRY(encode_map(&a.tmAa, qa, kDenseM, 16, kDenseM, 16, CU_TENSOR_MAP_SWIZZLE_32B));
+  BVSS_TRY(encode_map(&a.tmBa, va, nvec, 16, kDenseN, 16, CU_TENSOR_MAP_SWIZZLE_32B));
   a.KC = dpad / 64;
   size_t smem = 0;
   a.stages = dense_stages(a.KC, &smem);
@@ -584,12 +631,11 @@ int launch_dense_hausdorff(const __half* qd, int ntq, const __half* hd, int64_t 
   a.tile_s0 = tile_s0;
   a.tile_s1 = tile_s1;
   a.off = off;
-  a.vn = vn;
   a.lane_qid = lane_qid;
   a.lane_qn = lane_qn;
   a.qE = qE;
   a.tau0 = tau0;
-  a.cneg = cneg;
+  a.kappa = kappa;
   a.k = k;
   a.lists = lists;
   a.cnt = cnt;
