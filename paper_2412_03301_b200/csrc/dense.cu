@@ -157,6 +157,55 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "memory");
 }
 
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr)
+               : "memory");
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) { return fmaxf(a, fmaxf(b, c)); }  // FMNMX3
+
+// max over the first mvc (1..32) TMEM columns at taddr of this lane's row, with no per-column tests: whole
+// groups of 8 from one 32-column load, and the last 8 columns of the run (overlapping the groups: max is
+// idempotent) from a second 8-column load; runs shorter than 8 take a switch over the count
+__device__ __forceinline__ float set_max(uint32_t taddr, int mvc) {
+  const float NINF = __int_as_float(0xff800000);
+  float m = NINF;
+  if (mvc >= 8) {
+    uint32_t g[32], t[8];
+    tmem_ld32(taddr, g);
+    tmem_ld8(taddr + static_cast<uint32_t>(mvc - 8), t);
+    tc::tmem_ld_wait();
+#define BVSS_MAX8(R, o)                                                                        \
+  m = fmax3(m, __uint_as_float(R[o]), __uint_as_float(R[o + 1]));                            \
+  m = fmax3(m, __uint_as_float(R[o + 2]), __uint_as_float(R[o + 3]));                        \
+  m = fmax3(m, __uint_as_float(R[o + 4]), __uint_as_float(R[o + 5]));                        \
+  m = fmax3(m, __uint_as_float(R[o + 6]), __uint_as_float(R[o + 7]));
+    switch (mvc >> 3) {
+      case 4: BVSS_MAX8(g, 24) [[fallthrough]];
+      case 3: BVSS_MAX8(g, 16) [[fallthrough]];
+      case 2: BVSS_MAX8(g, 8) [[fallthrough]];
+      default: BVSS_MAX8(g, 0)
+    }
+    BVSS_MAX8(t, 0)
+#undef BVSS_MAX8
+  } else {
+    uint32_t t[8];
+    tmem_ld8(taddr, t);
+    tc::tmem_ld_wait();
+    switch (mvc) {
+      case 7: m = fmaxf(m, __uint_as_float(t[6])); [[fallthrough]];
+      case 6: m = fmaxf(m, __uint_as_float(t[5])); [[fallthrough]];
+      case 5: m = fmaxf(m, __uint_as_float(t[4])); [[fallthrough]];
+      case 4: m = fmaxf(m, __uint_as_float(t[3])); [[fallthrough]];
+      case 3: m = fmaxf(m, __uint_as_float(t[2])); [[fallthrough]];
+      case 2: m = fmaxf(m, __uint_as_float(t[1])); [[fallthrough]];
+      default: m = fmaxf(m, __uint_as_float(t[0]));
+    }
+  }
+  return m;
+}
+
 __device__ __forceinline__ float vload_volatile(const float* p) {
   float v;
   asm volatile("ld.volatile.global.f32 %0, [%1];" : "=f"(v) : "l"(p));
@@ -352,27 +401,9 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
           const int i = s0 + js;
           const int col0 = inf.col0[js];
           const int mv = inf.mv[js];
-          float run0 = -INF, run1 = -INF;  // max_v acc (kappa < 0: the min over v of D^2)
-          for (int j0 = 0; j0 < mv; j0 += 32) {
-            uint32_t g[32];
-            tmem_ld32(tb + static_cast<uint32_t>(col0 + j0), g);
-            tc::tmem_ld_wait();
-#pragma unroll
-            for (int j8 = 0; j8 < 32; j8 += 8) {  // whole groups of 8 columns without tests, then the tail
-              if (j0 + j8 >= mv) break;
-              if (j0 + j8 + 8 <= mv) {
-#pragma unroll
-                for (int j = j8; j < j8 + 8; j += 2) {
-                  run0 = fmaxf(run0, __uint_as_float(g[j]));
-                  run1 = fmaxf(run1, __uint_as_float(g[j + 1]));
-                }
-              } else {
-#pragma unroll
-                for (int j = j8; j < j8 + 8; ++j) run0 = fmaxf(run0, j0 + j < mv ? __uint_as_float(g[j]) : -INF);
-              }
-            }
-          }
-          const float rq = fmaxf(fmaf(a.kappa, fmaxf(run0, run1), qn), 0.0f);
+          float m = -INF;  // max_v acc (kappa < 0: the min over v of D^2)
+          for (int j0 = 0; j0 < mv; j0 += 32) m = fmaxf(m, set_max(tb + static_cast<uint32_t>(col0 + j0), min(32, mv - j0)));
+          const float rq = fmaxf(fmaf(a.kappa, m, qn), 0.0f);
           const unsigned pass = __ballot_sync(0xffffffffu, !valid || rq <= thr);
           unsigned sb = __ballot_sync(0xffffffffu, valid && (pass & segmask) == segmask);
           while (sb) {  // warp-uniform: one surviving query segment at a time
