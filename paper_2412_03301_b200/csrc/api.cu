@@ -812,7 +812,7 @@ int ensure_dense(bvss_index* idx) {
 // the dense path takes a batch when every query set fits one 32-lane warp of the query tile, the metric is
 // Hausdorff and d fits the resident query tile
 bool dense_supported(const bvss_index* idx, const bvss_search_ctx* c) {
-  return idx->metric == 0 && idx->terms != 0 && idx->dpad <= dense_max_dpad() && c->max_mq <= 32;
+  return idx->metric == 0 && idx->terms != 0 && idx->dpad <= dense_max_dpad() && c->max_mq <= 32 && c->k <= 32;
 }
 
 // BVSS_DENSE: 0 = never, 1 = whenever supported, unset = auto (the candidate budget is a large fraction of

@@ -121,6 +121,7 @@ struct DenseArgs {
 // (first set id, count, column and size of each)
 struct DenseInfo {
   int s0, nsets, pad0, pad1;
+  int ctr[4];  // next set of each TMEM lane quarter (dynamic split among the quarter's epilogue warps)
   int16_t col0[kDenseN];
   int16_t mv[kDenseN];
 };
@@ -357,6 +358,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
           inf.s0 = s0;
           inf.nsets = s1 - s0;
         }
+        if (lane < 4) inf.ctr[lane] = kEpiSub;  // sets 0 .. kEpiSub-1 go to the warps statically
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&S.info_full[slot]);
       }
@@ -367,6 +369,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
     const int sub = (warp - 2) >> 2;  // 0 .. kEpiSub-1: the quarter's warps take alternate sets
     const float INF = __int_as_float(0x7f800000);
     uint32_t tile_ctr = 0;
+    unsigned long long n_surv = 0, n_emit = 0;  // statistics, flushed once (a per-survivor global atomic on one
+                                                // address would serialise in L2)
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int qt = u / a.R, r = u % a.R;
       const int prow = qt * kDenseM + quarter * 32 + lane;
@@ -376,7 +380,6 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
       const unsigned segmask = __match_any_sync(0xffffffffu, qid);
       const float E = valid ? a.qE[qid] : 0.0f;
       const float* lq = valid ? a.lists + (static_cast<int64_t>(qid) * a.R + r) * kEpiSub * a.k : nullptr;
-      float* own = valid ? const_cast<float*>(lq) + sub * a.k : nullptr;
       float tau = valid ? a.tau0[qid] : INF;
       float other_k = INF;  // the other warps' k-th bounds, loaded one tile ahead (their latency stays hidden)
       int t0, t1;
@@ -397,7 +400,9 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
         tc::fence_after_sync();
         const int s0 = inf.s0, nsets = inf.nsets;
         const uint32_t tb = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * kDenseN;
-        for (int js = sub; js < nsets; js += kEpiSub) {
+        for (int js = sub; js < nsets;) {
+          int nxt = 0;  // the next set of this warp (taken now: the shared-memory atomic's latency overlaps the set)
+          if (lane == 0) nxt = atomicAdd(const_cast<int*>(&inf.ctr[quarter]), 1);
           const int i = s0 + js;
           const int col0 = inf.col0[js];
           const int mv = inf.mv[js];
@@ -435,37 +440,38 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
               }
             }
             const float h = fmaxf(A, B);
-            float newtau = tau;  // (uniform over the segment; taken from the leader below)
-            if (lane == leader) {
-              const float ub = h + E;
-              if (ub < tau) {  // insert into this warp's sorted list of k upper bounds
-                int p = a.k - 1;
-                while (p > 0 && own[p - 1] > ub) {
-                  own[p] = own[p - 1];
-                  --p;
-                }
-                own[p] = ub;
-                newtau = own[a.k - 1];
-#pragma unroll
-                for (int o = 1; o < kEpiSub; ++o)
-                  newtau = fminf(newtau, vload_volatile(lq + ((sub + o) % kEpiSub) * a.k + a.k - 1));
-              }
-              if (h - E <= newtau) {
-                const int slot = atomicAdd(a.cnt + q, 1);
-                if (slot < a.cap) {
-                  a.ids[static_cast<int64_t>(q) * a.cap + slot] = static_cast<int32_t>(a.id_base + i);
-                  a.vals[static_cast<int64_t>(q) * a.cap + slot] = h;
-                }
-                if (a.stat) atomicAdd(a.stat + 1, 1ull);
-              }
-              if (a.stat) atomicAdd(a.stat, 1ull);
+            const float Eq = __shfl_sync(0xffffffffu, E, leader);
+            const float tq = __shfl_sync(0xffffffffu, tau, leader);
+            const float ub = h + Eq;
+            float newtau = tq;
+            ++n_surv;
+            if (ub < tq) {  // warp-uniform: insert ub into this warp's sorted list of k bounds, lane-parallel
+              const float* lqq = a.lists + (static_cast<int64_t>(q) * a.R + r) * kEpiSub * a.k;
+              float* ownq = const_cast<float*>(lqq) + sub * a.k;
+              const float old = lane < a.k ? ownq[lane] : INF;
+              const float oth = lane < kEpiSub - 1 ? vload_volatile(lqq + ((sub + 1 + lane) % kEpiSub) * a.k + a.k - 1)
+                                                   : INF;
+              const int pos = __popc(__ballot_sync(0xffffffffu, lane < a.k && old <= ub));
+              const float up = __shfl_up_sync(0xffffffffu, old, 1);
+              const float nw = lane < pos ? old : (lane == pos ? ub : up);
+              if (lane < a.k) ownq[lane] = nw;
+              const float kth = __shfl_sync(0xffffffffu, nw, a.k - 1);
+              newtau = fminf(kth, __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(oth))));
             }
-            newtau = __shfl_sync(0xffffffffu, newtau, leader);
+            if (lane == leader && h - Eq <= newtau) {
+              const int slot = atomicAdd(a.cnt + q, 1);
+              if (slot < a.cap) {
+                a.ids[static_cast<int64_t>(q) * a.cap + slot] = static_cast<int32_t>(a.id_base + i);
+                a.vals[static_cast<int64_t>(q) * a.cap + slot] = h;
+              }
+              ++n_emit;
+            }
             if (inseg) {
               tau = newtau;
               thr = tau + E;
             }
           }
+          js = __shfl_sync(0xffffffffu, nxt, 0);
         }
         tc::fence_before_sync();
         __syncwarp();
@@ -474,6 +480,12 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
           tc::mbar_arrive(&S.info_empty[slot]);
         }
       }
+    }
+    unsigned int ne = static_cast<unsigned int>(n_emit);
+    ne = __reduce_add_sync(0xffffffffu, ne);  // emissions were counted by the segment leaders
+    if (a.stat && lane == 0) {
+      atomicAdd(a.stat, n_surv);
+      atomicAdd(a.stat + 1, static_cast<unsigned long long>(ne));
     }
   }
   __syncthreads();
