@@ -55,7 +55,9 @@ typedef enum {
   BVSS_ENOMEM = -3,       /* device or host allocation failed */
   BVSS_ECUDA = -4,        /* a CUDA runtime error (message has the CUDA error string) */
   BVSS_EUNSUPPORTED = -5, /* no sm_100 device, or a size beyond this build's limits */
-  BVSS_ESTATE = -6        /* call out of order (e.g. distributed phases) */
+  BVSS_ESTATE = -6,       /* call out of order (e.g. distributed phases) */
+  BVSS_ENCCL = -7         /* reserved for a collective failure; the sharded phases below leave the collectives
+                             to the caller (torch.distributed / NCCL), whose errors surface there */
 } bvss_status;
 
 typedef enum { BVSS_SKETCH_BINARY = 0, BVSS_SKETCH_COUNT_U8 = 1 } bvss_sketch_kind;

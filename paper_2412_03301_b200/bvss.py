@@ -18,7 +18,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BVSS_LIB") or os.path.join(_HERE, "libbvss.so")  # BVSS_LIB: developer A/B of builds
 
-OK, EINVAL, ENONFINITE, ENOMEM, ECUDA, EUNSUPPORTED, ESTATE = 0, -1, -2, -3, -4, -5, -6
+OK, EINVAL, ENONFINITE, ENOMEM, ECUDA, EUNSUPPORTED, ESTATE, ENCCL = 0, -1, -2, -3, -4, -5, -6, -7
 SKETCH_BINARY, SKETCH_COUNT_U8 = 0, 1
 DEVICE_PTRS, VALIDATE_FINITE, KEEP_CODES = 0x1, 0x2, 0x4
 

@@ -1806,6 +1806,21 @@ int bvss_dist_finish(bvss_search_ctx* c, const int64_t* all_eq_dev, int32_t worl
   bvss_index* idx = c->idx;
   DeviceGuard g(idx->device);
   BVSS_TRY(launch_select_quota(c->sel, all_eq_dev, static_cast<int>(c->nq), world, rank, idx->stream));
+  if (dense_wanted(idx, c->teff / world) && dense_supported(idx, c)) {
+    // large global budget: this rank's share of the global top-T as a bitmap over its shard, then the
+    // candidate-major refine of the shard (the same kernels as the single-GPU search at this T)
+    const int key_size = idx->sketch == BVSS_SKETCH_BINARY ? 2 : 4;
+    const int64_t words = (idx->n + 31) / 32;
+    uint32_t* mask;
+    BVSS_TRY(c->alloc(static_cast<size_t>(c->nq) * words * 4, reinterpret_cast<void**>(&mask)));
+    BVSS_CUDA(cudaMemsetAsync(mask, 0, static_cast<size_t>(c->nq) * words * 4, idx->stream));
+    BVSS_TRY(launch_select_bitmap(key_size, c->keys, c->key_stride, idx->n, static_cast<int>(c->nq), c->sel, c->T,
+                                  mask, words, idx->stream));
+    cudaEventRecord(idx->ev[3], idx->stream);
+    bool done = false;
+    BVSS_TRY(dense_refine_topk(idx, c, mask, words, -1, topk_ids_dev, topk_dist_dev, &done));
+    if (done) return BVSS_OK;
+  }
   BVSS_TRY(emit_candidates(idx, c));
   BVSS_TRY(refine_topk(idx, c, topk_ids_dev, topk_dist_dev));
   return BVSS_OK;
