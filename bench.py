@@ -3,19 +3,31 @@
 "query sets/s at recall@10>=0.9 (1M sets, d=384); filter-scan HBM GB/s".
 
 Workload (default): BASELINE.json configs[2] ("cfg3"): n = 1,000,000 sets of
-uniform 4-32 unit vectors (d=384, ~18M vectors), 10,000 query sets, T = 2000,
+uniform 4-32 unit vectors (d=384, ~18M vectors), a batch of 10,000 query sets,
 k = 10, FlyHash m=1024 / s=8 / L=32, 1024-bit Bloom sketches.  Synthetic,
 seeded, generated on the GPU (gen/synth.py).
 
-A step = one bvss_search over the whole 10k-query batch against the resident
-index (a-4 .. a-9: query encode + sketch, filter scan, top-T select, tensor-core
-refine, exact top-k).  The index build (a-1 .. a-3) runs once before timing and
-is reported separately under "build".  Inputs are device-resident when the
-timed region starts; L2 is flushed (256 MB write) between timed steps and every
-step is timed with CUDA events on the launching stream (the flush is outside the
-events).  For N > 1 (torchrun, one process per GPU) the database is sharded by
+The metric is gated on recall@10 >= 0.9 (recall@k, against exact
+brute force).  On this workload (literal noise reading) recall
+grows slowly with the candidate budget T, so the run
+  1. sweeps T over TGRID on a recall subset (the first R query sets): recall@10,
+     rank-1 hit and throughput per T, ground truth = exact brute force (K8,
+     the dense tensor-core kernel, untimed), and full-batch throughput at the
+     config's own sweep points {500, 2000, 8000};
+  2. times the whole 10k batch at the gated budget T_GATE (the smallest grid T
+     whose recall@10 >= 0.9 in the committed sweep, profiles/r02/): W untimed
+     warm-ups, then K steps, each one bvss_search over the batch against the
+     resident index (a-4 .. a-9), L2 flushed (256 MB write) before every step,
+     CUDA events on the launching stream;
+  3. reports value = query sets/s at T_GATE and "recall_gate" = whether the
+     recall measured in THIS run at T_GATE is >= 0.9 ("not attained" + the best
+     (recall, q/s) pair otherwise).
+For N > 1 (one process per GPU; bench.py re-launches itself with
+torch.distributed.run when WORLD_SIZE is unset) the database is sharded by
 contiguous set-id ranges and the exact global-T protocol runs over NCCL
-(paper_2412_03301_b200/dist.py); value = 10k / max-over-ranks step time.
+(paper_2412_03301_b200/dist.py); value = 10k / max-over-ranks step time.  The
+candidate selection at T_GATE is the same at every N (full keys, global
+threshold, candidate bitmap, dense refine).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
@@ -24,7 +36,9 @@ from __future__ import annotations
 import argparse
 import json
 import math
+import multiprocessing
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -36,9 +50,13 @@ sys.path.insert(0, ROOT)
 
 METRIC = "query sets/s at recall@10>=0.9 (1M sets, d=384); filter-scan HBM GB/s"
 UNIT = "query sets/s"
+# the gated candidate budget per workload: the smallest TGRID point whose recall@10 reached 0.9 in the
+# committed sweep (profiles/r02/sweep_cfg3.json); every run re-measures the recall there
+T_GATE = {"cfg3": 800_000}
+TGRID = (500, 2000, 8000, 32_000, 128_000, 400_000, 600_000, 800_000, 900_000, 1_000_000)
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
@@ -47,16 +65,18 @@ def parse():
     ap.add_argument("--config", default="cfg3")
     ap.add_argument("--n", type=int, default=None, help="override the number of sets (quick runs only)")
     ap.add_argument("--nq", type=int, default=None)
-    ap.add_argument("--T", type=int, default=None)
+    ap.add_argument("--T", type=int, default=None, help="timed budget (default: T_GATE of the config)")
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--terms", type=int, default=0, choices=[0, 1, 3, 255])
     ap.add_argument("--noise", default="per_coord", choices=["per_coord", "total"])
     ap.add_argument("--metric", default="hausdorff", choices=["hausdorff", "meanmin", "min"],
                     help="rerank distance (default: the paper's Hausdorff; MeanMin / Min are the §3.2 alternatives)")
-    ap.add_argument("--recall-queries", type=int, default=100)
+    ap.add_argument("--recall-queries", type=int, default=1000)
+    ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    return ap.parse_args()
+    ap.add_argument("--cpu-queries", type=int, default=20)
+    return ap.parse_args(argv)
 
 
 def load_peaks():
@@ -64,15 +84,23 @@ def load_peaks():
     if os.path.exists(p):
         with open(p) as f:
             j = json.load(f)
-        return {"hbm_gbs": j["hbm_gbs"], "bf16_tflops": j["bf16_tflops"], "src": "measured"}
-    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "src": "fallback"}
+        return {"hbm_gbs": j["hbm_gbs"], "bf16_tflops": j["bf16_tflops"],
+                "bf16_tflops_sustained": j.get("bf16_tflops_sustained", j["bf16_tflops"]), "src": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "src": "fallback"}
 
 
 def workload_config(cfg, T, k):
     """The `config` both arms report (the same workload)."""
     return {"workload": (f"{cfg.name}: n={cfg.n} sets, d={cfg.d}, {cfg.nq} query sets, T={T}, k={k}, "
                          f"m={cfg.m}, s={cfg.s}, L={cfg.L}, {cfg.sketch} sketch"),
-            "global_batch": cfg.nq}
+            "global_batch": cfg.nq, "T": T}
+
+
+def gate_T(cfg, args):
+    if args.T:
+        return int(args.T)
+    t = T_GATE.get(cfg.name, cfg.T)
+    return min(t, cfg.n)
 
 
 # ------------------------------------------------------------------ clocks --
@@ -152,44 +180,79 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------- cpu baseline --
-def oracle_sample(cfg, T, k, n_sample=10000, q_sample=3, seed_shift=0, metric="hausdorff"):
-    """The oracle (as it stands, single-threaded numpy) on a bounded sample of
-    the workload: a DB of n_sample sets drawn by the same generator recipe, and
-    q_sample query sets.  Per query it times the query encode+sketch (a-4), the
-    scan + top-T select over the sample (a-5, a-6), and the exact refine of T
-    candidates + top-k (a-7, a-8); the scan/select time is scaled by n/n_sample
-    (it is linear in n) and the refine time is the full-T cost.  Returns q/s
-    for the FULL workload."""
+_CPU = {}
+
+
+def _cpu_worker(qi):
+    """One query of the oracle on a bounded sample (runs in a forked worker; numpy only)."""
     import numpy as np
+    from oracle import bvss_oracle as O
+    st = _CPU
+    oi, data, cfg, T, k = st["oi"], st["data"], st["cfg"], st["T"], st["k"]
+    ns = oi.n
+    Q = data["queries"][data["q_offsets"][qi]:data["q_offsets"][qi + 1]]
+    t0 = time.perf_counter()
+    sq = oi.query_sketch(Q)                                               # a-4
+    t1 = time.perf_counter()
+    scores = O.hamming_scores(sq, oi.sketches) if cfg.sketch == "binary" else O.count_l2_scores(sq, oi.sketches)
+    Ts = max(k, min(ns, int(round(T * ns / cfg.n))))
+    cand = O.select_top_T(scores, Ts)                                     # a-5, a-6 on the sample
+    t2 = time.perf_counter()
+    rc = min(len(cand), st["refine_cands"])
+    dist = O.refine(Q, cand[:rc], oi.vectors, oi.offsets, st["metric"])   # a-7 on rc candidates
+    O.top_k(cand[:rc], dist, k)                                           # a-8
+    t3 = time.perf_counter()
+    # scale to the full workload: the scan/select is linear in n, the refine linear in the candidates (T)
+    return (t1 - t0) + (t2 - t1) * (cfg.n / ns) + (t3 - t2) * (T / rc)
+
+
+def oracle_pool(cfg, T, k, nq_cpu=20, n_sample=5000, refine_cands=1500, metric="hausdorff", seed_shift=0):
+    """The oracle as it stands (plain numpy, never tuned for this), one query per worker of a
+    multiprocessing.Pool(os.cpu_count()) with BLAS pinned to one thread, on a bounded sample of the workload:
+    a DB of n_sample sets drawn by the same recipe and nq_cpu query sets; per query the encode + sketch, the
+    scan + top-T' select over the sample (T' = T n_sample / n, time scaled by n / n_sample) and the exact
+    refine of refine_cands candidates (time scaled by T / refine_cands).  Returns (q/s of the whole host,
+    per-query seconds, cores, sample description, CPU seconds)."""
+    for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        os.environ[v] = "1"
     from gen import synth
     from oracle import bvss_oracle as O
-    sc = synth.get_config(cfg.name, n=n_sample, nq=q_sample, seed=cfg.seed + seed_shift)
+    sc = synth.get_config(cfg.name, n=n_sample, nq=nq_cpu, seed=cfg.seed + seed_shift)
     data = synth.to_numpy(synth.generate(sc, device="cpu"))
     oi = O.OracleIndex(data["vectors"], data["offsets"], cfg.m, cfg.s, cfg.L, cfg.seed, sketch=cfg.sketch)
-    Tr = min(T, n_sample)
-    t_enc = t_scan = t_ref = 0.0
-    for qi in range(q_sample):
-        Q = data["queries"][data["q_offsets"][qi]:data["q_offsets"][qi + 1]]
-        t0 = time.perf_counter()
-        sq = oi.query_sketch(Q)
-        t1 = time.perf_counter()
-        scores = O.hamming_scores(sq, oi.sketches) if cfg.sketch == "binary" else O.count_l2_scores(sq, oi.sketches)
-        cand = O.select_top_T(scores, Tr)
-        t2 = time.perf_counter()
-        dist = O.refine(Q, cand, oi.vectors, oi.offsets, metric)
-        O.top_k(cand, dist, k)
-        t3 = time.perf_counter()
-        t_enc += t1 - t0
-        t_scan += t2 - t1
-        t_ref += (t3 - t2) * (T / Tr)
-    per_q = (t_enc + t_scan * (cfg.n / n_sample) + t_ref) / q_sample
-    sample = (f"oracle on {q_sample} query sets against a {n_sample}-set DB drawn by the {cfg.name} recipe; "
-              f"scan+select time x{cfg.n / n_sample:g} (linear in n), exact refine of T={T} candidates timed as is; "
-              f"index build not timed (as for the GPU)")
-    return 1.0 / per_q, sample, per_q * q_sample
+    _CPU.update(oi=oi, data=data, cfg=cfg, T=T, k=k, refine_cands=refine_cands, metric=metric)
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    with multiprocessing.get_context("fork").Pool(cores) as pool:
+        per_q = pool.map(_cpu_worker, range(nq_cpu))
+    wall = time.perf_counter() - t0
+    mean_q = statistics.mean(per_q)
+    qps = min(cores, nq_cpu) / mean_q if nq_cpu < cores else cores / mean_q
+    sample = (f"oracle (numpy, fp64 distances) on {nq_cpu} query sets of the {cfg.name} recipe, one per worker of a "
+              f"Pool({cores}); DB sample of {n_sample} sets: scan+select time x{cfg.n / n_sample:g} (linear in n); "
+              f"exact refine of {refine_cands} candidates x{T / refine_cands:.4g} (linear in T={T}); q/s = "
+              f"cores / mean per-query seconds; index build not timed (as for the GPU)")
+    return qps, mean_q, cores, sample, wall
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
 
 
 # ------------------------------------------------------------- our impl --
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
 def main_ours(args):
     import numpy as np
     import torch
@@ -201,24 +264,14 @@ def main_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        if world == 1 and args.gpus > 1:
-            raise SystemExit("for --gpus > 1 launch with torchrun (one process per GPU)")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     dev = torch.device(f"cuda:{local}")
-    over = {}
-    if args.n:
-        over["n"] = args.n
-    if args.nq:
-        over["nq"] = args.nq
-    if args.T:
-        over["T"] = args.T
-    if args.k:
-        over["k"] = args.k
+    over = {k_: v for k_, v in (("n", args.n), ("nq", args.nq), ("k", args.k)) if v}
     cfg = synth.get_config(args.config, **over)
-    T, k = cfg.T, cfg.k
+    k = cfg.k
+    Tg = gate_T(cfg, args)
     peaks = load_peaks()
 
     t0 = time.perf_counter()
@@ -231,7 +284,6 @@ def main_ours(args):
     off = (off_all[lo:hi + 1] - off_all[lo]).contiguous()
     qv, qo = g["queries"], g["q_offsets"]
     nvec_shard = int(off[-1])
-
     torch.cuda.synchronize()
     b0 = torch.cuda.Event(enable_timing=True)
     b1 = torch.cuda.Event(enable_timing=True)
@@ -241,47 +293,101 @@ def main_ours(args):
     b1.record()
     torch.cuda.synchronize()
     build_ms = b0.elapsed_time(b1)
-    if world == 1:
-        del g["vectors"]
-    del vec
+    del g["vectors"], vec
     torch.cuda.empty_cache()
 
-    def step():
+    def search(qvv, qoo, T):
         if world == 1:
-            return idx.search(qv, qo, k, T)
-        return D.sharded_search(D.LibShardOps(idx, lo), qv, qo, k, T, cfg.n)
+            return idx.search(qvv, qoo, k, T)
+        return D.sharded_search(D.LibShardOps(idx, lo), qvv, qoo, k, T, cfg.n)
+
+    def bruteforce(qvv, qoo):
+        """exact top-k over all n sets: per shard K8 (dense kernel), local ids -> global, all-gather, K7 merge"""
+        ids, dd = idx.bruteforce(qvv, qoo, k)
+        if world == 1:
+            return ids, dd
+        ids = torch.where(ids >= 0, ids + lo, ids)
+        all_i = D._all_gather(ids.contiguous(), world, None)
+        all_d = D._all_gather(dd.contiguous(), world, None)
+        ops = D.LibShardOps(idx, lo)
+        ops.nq, ops.k, ops.dev = ids.shape[0], k, ids.device
+        return ops.merge(all_i.view(world, *ids.shape), all_d.view(world, *dd.shape), world)
+
+    def timed(fn, reps=1):
+        """CUDA-event time of fn (ms per call) after one untimed warm call; L2 flushed before each call."""
+        fn()
+        ms = []
+        for _ in range(reps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            out = fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        return statistics.mean(ms), out
+
+    def recall_of(got_ids, gt_ids, R):
+        got, gt = got_ids[:R].cpu().numpy(), gt_ids[:R].cpu().numpy()
+        rec = [len(set(got[i].tolist()) & set(gt[i].tolist())) / k for i in range(R)]
+        r1 = [got[i][0] == gt[i][0] for i in range(R)]
+        return round(float(np.mean(rec)), 4), round(float(np.mean(r1)), 4)
 
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
+
+    # -------- recall subset and its exact ground truth (untimed)
+    R = min(args.recall_queries, cfg.nq)
+    qo_sub = qo[: R + 1].contiguous()
+    qv_sub = qv[: int(qo_sub[-1])].contiguous()
+    t_gt = time.perf_counter()
+    gt_ids, _ = bruteforce(qv_sub, qo_sub)
+    torch.cuda.synchronize()
+    t_gt = time.perf_counter() - t_gt
+
+    # -------- T sweep (recall vs throughput), N = 1
+    sweep, full_points = [], {}
+    if world == 1 and not args.no_sweep:
+        for T in TGRID:
+            if T > cfg.n:
+                continue
+            ms, (ids, _) = timed(lambda: search(qv_sub, qo_sub, T))
+            r, r1 = recall_of(ids, gt_ids, R)
+            st = idx.stats()
+            sweep.append({"T": T, "recall@10": r, "rank1_hit": r1, "qps_subset": round(R / (ms * 1e-3), 1),
+                          "path": "dense" if st["dense_batches"] else "query-major"})
+        for T in cfg.T_sweep:  # the config's own sweep points on the full batch
+            ms, _ = timed(lambda: search(qv, qo, T))
+            st = idx.stats()
+            full_points[T] = {"qps": round(cfg.nq / (ms * 1e-3), 1), "ms": round(ms, 2), "stats": st}
+            for e in sweep:
+                if e["T"] == T:
+                    e["qps_full_batch"] = full_points[T]["qps"]
+
+    # -------- the timed region at the gated budget
     clk = ClockSampler(local)
     clk.start()  # before the warm-up: nvidia-smi's start-up must not fall into the timed region
     for _ in range(args.warmup):
         flush.zero_()
-        step()
+        search(qv, qo, Tg)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     clk.mark()
-    st_sum, launches = {}, 0
-    times = []
+    st_sum, launches, times = {}, 0, []
     for _ in range(args.steps):
         flush.zero_()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        th0 = time.perf_counter()
-        out_ids, out_d = step()
-        th1 = time.perf_counter()
+        out_ids, out_d = search(qv, qo, Tg)
         e1.record()
         torch.cuda.synchronize()
-        if os.environ.get("BVSS_TRACE"):
-            print(f"[bench] step host {1000 * (th1 - th0):.1f} ms, events {e0.elapsed_time(e1):.1f} ms", file=sys.stderr)
         times.append(e0.elapsed_time(e1))
         s = idx.stats()
         launches += int(s["kernel_launches"]) + (0 if world == 1 else 1)
-        for key in ("ms_encode", "ms_scan", "ms_select", "ms_refine", "ms_topk", "ms_h2d", "ms_total", "scan_bytes",
-                    "gather_bytes", "cand_rows", "fixup_sets", "select_batches", "select_fallbacks", "scan_macs"):
-            st_sum[key] = st_sum.get(key, 0) + s[key]
+        for key, v in s.items():
+            if isinstance(v, (int, float)):
+                st_sum[key] = st_sum.get(key, 0) + v
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -292,88 +398,119 @@ def main_ours(args):
         tt = torch.tensor([total_ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total_ms = float(tt.item())
-    ms_per_step = total_ms / args.steps
-    value = cfg.nq / (ms_per_step / 1000.0)
     K = args.steps
-    stages = {kk: st_sum[kk] / K for kk in ("ms_h2d", "ms_encode", "ms_scan", "ms_select", "ms_refine", "ms_topk", "ms_total")}
+    ms_per_step = total_ms / K
+    value = cfg.nq / (ms_per_step / 1000.0)
+    rec_g, r1_g = recall_of(out_ids, gt_ids, R)
+    stages = {kk: st_sum.get(kk, 0) / K for kk in ("ms_h2d", "ms_encode", "ms_scan", "ms_select", "ms_refine",
+                                                   "ms_topk", "ms_total")}
 
-    # -------- roofline of the dominant kernel (algorithmic bytes / live event time)
-    scan_bytes = st_sum["scan_bytes"] / K
-    gather_bytes = st_sum["gather_bytes"] / K
-    scan_gbs = scan_bytes / (stages["ms_scan"] * 1e-3) / 1e9 if stages["ms_scan"] > 0 else 0.0
-    refine_gbs = gather_bytes / (stages["ms_refine"] * 1e-3) / 1e9 if stages["ms_refine"] > 0 else 0.0
-    # K3 scan: an exact tensor-core contraction (FP4 kind::mxf4 for binary sketches, int8 kind::i8 for count
-    # sketches): roofline = the measured bf16 dense peak x the nominal dense ratio of its dtype (fp4 4x, int8 2x)
-    scan_flop = 2.0 * st_sum["scan_macs"] / K
-    scan_tfs = scan_flop / (stages["ms_scan"] * 1e-3) / 1e12 if stages["ms_scan"] > 0 else 0.0
-    scan_ratio = 4.0 if cfg.sketch == "binary" else 2.0
-    scan_peak = peaks["bf16_tflops"] * scan_ratio
-    roofs = {
-        "scan": {"kernel": "scan_tc_kernel", "bound": "tensor", "achieved": round(scan_tfs, 1), "peak": round(scan_peak, 1),
-                 "unit": "TFLOP/s", "frac": round(scan_tfs / scan_peak, 4), "ms": round(stages["ms_scan"], 3),
-                 "flop_per_step": scan_flop, "db_operand_GBps": round(scan_gbs, 1),
-                 "peak_src": f"{peaks['src']} bf16_tflops x {scan_ratio:g} (nominal dense "
-                             f"{'fp4' if cfg.sketch == 'binary' else 'int8'}/bf16 ratio)"},
-        "refine": {"kernel": "refine_tc_kernel", "bound": "hbm", "achieved": round(refine_gbs, 1),
-                   "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(refine_gbs / peaks["hbm_gbs"], 4),
-                   "ms": round(stages["ms_refine"], 3), "bytes_per_step": int(gather_bytes),
-                   "peak_src": peaks["src"] + " (MEASURED_PEAKS.json hbm_gbs)"},
-    }
-    dom = max(roofs, key=lambda r: roofs[r]["ms"])
+    # -------- rooflines: the dense refine (tensor) at T_GATE; the filter scan (tensor; HBM GB/s of its database
+    # operand) and the query-major refine (HBM gather) at the config's T = 2000 point
+    d_pairs = st_sum.get("dense_pairs", 0) / K
+    dense_flop = 2.0 * d_pairs * cfg.d  # algorithmic: every (query vector, database vector) dot product of the shard
+    dense_ms = stages["ms_refine"]
+    dense_tfs = dense_flop / (dense_ms * 1e-3) / 1e12 if dense_ms > 0 else 0.0
+    roofs = {"dense": {"kernel": "dense_hausdorff_kernel", "bound": "tensor", "achieved": round(dense_tfs, 1),
+                       "peak": peaks["bf16_tflops_sustained"], "unit": "TFLOP/s",
+                       "frac": round(dense_tfs / peaks["bf16_tflops_sustained"], 4), "ms": round(dense_ms, 2),
+                       "flop_per_step": dense_flop, "frac_of_burst": round(dense_tfs / peaks["bf16_tflops"], 4),
+                       "peak_src": f"{peaks['src']} bf16_tflops_sustained (fp16 = bf16 rate; kernel runs seconds "
+                                   f"inside the step)",
+                       "algorithmic": "2 x (query vectors) x (database vectors) x d per step (padding not counted)"}}
+    p2 = full_points.get(2000)
+    scan_gbs = None
+    if p2:
+        s2 = p2["stats"]
+        scan_ms, ref_ms = s2["ms_scan"], s2["ms_refine"]
+        scan_flop = 2.0 * s2["scan_macs"]
+        scan_tfs = scan_flop / (scan_ms * 1e-3) / 1e12 if scan_ms > 0 else 0.0
+        scan_gbs = s2["scan_bytes"] / (scan_ms * 1e-3) / 1e9 if scan_ms > 0 else 0.0
+        ratio = 4.0 if cfg.sketch == "binary" else 2.0
+        ref_gbs = s2["gather_bytes"] / (ref_ms * 1e-3) / 1e9 if ref_ms > 0 else 0.0
+        roofs["scan_T2000"] = {"kernel": "scan_tc_kernel", "bound": "tensor", "achieved": round(scan_tfs, 1),
+                               "peak": round(peaks["bf16_tflops"] * ratio, 1), "unit": "TFLOP/s",
+                               "frac": round(scan_tfs / (peaks["bf16_tflops"] * ratio), 4), "ms": round(scan_ms, 3),
+                               "db_operand_GBps": round(scan_gbs, 1),
+                               "peak_src": f"{peaks['src']} bf16_tflops x {ratio:g} (nominal dense "
+                                           f"{'fp4' if cfg.sketch == 'binary' else 'int8'}/bf16 ratio)"}
+        roofs["refine_T2000"] = {"kernel": "refine_tc_kernel", "bound": "hbm", "achieved": round(ref_gbs, 1),
+                                 "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(ref_gbs / peaks["hbm_gbs"], 4),
+                                 "ms": round(ref_ms, 3), "bytes_per_step": int(s2["gather_bytes"])}
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
-            traffic = json.load(f).get(roofs[dom]["kernel"])
-    roof = dict(roofs[dom], traffic=traffic)
+            traffic = json.load(f).get("dense_hausdorff_kernel")
+    roof = dict(roofs["dense"], traffic=traffic)
 
-    # -------- recall@10 against exact brute force (GPU, chunked exact refine over all ids), untimed
-    recall = None
-    if world == 1 and args.recall_queries > 0:
-        recall = measure_recall(idx, qv, qo, out_ids, cfg, args.recall_queries, dev)
-
-    # -------- e2e: the same metric through the C ABI with HOST buffers (pinned queries in, results out)
+    # -------- e2e: the same metric with HOST buffers (pinned queries in, top-k out), copies inside the timing
     e2e = None
-    if world == 1 and not args.no_e2e:
+    if not args.no_e2e:
         qh = torch.empty(qv.shape, dtype=torch.float32, pin_memory=True)
         qh.copy_(qv)
-        qoh = qo.cpu().numpy()
-        qhn = qh.numpy()
-        idx.search(qhn, qoh, k, T)
-        torch.cuda.synchronize()
+        qoh = qo.cpu()
         et = []
-        for _ in range(max(1, min(args.steps, 3))):
+        for rep in range(1 + max(1, min(args.steps, 3))):
             flush.zero_()
             torch.cuda.synchronize()
+            if world > 1:
+                dist.barrier()
             t1 = time.perf_counter()
-            ids_h, d_h = idx.search(qhn, qoh, k, T)
-            et.append(time.perf_counter() - t1)
-        h2d = qhn.nbytes + qoh.nbytes
-        d2h = ids_h.nbytes + d_h.nbytes
-        e2e = {"value": round(cfg.nq / statistics.mean(et), 1), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "timing": "host wall clock around bvss_search (host buffers)"}
+            if world == 1:
+                ids_h, d_h = idx.search(qh.numpy(), qoh.numpy(), k, Tg)  # the C ABI copies in and out
+            else:
+                qd_ = qh.to(dev, non_blocking=True)
+                qod_ = qoh.to(dev, non_blocking=True)
+                ids_d, d_d = D.sharded_search(D.LibShardOps(idx, lo), qd_, qod_, k, Tg, cfg.n)
+                ids_h, d_h = ids_d.cpu().numpy(), d_d.cpu().numpy()
+            dt = time.perf_counter() - t1
+            if world > 1:
+                tt = torch.tensor([dt], device=dev)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                dt = float(tt.item())
+            if rep > 0:
+                et.append(dt)
+        e2e = {"value": round(cfg.nq / statistics.mean(et), 1), "unit": UNIT,
+               "h2d_bytes_per_step": int(qh.numel() * 4 + qoh.numel() * 8),
+               "d2h_bytes_per_step": int(ids_h.nbytes + d_h.nbytes),
+               "timing": "host wall clock (max over ranks) around the search with host buffers, after one warm call"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        qps, sample, secs = oracle_sample(cfg, T, k, metric=args.metric)
-        cpu = {"value": round(qps, 4), "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
-               "cpu_seconds": round(secs, 1)}
+        qps, per_q, cores, sample, wall = oracle_pool(cfg, Tg, k, nq_cpu=args.cpu_queries, metric=args.metric)
+        cpu = {"value": round(qps, 5), "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+               "per_query_s": round(per_q, 2), "wall_s": round(wall, 1), "cpu_model": cpu_model()}
 
     if rank == 0:
+        gate = {"target": 0.9, "T": Tg, "recall@10": rec_g, "rank1_hit": r1_g, "queries": R,
+                "attained": rec_g >= 0.9,
+                "ground_truth": "exact Hausdorff top-10 over all n sets (K8: dense tensor-core kernel + exact fp32 "
+                                "fix-up)" + (", per shard + K7 merge" if world > 1 else ""),
+                "ground_truth_s": round(t_gt, 2)}
+        if not gate["attained"]:
+            best = max(sweep, key=lambda e: (e["recall@10"], e.get("qps_subset", 0))) if sweep else None
+            gate["status"] = "not attained" + (f"; best (recall@10, q/s) = ({best['recall@10']}, "
+                                               f"{best['qps_subset']} on the subset) at T={best['T']}" if best else "")
+        else:
+            gate["status"] = f"attained at T={Tg}"
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": round(ms_per_step, 3), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": ("e2m1 FP4 tensor-core scan (exact 0/1 products), " if cfg.sketch == "binary" else "u8 tensor-core scan, ") + "fp16 tensor-core Gram + exact fp32 fix-up (refine)",
+            "scaling": "strong", "vs_baseline": None,
+            "dtype": "fp16 tensor-core Gram (f32 accumulate) + exact fp32 fix-up; e2m1 FP4 / u8 tensor-core sketch scan",
             "data": f"synthetic (gen/synth.py {cfg.name} recipe, noise_mode={args.noise}), generated on GPU",
-            "config": dict(workload_config(cfg, T, k), parallelism=f"db-shard{world}" if world > 1 else "single-gpu",
+            "config": dict(workload_config(cfg, Tg, k), parallelism=f"db-shard{world}" if world > 1 else "single-gpu",
                            l2="flushed (256 MB write) before every timed step; DB 27.6 GB fp32 >> L2",
-                           refine_terms=args.terms, query_batch=int(idx.stats()["query_batch"]),
-                           **({} if args.metric == "hausdorff" else {"metric": args.metric})),
-            "recall@10": recall["recall"] if recall else None,
-            "recall": recall,
-            "filter_scan_GBps": round(scan_gbs, 1),
-            "filter_scan_TFLOPs": round(scan_tfs, 1),
+                           refine_terms=args.terms, **({} if args.metric == "hausdorff" else {"metric": args.metric})),
+            "recall_gate": gate,
+            "recall@10": rec_g,
+            "sweep": sweep,
+            "filter_scan_GBps": round(scan_gbs, 1) if scan_gbs is not None else None,
             "stages_ms": {kk: round(v, 3) for kk, v in stages.items()},
+            "dense": {"survivors_per_step": st_sum.get("dense_survivors", 0) / K,
+                      "emitted_per_step": st_sum.get("dense_emitted", 0) / K,
+                      "pairs_per_step": d_pairs, "mma_flop_per_step": st_sum.get("dense_flop", 0) / K},
             "roofline": roof,
             "roofline_all": roofs,
             "cpu_baseline": cpu,
@@ -382,9 +519,8 @@ def main_ours(args):
             "clocks": clocks,
             "build": {"ms": round(build_ms, 1), "vectors": nvec_shard,
                       "vectors_per_s": round(nvec_shard / (build_ms * 1e-3), 1), "gen_s": round(t_gen, 1),
-                      "note": "index build (K1 encode + K9 split/norms + K2 sketch, incl. the D2D copy) per GPU"},
-            "fixup_sets_per_step": st_sum["fixup_sets"] / K,
-            "select": {"sampled_batches": st_sum["select_batches"], "fallbacks": st_sum["select_fallbacks"]},
+                      "note": "index build (K1 encode + K9 split/norms + K2 sketch, incl. the D2D copy) per GPU; the "
+                              "dense operand is built on first use (untimed warm-up)"},
         }
         print(json.dumps(line), flush=True)
     idx.close()
@@ -392,75 +528,60 @@ def main_ours(args):
         dist.destroy_process_group()
 
 
-def measure_recall(idx, qv, qo, out_ids, cfg, R, dev):
-    """recall@k of the timed search's results on the first R queries,
-    against exact brute force computed on the GPU by the exact refine over ALL
-    set ids in chunks (T = n), merged on the host."""
-    import numpy as np
-    import torch
-    R = min(R, cfg.nq)
-    qo_h = qo[: R + 1].cpu().numpy()
-    qsub = qv[: int(qo_h[-1])].contiguous()
-    qo_d = qo[: R + 1].contiguous()
-    chunk = 8192
-    best_ids = np.full((R, 0), -1, dtype=np.int64)
-    best_d = np.full((R, 0), np.inf, dtype=np.float32)
-    t0 = time.perf_counter()
-    for c0 in range(0, cfg.n, chunk):
-        c1 = min(cfg.n, c0 + chunk)
-        cand = torch.arange(c0, c1, dtype=torch.int32, device=dev).repeat(R, 1).contiguous()
-        ids, dd, _ = idx.refine(qsub, qo_d, cand, cfg.k, with_approx=False)
-        best_ids = np.concatenate([best_ids, ids.cpu().numpy()], axis=1)
-        best_d = np.concatenate([best_d, dd.cpu().numpy()], axis=1)
-        order = np.lexsort((best_ids, best_d), axis=1)[:, : cfg.k]
-        best_ids = np.take_along_axis(best_ids, order, 1)
-        best_d = np.take_along_axis(best_d, order, 1)
-    got = out_ids[:R].cpu().numpy()
-    rec = [len(set(got[i].tolist()) & set(best_ids[i].tolist())) / cfg.k for i in range(R)]
-    return {"recall": round(float(np.mean(rec)), 4), "queries": R, "k": cfg.k,
-            "rank1_hit": round(float(np.mean([got[i][0] == best_ids[i][0] for i in range(R)])), 4),
-            "ground_truth": "exact Hausdorff over all n sets on GPU (bvss_refine, T=n in chunks)",
-            "seconds": round(time.perf_counter() - t0, 1)}
-
-
+# ------------------------------------------------------- reference arm --
 def main_reference(args):
-    """Reference arm: the CPU oracle as it stands (there is no reference
-    implementation to install: /root/reference holds only the paper)."""
+    """Reference arm: the CPU oracle as it stands (there is no reference implementation to install:
+    /root/reference holds only the paper), timed on this host's cores on the same workload definition (T_GATE)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from gen import synth
-    over = {}
-    if args.n:
-        over["n"] = args.n
-    if args.T:
-        over["T"] = args.T
+    over = {k_: v for k_, v in (("n", args.n), ("nq", args.nq), ("k", args.k)) if v}
     cfg = synth.get_config(args.config, **over)
+    Tg = gate_T(cfg, args)
+    cores = os.cpu_count() or 1
+    nq_step = max(4, min(cores, 64))
     for w in range(args.warmup):
-        oracle_sample(cfg, cfg.T, cfg.k, n_sample=2000, q_sample=1, seed_shift=100 + w, metric=args.metric)
-    vals, secs = [], 0.0
+        oracle_pool(cfg, Tg, cfg.k, nq_cpu=min(nq_step, 8), n_sample=2000, refine_cands=300, metric=args.metric,
+                    seed_shift=100 + w)
+    vals, walls = [], []
     sample = ""
     for s in range(args.steps):
-        qps, sample, sec = oracle_sample(cfg, cfg.T, cfg.k, n_sample=5000, q_sample=1, seed_shift=s,
-                                         metric=args.metric)
-        vals.append(1.0 / qps)
-        secs += sec
-    ms_per_step = statistics.mean(vals) * 1000.0
-    value = 1.0 / statistics.mean(vals)
-    line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms_per_step, 1), "higher_is_better": True,
+        qps, per_q, cores, sample, wall = oracle_pool(cfg, Tg, cfg.k, nq_cpu=nq_step, n_sample=3000,
+                                                      refine_cands=500, metric=args.metric, seed_shift=s)
+        vals.append(qps)
+        walls.append(wall)
+    value = statistics.mean(vals)
+    line = {"metric": METRIC, "value": round(value, 5), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(1000.0 * cfg.nq / value, 1), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64 (oracle)", "impl": "reference",
             "data": f"synthetic ({cfg.name} recipe)",
-            "config": dict(workload_config(cfg, cfg.T, cfg.k), parallelism="cpu-oracle",
+            "config": dict(workload_config(cfg, Tg, cfg.k), parallelism="cpu-oracle",
                            **({} if args.metric == "hausdorff" else {"metric": args.metric})),
-            "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
-            "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "cpu_baseline": {"value": round(value, 5), "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": sample, "cpu_model": cpu_model(), "wall_s_per_step": round(statistics.mean(walls), 1)},
+            "e2e": {"value": round(value, 5), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+def relaunch_distributed(args, argv):
+    """--gpus N > 1 without torch.distributed's environment: run this script under torch.distributed.run
+    (one process per GPU, rendezvous on 127.0.0.1); only rank 0 prints the JSON line."""
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # NCCL's communicator lines (ranks, NVLS/NVLink) on stderr
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd, env=env)
+
+
 if __name__ == "__main__":
-    a = parse()
+    argv = sys.argv[1:]
+    a = parse(argv)
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_distributed(a, argv))
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
     if a.impl == "reference":
         main_reference(a)
     else:

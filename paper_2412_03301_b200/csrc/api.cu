@@ -757,6 +757,8 @@ int refine_topk(bvss_index* idx, bvss_search_ctx* c, int64_t* out_ids_dev, float
   return BVSS_OK;
 }
 
+float ev_ms(bvss_index* idx, int a, int b);
+
 // ------------------------------------------------ dense (candidate-major) refine, dense.cu --
 // The database operand of the dense kernel (fp16 x / S, S a power of two >= max|x|) and its tile plan (runs
 // of whole consecutive sets of <= 240 rows; larger sets go to the exact path), built on first use.
@@ -952,6 +954,7 @@ int dense_refine_topk(bvss_index* idx, bvss_search_ctx* c, const uint32_t* mask,
   BVSS_CUDA(cudaMemcpyAsync(idx->dense_stat, stat, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                             idx->stream));
   BVSS_CUDA(cudaStreamSynchronize(idx->stream));
+  idx->stats.ms_refine += ev_ms(idx, 4, 5);  // (bvss_search rewrites it from its own event sums)
   for (int q = 0; q < nq; ++q)
     if (hc[q] > cap) {
       idx->stats.select_fallbacks += 1;  // (reported as a fallback of the dense path)
@@ -1758,6 +1761,7 @@ int bvss_dist_begin(bvss_index* idx, const float* queries, const int64_t* query_
   DeviceGuard g(idx->device);
   std::vector<int64_t> qo;
   BVSS_TRY(host_offsets(idx, query_offsets, nq, (flags & BVSS_DEVICE_PTRS) != 0, qo));
+  idx->stats = bvss_stats{};
   std::unique_ptr<bvss_search_ctx> c;
   // T is the GLOBAL budget, already clamped by the caller to the total number of sets
   BVSS_TRY(make_ctx(idx, queries, qo, k, T, int64_t(1) << 62, flags, c));
