@@ -227,7 +227,7 @@ def oracle_pool(cfg, T, k, nq_cpu=20, n_sample=5000, refine_cands=1500, metric="
         per_q = pool.map(_cpu_worker, range(nq_cpu))
     wall = time.perf_counter() - t0
     mean_q = statistics.mean(per_q)
-    qps = min(cores, nq_cpu) / mean_q if nq_cpu < cores else cores / mean_q
+    qps = cores / mean_q  # every core serves one query at a time
     sample = (f"oracle (numpy, fp64 distances) on {nq_cpu} query sets of the {cfg.name} recipe, one per worker of a "
               f"Pool({cores}); DB sample of {n_sample} sets: scan+select time x{cfg.n / n_sample:g} (linear in n); "
               f"exact refine of {refine_cands} candidates x{T / refine_cands:.4g} (linear in T={T}); q/s = "
