@@ -255,6 +255,93 @@ def select_top_T(scores: np.ndarray, T: int) -> np.ndarray:
 
 
 # ---------------------------------------------------------------------------
+# BioVSS++ stage 1: the inverted-index gate  (Alg 6 lines 1, 3-9 P:779-792;
+# Def 9 / Alg 4; defaults A = 3, M = 1 P:968; reading R27)
+# ---------------------------------------------------------------------------
+
+
+def stage1_positions(CQ: np.ndarray, A: int) -> np.ndarray:
+    """P = {pi(i) : i in [1, A]} with pi = ArgsortDescending(C_Q) (Alg 6 lines
+    3-4): the A positions of the query's count Bloom filter with the
+    largest counts.  Reading R27: among equal counts the lower position comes
+    first (a stable descending sort).  Returns int64 ``[min(A, m)]``."""
+    CQ = np.asarray(CQ, dtype=np.int64)
+    order = np.argsort(-CQ, kind="stable")
+    return order[:min(int(A), CQ.shape[0])].astype(np.int64)
+
+
+def inverted_index(C: np.ndarray) -> list:
+    """Build_Inverted_Index (Alg 4; Def 9): for every position i a
+    list of (j, c_i^(j)) over ALL sets j (zero counts included, Alg 4 lines
+    3-6), sorted by descending count (line 8; ties keep ascending j)."""
+    C = np.asarray(C, dtype=np.int64)
+    n, m = C.shape
+    I = []
+    for i in range(m):
+        lst = [(j, int(C[j, i])) for j in range(n)]
+        lst.sort(key=lambda t: -t[1])  # Python's sort is stable: equal counts keep ascending j
+        I.append(lst)
+    return I
+
+
+def stage1_gate_loops(I: list, P, M: int) -> np.ndarray:
+    """F1 of Alg 6 lines 5-9 written as its loops over the inverted
+    lists: for p in P, for (i, c) in I[p]: if c >= M, add i.  Returns the sorted
+    ids (int64).  Slow; used on small inputs only."""
+    F1 = set()
+    for p in P:
+        for i, c in I[int(p)]:
+            if c >= M:
+                F1.add(i)
+    return np.array(sorted(F1), dtype=np.int64)
+
+
+def stage1_gate(C: np.ndarray, P, M: int) -> np.ndarray:
+    """F1 as a mask over the count Bloom filters C [n][m]: set i passes iff
+    C_i[p] >= M for some p in P (the same set as stage1_gate_loops).  For a
+    binary index the counts are the binary sketch bits (S = (C > 0), Def 8 /
+    Def 10), which decides the gate exactly for M <= 1.  Returns bool ``[n]``."""
+    C = np.asarray(C, dtype=np.int64)
+    P = np.asarray(P, dtype=np.int64)
+    if P.size == 0:
+        return np.zeros(C.shape[0], dtype=bool) if M > 0 else np.ones(C.shape[0], dtype=bool)
+    return (C[:, P] >= M).any(axis=1)
+
+
+# ---------------------------------------------------------------------------
+# BioVSS Alg 2: Hamming-Hausdorff candidate scan over per-vector codes
+# (P:363-390; Haus^H P:378, described P:396)
+# ---------------------------------------------------------------------------
+
+
+def hamming_matrix(QH: np.ndarray, VH: np.ndarray) -> np.ndarray:
+    """hamming(q, v) = popcount(h_q XOR h_v) for every pair of packed codes
+    (uint32 rows), int64 ``[|Q|][|V|]``."""
+    QH = np.asarray(QH, dtype=np.uint32)
+    VH = np.asarray(VH, dtype=np.uint32)
+    x = np.bitwise_xor(QH[:, None, :], VH[None, :, :])
+    return np.bitwise_count(x).astype(np.int64).sum(axis=2)
+
+
+def haus_hamming(QH: np.ndarray, VH: np.ndarray) -> int:
+    """Haus^H(Q^H, H_j) (Alg 2 line 7): Def 4's aggregation with
+    hamming(q, v) in place of dist:
+    max( max_q min_v ham, max_v min_q ham )."""
+    Hm = hamming_matrix(QH, VH)
+    return int(max(Hm.min(axis=1).max(), Hm.min(axis=0).max()))
+
+
+def alg2_candidates(QH: np.ndarray, codes: np.ndarray, offsets: np.ndarray, c: int):
+    """Alg 2 lines 6-9: d_H for every database set, then F = the c
+    sets with the smallest d_H (readings R3/R4: exactly min(c, n), ties by
+    ascending id).  Returns (ids in (d_H, id) order, d_H of every set)."""
+    o = _check_offsets(offsets)
+    n = o.shape[0] - 1
+    dH = np.array([haus_hamming(QH, codes[o[j]:o[j + 1]]) for j in range(n)], dtype=np.int64)
+    return select_top_T(dH, c), dH
+
+
+# ---------------------------------------------------------------------------
 # a-7: Hausdorff distance  (Def 4 P:137-143)
 # ---------------------------------------------------------------------------
 
@@ -414,6 +501,44 @@ class OracleIndex:
 
     def filter(self, Q, T: int) -> np.ndarray:
         return select_top_T(self.scores(Q), T)
+
+    def query_counts(self, Q) -> np.ndarray:
+        """C_Q = Gen_Count_Bloom_Filter(Q) (Alg 6 line 1 P:779; Alg 3 / Def 8)."""
+        codes = encode(np.asarray(Q, dtype=np.float32), self.W, self.L)
+        return sketch_count(codes, np.array([0, codes.shape[0]], dtype=np.int64), self.m)[0]
+
+    def db_counts(self) -> np.ndarray:
+        """The database counters the gate reads: count sketches as stored, or the binary sketch bits (0/1),
+        which decide C_i[p] >= M exactly for M <= 1 (S = (C > 0))."""
+        if self.kind == "count":
+            return np.asarray(self.sketches, dtype=np.int64)
+        return unpack_bits(self.sketches, self.m).astype(np.int64)
+
+    def filter_gated(self, Q, T: int, A: int, M: int) -> np.ndarray:
+        """Alg 6 lines 1-18: F1 by the inverted-index gate (top-A query positions, count >= M),
+        then F2 = the first T of F1 by (score, id); |F1| < T gives F2 = F1."""
+        P = stage1_positions(self.query_counts(Q), A)
+        gate = stage1_gate(self.db_counts(), P, M)
+        sc = self.scores(Q)
+        ids = np.flatnonzero(gate)
+        order = np.lexsort((ids, sc[ids]))
+        return ids[order][:min(T, ids.shape[0])].astype(np.int64)
+
+    def search_gated(self, Q, k: int, T: int, A: int, M: int):
+        """BioVSS++ (Alg 6) with stage 1 enabled: gate, sketch filter, exact Hausdorff rerank, top-k."""
+        if T < k:
+            raise ValueError("T < k (reading R16)")
+        cand = self.filter_gated(Q, T, A, M)
+        return top_k(cand, refine(Q, cand, self.vectors, self.offsets), k)
+
+    def search_alg2(self, Q, k: int, c: int):
+        """BioVSS (Alg 2): Haus^H over the per-vector codes to c candidates, exact Hausdorff
+        rerank (lines 10-13), top-k (line 14).  Needs the database codes (built unless sketches were given)."""
+        if self.codes is None:
+            raise ValueError("Alg 2 needs the database codes")
+        QH = encode(np.asarray(Q, dtype=np.float32), self.W, self.L)
+        cand, _ = alg2_candidates(QH, self.codes, self.offsets, c)
+        return top_k(cand, refine(Q, cand, self.vectors, self.offsets), k)
 
     def set_vectors(self, i: int) -> np.ndarray:
         return self.vectors[self.offsets[i]:self.offsets[i + 1]]

@@ -514,3 +514,118 @@ def test_filter_monotone_in_T_and_recall():
         prev = cur
     assert O.recall_at_k(np.array([1, 2, 3]), np.array([3, 2, 1])) == 1.0
     assert O.recall_at_k(np.array([1, 7, -1]), np.array([3, 2, 1])) == pytest.approx(1 / 3)
+
+
+# ------------------------------------------- BioVSS++ stage-1 gate (Alg 6 lines 1, 3-9; Alg 4)
+
+def test_stage1_positions_hand_built():
+    """pi = ArgsortDescending(C_Q), P = the first A; ties -> lower position (reading R27)."""
+    CQ = np.array([3, 1, 3, 0, 2])
+    assert O.stage1_positions(CQ, 1).tolist() == [0]
+    assert O.stage1_positions(CQ, 2).tolist() == [0, 2]
+    assert O.stage1_positions(CQ, 3).tolist() == [0, 2, 4]
+    assert O.stage1_positions(CQ, 9).tolist() == [0, 2, 4, 1, 3]
+
+
+def test_stage1_gate_hand_built_and_alg4_loops():
+    """F1 = {i : C_i[p] >= M for some p in P} on hand-made counters, against the literal loops of
+    Alg 6 over the inverted index of Alg 4 (every (j, c) pair inserted, zeros included, lists sorted by
+    descending count)."""
+    C = np.array([[0, 5, 0, 5, 5],   # nothing at P = {0, 2}
+                  [1, 0, 0, 0, 0],   # count 1 at p = 0
+                  [0, 0, 2, 0, 0],   # count 2 at p = 2
+                  [3, 0, 1, 0, 0]])  # counts 3 / 1
+    P = O.stage1_positions(np.array([3, 1, 3, 0, 2]), 2)
+    want = {0: [0, 1, 2, 3], 1: [1, 2, 3], 2: [2, 3], 3: [3], 4: []}
+    I = O.inverted_index(C)
+    assert [t[1] for t in I[0]] == [3, 1, 0, 0]  # Alg 4 line 8: descending counts
+    for M, ids in want.items():
+        assert np.flatnonzero(O.stage1_gate(C, P, M)).tolist() == ids
+        assert O.stage1_gate_loops(I, P, M).tolist() == ids
+
+
+def test_stage1_gate_random_loops_nesting_and_binary_equivalence():
+    rng = np.random.default_rng(4)
+    C = rng.integers(0, 4, size=(60, 32))
+    I = O.inverted_index(C)
+    CQ = rng.integers(0, 6, size=32)
+    for A in (1, 3, 7):
+        P = O.stage1_positions(CQ, A)
+        for M in (0, 1, 2, 3):
+            g = O.stage1_gate(C, P, M)
+            assert np.flatnonzero(g).tolist() == O.stage1_gate_loops(I, P, M).tolist()
+            # nesting: more lists -> more sets; a higher minimum count -> fewer
+            assert np.all(g <= O.stage1_gate(C, O.stage1_positions(CQ, A + 1), M))
+            assert np.all(O.stage1_gate(C, P, M + 1) <= g)
+        assert O.stage1_gate(C, P, 0).all()  # M = 0: Alg 4 lists every set with its (possibly zero) count
+        # M = 1 on the counters == any binary bit set at P (S = (C > 0))
+        assert np.array_equal(O.stage1_gate(C, P, 1), O.stage1_gate((C > 0).astype(np.int64), P, 1))
+
+
+def test_gated_search_reduces_to_open_search_and_filters():
+    """A = m, M = 0 opens stage 1 (F1 = D) and the gated search equals Alg 6 without the gate; with the paper's
+    defaults (A = 3, M = 1) every returned set passes the gate; |F1| < T returns F1 whole."""
+    rng = np.random.default_rng(7)
+    V = rng.standard_normal((120, 16)).astype(np.float32)
+    off = np.concatenate([[0], np.cumsum(rng.integers(1, 5, size=40))])
+    off = off[off <= 120]
+    off[-1] = 120
+    oi = O.OracleIndex(V, off, 64, 3, 6, 1)
+    Q = V[off[3]:off[4]] + 0.01
+    a = oi.search(Q, 5, 20)
+    b = oi.search_gated(Q, 5, 20, A=64, M=0)
+    assert a[0].tolist() == b[0].tolist()
+    P = O.stage1_positions(oi.query_counts(Q), 3)
+    gate = O.stage1_gate(oi.db_counts(), P, 1)
+    f = oi.filter_gated(Q, 1000, 3, 1)
+    assert sorted(f.tolist()) == np.flatnonzero(gate).tolist()
+    assert all(gate[i] for i in oi.search_gated(Q, 5, 20, 3, 1)[0] if i >= 0)
+    # query counts = the fold of the query codes
+    assert oi.query_counts(Q).sum() == Q.shape[0] * 6
+
+
+# ------------------------------------------- BioVSS Alg 2: Hamming-Hausdorff over codes
+
+def _pack(rows):
+    return O.pack_bits(np.array([[c == "1" for c in r] + [False] * (32 - len(r)) for r in rows]))
+
+
+def test_haus_hamming_hand_worked():
+    """Haus^H: Def 4 with hamming distance.  Hand-worked on 4-bit codes:
+    Q = {1100, 0011}, V = {1010}: hams (2, 2) -> 2;
+    Q = {1100}, V = {1100, 0011}: directed q->V = min(0, 4) = 0, V->Q = max(0, 4) = 4 -> 4 (the asymmetric
+    case Def 4's outer max exists for)."""
+    assert O.haus_hamming(_pack(["1100", "0011"]), _pack(["1010"])) == 2
+    assert O.haus_hamming(_pack(["1100"]), _pack(["1100", "0011"])) == 4
+    assert O.haus_hamming(_pack(["1100", "0011"]), _pack(["1100", "0011"])) == 0
+
+
+def test_haus_hamming_metric_identity_and_codes():
+    rng = np.random.default_rng(2)
+    L, m = 8, 64
+    def codes(nv):
+        a = rng.standard_normal((nv, m))
+        return O.pack_bits(O.wta(a.astype(np.float32), L))
+    sets = [codes(int(rng.integers(1, 6))) for _ in range(8)]
+    for X in sets:
+        for Y in sets:
+            h = O.haus_hamming(X, Y)
+            assert h == O.haus_hamming(Y, X)                      # symmetric
+            # ham = 2L - 2 <h_q, h_v> on codes with exactly L ones
+            dots = (O.unpack_bits(X, m).astype(int) @ O.unpack_bits(Y, m).astype(int).T)
+            assert np.array_equal(O.hamming_matrix(X, Y), 2 * L - 2 * dots)
+            for Z in sets:
+                assert O.haus_hamming(X, Z) <= h + O.haus_hamming(Y, Z)  # triangle inequality
+        assert O.haus_hamming(X, X) == 0
+
+
+def test_alg2_search_with_c_equal_n_is_bruteforce():
+    rng = np.random.default_rng(9)
+    V = rng.standard_normal((90, 12)).astype(np.float32)
+    off = np.array([0, 3, 7, 8, 15, 20, 26, 30, 41, 50, 60, 61, 70, 80, 90])
+    oi = O.OracleIndex(V, off, 64, 3, 8, 5)
+    Q = V[off[4]:off[5]] + 0.02
+    n = off.shape[0] - 1
+    assert O.top_k(*oi.search_alg2(Q, 4, n), 4)[0].tolist() == oi.bruteforce(Q, 4)[0].tolist()
+    cand, dH = O.alg2_candidates(O.encode(Q, oi.W, 8), oi.codes, off, 5)
+    assert cand.tolist() == O.select_top_T(dH, 5).tolist() and len(cand) == 5
