@@ -52,8 +52,8 @@ METRIC = "query sets/s at recall@10>=0.9 (1M sets, d=384); filter-scan HBM GB/s"
 UNIT = "query sets/s"
 # the gated candidate budget per workload: the smallest TGRID point whose recall@10 reached 0.9 in the
 # committed sweep (profiles/r02/sweep_cfg3.json); every run re-measures the recall there
-T_GATE = {"cfg3": 800_000}
-TGRID = (500, 2000, 8000, 32_000, 128_000, 400_000, 600_000, 800_000, 900_000, 1_000_000)
+T_GATE = {"cfg3": 600_000}
+TGRID = (500, 2000, 8000, 32_000, 128_000, 400_000, 500_000, 600_000, 700_000, 800_000, 1_000_000)
 
 
 def parse(argv=None):
@@ -570,13 +570,14 @@ def relaunch_distributed(args, argv):
     (one process per GPU, rendezvous on 127.0.0.1); only rank 0 prints the JSON line."""
     env = dict(os.environ)
     env.setdefault("NCCL_DEBUG", "INFO")  # NCCL's communicator lines (ranks, NVLS/NVLink) on stderr
+    env["BVSS_BENCH_ARGV"] = json.dumps(argv)  # (torchrun's own parser would take abbreviations like --n)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
-           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *argv]
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)]
     return subprocess.call(cmd, env=env)
 
 
 if __name__ == "__main__":
-    argv = sys.argv[1:]
+    argv = json.loads(os.environ["BVSS_BENCH_ARGV"]) if "BVSS_BENCH_ARGV" in os.environ else sys.argv[1:]
     a = parse(argv)
     if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(relaunch_distributed(a, argv))
