@@ -99,6 +99,19 @@ typedef struct {
                             index (bvss_get_info / bvss_export_sketches then report binary sketches);
                             3 = L1 (reading R26): sum_j |C_Q[j] - C_i[j]| for count sketches (SIMT
                             vabsdiffu4 / dp4a scan, full-key select); on binary sketches L1 = Hamming. */
+  uint32_t gate_A;       /* BioVSS++ stage 1 (Alg 6 lines 1, 3-9; the inverted index of Alg 4):
+                            the query's count Bloom filter picks its gate_A largest positions P (ties -> lower
+                            position, reading R27) and only sets with C_i[p] >= gate_M for some p in P are
+                            candidates; 0 = stage 1 open (F1 = D, reading R6); at most min(64, m).  The paper's
+                            defaults are A = 3, M = 1.  A binary-sketch index supports gate_M <= 1
+                            (S = (C > 0)).  Candidates are then the first T of F1 by (score, id); |F1| < T
+                            returns F1 whole (bvss_filter pads with -1). */
+  uint32_t gate_M;       /* the gate's minimum count M (0 = open) */
+  uint32_t filter;       /* candidate generation: 0 = the sketch scan of Alg 6 (default); 1 = BioVSS Alg 2
+                            (P:363-390): Haus^H(Q^H, H_j), the Hausdorff aggregation of Hamming distances
+                            between per-vector codes, ranks every set and the c = T smallest
+                            (ties by id) are refined; the index keeps its codes.  bvss_filter reports Haus^H
+                            as the score. */
 } bvss_params;
 
 typedef enum { BVSS_SCORE_DEFAULT = 0, BVSS_SCORE_OVERLAP = 1, BVSS_SCORE_BINARIZED = 2, BVSS_SCORE_L1 = 3 } bvss_score_kind;

@@ -43,10 +43,12 @@ class Params(C.Structure):
     _fields_ = [("m", C.c_uint32), ("s", C.c_uint32), ("L", C.c_uint32), ("sketch", C.c_uint32),
                 ("seed", C.c_uint64), ("projection", C.c_void_p), ("device", C.c_int32), ("flags", C.c_uint32),
                 ("query_batch", C.c_uint32), ("refine_terms", C.c_uint32),
-                ("select_mode", C.c_uint32), ("metric", C.c_uint32), ("score", C.c_uint32)]
+                ("select_mode", C.c_uint32), ("metric", C.c_uint32), ("score", C.c_uint32),
+                ("gate_A", C.c_uint32), ("gate_M", C.c_uint32), ("filter", C.c_uint32)]
 
 METRICS = {"hausdorff": 0, "meanmin": 1, "min": 2}  # bvss_metric (rerank distance)
 SCORES = {"default": 0, "overlap": 1, "binarized": 2, "l1": 3}  # bvss_score_kind (filter score)
+FILTERS = {"sketch": 0, "alg2": 1}  # candidate generation (bvss_params.filter)
 
 
 class Info(C.Structure):
@@ -141,7 +143,9 @@ class Index:
 
     def __init__(self, vectors, offsets, *, m, s, L, sketch="binary", seed=0, device=0, keep_codes=False,
                  validate=False, projection=None, refine_terms=0, query_batch=0, select_mode=0,
-                 metric="hausdorff", score="default"):
+                 metric="hausdorff", score="default", gate_A=0, gate_M=1, filter="sketch"):
+        """gate_A / gate_M: BioVSS++ stage 1 (Alg 6 lines 1, 3-9; 0 = open); filter: "sketch" (Alg 6's sketch
+        scan) or "alg2" (BioVSS Alg 2: Haus^H over the per-vector codes)."""
         dev = _is_cuda(vectors)
         if dev != _is_cuda(offsets):
             raise ValueError("vectors and offsets must both be host arrays or both CUDA tensors")
@@ -161,7 +165,8 @@ class Index:
                    projection=(proj.ctypes.data if proj is not None else None), device=device,
                    flags=(DEVICE_PTRS if dev else 0) | (KEEP_CODES if keep_codes else 0) |
                    (VALIDATE_FINITE if validate else 0), query_batch=query_batch, refine_terms=refine_terms,
-                   select_mode=select_mode, metric=METRICS[metric], score=SCORES[score])
+                   select_mode=select_mode, metric=METRICS[metric], score=SCORES[score], gate_A=gate_A,
+                   gate_M=gate_M if gate_A else 0, filter=FILTERS[filter])
         self._h = C.c_void_p()
         vp, _k1 = _ptr(vectors)
         op, _k2 = _ptr(offsets)

@@ -91,7 +91,17 @@ int launch_select_resolve(const int32_t* hist, SelectState st, int nq, int key_b
 int launch_select_quota(SelectState st, const int64_t* all_eq, int nq, int world, int rank, cudaStream_t s);
 int launch_select_tiecount(const int32_t* local_hist, SelectState st, int nq, int64_t* eq_out, cudaStream_t s);
 int launch_select_emit(int key_size, const void* keys, int64_t key_stride, int64_t n, int nq, SelectState st, int T,
-                       int64_t id_base, int32_t* cand, int32_t* score, int32_t* count, cudaStream_t s);
+                       int64_t id_base, int32_t* cand, int32_t* score, int32_t* count, cudaStream_t s,
+                       uint32_t key_limit);
+int launch_gate_planes(const void* S, int64_t n, int m, int kind, int M, uint32_t* planes, int64_t W, int num_sms,
+                       cudaStream_t st);
+int launch_gate_positions(const uint32_t* qcodes, const int64_t* qoff, int nq, int m, int A, int32_t* pos,
+                          cudaStream_t st);
+int launch_gate_keys(int key_size, void* keys, int64_t key_stride, int64_t n, int nq, const int32_t* pos, int A,
+                     const uint32_t* planes, int64_t W, int num_sms, cudaStream_t st);
+int launch_alg2_keys(const uint32_t* qcodes, const int64_t* qoff, int nq, int max_mq, const uint32_t* codes,
+                     const int64_t* off, int64_t n, int m, uint16_t* keys, int64_t key_stride, int num_sms,
+                     cudaStream_t st);
 int launch_refine_tc(const __half* hs, const __half* ls, const float* vscale, int64_t prows, const int64_t* pbase,
                      const float* vnorm, const int64_t* off, int dpad, const __half* qhs, const __half* qls,
                      const float* qscale, int64_t qrows, const int64_t* qrow, const float* qnorm, const int64_t* qoff, int max_mq, const int32_t* cand,
@@ -107,7 +117,7 @@ int launch_topk_fixup(const float* approx, const int32_t* cand, const int32_t* c
 int launch_merge_topk(const int64_t* ids, const float* dist, int P, int64_t nq, int k, int64_t* out_ids,
                       float* out_dist, cudaStream_t st);
 int launch_select_bitmap(int key_size, const void* keys, int64_t key_stride, int64_t n, int nq, SelectState st,
-                         int T, uint32_t* bitmap, int64_t words, cudaStream_t s);
+                         int T, uint32_t* bitmap, int64_t words, cudaStream_t s, uint32_t key_limit);
 int dense_max_dpad();
 int dense_epi_sub();
 int launch_dense_db_operand(const float* V, int64_t nvec, int d, int dpad, float inv_s, __half* hd, int num_sms,
@@ -286,6 +296,11 @@ struct bvss_index {
   std::vector<uint16_t> pend_proj;
   bvss_params pend_p{};
   float* pend_V = nullptr;
+  // candidate generation variants (gate.cu): BioVSS++ stage 1 (A, M) and BioVSS Alg 2
+  uint32_t gate_A = 0, gate_M = 0;  // stage-1 gate: A query positions, minimum count M (A = 0: open)
+  uint32_t filter = 0;              // 0 = sketch scan (Alg 6), 1 = Haus^H over per-vector codes (Alg 2)
+  uint32_t* planes = nullptr;       // [m][ceil(n/32)] gate bit planes
+  int64_t gW = 0;
   // dense (candidate-major) refine, dense.cu: built on first use
   std::vector<int64_t> off_h;   // host copy of the set offsets
   __half* hd = nullptr;         // [nvec][dpad] fp16 = x / dense_s
@@ -336,6 +351,7 @@ struct bvss_search_ctx {
   void* qsk = nullptr;        // query sketches, row-major padded to whole chunks
   int32_t* qmass = nullptr;   // query sketch masses
   uint32_t* qcodes = nullptr; // query codes
+  int32_t* gate_pos = nullptr; // [nq][gate_A] stage-1 positions of every query (gate.cu)
   int nalloc = 0;
   // buffers come from the index workspace (grow-only, reused across calls in the same order)
   int alloc(size_t bytes, void** p);
@@ -393,6 +409,15 @@ struct DeviceGuard {
 // OVERLAP (R24) key offset: K0 - 2 <S_Q, S_i> >= 0 for every pair (binary: <.,.> <= m; count: <= m 255^2)
 int64_t overlap_k0(const bvss_index* idx) {
   return idx->sketch == BVSS_SKETCH_BINARY ? 2ll * idx->m : 2ll * idx->m * 255 * 255;
+}
+
+bool gated(const bvss_index* idx) { return idx->gate_A > 0 && idx->gate_M > 0; }
+// key rows: u16 for binary sketches and for Alg 2's Haus^H; u32 for count-sketch scores
+int key_size_of(const bvss_index* idx) { return (idx->sketch == BVSS_SKETCH_BINARY || idx->filter == 1) ? 2 : 4; }
+// keys at or above the limit are the stage-1 gate's rejects (their top bit set): never candidates
+uint32_t key_limit_of(const bvss_index* idx) {
+  if (!gated(idx)) return 0xFFFFFFFFu;
+  return key_size_of(idx) == 2 ? 0x8000u : 0x80000000u;
 }
 
 int chunks_per_set(const bvss_index* idx) {
@@ -490,6 +515,12 @@ int prepare_queries(bvss_index* idx, bvss_search_ctx* c, const float* queries, c
     idx->stats.kernel_launches += 1;
     BVSS_TRY(post_launch("fill_i32_kernel", idx->stream));
   }
+  if (gated(idx)) {  // stage 1 (Alg 6 lines 1, 3-4): the top-A positions of every query's count Bloom filter
+    BVSS_TRY(c->alloc(static_cast<size_t>(nq) * idx->gate_A * 4, reinterpret_cast<void**>(&c->gate_pos)));
+    BVSS_TRY(launch_gate_positions(c->qcodes, c->qoff, static_cast<int>(nq), static_cast<int>(idx->m),
+                                   static_cast<int>(idx->gate_A), c->gate_pos, idx->stream));
+    idx->stats.kernel_launches += 1;
+  }
   cudaEventRecord(idx->ev[2], idx->stream);
   idx->stats.kernel_launches += 2;
   return BVSS_OK;
@@ -525,7 +556,9 @@ int alloc_select_state(bvss_index* idx, bvss_search_ctx* c) {
   BVSS_TRY(c->alloc(nq * sizeof(int64_t), reinterpret_cast<void**>(&c->sel.quota)));
   BVSS_TRY(c->alloc(nq * sizeof(int32_t), reinterpret_cast<void**>(&c->sel.digit)));
   BVSS_TRY(c->alloc(static_cast<size_t>(nq) * kHistBins * sizeof(int32_t), reinterpret_cast<void**>(&c->local_hist)));
-  c->key_bits = key_bits_for(idx->sketch, idx->m);
+  c->key_bits = key_bits_for(idx->filter == 1 ? static_cast<int>(BVSS_SKETCH_BINARY) : static_cast<int>(idx->sketch),
+                             idx->m);  // (Alg 2: Haus^H <= m, like a binary Hamming score)
+  if (gated(idx)) c->key_bits = 8 * key_size_of(idx);  // the gate's top bit
   if (idx->score == 1) {  // OVERLAP keys span [0, K0]
     c->key_bits = 1;
     while ((overlap_k0(idx) >> c->key_bits) != 0) ++c->key_bits;
@@ -535,29 +568,49 @@ int alloc_select_state(bvss_index* idx, bvss_search_ctx* c) {
   return BVSS_OK;
 }
 
+// Key rows of queries [q0, q0 + ns) of a prepared batch over all n sets: the sketch scan (K3, tensor core or
+// SIMT) or Alg 2's Haus^H over the per-vector codes (gate.cu), then the stage-1 gate's top bit on rejected sets.
+int scan_keys(bvss_index* idx, bvss_search_ctx* c, int q0, int ns, void* keys, int64_t key_stride) {
+  const int64_t n = idx->n;
+  if (idx->filter == 1) {
+    BVSS_TRY(launch_alg2_keys(c->qcodes, c->qoff + q0, ns, c->max_mq, idx->codes, idx->off, n, idx->m,
+                              static_cast<uint16_t*>(keys), key_stride, idx->num_sms, idx->stream));
+    idx->stats.kernel_launches += 1;
+  } else {
+    const int cps = chunks_per_set(idx);
+    const void* sq = static_cast<const uint8_t*>(c->qsk) + static_cast<size_t>(q0) * cps * 16;
+    if (use_tc_scan(idx)) {
+      BVSS_TRY(expand_alloc(idx, c));
+      int* wc;
+      BVSS_TRY(idx->ws.get("scan_counter", sizeof(int), reinterpret_cast<void**>(&wc)));
+      BVSS_TRY(launch_scan_tc(idx->sketch, scan_operand(idx, false), idx->mass, n, n, idx->m, sq, c->qmass + q0, ns,
+                              c->qx, c->qpad, keys, key_stride, wc, idx->num_sms, idx->stream, nullptr, nullptr,
+                              nullptr, nullptr, 0, 0, true));
+      idx->stats.kernel_launches += 2;
+      idx->stats.scan_bytes += scan_tc_db_bytes(idx->sketch, idx->m, n, ns, idx->num_sms);
+    } else {
+      BVSS_TRY(launch_scan(scan_kind(idx), idx->sk, idx->mass, n, n, idx->m, sq, c->qmass + q0, ns, keys, key_stride,
+                           idx->num_sms, idx->stream));
+      idx->stats.kernel_launches += 1;
+      idx->stats.scan_bytes += static_cast<uint64_t>(ceil_div<int64_t>(ns, 8)) * n * chunks_per_set(idx) * 16;
+    }
+    idx->stats.scan_macs += static_cast<uint64_t>(ns) * n * idx->m;
+  }
+  if (gated(idx)) {
+    BVSS_TRY(launch_gate_keys(key_size_of(idx), keys, key_stride, n, ns, c->gate_pos + static_cast<int64_t>(q0) * idx->gate_A,
+                              static_cast<int>(idx->gate_A), idx->planes, idx->gW, idx->num_sms, idx->stream));
+    idx->stats.kernel_launches += 1;
+  }
+  return BVSS_OK;
+}
+
 // full-key scan (every score written) + select state init; the caller drives the select rounds
 int scan_batch(bvss_index* idx, bvss_search_ctx* c) {
   const int64_t n = idx->n;
-  const int key_size = idx->sketch == BVSS_SKETCH_BINARY ? 2 : 4;
+  const int key_size = key_size_of(idx);
   c->key_stride = (n + 7) & ~int64_t(7);
   BVSS_TRY(idx->ws.get("keys", static_cast<size_t>(c->nq) * c->key_stride * key_size, &c->keys));
-  if (use_tc_scan(idx)) {
-    BVSS_TRY(expand_alloc(idx, c));
-    int* wc;
-    BVSS_TRY(idx->ws.get("scan_counter", sizeof(int), reinterpret_cast<void**>(&wc)));
-    BVSS_TRY(launch_scan_tc(idx->sketch, scan_operand(idx, false), idx->mass, n, n, idx->m, c->qsk, c->qmass, static_cast<int>(c->nq),
-                            c->qx, c->qpad, c->keys, c->key_stride, wc, idx->num_sms, idx->stream, nullptr, nullptr,
-                            nullptr, nullptr, 0, 0, true));
-    idx->stats.kernel_launches += 2;
-    idx->stats.scan_bytes += scan_tc_db_bytes(idx->sketch, idx->m, n, static_cast<int>(c->nq), idx->num_sms);
-    idx->stats.scan_macs += static_cast<uint64_t>(c->nq) * n * idx->m;
-  } else {
-    BVSS_TRY(launch_scan(scan_kind(idx), idx->sk, idx->mass, n, n, idx->m, c->qsk, c->qmass, static_cast<int>(c->nq),
-                         c->keys, c->key_stride, idx->num_sms, idx->stream));
-    idx->stats.kernel_launches += 1;
-    idx->stats.scan_bytes += static_cast<uint64_t>(ceil_div<int64_t>(c->nq, 8)) * n * chunks_per_set(idx) * 16;
-    idx->stats.scan_macs += static_cast<uint64_t>(c->nq) * n * idx->m;
-  }
+  BVSS_TRY(scan_keys(idx, c, 0, static_cast<int>(c->nq), c->keys, c->key_stride));
   cudaEventRecord(idx->ev[3], idx->stream);
   BVSS_TRY(alloc_select_state(idx, c));
   BVSS_TRY(launch_select_init(c->sel, static_cast<int>(c->nq), c->teff, idx->stream));
@@ -565,7 +618,7 @@ int scan_batch(bvss_index* idx, bvss_search_ctx* c) {
 }
 
 bool sampled_select_eligible(const bvss_index* idx) {
-  if (!use_tc_scan(idx) || idx->ns == 0) return false;
+  if (!use_tc_scan(idx) || idx->ns == 0 || gated(idx) || idx->filter == 1) return false;
   if (idx->select_mode == 2) return true;
   if (idx->select_mode == 1) return false;
   // auto: binary sketches only.  Count-sketch L2^2 keys of small sets tie massively (a singleton's key
@@ -583,7 +636,7 @@ bool sampled_select_eligible(const bvss_index* idx) {
 int select_sampled(bvss_index* idx, bvss_search_ctx* c, bool* ok) {
   const int nq = static_cast<int>(c->nq);
   const int64_t n = idx->n, ns = idx->ns;
-  const int key_size = idx->sketch == BVSS_SKETCH_BINARY ? 2 : 4;
+  const int key_size = key_size_of(idx);
   const double f = static_cast<double>(ns) / static_cast<double>(n);
   const double mu = static_cast<double>(c->teff) * f;
   int64_t ks = static_cast<int64_t>(std::ceil(mu + 5.0 * std::sqrt(mu) + 4.0));
@@ -646,11 +699,11 @@ int select_sampled(bvss_index* idx, bvss_search_ctx* c, bool* ok) {
 
 int emit_candidates(bvss_index* idx, bvss_search_ctx* c) {
   const int nq = static_cast<int>(c->nq);
-  const int key_size = idx->sketch == BVSS_SKETCH_BINARY ? 2 : 4;
+  const int key_size = key_size_of(idx);
   BVSS_TRY(c->alloc(static_cast<size_t>(nq) * c->T * sizeof(int32_t), reinterpret_cast<void**>(&c->cand)));
   BVSS_TRY(c->alloc(nq * sizeof(int32_t), reinterpret_cast<void**>(&c->count)));
   BVSS_TRY(launch_select_emit(key_size, c->keys, c->key_stride, idx->n, nq, c->sel, c->T, c->id_base, c->cand, nullptr,
-                              c->count, idx->stream));
+                              c->count, idx->stream, key_limit_of(idx)));
   cudaEventRecord(idx->ev[4], idx->stream);
   idx->stats.kernel_launches += 1;
   return BVSS_OK;
@@ -661,7 +714,7 @@ int emit_candidates(bvss_index* idx, bvss_search_ctx* c) {
 int fallback_full(bvss_index* idx, bvss_search_ctx* c) {
   const int nq = static_cast<int>(c->nq);
   const int64_t n = idx->n;
-  const int key_size = idx->sketch == BVSS_SKETCH_BINARY ? 2 : 4;
+  const int key_size = key_size_of(idx);
   const int64_t key_stride = (n + 7) & ~int64_t(7);
   double sub_bytes = 4.0 * (1ull << 30);
   if (const char* e = getenv("BVSS_DEBUG_SUBBATCH_BYTES")) sub_bytes = atof(e);  // test switch: many sub-batches
@@ -673,21 +726,9 @@ int fallback_full(bvss_index* idx, bvss_search_ctx* c) {
   BVSS_TRY(alloc_select_state(idx, c));
   BVSS_TRY(c->alloc(static_cast<size_t>(nq) * c->T * sizeof(int32_t), reinterpret_cast<void**>(&c->cand)));
   BVSS_TRY(c->alloc(nq * sizeof(int32_t), reinterpret_cast<void**>(&c->count)));
-  BVSS_TRY(expand_alloc(idx, c));
-  int* wc;
-  BVSS_TRY(idx->ws.get("scan_counter", sizeof(int), reinterpret_cast<void**>(&wc)));
-  const int cps = chunks_per_set(idx);
   for (int q0 = 0; q0 < nq; q0 += static_cast<int>(sub)) {
     const int ns = static_cast<int>(q0 + sub <= nq ? sub : nq - q0);
-    const void* sq = static_cast<const uint8_t*>(c->qsk) + static_cast<size_t>(q0) * cps * 16;
-    if (use_tc_scan(idx)) {
-      BVSS_TRY(launch_scan_tc(idx->sketch, scan_operand(idx, false), idx->mass, n, n, idx->m, sq, c->qmass + q0, ns,
-                              c->qx, c->qpad, keys, key_stride, wc, idx->num_sms, idx->stream, nullptr, nullptr,
-                              nullptr, nullptr, 0, 0, true));
-    } else {
-      BVSS_TRY(launch_scan(scan_kind(idx), idx->sk, idx->mass, n, n, idx->m, sq, c->qmass + q0, ns, keys, key_stride,
-                           idx->num_sms, idx->stream));
-    }
+    BVSS_TRY(scan_keys(idx, c, q0, ns, keys, key_stride));
     SelectState s2 = c->sel;
     s2.prefix += q0;
     s2.below += q0;
@@ -701,7 +742,8 @@ int fallback_full(bvss_index* idx, bvss_search_ctx* c) {
       BVSS_TRY(launch_select_resolve(c->local_hist, s2, ns, c->key_bits, r, idx->stream));
     }
     BVSS_TRY(launch_select_emit(key_size, keys, key_stride, n, ns, s2, c->T, c->id_base,
-                                c->cand + static_cast<int64_t>(q0) * c->T, nullptr, c->count + q0, idx->stream));
+                                c->cand + static_cast<int64_t>(q0) * c->T, nullptr, c->count + q0, idx->stream,
+                                key_limit_of(idx)));
     idx->stats.kernel_launches += 4 + 2 * c->rounds;
   }
   cudaEventRecord(idx->ev[4], idx->stream);
@@ -986,7 +1028,7 @@ int dense_refine_topk(bvss_index* idx, bvss_search_ctx* c, const uint32_t* mask,
 int dense_mask(bvss_index* idx, bvss_search_ctx* c, uint32_t** mask, int64_t* stride) {
   const int nq = static_cast<int>(c->nq);
   const int64_t n = idx->n;
-  const int key_size = idx->sketch == BVSS_SKETCH_BINARY ? 2 : 4;
+  const int key_size = key_size_of(idx);
   const int64_t key_stride = (n + 7) & ~int64_t(7);
   double sub_bytes = 4.0 * (1ull << 30);
   if (const char* e = getenv("BVSS_DEBUG_SUBBATCH_BYTES")) sub_bytes = atof(e);
@@ -1000,26 +1042,9 @@ int dense_mask(bvss_index* idx, bvss_search_ctx* c, uint32_t** mask, int64_t* st
   void* keys;
   BVSS_TRY(idx->ws.get("keys", static_cast<size_t>(sub) * key_stride * key_size, &keys));
   BVSS_TRY(alloc_select_state(idx, c));
-  const bool tcs = use_tc_scan(idx);
-  int* wc = nullptr;
-  if (tcs) {
-    BVSS_TRY(expand_alloc(idx, c));
-    BVSS_TRY(idx->ws.get("scan_counter", sizeof(int), reinterpret_cast<void**>(&wc)));
-  }
-  const int cps = chunks_per_set(idx);
   for (int q0 = 0; q0 < nq; q0 += static_cast<int>(sub)) {
     const int ns = static_cast<int>(q0 + sub <= nq ? sub : nq - q0);
-    const void* sq = static_cast<const uint8_t*>(c->qsk) + static_cast<size_t>(q0) * cps * 16;
-    if (tcs) {
-      BVSS_TRY(launch_scan_tc(idx->sketch, scan_operand(idx, false), idx->mass, n, n, idx->m, sq, c->qmass + q0, ns,
-                              c->qx, c->qpad, keys, key_stride, wc, idx->num_sms, idx->stream, nullptr, nullptr,
-                              nullptr, nullptr, 0, 0, true));
-      idx->stats.scan_bytes += scan_tc_db_bytes(idx->sketch, idx->m, n, ns, idx->num_sms);
-    } else {
-      BVSS_TRY(launch_scan(scan_kind(idx), idx->sk, idx->mass, n, n, idx->m, sq, c->qmass + q0, ns, keys, key_stride,
-                           idx->num_sms, idx->stream));
-    }
-    idx->stats.scan_macs += static_cast<uint64_t>(ns) * n * idx->m;
+    BVSS_TRY(scan_keys(idx, c, q0, ns, keys, key_stride));
     SelectState s2 = c->sel;
     s2.prefix += q0;
     s2.below += q0;
@@ -1033,8 +1058,8 @@ int dense_mask(bvss_index* idx, bvss_search_ctx* c, uint32_t** mask, int64_t* st
       BVSS_TRY(launch_select_resolve(c->local_hist, s2, ns, c->key_bits, r, idx->stream));
     }
     BVSS_TRY(launch_select_bitmap(key_size, keys, key_stride, n, ns, s2, c->T, *mask + static_cast<int64_t>(q0) * words,
-                                  words, idx->stream));
-    idx->stats.kernel_launches += 3 + 2 * c->rounds;
+                                  words, idx->stream, key_limit_of(idx)));
+    idx->stats.kernel_launches += 1 + 2 * c->rounds;
   }
   return BVSS_OK;
 }
@@ -1047,7 +1072,7 @@ float ev_ms(bvss_index* idx, int a, int b) {
 
 int run_select_single(bvss_index* idx, bvss_search_ctx* c) {
   const int nq = static_cast<int>(c->nq);
-  const int key_size = idx->sketch == BVSS_SKETCH_BINARY ? 2 : 4;
+  const int key_size = key_size_of(idx);
   for (int r = 0; r < c->rounds; ++r) {
     BVSS_TRY(launch_select_hist(key_size, c->keys, c->key_stride, idx->n, nq, c->sel, c->key_bits, r, c->local_hist,
                                 idx->stream));
@@ -1086,7 +1111,7 @@ int64_t batch_size(const bvss_index* idx, int64_t nq) {
   if (idx->query_batch) return idx->query_batch < nq ? idx->query_batch : nq;
   // sampled-threshold selection needs no key rows (its fallback runs in sub-batches): large batches
   if (sampled_select_eligible(idx)) return nq < 16384 ? nq : 16384;
-  const int key_size = idx->sketch == BVSS_SKETCH_BINARY ? 2 : 4;
+  const int key_size = key_size_of(idx);
   const double per_q = static_cast<double>((idx->n + 7) & ~int64_t(7)) * key_size;
   int64_t b = static_cast<int64_t>((4.0 * (1ull << 30)) / per_q);
   if (b > 4096) b = 4096;
@@ -1115,6 +1140,18 @@ int bvss_device_count(void) {
 }  // extern "C"
 
 namespace {
+// candidate-generation variants (gate.cu): stage-1 gate (A, M) and Alg 2
+int validate_variants(const bvss_params* p) {
+  if (p->filter > 1) BVSS_FAIL(BVSS_EINVAL, "filter must be 0 (sketch scan, Alg 6) or 1 (Haus^H over codes, Alg 2)");
+  if (p->gate_A > 64 || p->gate_A > p->m) BVSS_FAIL(BVSS_EINVAL, "gate_A must be in [0, min(64, m)]");
+  if (p->gate_A > 0 && p->gate_M > 255) BVSS_FAIL(BVSS_EINVAL, "gate_M must be <= 255 (u8 counters)");
+  const bool binary = p->sketch == BVSS_SKETCH_BINARY || p->score == 2;
+  if (p->gate_A > 0 && binary && p->gate_M > 1)
+    BVSS_FAIL(BVSS_EINVAL, "a binary-sketch index holds no counts: the stage-1 gate needs gate_M <= 1 (S = (C > 0))");
+  if (p->gate_A > 0 && p->score == 1) BVSS_FAIL(BVSS_EINVAL, "the stage-1 gate is not combined with the OVERLAP score");
+  return BVSS_OK;
+}
+
 int validate_params(int64_t n, int32_t d, const bvss_params* p) {
   if (n < 1) BVSS_FAIL(BVSS_EINVAL, "n must be >= 1");
   if (d < 1 || d > 65535) BVSS_FAIL(BVSS_EINVAL, "d must be in [1, 65535]");
@@ -1127,7 +1164,7 @@ int validate_params(int64_t n, int32_t d, const bvss_params* p) {
   if (p->select_mode > 2) BVSS_FAIL(BVSS_EINVAL, "select_mode must be 0 (auto), 1 (full keys) or 2 (sampled)");
   if (p->metric > 2) BVSS_FAIL(BVSS_EINVAL, "metric must be 0 (Hausdorff), 1 (MeanMin) or 2 (Min)");
   if (p->score > 3) BVSS_FAIL(BVSS_EINVAL, "score must be 0 (Hamming / L2^2), 1 (OVERLAP), 2 (BINARIZED) or 3 (L1)");
-  return BVSS_OK;
+  return validate_variants(p);
 }
 
 // The build (Algs 1, 3, 5).  adopt_V: a device buffer [nvec][d] the index takes over (streaming build) instead of
@@ -1148,6 +1185,7 @@ int build_impl(const float* vectors, const int64_t* set_offsets, int64_t n, int3
   if (p->select_mode > 2) BVSS_FAIL(BVSS_EINVAL, "select_mode must be 0 (auto), 1 (full keys) or 2 (sampled)");
   if (p->metric > 2) BVSS_FAIL(BVSS_EINVAL, "metric must be 0 (Hausdorff), 1 (MeanMin) or 2 (Min)");
   if (p->score > 3) BVSS_FAIL(BVSS_EINVAL, "score must be 0 (Hamming / L2^2), 1 (OVERLAP), 2 (BINARIZED) or 3 (L1)");
+  BVSS_TRY(validate_variants(p));
   int num_sms = 0;
   BVSS_TRY(check_device(p->device, &num_sms));
   DeviceGuard g(p->device);
@@ -1179,6 +1217,9 @@ int build_impl(const float* vectors, const int64_t* set_offsets, int64_t n, int3
   idx->select_mode = p->select_mode;
   idx->metric = static_cast<int>(p->metric);
   idx->score = static_cast<int>(p->score);
+  idx->gate_A = p->gate_A;
+  idx->gate_M = p->gate_A > 0 ? p->gate_M : 0;
+  idx->filter = p->filter;
   BVSS_CUDA(cudaStreamCreateWithFlags(&idx->own_stream, cudaStreamNonBlocking));
   idx->stream = idx->own_stream;
   for (auto& e : idx->ev) BVSS_CUDA(cudaEventCreate(&e));
@@ -1249,7 +1290,7 @@ int build_impl(const float* vectors, const int64_t* set_offsets, int64_t n, int3
   BVSS_TRY(post_launch("pad_rows_kernel", st));
   BVSS_TRY(dalloc(static_cast<size_t>(nvec) * 4, reinterpret_cast<void**>(&idx->vnorm)));
   uint32_t* codes = nullptr;
-  const bool keep = (p->flags & BVSS_KEEP_CODES) != 0;
+  const bool keep = (p->flags & BVSS_KEEP_CODES) != 0 || p->filter == 1;  // Alg 2 scans the per-vector codes
   if (keep) {
     BVSS_TRY(dalloc(static_cast<size_t>(nvec) * R * 4, reinterpret_cast<void**>(&idx->codes)));
     codes = idx->codes;
@@ -1263,6 +1304,12 @@ int build_impl(const float* vectors, const int64_t* set_offsets, int64_t n, int3
   BVSS_TRY(dalloc(static_cast<size_t>(n) * 4, reinterpret_cast<void**>(&idx->mass)));
   BVSS_TRY(launch_sketch(codes, p->m, idx->off, n, idx->sketch, idx->sk, idx->mass, n, 1, num_sms, st));
   if (idx->score == 1) BVSS_CUDA(cudaMemsetAsync(idx->mass, 0, static_cast<size_t>(n) * 4, st));  // OVERLAP (R24)
+  if (gated(idx.get())) {  // stage-1 gate (gate.cu): one bit plane per position, bit i = (C_i[p] >= M)
+    idx->gW = (n + 31) / 32;
+    BVSS_TRY(dalloc(static_cast<size_t>(p->m) * idx->gW * 4, reinterpret_cast<void**>(&idx->planes)));
+    BVSS_TRY(launch_gate_planes(idx->sk, n, static_cast<int>(p->m), static_cast<int>(idx->sketch),
+                                static_cast<int>(idx->gate_M), idx->planes, idx->gW, num_sms, st));
+  }
   if (use_tc_scan(idx.get())) {
     // strided database sample for the sampled-threshold select
     idx->ns = n < 16384 ? n : 16384;
@@ -1379,6 +1426,7 @@ int bvss_index_finish(bvss_index* idx) {
   built->sk = built->smp_sk = built->skx = built->smp_skx = nullptr;
   built->mass = built->smp_mass = nullptr;
   built->hd = built->va = nullptr;
+  built->planes = nullptr;
   built->dtile_s0 = built->dtile_s1 = built->dhuge = nullptr;
   for (auto& e : built->ev) e = nullptr;
   delete built;
@@ -1392,7 +1440,8 @@ void bvss_free_index(bvss_index* idx) {
   if (idx->stream) cudaStreamSynchronize(idx->stream);
   void* ptrs[] = {idx->Wt,    idx->V,     idx->off,   idx->hi,   idx->lo,     idx->vscale, idx->pbase,
                   idx->vnorm, idx->codes, idx->sk,    idx->mass, idx->smp_sk, idx->smp_mass,
-                  idx->skx,   idx->smp_skx, idx->hd, idx->va, idx->dtile_s0, idx->dtile_s1, idx->dhuge};
+                  idx->skx,   idx->smp_skx, idx->hd, idx->va, idx->dtile_s0, idx->dtile_s1, idx->dhuge,
+                  idx->planes};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (idx->pend_V) cudaFree(idx->pend_V);
@@ -1502,12 +1551,12 @@ int bvss_filter(bvss_index* idx, const float* queries, const int64_t* query_offs
   std::unique_ptr<bvss_search_ctx> c;
   BVSS_TRY(make_ctx(idx, queries, qo, 1, T, idx->n, flags, c));
   BVSS_TRY(run_select_single(idx, c.get()));
-  const int key_size = idx->sketch == BVSS_SKETCH_BINARY ? 2 : 4;
+  const int key_size = key_size_of(idx);
   int32_t *cand, *score;
   BVSS_TRY(c->alloc(static_cast<size_t>(nq) * T * 4, reinterpret_cast<void**>(&cand)));
   BVSS_TRY(c->alloc(static_cast<size_t>(nq) * T * 4, reinterpret_cast<void**>(&score)));
   BVSS_TRY(launch_select_emit(key_size, c->keys, c->key_stride, idx->n, static_cast<int>(nq), c->sel, T, 0, cand, score,
-                              nullptr, idx->stream));
+                              nullptr, idx->stream, key_limit_of(idx)));
   BVSS_TRY(from_device(idx, out_cand, cand, static_cast<size_t>(nq) * T * 4, dev));
   if (out_score) BVSS_TRY(from_device(idx, out_score, score, static_cast<size_t>(nq) * T * 4, dev));
   BVSS_CUDA(cudaStreamSynchronize(idx->stream));
@@ -1776,7 +1825,7 @@ int bvss_dist_hist(bvss_search_ctx* c, int32_t round, int32_t* hist_dev) {
   if (round != c->next_round || round >= c->rounds) BVSS_FAIL(BVSS_ESTATE, "rounds must run in order");
   bvss_index* idx = c->idx;
   DeviceGuard g(idx->device);
-  const int key_size = idx->sketch == BVSS_SKETCH_BINARY ? 2 : 4;
+  const int key_size = key_size_of(idx);
   BVSS_TRY(launch_select_hist(key_size, c->keys, c->key_stride, idx->n, static_cast<int>(c->nq), c->sel, c->key_bits,
                               round, c->local_hist, idx->stream));
   BVSS_CUDA(cudaMemcpyAsync(hist_dev, c->local_hist, static_cast<size_t>(c->nq) * kHistBins * 4,
@@ -1813,13 +1862,13 @@ int bvss_dist_finish(bvss_search_ctx* c, const int64_t* all_eq_dev, int32_t worl
   if (dense_wanted(idx, c->teff / world) && dense_supported(idx, c)) {
     // large global budget: this rank's share of the global top-T as a bitmap over its shard, then the
     // candidate-major refine of the shard (the same kernels as the single-GPU search at this T)
-    const int key_size = idx->sketch == BVSS_SKETCH_BINARY ? 2 : 4;
+    const int key_size = key_size_of(idx);
     const int64_t words = (idx->n + 31) / 32;
     uint32_t* mask;
     BVSS_TRY(c->alloc(static_cast<size_t>(c->nq) * words * 4, reinterpret_cast<void**>(&mask)));
     BVSS_CUDA(cudaMemsetAsync(mask, 0, static_cast<size_t>(c->nq) * words * 4, idx->stream));
     BVSS_TRY(launch_select_bitmap(key_size, c->keys, c->key_stride, idx->n, static_cast<int>(c->nq), c->sel, c->T,
-                                  mask, words, idx->stream));
+                                  mask, words, idx->stream, key_limit_of(idx)));
     cudaEventRecord(idx->ev[3], idx->stream);
     bool done = false;
     BVSS_TRY(dense_refine_topk(idx, c, mask, words, -1, topk_ids_dev, topk_dist_dev, &done));

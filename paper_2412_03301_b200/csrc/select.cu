@@ -183,7 +183,7 @@ template <typename K>
 __global__ void __launch_bounds__(256) select_emit_kernel(const K* __restrict__ keys, int64_t key_stride, int64_t n,
                                                           SelectState st, int T, int64_t id_base,
                                                           int32_t* __restrict__ cand, int32_t* __restrict__ score,
-                                                          int32_t* __restrict__ count) {
+                                                          int32_t* __restrict__ count, uint32_t key_limit) {
   __shared__ uint32_t sw[8];
   const int q = blockIdx.x;
   const uint32_t tau = st.prefix[q];
@@ -202,8 +202,8 @@ __global__ void __launch_bounds__(256) select_emit_kernel(const K* __restrict__ 
       for (int i = 0; i < 8; ++i) {
         const uint32_t kk = static_cast<uint32_t>(k[i]);
         const bool valid = base + i < n;
-        nlt += (valid && kk < tau) ? 1u : 0u;
-        neq += (valid && kk == tau) ? 1u : 0u;
+        nlt += (valid && kk < tau && kk < key_limit) ? 1u : 0u;  // key_limit: keys at or above it (the stage-1
+        neq += (valid && kk == tau && kk < key_limit) ? 1u : 0u; // gate's rejects, gate.cu) are never taken
       }
     }
     uint32_t total;
@@ -219,7 +219,8 @@ __global__ void __launch_bounds__(256) select_emit_kernel(const K* __restrict__ 
         const uint32_t kk = static_cast<uint32_t>(k[i]);
         if (base + i >= n) break;
         bool take = false;
-        if (kk < tau) take = true;
+        if (kk >= key_limit) take = false;
+        else if (kk < tau) take = true;
         else if (kk == tau) { take = my_eq < quota; ++my_eq; }
         if (take && pos < T) {
           crow[pos] = static_cast<int32_t>(id_base + base + i);
@@ -246,7 +247,7 @@ __global__ void __launch_bounds__(256) select_emit_kernel(const K* __restrict__ 
 template <typename K>
 __global__ void __launch_bounds__(256) select_bitmap_kernel(const K* __restrict__ keys, int64_t key_stride, int64_t n,
                                                             SelectState st, int T, uint32_t* __restrict__ bitmap,
-                                                            int64_t words) {
+                                                            int64_t words, uint32_t key_limit) {
   __shared__ uint32_t sw[8];
   const int q = blockIdx.x;
   const int lane = threadIdx.x & 31;
@@ -265,8 +266,8 @@ __global__ void __launch_bounds__(256) select_bitmap_kernel(const K* __restrict_
       for (int i = 0; i < 8; ++i) {
         const uint32_t kk = static_cast<uint32_t>(k[i]);
         const bool valid = base + i < n;
-        nlt += (valid && kk < tau) ? 1u : 0u;
-        neq += (valid && kk == tau) ? 1u : 0u;
+        nlt += (valid && kk < tau && kk < key_limit) ? 1u : 0u;  // key_limit: keys at or above it (the stage-1
+        neq += (valid && kk == tau && kk < key_limit) ? 1u : 0u; // gate's rejects, gate.cu) are never taken
       }
     }
     uint32_t total;
@@ -282,7 +283,8 @@ __global__ void __launch_bounds__(256) select_bitmap_kernel(const K* __restrict_
         const uint32_t kk = static_cast<uint32_t>(k[i]);
         if (base + i >= n) break;
         bool take = false;
-        if (kk < tau) take = true;
+        if (kk >= key_limit) take = false;
+        else if (kk < tau) take = true;
         else if (kk == tau) { take = my_eq < quota; ++my_eq; }
         if (take) bits |= 1u << i;
       }
@@ -370,25 +372,26 @@ int launch_select_tiecount(const int32_t* local_hist, SelectState st, int nq, in
 }
 
 int launch_select_bitmap(int key_size, const void* keys, int64_t key_stride, int64_t n, int nq, SelectState st,
-                         int T, uint32_t* bitmap, int64_t words, cudaStream_t s) {
+                         int T, uint32_t* bitmap, int64_t words, cudaStream_t s, uint32_t key_limit) {
   if (key_size == 2)
     select_bitmap_kernel<uint16_t><<<nq, 256, 0, s>>>(static_cast<const uint16_t*>(keys), key_stride, n, st, T, bitmap,
-                                                      words);
+                                                      words, key_limit);
   else
     select_bitmap_kernel<uint32_t><<<nq, 256, 0, s>>>(static_cast<const uint32_t*>(keys), key_stride, n, st, T, bitmap,
-                                                      words);
+                                                      words, key_limit);
   BVSS_TRY(post_launch(__func__, s));
   return BVSS_OK;
 }
 
 int launch_select_emit(int key_size, const void* keys, int64_t key_stride, int64_t n, int nq, SelectState st, int T,
-                       int64_t id_base, int32_t* cand, int32_t* score, int32_t* count, cudaStream_t s) {
+                       int64_t id_base, int32_t* cand, int32_t* score, int32_t* count, cudaStream_t s,
+                       uint32_t key_limit) {
   if (key_size == 2)
     select_emit_kernel<uint16_t><<<nq, 256, 0, s>>>(static_cast<const uint16_t*>(keys), key_stride, n, st, T, id_base,
-                                                    cand, score, count);
+                                                    cand, score, count, key_limit);
   else
     select_emit_kernel<uint32_t><<<nq, 256, 0, s>>>(static_cast<const uint32_t*>(keys), key_stride, n, st, T, id_base,
-                                                    cand, score, count);
+                                                    cand, score, count, key_limit);
   BVSS_TRY(post_launch(__func__, s));
   return BVSS_OK;
 }
