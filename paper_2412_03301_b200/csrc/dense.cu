@@ -115,6 +115,7 @@ struct DenseArgs {
   int64_t mask_stride;          // words per query row (0: one row shared by every query)
   int64_t id_base;
   unsigned long long* stat;     // [2]: survivors, emitted (may be null)
+  int debug;                    // developer switch BVSS_DENSE_DEBUG: 1 = epilogue skips its work, 2 = no MMAs
 };
 
 // per-tile metadata the info warp stages for the epilogue (shared memory): the database sets of the tile
@@ -303,7 +304,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
           tc::fence_after_sync();
           if (lane == 0) {
             const uint32_t bs = ring_s + st * kBChunkBytes;
-            if (kc < a.KC) {
+            if (a.debug == 2) {
+            } else if (kc < a.KC) {
               const uint32_t as = a_s + kc * kAChunkBytes;
 #pragma unroll
               for (int kk = 0; kk < 4; ++kk)
@@ -400,7 +402,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
         tc::fence_after_sync();
         const int s0 = inf.s0, nsets = inf.nsets;
         const uint32_t tb = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * kDenseN;
-        for (int js = sub; js < nsets;) {
+        for (int js = a.debug == 1 ? nsets : sub; js < nsets;) {
           int nxt = 0;  // the next set of this warp (taken now: the shared-memory atomic's latency overlaps the set)
           if (lane == 0) nxt = atomicAdd(const_cast<int*>(&inf.ctr[quarter]), 1);
           const int i = s0 + js;
@@ -689,6 +691,10 @@ int launch_dense_hausdorff(const __half* qd, int ntq, const __half* hd, int64_t 
   a.mask_stride = mask_stride;
   a.id_base = id_base;
   a.stat = stat;
+  {
+    const char* e = getenv("BVSS_DENSE_DEBUG");
+    a.debug = e ? atoi(e) : 0;
+  }
   const int units = ntq * R;
   const int grid = units < num_sms ? units : num_sms;
   BVSS_CUDA(cudaFuncSetAttribute(dense_hausdorff_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
