@@ -120,6 +120,7 @@ int launch_select_bitmap(int key_size, const void* keys, int64_t key_stride, int
                          int T, uint32_t* bitmap, int64_t words, cudaStream_t s, uint32_t key_limit);
 int dense_max_dpad();
 int dense_epi_sub();
+int dense_tile_rows();
 int launch_dense_db_operand(const float* V, int64_t nvec, int d, int dpad, float inv_s, __half* hd, int num_sms,
                             cudaStream_t st);
 int launch_dense_query_operand(const float* Qv, const float* qnorm, const int32_t* rowmap, const int32_t* rowq,
@@ -134,7 +135,8 @@ int launch_dense_hausdorff(const __half* qd, int ntq, const __half* hd, int64_t 
                            const int32_t* tile_s0, const int32_t* tile_s1, const int64_t* off, const __half* va,
                            const __half* qa, const int32_t* lane_qid, const float* lane_qn, const float* qE,
                            const float* tau0,
-                           float kappa, int k, int R, float* lists, int32_t* cnt, int32_t* ids, float* vals, int cap,
+                           float kappa, float alpha, int k, int R, float* lists, int32_t* cnt, int32_t* ids,
+                           float* vals, int cap,
                            const uint32_t* mask, int64_t mask_stride, int64_t id_base, unsigned long long* stat,
                            int num_sms, cudaStream_t st);
 
@@ -803,7 +805,7 @@ float ev_ms(bvss_index* idx, int a, int b);
 
 // ------------------------------------------------ dense (candidate-major) refine, dense.cu --
 // The database operand of the dense kernel (fp16 x / S, S a power of two >= max|x|) and its tile plan (runs
-// of whole consecutive sets of <= 240 rows; larger sets go to the exact path), built on first use.
+// of whole consecutive sets of <= 144 rows; larger sets go to the exact path), built on first use.
 int ensure_dense(bvss_index* idx) {
   if (idx->hd) return BVSS_OK;
   if (idx->dpad > dense_max_dpad()) BVSS_FAIL(BVSS_EUNSUPPORTED, "dense refine needs d <= %d", dense_max_dpad());
@@ -823,7 +825,7 @@ int ensure_dense(bvss_index* idx) {
                                      idx->num_sms, idx->stream));
   std::vector<int32_t> s0, s1, huge;
   const std::vector<int64_t>& o = idx->off_h;
-  const int64_t cap_rows = 240;  // dense.cu kDenseN
+  const int64_t cap_rows = dense_tile_rows();  // dense.cu kDenseN
   for (int64_t i = 0; i < idx->n;) {
     if (o[i + 1] - o[i] > cap_rows) {
       huge.push_back(static_cast<int32_t>(i));
@@ -985,7 +987,8 @@ int dense_refine_topk(bvss_index* idx, bvss_search_ctx* c, const uint32_t* mask,
                              idx->num_sms, idx->stream));
   cudaEventRecord(idx->ev[4], idx->stream);
   BVSS_TRY(launch_dense_hausdorff(qd, ntq, idx->hd, idx->nvec, idx->dpad, ntiles, idx->dtile_s0, idx->dtile_s1,
-                                  idx->off, idx->va, qa, lane_qid, lane_qn, qE, tau0, -2.0f * sq * idx->dense_s, k, R,
+                                  idx->off, idx->va, qa, lane_qid, lane_qn, qE, tau0, -2.0f * sq * idx->dense_s, alpha,
+                                  k, R,
                                   lists, cnt, ids, vals, static_cast<int>(cap), mask, mask_stride, c->id_base, stat,
                                   idx->num_sms, idx->stream));
   cudaEventRecord(idx->ev[5], idx->stream);
@@ -1018,7 +1021,7 @@ int dense_refine_topk(bvss_index* idx, bvss_search_ctx* c, const uint32_t* mask,
   idx->stats.dense_pairs += static_cast<uint64_t>(c->nqvec) * static_cast<uint64_t>(
       ntiles_use >= idx->dntiles ? idx->nvec : idx->off_h[idx->dtile_s0_h[ntiles_use]]);
   idx->stats.dense_flop += 2.0 * static_cast<double>(rows) * idx->dpad *
-                           static_cast<double>(ntiles_use) * 240.0;
+                           static_cast<double>(ntiles_use) * dense_tile_rows();
   *done = true;
   return BVSS_OK;
 }
