@@ -279,18 +279,17 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
   const int units = a.ntq * a.R;
 
   if (warp == 0) {
-    // =========================== TMA producer ===========================
-    uint32_t stage_ctr = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int r = u % a.R;
-      int t0, t1;
-      range_tiles(r, a.R, a.ntiles, &t0, &t1);
-      for (int t = t0; t < t1; ++t) {
-        const int row0 = static_cast<int>(a.off[a.tile_s0[t]]);
-        for (int kc = 0; kc <= a.KC; ++kc, ++stage_ctr) {  // kc == KC: the norm chunk
-          const uint32_t st = stage_ctr % NST;
-          tc::mbar_wait(&S.empty[st], ((stage_ctr / NST) & 1u) ^ 1u);
-          if (lane == 0) {
+    // =========================== TMA producer (one thread) ===========================
+    if (lane == 0) {
+      uint32_t st = 0, ph = 0;  // ring slot and its phase bit
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int r = u % a.R;
+        int t0, t1;
+        range_tiles(r, a.R, a.ntiles, &t0, &t1);
+        for (int t = t0; t < t1; ++t) {
+          const int row0 = static_cast<int>(a.off[a.tile_s0[t]]);
+          for (int kc = 0; kc <= a.KC; ++kc) {  // kc == KC: the norm chunk
+            tc::mbar_wait(&S.empty[st], ph ^ 1u);
             if (kc < a.KC) {
               expect_tx(&S.full[st], kBChunkBytes);
               tma_2d(ring_s + st * kBChunkBytes, &a.tmB, kc * 64, row0, &S.full[st]);
@@ -298,50 +297,62 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
               expect_tx(&S.full[st], kBAugBytes);
               tma_2d(ring_s + st * kBChunkBytes, &a.tmBa, 0, row0, &S.full[st]);
             }
+            if (++st == static_cast<uint32_t>(NST)) {
+              st = 0;
+              ph ^= 1u;
+            }
           }
-          __syncwarp();
         }
       }
     }
+    __syncwarp();
   } else if (warp == 1) {
-    // =========================== MMA issuer ===========================
-    uint32_t stage_ctr = 0, tile_ctr = 0, ua = 0;
-    const uint32_t idesc = tc::idesc_f16_f32(kDenseM, kDenseN);
-    for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
-      const int r = u % a.R;
-      tc::mbar_wait(&S.a_full, ua & 1u);
-      tc::fence_after_sync();
-      int t0, t1;
-      range_tiles(r, a.R, a.ntiles, &t0, &t1);
-      for (int t = t0; t < t1; ++t, ++tile_ctr) {
-        const uint32_t acc = tile_ctr & 1u;
-        tc::mbar_wait(&S.tempty[acc], ((tile_ctr >> 1) & 1u) ^ 1u);
+    // =========================== MMA issuer (one thread) ===========================
+    // one thread runs the whole loop: no warp-wide waits, elections or uniform-register moves per MMA, and the
+    // descriptors are precomputed (the start-address field is the low 14 bits of addr >> 4: adding a byte
+    // offset >> 4 moves it as long as the address stays below 256 KB)
+    if (lane == 0) {
+      uint32_t st = 0, ph = 0, tile_ctr = 0, ua = 0;
+      const uint32_t idesc = tc::idesc_f16_f32(kDenseM, kDenseN);
+      const uint64_t bdesc0 = tc::sw128_desc(ring_s), adesc0 = sw32_desc(ring_s);
+      const int KC = a.KC;
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
+        const int r = u % a.R;
+        tc::mbar_wait(&S.a_full, ua & 1u);
         tc::fence_after_sync();
-        const uint32_t d_tmem = tmem + acc * kDenseN;
-        for (int kc = 0; kc <= a.KC; ++kc, ++stage_ctr) {
-          const uint32_t st = stage_ctr % NST;
-          tc::mbar_wait(&S.full[st], (stage_ctr / NST) & 1u);
+        int t0, t1;
+        range_tiles(r, a.R, a.ntiles, &t0, &t1);
+        for (int t = t0; t < t1; ++t, ++tile_ctr) {
+          const uint32_t acc = tile_ctr & 1u;
+          tc::mbar_wait(&S.tempty[acc], ((tile_ctr >> 1) & 1u) ^ 1u);
           tc::fence_after_sync();
-          if (lane == 0) {
-            const uint32_t bs = ring_s + st * kBChunkBytes;
+          const uint32_t d_tmem = tmem + acc * kDenseN;
+          for (int kc = 0; kc <= KC; ++kc) {
+            tc::mbar_wait(&S.full[st], ph);
+            tc::fence_after_sync();
+            const uint64_t soff = static_cast<uint64_t>((st * kBChunkBytes) >> 4);
             if (a.debug == 2) {
-            } else if (kc < a.KC) {
-#pragma unroll
-              for (int kk = 0; kk < 4; ++kk)
-                umma_tmem_a(d_tmem, tmem + kACol + static_cast<uint32_t>(kc * 32 + kk * 8),
-                            tc::sw128_desc(bs + kk * 32u), idesc, (kc | kk) ? 1u : 0u);
+            } else if (kc < KC) {
+              const uint32_t acol = tmem + kACol + static_cast<uint32_t>(kc * 32);
+              umma_tmem_a(d_tmem, acol, bdesc0 + soff, idesc, kc ? 1u : 0u);
+              umma_tmem_a(d_tmem, acol + 8, bdesc0 + soff + 2, idesc, 1u);
+              umma_tmem_a(d_tmem, acol + 16, bdesc0 + soff + 4, idesc, 1u);
+              umma_tmem_a(d_tmem, acol + 24, bdesc0 + soff + 6, idesc, 1u);
             } else {  // + alpha (h + l): the database row norms
-              umma_tmem_a(d_tmem, tmem + kACol + static_cast<uint32_t>(a.KC * 32), sw32_desc(bs), idesc, 1u);
+              umma_tmem_a(d_tmem, tmem + kACol + static_cast<uint32_t>(KC * 32), adesc0 + soff, idesc, 1u);
             }
             tc::umma_commit(&S.empty[st]);
-            if (kc == a.KC) tc::umma_commit(&S.tfull[acc]);
+            if (++st == static_cast<uint32_t>(NST)) {
+              st = 0;
+              ph ^= 1u;
+            }
           }
-          __syncwarp();
+          tc::umma_commit(&S.tfull[acc]);
         }
+        tc::umma_commit(&S.a_empty);  // the query tile may be overwritten once these MMAs are done
       }
-      if (lane == 0) tc::umma_commit(&S.a_empty);  // the query tile may be overwritten once these MMAs are done
-      __syncwarp();
     }
+    __syncwarp();
   } else if (warp == kInfoWarp) {
     // =========================== tile info (sets, columns, norms) ===========================
     uint32_t tile_ctr = 0;
