@@ -60,13 +60,10 @@
 
 namespace bvss {
 
-// TMEM: two 144-column accumulators [0, 144) and [144, 288), the query tile (A operand) at [304, 504):
-// dpad/2 columns of fp16 pairs + 8 columns for the norm chunk.  A in TMEM takes the A reads off the shared
-// memory port (with A in shared memory the MMA is bound by shared-memory bandwidth: ncu), and a
-// 32-column tcgen05.ld that starts at any set of the second accumulator stays inside the 512-column allocation
+// database rows per tile (MMA N): two 240-column accumulators leave 32 spare TMEM columns, so a 32-column
+// tcgen05.ld that starts at any set inside the second accumulator stays inside the 512-column allocation
 // (a load past it faults: tools/test_tmem_ld.cu); sets start at any column (unaligned loads are legal)
-constexpr int kDenseN = 144;        // database rows per tile (MMA N)
-constexpr uint32_t kACol = 304;     // first TMEM column of the query tile
+constexpr int kDenseN = 240;
 constexpr int kDenseM = 128;      // packed query rows per tile (MMA M)
 constexpr int kEpiSub = 3;                                  // epilogue warps per TMEM lane quarter
 constexpr int kEpiWarpsD = 4 * kEpiSub;
@@ -74,8 +71,10 @@ constexpr int kInfoWarp = 2 + kEpiWarpsD;
 constexpr int kDenseThreads = 32 * (kInfoWarp + 1);        // producer, MMA, epilogue, tile info
 constexpr int kInfoSlotsD = 4;
 constexpr int kDenseMaxStages = 8;
-constexpr uint32_t kBChunkBytes = kDenseN * 128;  // one K chunk of a database tile (18 KB, 1024-aligned)
-constexpr uint32_t kBAugBytes = kDenseN * 32;     // a database tile's norm chunk (4.5 KB)
+constexpr uint32_t kAChunkBytes = kDenseM * 128;  // one 64-element K chunk of the query tile (16 KB)
+constexpr uint32_t kBChunkBytes = kDenseN * 128;  // one K chunk of a database tile (30 KB, 1024-aligned)
+constexpr uint32_t kAAugBytes = kDenseM * 32;     // the query tile's norm chunk (K = 16 halves = 32 B rows)
+constexpr uint32_t kBAugBytes = kDenseN * 32;     // a database tile's norm chunk (7.5 KB)
 
 // SWIZZLE_32B K-major descriptor (8-row atoms of 8 x 32 B, SBO = 256 B; layout type 6, version 1)
 __device__ __forceinline__ uint64_t sw32_desc(uint32_t saddr) {
@@ -89,11 +88,10 @@ __device__ __forceinline__ uint64_t sw32_desc(uint32_t saddr) {
 }
 
 struct DenseArgs {
-  CUtensorMap tmB;              // hd [nvec][dpad] fp16, box {64, 144}, SWIZZLE_128B
-  CUtensorMap tmBa;             // va [nvec][16] fp16 (h, l, 0...), box {16, 144}, SWIZZLE_32B
-  const __half* qd;             // [ntq*128][dpad] fp16 packed query rows (the epilogue writes them into TMEM)
-  int dpad;
-  float alpha;                  // the query norm chunk value: -S_db / (2 S_q)
+  CUtensorMap tmA;              // qd [ntq*128][dpad] fp16, box {64, 128}, SWIZZLE_128B
+  CUtensorMap tmB;              // hd [nvec][dpad] fp16, box {64, 240}, SWIZZLE_128B
+  CUtensorMap tmAa;             // qa [128][16] fp16 (alpha, alpha, 0...), box {16, 128}, SWIZZLE_32B
+  CUtensorMap tmBa;             // va [nvec][16] fp16 (h, l, 0...), box {16, 240}, SWIZZLE_32B
   int KC;                       // dpad / 64
   int stages;
   int ntq;                      // query tiles
@@ -216,32 +214,6 @@ __device__ __forceinline__ float vload_volatile(const float* p) {
   return v;
 }
 
-// D[tmem] (+)= A[tmem] * B[smem]^T, kind::f16 (fp16 in, fp32 accumulate), cta_group::1
-__device__ __forceinline__ void umma_tmem_a(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
-                                            uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-// 32 lanes x 32 bit, 32 consecutive columns <- 32 registers per thread
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
-      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
-      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
-      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
-      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
-      : "memory");
-}
-__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
-               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
-               : "memory");
-}
-
 __device__ __forceinline__ void range_tiles(int r, int R, int ntiles, int* t0, int* t1) {
   *t0 = static_cast<int>((static_cast<int64_t>(ntiles) * r) / R);
   *t1 = static_cast<int>((static_cast<int64_t>(ntiles) * (r + 1)) / R);
@@ -251,7 +223,9 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
   extern __shared__ __align__(1024) uint8_t dsm_raw[];
   __shared__ DenseCtl S;
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
-  const uint32_t ring_s = smem_u32(base);  // stages x 18 KB
+  const uint32_t a_s = smem_u32(base);                                  // KC x 16 KB query tile
+  const uint32_t aa_s = a_s + static_cast<uint32_t>(a.KC) * kAChunkBytes;  // 4 KB norm chunk of the query tile
+  const uint32_t ring_s = aa_s + kAAugBytes;                               // stages x 30 KB
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int NST = a.stages;
   if (tid == 0) {
@@ -259,7 +233,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
       tc::mbar_init(&S.full[s], 1);
       tc::mbar_init(&S.empty[s], 1);
     }
-    tc::mbar_init(&S.a_full, 4);  // one epilogue warp per TMEM lane quarter writes its 32 query rows
+    tc::mbar_init(&S.a_full, 1);
     tc::mbar_init(&S.a_empty, 1);
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&S.tfull[b], 1);
@@ -281,9 +255,13 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
   if (warp == 0) {
     // =========================== TMA producer (one thread) ===========================
     if (lane == 0) {
-      uint32_t st = 0, ph = 0;  // ring slot and its phase bit
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
-        const int r = u % a.R;
+      uint32_t st = 0, ph = 0, ua = 0;  // ring slot and its phase bit
+      for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
+        const int qt = u / a.R, r = u % a.R;
+        tc::mbar_wait(&S.a_empty, (ua & 1u) ^ 1u);
+        expect_tx(&S.a_full, static_cast<uint32_t>(a.KC) * kAChunkBytes + kAAugBytes);
+        for (int kc = 0; kc < a.KC; ++kc) tma_2d(a_s + kc * kAChunkBytes, &a.tmA, kc * 64, qt * kDenseM, &S.a_full);
+        tma_2d(aa_s, &a.tmAa, 0, 0, &S.a_full);
         int t0, t1;
         range_tiles(r, a.R, a.ntiles, &t0, &t1);
         for (int t = t0; t < t1; ++t) {
@@ -308,13 +286,14 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
     __syncwarp();
   } else if (warp == 1) {
     // =========================== MMA issuer (one thread) ===========================
-    // one thread runs the whole loop: no warp-wide waits, elections or uniform-register moves per MMA, and the
-    // descriptors are precomputed (the start-address field is the low 14 bits of addr >> 4: adding a byte
-    // offset >> 4 moves it as long as the address stays below 256 KB)
+    // one thread runs the whole loop (no warp-wide waits or elections per MMA) with precomputed descriptors:
+    // the start-address field is the low 14 bits of addr >> 4, so adding (byte offset >> 4) moves it while the
+    // address stays below 256 KB
     if (lane == 0) {
       uint32_t st = 0, ph = 0, tile_ctr = 0, ua = 0;
       const uint32_t idesc = tc::idesc_f16_f32(kDenseM, kDenseN);
-      const uint64_t bdesc0 = tc::sw128_desc(ring_s), adesc0 = sw32_desc(ring_s);
+      const uint64_t adesc0 = tc::sw128_desc(a_s), bdesc0 = tc::sw128_desc(ring_s);
+      const uint64_t aadesc = sw32_desc(aa_s), badesc0 = sw32_desc(ring_s);
       const int KC = a.KC;
       for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
         const int r = u % a.R;
@@ -333,13 +312,13 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
             const uint64_t soff = static_cast<uint64_t>((st * kBChunkBytes) >> 4);
             if (a.debug == 2) {
             } else if (kc < KC) {
-              const uint32_t acol = tmem + kACol + static_cast<uint32_t>(kc * 32);
-              umma_tmem_a(d_tmem, acol, bdesc0 + soff, idesc, kc ? 1u : 0u);
-              umma_tmem_a(d_tmem, acol + 8, bdesc0 + soff + 2, idesc, 1u);
-              umma_tmem_a(d_tmem, acol + 16, bdesc0 + soff + 4, idesc, 1u);
-              umma_tmem_a(d_tmem, acol + 24, bdesc0 + soff + 6, idesc, 1u);
+              const uint64_t ad = adesc0 + static_cast<uint64_t>((kc * kAChunkBytes) >> 4), bd = bdesc0 + soff;
+              tc::umma_bf16(d_tmem, ad, bd, idesc, kc ? 1u : 0u);
+              tc::umma_bf16(d_tmem, ad + 2, bd + 2, idesc, 1u);
+              tc::umma_bf16(d_tmem, ad + 4, bd + 4, idesc, 1u);
+              tc::umma_bf16(d_tmem, ad + 6, bd + 6, idesc, 1u);
             } else {  // + alpha (h + l): the database row norms
-              umma_tmem_a(d_tmem, tmem + kACol + static_cast<uint32_t>(KC * 32), adesc0 + soff, idesc, 1u);
+              tc::umma_bf16(d_tmem, aadesc, badesc0 + soff, idesc, 1u);
             }
             tc::umma_commit(&S.empty[st]);
             if (++st == static_cast<uint32_t>(NST)) {
@@ -400,35 +379,12 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
     const int quarter = warp & 3;
     const int sub = (warp - 2) >> 2;  // 0 .. kEpiSub-1: the quarter's warps take alternate sets
     const float INF = __int_as_float(0x7f800000);
-    uint32_t tile_ctr = 0, ua = 0;
+    uint32_t tile_ctr = 0;
     unsigned long long n_surv = 0, n_emit = 0;  // statistics, flushed once (a per-survivor global atomic on one
                                                 // address would serialise in L2)
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       const int qt = u / a.R, r = u % a.R;
       const int prow = qt * kDenseM + quarter * 32 + lane;
-      if (sub == 0) {  // this quarter's 32 query rows into TMEM (A operand): lane = row, column = 2 fp16 of K
-        tc::mbar_wait(&S.a_empty, (ua & 1u) ^ 1u);  // the previous unit's MMAs are done reading A
-        tc::fence_after_sync();
-        const uint4* src = reinterpret_cast<const uint4*>(a.qd + static_cast<int64_t>(prow) * a.dpad);
-        const uint32_t ta = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + kACol;
-        for (int c0 = 0; c0 < a.dpad / 2; c0 += 32) {
-          uint32_t w[32];
-#pragma unroll
-          for (int v = 0; v < 8; ++v) {
-            const uint4 x = __ldg(src + c0 / 4 + v);
-            w[4 * v] = x.x; w[4 * v + 1] = x.y; w[4 * v + 2] = x.z; w[4 * v + 3] = x.w;
-          }
-          tmem_st32(ta + static_cast<uint32_t>(c0), w);
-        }
-        const __half2 al = __floats2half2_rn(a.alpha, a.alpha);
-        uint32_t w8[8] = {*reinterpret_cast<const uint32_t*>(&al), 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-        tmem_st8(ta + static_cast<uint32_t>(a.dpad / 2), w8);
-        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-        tc::fence_before_sync();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&S.a_full);
-      }
-      ++ua;
       const int qid = a.lane_qid[prow];
       const bool valid = qid >= 0;
       const float qn = valid ? a.lane_qn[prow] : 0.0f;
@@ -655,15 +611,14 @@ static int encode_map(CUtensorMap* map, const void* base, int64_t rows, int dpad
   return BVSS_OK;
 }
 
-int dense_max_dpad() { return 384; }  // the query tile must fit TMEM next to the accumulators (kACol)
+int dense_max_dpad() { return 512; }
 int dense_tile_rows() { return kDenseN; }
 int dense_epi_sub() { return kEpiSub; }
 
 // stages that fit next to a query tile of KC chunks
 static int dense_stages(int KC, size_t* smem) {
   const size_t budget = 227 * 1024 - sizeof(DenseCtl) - 1024;  // static shared memory (DenseCtl, 1 KB aligned)
-  (void)KC;
-  const size_t fixed = 1024;
+  const size_t fixed = 1024 + static_cast<size_t>(KC) * kAChunkBytes + kAAugBytes;
   if (fixed + 2 * kBChunkBytes > budget) return 0;
   int st = static_cast<int>((budget - fixed) / kBChunkBytes);
   if (st > kDenseMaxStages) st = kDenseMaxStages;
@@ -718,12 +673,10 @@ int launch_dense_hausdorff(const __half* qd, int ntq, const __half* hd, int64_t 
   if (dpad % 64 || dpad > dense_max_dpad()) BVSS_FAIL(BVSS_EUNSUPPORTED, "dense path needs dpad <= 512");
   DenseArgs a;
   std::memset(&a, 0, sizeof(a));
+  BVSS_TRY(encode_map(&a.tmA, qd, static_cast<int64_t>(ntq) * kDenseM, dpad, kDenseM));
   BVSS_TRY(encode_map(&a.tmB, hd, nvec, dpad, kDenseN));
+  BVSS_TRY(encode_map(&a.tmAa, qa, kDenseM, 16, kDenseM, 16, CU_TENSOR_MAP_SWIZZLE_32B));
   BVSS_TRY(encode_map(&a.tmBa, va, nvec, 16, kDenseN, 16, CU_TENSOR_MAP_SWIZZLE_32B));
-  (void)qa;
-  a.qd = qd;
-  a.dpad = dpad;
-  a.alpha = alpha;
   a.KC = dpad / 64;
   size_t smem = 0;
   a.stages = dense_stages(a.KC, &smem);
@@ -739,6 +692,7 @@ int launch_dense_hausdorff(const __half* qd, int ntq, const __half* hd, int64_t 
   a.qE = qE;
   a.tau0 = tau0;
   a.kappa = kappa;
+  (void)alpha;  // (the query tile's norm chunk comes from qa by TMA)
   a.k = k;
   a.lists = lists;
   a.cnt = cnt;
