@@ -167,45 +167,100 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
 }
 __device__ __forceinline__ float fmax3(float a, float b, float c) { return fmaxf(a, fmaxf(b, c)); }  // FMNMX3
 
-// max over the first mvc (1..32) TMEM columns at taddr of this lane's row, with no per-column tests: whole
-// groups of 8 from one 32-column load, and the last 8 columns of the run (overlapping the groups: max is
-// idempotent) from a second 8-column load; runs shorter than 8 take a switch over the count
-__device__ __forceinline__ float set_max(uint32_t taddr, int mvc) {
+// The columns of a set of mvc (1..32) database rows starting at TMEM address taddr, for this lane's query row:
+// whole groups of 8 from one 32-column load (g) and the last 8 columns of the run (t, overlapping the groups:
+// max and max-of-min are idempotent); runs shorter than 8 are the first mvc columns of t.
+struct SetCols {
+  uint32_t g[32], t[8];
+};
+__device__ __forceinline__ void load_set(uint32_t taddr, int mvc, SetCols& c) {
+  if (mvc >= 8) {
+    tmem_ld32(taddr, c.g);
+    tmem_ld8(taddr + static_cast<uint32_t>(mvc - 8), c.t);
+  } else {
+    tmem_ld8(taddr, c.t);
+  }
+  tc::tmem_ld_wait();
+}
+// max over the run's columns (no per-column tests)
+__device__ __forceinline__ float set_max(const SetCols& c, int mvc) {
   const float NINF = __int_as_float(0xff800000);
   float m = NINF;
   if (mvc >= 8) {
-    uint32_t g[32], t[8];
-    tmem_ld32(taddr, g);
-    tmem_ld8(taddr + static_cast<uint32_t>(mvc - 8), t);
-    tc::tmem_ld_wait();
 #define BVSS_MAX8(R, o)                                                                        \
   m = fmax3(m, __uint_as_float(R[o]), __uint_as_float(R[o + 1]));                            \
   m = fmax3(m, __uint_as_float(R[o + 2]), __uint_as_float(R[o + 3]));                        \
   m = fmax3(m, __uint_as_float(R[o + 4]), __uint_as_float(R[o + 5]));                        \
   m = fmax3(m, __uint_as_float(R[o + 6]), __uint_as_float(R[o + 7]));
     switch (mvc >> 3) {
-      case 4: BVSS_MAX8(g, 24) [[fallthrough]];
-      case 3: BVSS_MAX8(g, 16) [[fallthrough]];
-      case 2: BVSS_MAX8(g, 8) [[fallthrough]];
-      default: BVSS_MAX8(g, 0)
+      case 4: BVSS_MAX8(c.g, 24) [[fallthrough]];
+      case 3: BVSS_MAX8(c.g, 16) [[fallthrough]];
+      case 2: BVSS_MAX8(c.g, 8) [[fallthrough]];
+      default: BVSS_MAX8(c.g, 0)
     }
-    BVSS_MAX8(t, 0)
+    BVSS_MAX8(c.t, 0)
 #undef BVSS_MAX8
   } else {
-    uint32_t t[8];
-    tmem_ld8(taddr, t);
-    tc::tmem_ld_wait();
     switch (mvc) {
-      case 7: m = fmaxf(m, __uint_as_float(t[6])); [[fallthrough]];
-      case 6: m = fmaxf(m, __uint_as_float(t[5])); [[fallthrough]];
-      case 5: m = fmaxf(m, __uint_as_float(t[4])); [[fallthrough]];
-      case 4: m = fmaxf(m, __uint_as_float(t[3])); [[fallthrough]];
-      case 3: m = fmaxf(m, __uint_as_float(t[2])); [[fallthrough]];
-      case 2: m = fmaxf(m, __uint_as_float(t[1])); [[fallthrough]];
-      default: m = fmaxf(m, __uint_as_float(t[0]));
+      case 7: m = fmaxf(m, __uint_as_float(c.t[6])); [[fallthrough]];
+      case 6: m = fmaxf(m, __uint_as_float(c.t[5])); [[fallthrough]];
+      case 5: m = fmaxf(m, __uint_as_float(c.t[4])); [[fallthrough]];
+      case 4: m = fmaxf(m, __uint_as_float(c.t[3])); [[fallthrough]];
+      case 3: m = fmaxf(m, __uint_as_float(c.t[2])); [[fallthrough]];
+      case 2: m = fmaxf(m, __uint_as_float(c.t[1])); [[fallthrough]];
+      default: m = fmaxf(m, __uint_as_float(c.t[0]));
     }
   }
   return m;
+}
+// B part of a survivor: max over the run's columns of min over the segment's lanes of D^2 (the same registers)
+__device__ __forceinline__ float set_colmin_max(const SetCols& c, int mvc, float kappa, float qn, bool inseg) {
+  float B = 0.0f;
+  auto col = [&](uint32_t x) {
+    const float d2 = fmaxf(fmaf(kappa, __uint_as_float(x), qn), 0.0f);
+    B = fmaxf(B, __uint_as_float(__reduce_min_sync(0xffffffffu, inseg ? __float_as_uint(d2) : 0xffffffffu)));
+  };
+  if (mvc >= 8) {
+#pragma unroll
+    for (int j8 = 0; j8 < 32; j8 += 8) {
+      if (j8 + 8 > mvc) break;
+#pragma unroll
+      for (int j = j8; j < j8 + 8; ++j) col(c.g[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) col(c.t[j]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (j < mvc) col(c.t[j]);
+  }
+  return B;
+}
+
+__device__ __forceinline__ float vload_volatile(const float* p);
+
+// k-th smallest value of the union of a query's bound lists over nr ranges (from range r on) x kEpiSub warps:
+// any k distinct sets' upper bounds bound the exact k-th H^2 from above, so the union's k-th is a valid (and
+// much tighter) tau.  Warp-wide radix select on the (non-negative) float bits.
+__device__ float union_kth(const float* lq0 /* lists of (q, range 0) */, int R, int r, int nr, int k, int lane) {
+  const int per_range = kEpiSub * k, total = nr * per_range;
+  float v[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int x = lane + 32 * e;
+    v[e] = __int_as_float(0x7f800000);
+    if (x < total) v[e] = vload_volatile(lq0 + static_cast<int64_t>((r + x / per_range) % R) * per_range + x % per_range);
+  }
+  uint32_t prefix = 0;
+  for (int bit = 30; bit >= 0; --bit) {  // largest x with count(< x) < k: the k-th smallest
+    const uint32_t cand = prefix | (1u << bit);
+    int c = 0;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) c += __float_as_uint(v[e]) < cand ? 1 : 0;
+    c = __reduce_add_sync(0xffffffffu, c);
+    if (c < k) prefix = cand;
+  }
+  return __uint_as_float(prefix);
 }
 
 __device__ __forceinline__ float vload_volatile(const float* p) {
@@ -399,6 +454,18 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
         const uint32_t acc = tile_ctr & 1u;
         const int slot = tile_ctr % kInfoSlotsD;
         tau = fminf(tau, other_k);
+        if (((tile_ctr + 8u * static_cast<uint32_t>(sub)) & 31u) == 0u) {  // every 32 tiles (staggered): the k-th of
+          unsigned pend = __ballot_sync(0xffffffffu, valid);               // the union of the query's lists
+          while (pend) {
+            const int ld = __ffs(pend) - 1;
+            const unsigned sm = __shfl_sync(0xffffffffu, segmask, ld);
+            pend &= ~sm;
+            const int qq = __shfl_sync(0xffffffffu, qid, ld);
+            const int nr = a.R < 8 ? a.R : 8;
+            const float uk = union_kth(a.lists + static_cast<int64_t>(qq) * a.R * kEpiSub * a.k, a.R, r, nr, a.k, lane);
+            if ((sm >> lane) & 1u) tau = fminf(tau, uk);
+          }
+        }
         if (valid) {
           other_k = INF;
 #pragma unroll
@@ -417,8 +484,13 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
           const int i = s0 + js;
           const int col0 = inf.col0[js];
           const int mv = inf.mv[js];
+          SetCols cols;  // (sets of <= 32 rows keep their columns in registers for the survivor's B)
           float m = -INF;  // max_v acc (kappa < 0: the min over v of D^2)
-          for (int j0 = 0; j0 < mv; j0 += 32) m = fmaxf(m, set_max(tb + static_cast<uint32_t>(col0 + j0), min(32, mv - j0)));
+          for (int j0 = 0; j0 < mv; j0 += 32) {
+            const int mvc = min(32, mv - j0);
+            load_set(tb + static_cast<uint32_t>(col0 + j0), mvc, cols);
+            m = fmaxf(m, set_max(cols, mvc));
+          }
           const float rq = fmaxf(fmaf(a.kappa, m, qn), 0.0f);
           const unsigned pass = __ballot_sync(0xffffffffu, !valid || rq <= thr);
           unsigned sb = __ballot_sync(0xffffffffu, valid && (pass & segmask) == segmask);
@@ -434,20 +506,16 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
             }
             const bool inseg = (smask >> lane) & 1u;
             const float A = __uint_as_float(__reduce_max_sync(0xffffffffu, inseg ? __float_as_uint(rq) : 0u));
-            float B = 0.0f;
-            for (int j0 = 0; j0 < mv; j0 += 32) {
-              uint32_t g[32];
-              tmem_ld32(tb + static_cast<uint32_t>(col0 + j0), g);
-              tc::tmem_ld_wait();
-#pragma unroll
-              for (int j8 = 0; j8 < 32; j8 += 8) {
-                if (j0 + j8 >= mv) break;
-#pragma unroll
-                for (int j = j8; j < j8 + 8; ++j) {  // columns past the set contribute 0 (never raise the max)
-                  const float d2 = (j0 + j < mv) ? fmaxf(fmaf(a.kappa, __uint_as_float(g[j]), qn), 0.0f) : 0.0f;
-                  const uint32_t cm = __reduce_min_sync(0xffffffffu, inseg ? __float_as_uint(d2) : 0xffffffffu);
-                  B = fmaxf(B, __uint_as_float(cm));
-                }
+            float B;
+            if (mv <= 32) {
+              B = set_colmin_max(cols, mv, a.kappa, qn, inseg);
+            } else {
+              B = 0.0f;
+              for (int j0 = 0; j0 < mv; j0 += 32) {
+                SetCols cb;
+                const int mvc = min(32, mv - j0);
+                load_set(tb + static_cast<uint32_t>(col0 + j0), mvc, cb);
+                B = fmaxf(B, set_colmin_max(cb, mvc, a.kappa, qn, inseg));
               }
             }
             const float h = fmaxf(A, B);
