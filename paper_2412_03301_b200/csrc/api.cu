@@ -911,7 +911,7 @@ int dense_refine_topk(bvss_index* idx, bvss_search_ctx* c, const uint32_t* mask,
     fill[b] += m;
     by_space[32 - fill[b]].push_back(b);
   }
-  const int ntq = static_cast<int>((bins.size() + 3) / 4);
+  const int ntq = static_cast<int>(((bins.size() + 3) / 4 + 1) & ~size_t(1));  // (the kernel pairs query tiles)
   const int64_t rows = static_cast<int64_t>(ntq) * 128;
   std::vector<int32_t> rowmap(rows, -1), rowq(rows, -1);
   for (size_t b = 0; b < bins.size(); ++b) {

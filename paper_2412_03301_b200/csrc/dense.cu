@@ -72,9 +72,13 @@ constexpr int kDenseThreads = 32 * (kInfoWarp + 1);        // producer, MMA, epi
 constexpr int kInfoSlotsD = 4;
 constexpr int kDenseMaxStages = 8;
 constexpr uint32_t kAChunkBytes = kDenseM * 128;  // one 64-element K chunk of the query tile (16 KB)
-constexpr uint32_t kBChunkBytes = kDenseN * 128;  // one K chunk of a database tile (30 KB, 1024-aligned)
+// CTA pairs (cta_group::2): one tcgen05.mma M=256 N=240 per K step covers the two CTAs' query tiles (128
+// rows each, A in each CTA's shared memory) against one database tile whose rows are split between the
+// CTAs (120 each): every SM streams half of the tile, so the L2 -> SM traffic per flop halves
+constexpr int kHalfN = kDenseN / 2;
+constexpr uint32_t kBChunkBytes = kHalfN * 128;   // this CTA's half of one K chunk of a database tile (15 KB)
 constexpr uint32_t kAAugBytes = kDenseM * 32;     // the query tile's norm chunk (K = 16 halves = 32 B rows)
-constexpr uint32_t kBAugBytes = kDenseN * 32;     // a database tile's norm chunk (7.5 KB)
+constexpr uint32_t kBAugBytes = kHalfN * 32;      // this CTA's half of a database tile's norm chunk
 
 // SWIZZLE_32B K-major descriptor (8-row atoms of 8 x 32 B, SBO = 256 B; layout type 6, version 1)
 __device__ __forceinline__ uint64_t sw32_desc(uint32_t saddr) {
@@ -89,9 +93,9 @@ __device__ __forceinline__ uint64_t sw32_desc(uint32_t saddr) {
 
 struct DenseArgs {
   CUtensorMap tmA;              // qd [ntq*128][dpad] fp16, box {64, 128}, SWIZZLE_128B
-  CUtensorMap tmB;              // hd [nvec][dpad] fp16, box {64, 240}, SWIZZLE_128B
+  CUtensorMap tmB;              // hd [nvec][dpad] fp16, box {64, 120}, SWIZZLE_128B
   CUtensorMap tmAa;             // qa [128][16] fp16 (alpha, alpha, 0...), box {16, 128}, SWIZZLE_32B
-  CUtensorMap tmBa;             // va [nvec][16] fp16 (h, l, 0...), box {16, 240}, SWIZZLE_32B
+  CUtensorMap tmBa;             // va [nvec][16] fp16 (h, l, 0...), box {16, 120}, SWIZZLE_32B
   int KC;                       // dpad / 64
   int stages;
   int ntq;                      // query tiles
@@ -115,7 +119,8 @@ struct DenseArgs {
   int64_t mask_stride;          // words per query row (0: one row shared by every query)
   int64_t id_base;
   unsigned long long* stat;     // [2]: survivors, emitted (may be null)
-  int debug;                    // developer switch BVSS_DENSE_DEBUG: 1 = epilogue skips its work, 2 = no MMAs
+  int debug;                    // developer switch BVSS_DENSE_DEBUG: 1 = epilogue skips its work, 2 = no MMAs,
+                                // 3 = no survivor work, 4 = no database loads and no epilogue (timing only)
 };
 
 // per-tile metadata the info warp stages for the epilogue (shared memory): the database sets of the tile
@@ -143,6 +148,64 @@ __device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, int
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
 }
+// the same TMA with the pair's completion barrier in the leader CTA (cta_group::2: the bytes of both CTAs'
+// loads complete on the leader's barrier, whose MMA thread consumes both halves)
+__device__ __forceinline__ void tma_2d_pair(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar_leader) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar_leader)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t cluster_id_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t nclusters_x() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same shared-memory offset in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t map_to(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void expect_tx_remote(uint32_t cluster_addr, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_addr),
+               "r"(bytes)
+               : "memory");
+}
+// the pair's MMA (issued by the leader): D[both CTAs' TMEM] (+)= A[both CTAs' smem] * B[both halves]^T
+__device__ __forceinline__ void umma_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// arrive on the barrier at this offset in both CTAs once the leader's prior MMAs are done
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ void expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
@@ -292,7 +355,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
     tc::mbar_init(&S.a_empty, 1);
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&S.tfull[b], 1);
-      tc::mbar_init(&S.tempty[b], kEpiWarpsD);
+      tc::mbar_init(&S.tempty[b], 2 * kEpiWarpsD);  // (the leader's: both CTAs' epilogue warps arrive)
     }
     for (int b = 0; b < kInfoSlotsD; ++b) {
       tc::mbar_init(&S.info_full[b], 1);
@@ -300,35 +363,51 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
     }
     tc::fence_mbar_init();
   }
-  if (warp == 1) tc::tmem_alloc(&S.tmem_base, 512);
+  cluster_sync_all();  // the leader's barriers exist before the peer's loads and arrivals target them
+  if (warp == 1) {     // the pair's TMEM (same columns in both CTAs), allocated by the same warp of each CTA
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&S.tmem_base))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
   tc::fence_before_sync();
   __syncthreads();
+  cluster_sync_all();
   tc::fence_after_sync();
   const uint32_t tmem = S.tmem_base;
-  const int units = a.ntq * a.R;
+  const uint32_t crank = cluster_rank();
+  const bool leader = crank == 0;
+  const int pair = static_cast<int>(cluster_id_x()), npairs = static_cast<int>(nclusters_x());
+  const int units = (a.ntq / 2) * a.R;  // pair units: (query tile pair, database range); ntq is even
+  const uint32_t full_l0 = map_to(&S.full[0], 0), a_full_l = map_to(&S.a_full, 0);
+  const uint32_t tempty_l0 = map_to(&S.tempty[0], 0);
 
   if (warp == 0) {
-    // =========================== TMA producer (one thread) ===========================
+    // =========================== TMA producer (one thread per CTA) ===========================
+    // each CTA loads its own query tile and its half of every database tile; the bytes of both CTAs complete
+    // on the leader's barriers, armed (expect_tx of the pair's bytes) by the leader's producer
     if (lane == 0) {
       uint32_t st = 0, ph = 0, ua = 0;  // ring slot and its phase bit
-      for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
-        const int qt = u / a.R, r = u % a.R;
+      for (int u = pair; u < units; u += npairs, ++ua) {
+        const int qt = 2 * (u / a.R) + static_cast<int>(crank), r = u % a.R;
         tc::mbar_wait(&S.a_empty, (ua & 1u) ^ 1u);
-        expect_tx(&S.a_full, static_cast<uint32_t>(a.KC) * kAChunkBytes + kAAugBytes);
-        for (int kc = 0; kc < a.KC; ++kc) tma_2d(a_s + kc * kAChunkBytes, &a.tmA, kc * 64, qt * kDenseM, &S.a_full);
-        tma_2d(aa_s, &a.tmAa, 0, 0, &S.a_full);
+        if (leader) expect_tx(&S.a_full, 2u * (static_cast<uint32_t>(a.KC) * kAChunkBytes + kAAugBytes));
+        for (int kc = 0; kc < a.KC; ++kc) tma_2d_pair(a_s + kc * kAChunkBytes, &a.tmA, kc * 64, qt * kDenseM, a_full_l);
+        tma_2d_pair(aa_s, &a.tmAa, 0, 0, a_full_l);
         int t0, t1;
         range_tiles(r, a.R, a.ntiles, &t0, &t1);
         for (int t = t0; t < t1; ++t) {
-          const int row0 = static_cast<int>(a.off[a.tile_s0[t]]);
+          const int row0 = static_cast<int>(a.off[a.tile_s0[t]]) + static_cast<int>(crank) * kHalfN;
           for (int kc = 0; kc <= a.KC; ++kc) {  // kc == KC: the norm chunk
             tc::mbar_wait(&S.empty[st], ph ^ 1u);
-            if (kc < a.KC) {
-              expect_tx(&S.full[st], kBChunkBytes);
-              tma_2d(ring_s + st * kBChunkBytes, &a.tmB, kc * 64, row0, &S.full[st]);
+            const uint32_t fb = full_l0 + st * 8u;
+            if (a.debug == 4) {  // developer: no database loads (stale tiles; times the MMA issue alone)
+              if (leader) tc::mbar_arrive(&S.full[st]);
+            } else if (kc < a.KC) {
+              if (leader) expect_tx(&S.full[st], 2u * kBChunkBytes);
+              tma_2d_pair(ring_s + st * kBChunkBytes, &a.tmB, kc * 64, row0, fb);
             } else {
-              expect_tx(&S.full[st], kBAugBytes);
-              tma_2d(ring_s + st * kBChunkBytes, &a.tmBa, 0, row0, &S.full[st]);
+              if (leader) expect_tx(&S.full[st], 2u * kBAugBytes);
+              tma_2d_pair(ring_s + st * kBChunkBytes, &a.tmBa, 0, row0, fb);
             }
             if (++st == static_cast<uint32_t>(NST)) {
               st = 0;
@@ -344,13 +423,13 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
     // one thread runs the whole loop (no warp-wide waits or elections per MMA) with precomputed descriptors:
     // the start-address field is the low 14 bits of addr >> 4, so adding (byte offset >> 4) moves it while the
     // address stays below 256 KB
-    if (lane == 0) {
+    if (lane == 0 && leader) {
       uint32_t st = 0, ph = 0, tile_ctr = 0, ua = 0;
-      const uint32_t idesc = tc::idesc_f16_f32(kDenseM, kDenseN);
+      const uint32_t idesc = tc::idesc_f16_f32(2 * kDenseM, kDenseN);
       const uint64_t adesc0 = tc::sw128_desc(a_s), bdesc0 = tc::sw128_desc(ring_s);
       const uint64_t aadesc = sw32_desc(aa_s), badesc0 = sw32_desc(ring_s);
       const int KC = a.KC;
-      for (int u = blockIdx.x; u < units; u += gridDim.x, ++ua) {
+      for (int u = pair; u < units; u += npairs, ++ua) {
         const int r = u % a.R;
         tc::mbar_wait(&S.a_full, ua & 1u);
         tc::fence_after_sync();
@@ -368,29 +447,29 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
             if (a.debug == 2) {
             } else if (kc < KC) {
               const uint64_t ad = adesc0 + static_cast<uint64_t>((kc * kAChunkBytes) >> 4), bd = bdesc0 + soff;
-              tc::umma_bf16(d_tmem, ad, bd, idesc, kc ? 1u : 0u);
-              tc::umma_bf16(d_tmem, ad + 2, bd + 2, idesc, 1u);
-              tc::umma_bf16(d_tmem, ad + 4, bd + 4, idesc, 1u);
-              tc::umma_bf16(d_tmem, ad + 6, bd + 6, idesc, 1u);
+              umma_pair(d_tmem, ad, bd, idesc, kc ? 1u : 0u);
+              umma_pair(d_tmem, ad + 2, bd + 2, idesc, 1u);
+              umma_pair(d_tmem, ad + 4, bd + 4, idesc, 1u);
+              umma_pair(d_tmem, ad + 6, bd + 6, idesc, 1u);
             } else {  // + alpha (h + l): the database row norms
-              tc::umma_bf16(d_tmem, aadesc, badesc0 + soff, idesc, 1u);
+              umma_pair(d_tmem, aadesc, badesc0 + soff, idesc, 1u);
             }
-            tc::umma_commit(&S.empty[st]);
+            umma_commit_pair(&S.empty[st]);
             if (++st == static_cast<uint32_t>(NST)) {
               st = 0;
               ph ^= 1u;
             }
           }
-          tc::umma_commit(&S.tfull[acc]);
+          umma_commit_pair(&S.tfull[acc]);
         }
-        tc::umma_commit(&S.a_empty);  // the query tile may be overwritten once these MMAs are done
+        umma_commit_pair(&S.a_empty);  // the query tiles may be overwritten once these MMAs are done
       }
     }
     __syncwarp();
   } else if (warp == kInfoWarp) {
     // =========================== tile info (sets, columns, norms) ===========================
     uint32_t tile_ctr = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    for (int u = pair; u < units; u += npairs) {
       const int r = u % a.R;
       int t0, t1;
       range_tiles(r, a.R, a.ntiles, &t0, &t1);
@@ -437,8 +516,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
     uint32_t tile_ctr = 0;
     unsigned long long n_surv = 0, n_emit = 0;  // statistics, flushed once (a per-survivor global atomic on one
                                                 // address would serialise in L2)
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
-      const int qt = u / a.R, r = u % a.R;
+    for (int u = pair; u < units; u += npairs) {
+      const int qt = 2 * (u / a.R) + static_cast<int>(crank), r = u % a.R;
       const int prow = qt * kDenseM + quarter * 32 + lane;
       const int qid = a.lane_qid[prow];
       const bool valid = qid >= 0;
@@ -478,7 +557,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
         tc::fence_after_sync();
         const int s0 = inf.s0, nsets = inf.nsets;
         const uint32_t tb = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * kDenseN;
-        for (int js = a.debug == 1 ? nsets : sub; js < nsets;) {
+        for (int js = (a.debug == 1 || a.debug == 4) ? nsets : sub; js < nsets;) {
           int nxt = 0;  // the next set of this warp (taken now: the shared-memory atomic's latency overlaps the set)
           if (lane == 0) nxt = atomicAdd(const_cast<int*>(&inf.ctr[quarter]), 1);
           const int i = s0 + js;
@@ -494,6 +573,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
           const float rq = fmaxf(fmaf(a.kappa, m, qn), 0.0f);
           const unsigned pass = __ballot_sync(0xffffffffu, !valid || rq <= thr);
           unsigned sb = __ballot_sync(0xffffffffu, valid && (pass & segmask) == segmask);
+          if (a.debug == 3) sb = 0u;  // developer: no survivor work (times the base epilogue)
           while (sb) {  // warp-uniform: one surviving query segment at a time
             const int leader = __ffs(sb) - 1;
             const unsigned smask = __shfl_sync(0xffffffffu, segmask, leader);
@@ -555,7 +635,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
         tc::fence_before_sync();
         __syncwarp();
         if (lane == 0) {
-          tc::mbar_arrive(&S.tempty[acc]);
+          arrive_remote(tempty_l0 + acc * 8u);  // the leader's barrier (its MMA thread reuses the accumulator)
           tc::mbar_arrive(&S.info_empty[slot]);
         }
       }
@@ -567,10 +647,12 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
       atomicAdd(a.stat + 1, static_cast<unsigned long long>(ne));
     }
   }
+  tc::fence_before_sync();
   __syncthreads();
+  cluster_sync_all();  // neither CTA leaves while the other still signals its barriers or uses the pair's TMEM
   if (warp == 1) {
     tc::fence_after_sync();
-    tc::tmem_dealloc(tmem, 512);
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
 }
 
@@ -742,9 +824,9 @@ int launch_dense_hausdorff(const __half* qd, int ntq, const __half* hd, int64_t 
   DenseArgs a;
   std::memset(&a, 0, sizeof(a));
   BVSS_TRY(encode_map(&a.tmA, qd, static_cast<int64_t>(ntq) * kDenseM, dpad, kDenseM));
-  BVSS_TRY(encode_map(&a.tmB, hd, nvec, dpad, kDenseN));
+  BVSS_TRY(encode_map(&a.tmB, hd, nvec, dpad, kHalfN));
   BVSS_TRY(encode_map(&a.tmAa, qa, kDenseM, 16, kDenseM, 16, CU_TENSOR_MAP_SWIZZLE_32B));
-  BVSS_TRY(encode_map(&a.tmBa, va, nvec, 16, kDenseN, 16, CU_TENSOR_MAP_SWIZZLE_32B));
+  BVSS_TRY(encode_map(&a.tmBa, va, nvec, 16, kHalfN, 16, CU_TENSOR_MAP_SWIZZLE_32B));
   a.KC = dpad / 64;
   size_t smem = 0;
   a.stages = dense_stages(a.KC, &smem);
@@ -775,11 +857,25 @@ int launch_dense_hausdorff(const __half* qd, int ntq, const __half* hd, int64_t 
     const char* e = getenv("BVSS_DENSE_DEBUG");
     a.debug = e ? atoi(e) : 0;
   }
-  const int units = ntq * R;
-  const int grid = units < num_sms ? units : num_sms;
+  if (ntq % 2) BVSS_FAIL(BVSS_EINVAL, "dense kernel: the query tiles come in pairs (ntq must be even)");
+  const int units = (ntq / 2) * R;
+  int pairs = num_sms / 2;
+  if (pairs > units) pairs = units;
   BVSS_CUDA(cudaFuncSetAttribute(dense_hausdorff_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
-  dense_hausdorff_kernel<<<grid, kDenseThreads, smem, st>>>(a);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs));
+  cfg.blockDim = dim3(kDenseThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  BVSS_CUDA(cudaLaunchKernelEx(&cfg, dense_hausdorff_kernel, a));
   return post_launch("dense_hausdorff_kernel", st);
 }
 
