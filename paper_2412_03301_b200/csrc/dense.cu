@@ -180,8 +180,10 @@ __device__ __forceinline__ uint32_t map_to(const void* p, uint32_t rank) {
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// relaxed: the accumulator hand-back needs no memory ordering (tcgen05.wait::ld has completed the TMEM reads,
+// and the release form costs a GPU-scope MEMBAR per tile: ncu)
 __device__ __forceinline__ void arrive_remote(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 __device__ __forceinline__ void expect_tx_remote(uint32_t cluster_addr, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_addr),
@@ -635,7 +637,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
         tc::fence_before_sync();
         __syncwarp();
         if (lane == 0) {
-          arrive_remote(tempty_l0 + acc * 8u);  // the leader's barrier (its MMA thread reuses the accumulator)
+          if (leader) tc::mbar_arrive(&S.tempty[acc]);  // the leader's barrier (its MMA thread reuses the accumulator)
+          else arrive_remote(tempty_l0 + acc * 8u);
           tc::mbar_arrive(&S.info_empty[slot]);
         }
       }
