@@ -1,0 +1,14 @@
+#!/bin/bash
+# Round-2 evidence (developer tool): launch list of the bench step and ncu --set full of the dense kernel,
+# each only after the same command exited 0 without ncu.  Output under gpurun_out/r02/.
+O=gpurun_out/r02; mkdir -p $O
+CMD="bench.py --steps 2 --warmup 3 --no-sweep --recall-queries 200 --no-cpu-baseline --no-e2e"
+KR='regex:scan|select|refine|topk|encode|flyhash|sketch|expand|gather_sample|merge|pad_rows|max_float|dense|gate|alg2|fill'
+timeout 900 python $CMD > $O/plain.log 2>&1 && \
+timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none -k "$KR" -c 3000 --csv --log-file $O/launches.csv \
+  python $CMD > $O/ncu_launch.log 2>&1; echo "rc=$?" >> $O/ncu_launch.log
+CMD1="tools/dense_smoke.py 1000000 2000"
+timeout 300 python $CMD1 > $O/plain1.log 2>&1 && \
+timeout 1500 ncu --set full --clock-control none --import-source on -k regex:dense_hausdorff -c 1 \
+  -o $O/dense_full python $CMD1 > $O/ncu_full.log 2>&1; echo "rc=$?" >> $O/ncu_full.log
+cuobjdump -sass paper_2412_03301_b200/libbvss.so > $O/libbvss.sass 2>/dev/null
