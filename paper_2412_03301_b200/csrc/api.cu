@@ -1170,6 +1170,28 @@ int validate_params(int64_t n, int32_t d, const bvss_params* p) {
   return validate_variants(p);
 }
 
+void free_index_resources(bvss_index* idx);
+
+// Owns a partially built index: on any early return of the build its device buffers, stream and events are
+// released (a failure after the stream was created leaked everything); an adopted vector buffer is
+// left to the caller's handle, which still owns it until the build succeeds.
+struct IndexGuard {
+  bvss_index* p;
+  float* adopted;
+  ~IndexGuard() {
+    if (!p) return;
+    if (p->V == adopted) p->V = nullptr;
+    free_index_resources(p);
+    delete p;
+  }
+  bvss_index* operator->() const { return p; }
+  bvss_index* release() {
+    bvss_index* r = p;
+    p = nullptr;
+    return r;
+  }
+};
+
 // The build (Algs 1, 3, 5).  adopt_V: a device buffer [nvec][d] the index takes over (streaming build) instead of
 // copying `vectors`.
 int build_impl(const float* vectors, const int64_t* set_offsets, int64_t n, int32_t d, const bvss_params* p,
@@ -1200,7 +1222,7 @@ int build_impl(const float* vectors, const int64_t* set_offsets, int64_t n, int3
     std::memcpy(off_h.data(), set_offsets, (n + 1) * sizeof(int64_t));
   }
   BVSS_TRY(check_offsets(off_h.data(), n, "database"));
-  std::unique_ptr<bvss_index> idx(new bvss_index());
+  IndexGuard idx{new bvss_index(), adopt_V};
   idx->device = p->device;
   idx->num_sms = num_sms;
   idx->n = n;
@@ -1260,7 +1282,7 @@ int build_impl(const float* vectors, const int64_t* set_offsets, int64_t n, int3
     BVSS_TRY(dalloc(static_cast<size_t>(nvec) * d * 4, reinterpret_cast<void**>(&idx->V)));
   }
   BVSS_TRY(dalloc((n + 1) * 8, reinterpret_cast<void**>(&idx->off)));
-  if (!adopt_V) BVSS_TRY(to_device(idx.get(), idx->V, vectors, static_cast<size_t>(nvec) * d * 4, dev_ptrs));
+  if (!adopt_V) BVSS_TRY(to_device(idx.p, idx->V, vectors, static_cast<size_t>(nvec) * d * 4, dev_ptrs));
   BVSS_CUDA(cudaMemcpyAsync(idx->off, off_h.data(), (n + 1) * 8, cudaMemcpyHostToDevice, st));
   if (p->flags & BVSS_VALIDATE_FINITE) {
     int* bad;
@@ -1302,18 +1324,18 @@ int build_impl(const float* vectors, const int64_t* set_offsets, int64_t n, int3
   }
   BVSS_TRY(launch_encode(idx->V, nvec, d, idx->Wt, p->m, p->s, p->L, codes, idx->vnorm, idx->hi, idx->lo, idx->vscale,
                          idx->dpad, idx->prows, dst_row, refine_kcs(idx->dpad), num_sms, st));
-  const int cps = chunks_per_set(idx.get());
+  const int cps = chunks_per_set(idx.p);
   BVSS_TRY(dalloc(static_cast<size_t>(n) * cps * 16, &idx->sk));
   BVSS_TRY(dalloc(static_cast<size_t>(n) * 4, reinterpret_cast<void**>(&idx->mass)));
   BVSS_TRY(launch_sketch(codes, p->m, idx->off, n, idx->sketch, idx->sk, idx->mass, n, 1, num_sms, st));
   if (idx->score == 1) BVSS_CUDA(cudaMemsetAsync(idx->mass, 0, static_cast<size_t>(n) * 4, st));  // OVERLAP (R24)
-  if (gated(idx.get())) {  // stage-1 gate (gate.cu): one bit plane per position, bit i = (C_i[p] >= M)
+  if (gated(idx.p)) {  // stage-1 gate (gate.cu): one bit plane per position, bit i = (C_i[p] >= M)
     idx->gW = (n + 31) / 32;
     BVSS_TRY(dalloc(static_cast<size_t>(p->m) * idx->gW * 4, reinterpret_cast<void**>(&idx->planes)));
     BVSS_TRY(launch_gate_planes(idx->sk, n, static_cast<int>(p->m), static_cast<int>(idx->sketch),
                                 static_cast<int>(idx->gate_M), idx->planes, idx->gW, num_sms, st));
   }
-  if (use_tc_scan(idx.get())) {
+  if (use_tc_scan(idx.p)) {
     // strided database sample for the sampled-threshold select
     idx->ns = n < 16384 ? n : 16384;
     BVSS_TRY(dalloc(static_cast<size_t>(idx->ns) * cps * 16, &idx->smp_sk));
@@ -1439,6 +1461,14 @@ int bvss_index_finish(bvss_index* idx) {
 
 void bvss_free_index(bvss_index* idx) {
   if (!idx) return;
+  free_index_resources(idx);
+  delete idx;
+}
+
+}  // extern "C"
+
+namespace {
+void free_index_resources(bvss_index* idx) {
   DeviceGuard g(idx->device);
   if (idx->stream) cudaStreamSynchronize(idx->stream);
   void* ptrs[] = {idx->Wt,    idx->V,     idx->off,   idx->hi,   idx->lo,     idx->vscale, idx->pbase,
@@ -1452,8 +1482,11 @@ void bvss_free_index(bvss_index* idx) {
   for (auto& e : idx->ev)
     if (e) cudaEventDestroy(e);
   if (idx->own_stream) cudaStreamDestroy(idx->own_stream);
-  delete idx;
+  idx->own_stream = idx->stream = nullptr;
 }
+}  // namespace
+
+extern "C" {
 
 int bvss_set_stream(bvss_index* idx, void* stream) {
   if (!idx) BVSS_FAIL(BVSS_EINVAL, "null index");
