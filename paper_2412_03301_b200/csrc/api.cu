@@ -925,6 +925,7 @@ int dense_refine_topk(bvss_index* idx, bvss_search_ctx* c, const uint32_t* mask,
   const int ntiles = ntiles_use;
   int R = static_cast<int>(ceil_div<int64_t>(2 * idx->num_sms, ntq));
   if (R < 4) R = 4;
+  if (const char* e = getenv("BVSS_DENSE_R")) R = atoi(e) > 0 ? atoi(e) : R;  // developer switch: database ranges
   if (R > ntiles) R = ntiles < 1 ? 1 : ntiles;
   const double spl = std::max(1.0, static_cast<double>(idx->n) / (static_cast<double>(R) * dense_epi_sub() * k));
   const double lists_pq = static_cast<double>(R) * dense_epi_sub();  // bound lists per query

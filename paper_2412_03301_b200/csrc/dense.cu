@@ -53,6 +53,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <vector>
 
@@ -119,6 +120,7 @@ struct DenseArgs {
   int64_t mask_stride;          // words per query row (0: one row shared by every query)
   int64_t id_base;
   unsigned long long* stat;     // [2]: survivors, emitted (may be null)
+  unsigned long long* prof;     // developer per-role cycle counters (env BVSS_DENSE_PROF) or null
   int debug;                    // developer switch BVSS_DENSE_DEBUG: 1 = epilogue skips its work, 2 = no MMAs,
                                 // 3 = no survivor work, 4 = no database loads and no epilogue (timing only)
 };
@@ -339,6 +341,18 @@ __device__ __forceinline__ void range_tiles(int r, int R, int ntiles, int* t0, i
   *t1 = static_cast<int>((static_cast<int64_t>(ntiles) * (r + 1)) / R);
 }
 
+// developer instrumentation: cycles spent in `call` added to prof[slot] (one counter per role and wait)
+#define DPROF(slot, call)                                                   \
+  do {                                                                      \
+    if (a.prof) {                                                           \
+      const long long t0_ = clock64();                                      \
+      call;                                                                 \
+      if ((threadIdx.x & 31) == 0) atomicAdd(&a.prof[slot], (unsigned long long)(clock64() - t0_)); \
+    } else {                                                                \
+      call;                                                                 \
+    }                                                                       \
+  } while (0)
+
 __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const __grid_constant__ DenseArgs a) {
   extern __shared__ __align__(1024) uint8_t dsm_raw[];
   __shared__ DenseCtl S;
@@ -382,6 +396,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
   const int units = (a.ntq / 2) * a.R;  // pair units: (query tile pair, database range); ntq is even
   const uint32_t full_l0 = map_to(&S.full[0], 0), a_full_l = map_to(&S.a_full, 0);
   const uint32_t tempty_l0 = map_to(&S.tempty[0], 0);
+  const long long t_start = clock64();
 
   if (warp == 0) {
     // =========================== TMA producer (one thread per CTA) ===========================
@@ -400,7 +415,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
         for (int t = t0; t < t1; ++t) {
           const int row0 = static_cast<int>(a.off[a.tile_s0[t]]) + static_cast<int>(crank) * kHalfN;
           for (int kc = 0; kc <= a.KC; ++kc) {  // kc == KC: the norm chunk
-            tc::mbar_wait(&S.empty[st], ph ^ 1u);
+            DPROF(0, tc::mbar_wait(&S.empty[st], ph ^ 1u));
             const uint32_t fb = full_l0 + st * 8u;
             if (a.debug == 4) {  // developer: no database loads (stale tiles; times the MMA issue alone)
               if (leader) tc::mbar_arrive(&S.full[st]);
@@ -439,11 +454,11 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
         range_tiles(r, a.R, a.ntiles, &t0, &t1);
         for (int t = t0; t < t1; ++t, ++tile_ctr) {
           const uint32_t acc = tile_ctr & 1u;
-          tc::mbar_wait(&S.tempty[acc], ((tile_ctr >> 1) & 1u) ^ 1u);
+          DPROF(1, tc::mbar_wait(&S.tempty[acc], ((tile_ctr >> 1) & 1u) ^ 1u));
           tc::fence_after_sync();
           const uint32_t d_tmem = tmem + acc * kDenseN;
           for (int kc = 0; kc <= KC; ++kc) {
-            tc::mbar_wait(&S.full[st], ph);
+            DPROF(2, tc::mbar_wait(&S.full[st], ph));
             tc::fence_after_sync();
             const uint64_t soff = static_cast<uint64_t>((st * kBChunkBytes) >> 4);
             if (a.debug == 2) {
@@ -553,9 +568,9 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
           for (int o = 1; o < kEpiSub; ++o) other_k = fminf(other_k, vload_volatile(lq + ((sub + o) % kEpiSub) * a.k + a.k - 1));
         }
         float thr = tau + E;
-        tc::mbar_wait(&S.info_full[slot], (tile_ctr / kInfoSlotsD) & 1u);
+        DPROF(3, tc::mbar_wait(&S.info_full[slot], (tile_ctr / kInfoSlotsD) & 1u));
         const DenseInfo& inf = S.info[slot];
-        tc::mbar_wait(&S.tfull[acc], (tile_ctr >> 1) & 1u);
+        DPROF(4, tc::mbar_wait(&S.tfull[acc], (tile_ctr >> 1) & 1u));
         tc::fence_after_sync();
         const int s0 = inf.s0, nsets = inf.nsets;
         const uint32_t tb = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * kDenseN;
@@ -650,6 +665,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
       atomicAdd(a.stat + 1, static_cast<unsigned long long>(ne));
     }
   }
+  if (a.prof && lane == 0) atomicAdd(&a.prof[8 + (warp == 0 ? 0 : warp == 1 ? 1 : warp == kInfoWarp ? 2 : 3)],
+                                     (unsigned long long)(clock64() - t_start));
   tc::fence_before_sync();
   __syncthreads();
   cluster_sync_all();  // neither CTA leaves while the other still signals its barriers or uses the pair's TMEM
@@ -860,6 +877,13 @@ int launch_dense_hausdorff(const __half* qd, int ntq, const __half* hd, int64_t 
     const char* e = getenv("BVSS_DENSE_DEBUG");
     a.debug = e ? atoi(e) : 0;
   }
+  static unsigned long long* prof = nullptr;
+  a.prof = nullptr;
+  if (getenv("BVSS_DENSE_PROF")) {
+    if (!prof) cudaMalloc(&prof, 16 * sizeof(unsigned long long));
+    cudaMemsetAsync(prof, 0, 16 * sizeof(unsigned long long), st);
+    a.prof = prof;
+  }
   if (ntq % 2) BVSS_FAIL(BVSS_EINVAL, "dense kernel: the query tiles come in pairs (ntq must be even)");
   const int units = (ntq / 2) * R;
   int pairs = num_sms / 2;
@@ -879,7 +903,19 @@ int launch_dense_hausdorff(const __half* qd, int ntq, const __half* hd, int64_t 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   BVSS_CUDA(cudaLaunchKernelEx(&cfg, dense_hausdorff_kernel, a));
-  return post_launch("dense_hausdorff_kernel", st);
+  BVSS_TRY(post_launch("dense_hausdorff_kernel", st));
+  if (a.prof) {  // developer instrumentation: per-CTA Mcycles per role and wait (epilogue: per warp)
+    unsigned long long h[16];
+    cudaMemcpyAsync(h, a.prof, sizeof(h), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    const double g = 2.0 * pairs, ew = g * kEpiWarpsD;
+    fprintf(stderr,
+            "[dense prof] Mcycles per CTA: producer %.1f (empty wait %.1f) | mma %.1f (tempty %.1f, full %.1f) | "
+            "info %.1f | per epilogue warp %.1f (info wait %.1f, tfull wait %.1f)\n",
+            h[8] / g / 1e6, h[0] / g / 1e6, h[9] / (g / 2) / 1e6, h[1] / (g / 2) / 1e6, h[2] / (g / 2) / 1e6,
+            h[10] / g / 1e6, h[11] / ew / 1e6, h[3] / ew / 1e6, h[4] / ew / 1e6);
+  }
+  return BVSS_OK;
 }
 
 }  // namespace bvss
