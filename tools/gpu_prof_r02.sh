@@ -11,4 +11,4 @@ CMD1="tools/dense_smoke.py 1000000 2000"
 timeout 300 python $CMD1 > $O/plain1.log 2>&1 && \
 timeout 1500 ncu --set full --clock-control none --import-source on -k regex:dense_hausdorff -c 1 \
   -o $O/dense_full python $CMD1 > $O/ncu_full.log 2>&1; echo "rc=$?" >> $O/ncu_full.log
-cuobjdump -sass paper_2412_03301_b200/libbvss.so > $O/libbvss.sass 2>/dev/null
+BVSS_DENSE_PROF=1 timeout 300 python tools/dense_smoke.py 1000000 2000 > $O/dense_prof.log 2>&1
