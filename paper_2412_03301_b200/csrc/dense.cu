@@ -415,7 +415,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
         for (int t = t0; t < t1; ++t) {
           const int row0 = static_cast<int>(a.off[a.tile_s0[t]]) + static_cast<int>(crank) * kHalfN;
           for (int kc = 0; kc <= a.KC; ++kc) {  // kc == KC: the norm chunk
-            DPROF(0, tc::mbar_wait(&S.empty[st], ph ^ 1u));
+            DPROF(0, tc::mbar_wait_sleep(&S.empty[st], ph ^ 1u));
             const uint32_t fb = full_l0 + st * 8u;
             if (a.debug == 4) {  // developer: no database loads (stale tiles; times the MMA issue alone)
               if (leader) tc::mbar_arrive(&S.full[st]);
@@ -507,7 +507,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
             ml[c] = static_cast<int16_t>(a.off[s0 + j + 1] - v0);
           }
         }
-        tc::mbar_wait(&S.info_empty[slot], ((tile_ctr / kInfoSlotsD) & 1u) ^ 1u);
+        tc::mbar_wait_sleep(&S.info_empty[slot], ((tile_ctr / kInfoSlotsD) & 1u) ^ 1u);
 #pragma unroll
         for (int c = 0; c < (kDenseN + 31) / 32; ++c) {
           const int j = lane + 32 * c;
@@ -568,9 +568,9 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
           for (int o = 1; o < kEpiSub; ++o) other_k = fminf(other_k, vload_volatile(lq + ((sub + o) % kEpiSub) * a.k + a.k - 1));
         }
         float thr = tau + E;
-        DPROF(3, tc::mbar_wait(&S.info_full[slot], (tile_ctr / kInfoSlotsD) & 1u));
+        DPROF(3, tc::mbar_wait_sleep(&S.info_full[slot], (tile_ctr / kInfoSlotsD) & 1u));
         const DenseInfo& inf = S.info[slot];
-        DPROF(4, tc::mbar_wait(&S.tfull[acc], (tile_ctr >> 1) & 1u));
+        DPROF(4, tc::mbar_wait_sleep(&S.tfull[acc], (tile_ctr >> 1) & 1u));
         tc::fence_after_sync();
         const int s0 = inf.s0, nsets = inf.nsets;
         const uint32_t tb = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * kDenseN;

@@ -300,15 +300,15 @@ __device__ __forceinline__ void stage_rows(float* dst, int stride4, const float*
 
 __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
     const float* __restrict__ approx, const int32_t* __restrict__ cand, const int32_t* __restrict__ count, int T, int k,
-    const float* __restrict__ V, const int64_t* __restrict__ off, int64_t id_base, int d, int d4, int stride4, int RB,
+    const float* __restrict__ V, const int64_t* __restrict__ off, int64_t id_base, int d, int d4, int stride4, int RB, int RBV,
     const float* __restrict__ Qv, const int64_t* __restrict__ qoff, const float* __restrict__ qnorm, float vmax2,
     float c1, float c2, int exact_all, int32_t* __restrict__ win_g, float* __restrict__ ex_g,
     int64_t* __restrict__ out_ids, float* __restrict__ out_dist, int64_t* __restrict__ fixup_counter, int metric,
     const float* __restrict__ approx_err) {
   extern __shared__ __align__(16) float txs[];
-  float* Qs = txs;                                          // [RB][stride4*4]
-  float* Vs0 = Qs + static_cast<int64_t>(RB) * stride4 * 4;   // [RB][stride4*4]
-  float* red = Vs0 + static_cast<int64_t>(RB) * stride4 * 4;  // [kTxThreads][4] partial sums
+  float* Qs = txs;                                            // [RB][stride4*4] query rows
+  float* Vs0 = Qs + static_cast<int64_t>(RB) * stride4 * 4;     // [2][RBV][stride4*4] set rows, double-buffered:
+  float* red = Vs0 + static_cast<int64_t>(2 * RBV) * stride4 * 4;  // the next block stages during this one's math
   __shared__ TxSmem S;
   __shared__ float bred[32];
   const int q = blockIdx.x;
@@ -439,24 +439,37 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
       v0 = off[cid];
       mi = static_cast<int>(off[cid + 1] - v0);
     }
-    *src = V + (v0 + static_cast<int64_t>(vb) * RB) * d;
-    *rows = min(RB, mi - vb * RB);
+    *src = V + (v0 + static_cast<int64_t>(vb) * RBV) * d;
+    *rows = min(RBV, mi - vb * RBV);
     return mi;
   };
-  int w = 0, vb = 0;
+  int w = 0, vb = 0, buf = 0;
+  if (nw > 0) {  // stage the first job
+    const float* src0;
+    int rows0;
+    job_rows(0, 0, &src0, &rows0);
+    stage_rows(Vs0, stride4, src0, rows0, d, d4);
+  }
   while (w < nw) {
     const float* src;
     int rowsv;
     const int mi = job_rows(w, vb, &src, &rowsv);
     int nw_ = w, nvb = vb + 1;  // next job
-    if (nvb * RB >= mi) {
+    if (nvb * RBV >= mi) {
       nw_ = w + 1;
       nvb = 0;
     }
-    stage_rows(Vs0, stride4, src, rowsv, d, d4);  // (two CTAs per SM overlap one's staging with the other's math)
-    tc::cp_async_wait<0>();
+    if (nw_ < nw) {  // prefetch the next job into the other buffer, then wait for this one (all but 1 group)
+      const float* nsrc;
+      int nrows;
+      job_rows(nw_, nvb, &nsrc, &nrows);
+      stage_rows(Vs0 + static_cast<int64_t>(buf ^ 1) * RBV * stride4 * 4, stride4, nsrc, nrows, d, d4);
+      tc::cp_async_wait<1>();
+    } else {
+      tc::cp_async_wait<0>();
+    }
     __syncthreads();
-    const float* Vb = Vs0;
+    const float* Vb = Vs0 + static_cast<int64_t>(buf) * RBV * stride4 * 4;
     for (int qb = 0; qb < nqb; ++qb) {
       const int rowsq = min(RB, mq - qb * RB);
       if (nqb > 1) {  // query blocks restaged per (candidate block, query block): only for m_q > RB
@@ -561,9 +574,10 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
         S.hv = 0.0f;
       }
     }
-    __syncthreads();
+    __syncthreads();  // (the next iteration's prefetch overwrites this buffer)
     w = nw_;
     vb = nvb;
+    buf ^= 1;
   }
   __syncthreads();
   // ---- 3. the k smallest by (exact H^2, id)
@@ -632,9 +646,9 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
 
 size_t topk_smem_bytes(int T) { return static_cast<size_t>(T) * 12; }
 
-// shared memory of topk_exact_kernel for row blocks of RB rows
-static size_t tx_smem(int stride4, int RB) {
-  return (2 * static_cast<size_t>(RB) * stride4 + kTxThreads) * 16;
+// shared memory of topk_exact_kernel: RB query rows, two buffers of RBV set rows, the partial sums
+static size_t tx_smem(int stride4, int RB, int RBV) {
+  return (static_cast<size_t>(RB + 2 * RBV) * stride4 + kTxThreads) * 16;
 }
 
 int launch_topk_fixup(const float* approx, const int32_t* cand, const int32_t* count, int T, int k, const float* V,
@@ -646,14 +660,17 @@ int launch_topk_fixup(const float* approx, const int32_t* cand, const int32_t* c
   if (k > T) BVSS_FAIL(BVSS_EINVAL, "k > T");
   const int d4 = (d + 3) / 4;
   const int stride4 = (d4 & 1) ? d4 + 2 : d4 + 1;  // odd stride in float4: conflict-free row-parallel reads
-  int RB = 32;
-  while (RB > 4 && tx_smem(stride4, RB) > 110 * 1024) RB >>= 1;  // two CTAs per SM
-  if (scratch && tx_smem(stride4, RB) <= 110 * 1024) {
-    const size_t smem = tx_smem(stride4, RB);
+  int RB = 32, RBV = 16;  // query rows per block; set rows per (double-buffered) block
+  while (RB > 4 && tx_smem(stride4, RB, RBV) > 110 * 1024) {  // two CTAs per SM
+    if (RBV > 4) RBV >>= 1;
+    else RB >>= 1;
+  }
+  if (scratch && tx_smem(stride4, RB, RBV) <= 110 * 1024) {
+    const size_t smem = tx_smem(stride4, RB, RBV);
     int32_t* win = static_cast<int32_t*>(scratch);
     float* ex = reinterpret_cast<float*>(win + static_cast<int64_t>(nq) * T);
     BVSS_CUDA(cudaFuncSetAttribute(topk_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    topk_exact_kernel<<<nq, kTxThreads, smem, st>>>(approx, cand, count, T, k, V, off, id_base, d, d4, stride4, RB, Qv,
+    topk_exact_kernel<<<nq, kTxThreads, smem, st>>>(approx, cand, count, T, k, V, off, id_base, d, d4, stride4, RB, RBV, Qv,
                                                     qoff, qnorm, vmax2, c1, c2, exact_all, win, ex, out_ids, out_dist,
                                                     fixup_counter, metric, approx_err);
     BVSS_TRY(post_launch("topk_exact_kernel", st));
