@@ -508,6 +508,9 @@ def main_ours(args):
             "sweep": sweep,
             "filter_scan_GBps": round(scan_gbs, 1) if scan_gbs is not None else None,
             "stages_ms": {kk: round(v, 3) for kk, v in stages.items()},
+            "stages_ms_T2000": ({kk: round(full_points[2000]["stats"][kk], 3) for kk in
+                                 ("ms_encode", "ms_scan", "ms_select", "ms_refine", "ms_topk", "ms_total")}
+                                if 2000 in full_points else None),
             "dense": {"survivors_per_step": st_sum.get("dense_survivors", 0) / K,
                       "emitted_per_step": st_sum.get("dense_emitted", 0) / K,
                       "pairs_per_step": d_pairs, "mma_flop_per_step": st_sum.get("dense_flop", 0) / K},
