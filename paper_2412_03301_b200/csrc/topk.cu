@@ -427,6 +427,61 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
     S.jmi[x] = static_cast<int>(off[cid + 1] - v0);
   }
   __syncthreads();
+  // Warp path (every window candidate and the query have <= 32 rows, d % 4 == 0): one warp per candidate,
+  // lane j = set row j streamed from global memory in 32-float chunks, the query rows resident in shared
+  // memory; acc[i] = D^2(q_i, v_j) by fp32 direct differences (FFMA2); row minima by redux over the lanes,
+  // column minima per lane: no CTA-wide barrier per candidate (the CTA path below needs four per row block)
+  bool small = nqb == 1 && mq <= 32 && (d & 3) == 0 && nw <= kTxCache;
+  if (small)
+    for (int x = tid; x < nw; x += blockDim.x) small &= S.jmi[x] <= 32;
+  small = __syncthreads_and(small) != 0;
+  if (small) {
+    tc::cp_async_wait<0>();
+    __syncthreads();
+    const float4* Q4 = reinterpret_cast<const float4*>(Qs);
+    for (int x = warp; x < nw; x += kTxThreads / 32) {
+      const int64_t v0 = S.jv0[x];
+      const int mi = S.jmi[x];
+      const bool vj = lane < mi;
+      const float4* vrow = reinterpret_cast<const float4*>(V + (v0 + (vj ? lane : 0)) * d);
+      float2 acc[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) acc[i] = make_float2(0.f, 0.f);
+      const float2 m1 = make_float2(-1.0f, -1.0f);
+      for (int c0 = 0; c0 < d4; c0 += 8) {
+        float4 v[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) v[c] = (c0 + c < d4) ? __ldg(vrow + c0 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          if (i >= mq) break;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            if (c0 + c >= d4) break;
+            const float4 qv = Q4[i * stride4 + c0 + c];
+            const float2 t0 = __ffma2_rn(make_float2(v[c].x, v[c].y), m1, make_float2(qv.x, qv.y));
+            const float2 t1 = __ffma2_rn(make_float2(v[c].z, v[c].w), m1, make_float2(qv.z, qv.w));
+            acc[i] = __ffma2_rn(t0, t0, acc[i]);
+            acc[i] = __ffma2_rn(t1, t1, acc[i]);
+          }
+        }
+      }
+      float colmin = __int_as_float(0x7f800000), hq = 0.0f, sq = 0.0f, mn = __int_as_float(0x7f800000);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        if (i >= mq) break;
+        const float a2 = acc[i].x + acc[i].y;
+        colmin = fminf(colmin, a2);
+        const float rm = __uint_as_float(__reduce_min_sync(0xffffffffu, vj ? __float_as_uint(a2) : 0x7f800000u));
+        hq = fmaxf(hq, rm);
+        sq += sqrtf(rm);
+        mn = fminf(mn, rm);
+      }
+      const float hv = __uint_as_float(__reduce_max_sync(0xffffffffu, vj ? __float_as_uint(colmin) : 0u));
+      if (lane == 0)
+        ex[x] = metric == 1 ? sq / static_cast<float>(mq) : (metric == 2 ? mn : fmaxf(hq, hv));
+    }
+  } else {
   // job sequence: (window entry w, set-row block vb)
   auto job_rows = [&](int w, int vb, const float** src, int* rows) {
     int64_t v0;
@@ -579,6 +634,7 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
     vb = nvb;
     buf ^= 1;
   }
+  }  // (CTA path)
   __syncthreads();
   // ---- 3. the k smallest by (exact H^2, id)
   if (nw <= kTxCache) {  // one pass: every window entry's rank among the (distance, id) keys (unique ids)
