@@ -513,6 +513,7 @@ def main_ours(args):
             "stages_ms_T2000": ({kk: round(full_points[2000]["stats"][kk], 3) for kk in
                                  ("ms_encode", "ms_scan", "ms_select", "ms_refine", "ms_topk", "ms_total")}
                                 if 2000 in full_points else None),
+            "fixup_sets_per_query": round(st_sum.get("fixup_sets", 0) / K / cfg.nq, 2),
             "dense": {"survivors_per_step": st_sum.get("dense_survivors", 0) / K,
                       "emitted_per_step": st_sum.get("dense_emitted", 0) / K,
                       "pairs_per_step": d_pairs, "mma_flop_per_step": st_sum.get("dense_flop", 0) / K},

@@ -113,7 +113,7 @@ int launch_topk_fixup(const float* approx, const int32_t* cand, const int32_t* c
                       const int64_t* off, int64_t id_base, int d, const float* Qv, const int64_t* qoff,
                       const float* qnorm, float vmax2, float c1, float c2, int exact_all, int64_t* out_ids,
                       float* out_dist, int nq, int64_t* fixup_counter, void* scratch, int metric,
-                      const float* approx_err, cudaStream_t st);
+                      const float* approx_err, int max_rows, int max_mq, cudaStream_t st);
 int launch_merge_topk(const int64_t* ids, const float* dist, int P, int64_t nq, int k, int64_t* out_ids,
                       float* out_dist, cudaStream_t st);
 int launch_select_bitmap(int key_size, const void* keys, int64_t key_stride, int64_t n, int nq, SelectState st,
@@ -264,6 +264,7 @@ struct bvss_index {
   int num_sms = 148;
   int64_t n = 0, nvec = 0;
   int d = 0, dpad = 0;
+  int max_rows = 0;             // largest set (rows): selects the packed K6 variant
   uint32_t m = 0, s = 0, L = 0, sketch = 0;
   uint64_t seed = 0;
   int terms = 3;
@@ -795,7 +796,7 @@ int refine_topk(bvss_index* idx, bvss_search_ctx* c, int64_t* out_ids_dev, float
   BVSS_TRY(idx->ws.get("topk_scratch", static_cast<size_t>(nq) * c->T * 8, &scratch));
   BVSS_TRY(launch_topk_fixup(c->approx, c->cand, c->count, c->T, c->k, idx->V, idx->off, c->id_base, idx->d, c->qv,
                              c->qoff, c->qnorm, idx->vmax2, c1, c2, exact_all, out_ids_dev, out_dist_dev, nq, fix,
-                             scratch, idx->metric, c->approx_err, idx->stream));
+                             scratch, idx->metric, c->approx_err, idx->max_rows, c->max_mq, idx->stream));
   cudaEventRecord(idx->ev[6], idx->stream);
   idx->stats.kernel_launches += 1;
   return BVSS_OK;
@@ -1013,7 +1014,7 @@ int dense_refine_topk(bvss_index* idx, bvss_search_ctx* c, const uint32_t* mask,
   BVSS_TRY(idx->ws.get("topk_scratch", static_cast<size_t>(nq) * cap * 8, &scratch));
   BVSS_TRY(launch_topk_fixup(vals, ids, cnt, static_cast<int>(cap), k, idx->V, idx->off, c->id_base, idx->d, c->qv,
                              c->qoff, c->qnorm, idx->vmax2, c1, c2, 0, out_ids_dev, out_dist_dev, nq, fix, scratch, 0,
-                             nullptr, idx->stream));
+                             nullptr, idx->max_rows, c->max_mq, idx->stream));
   cudaEventRecord(idx->ev[6], idx->stream);
   idx->stats.kernel_launches += 1;
   idx->stats.dense_batches += 1;
@@ -1301,6 +1302,8 @@ int build_impl(const float* vectors, const int64_t* set_offsets, int64_t n, int3
   for (int64_t i = 0; i < n; ++i) pb[i + 1] = pb[i] + ((off_h[i + 1] - off_h[i] + 7) & ~int64_t(7));
   idx->prows = pb[n];
   idx->off_h = off_h;
+  for (int64_t i = 0; i < n; ++i)
+    idx->max_rows = static_cast<int>(std::max<int64_t>(idx->max_rows, std::min<int64_t>(off_h[i + 1] - off_h[i], 1 << 30)));
   BVSS_TRY(dalloc((n + 1) * 8, reinterpret_cast<void**>(&idx->pbase)));
   BVSS_CUDA(cudaMemcpyAsync(idx->pbase, pb.data(), (n + 1) * 8, cudaMemcpyHostToDevice, st));
   BVSS_TRY(dalloc(static_cast<size_t>(idx->prows) * idx->dpad * 2, reinterpret_cast<void**>(&idx->hi)));
@@ -1730,7 +1733,7 @@ int bvss_refine(bvss_index* idx, const float* queries, const int64_t* query_offs
   BVSS_TRY(idx->ws.get("topk_scratch", static_cast<size_t>(nq) * T * 8, &scratch));
   BVSS_TRY(launch_topk_fixup(c->approx, c->cand, c->count, T, k, idx->V, idx->off, 0, idx->d, c->qv, c->qoff, c->qnorm,
                              idx->vmax2, c1, c2, exact_all, oid, odist, static_cast<int>(nq), nullptr, scratch,
-                             idx->metric, c->approx_err, idx->stream));
+                             idx->metric, c->approx_err, idx->max_rows, c->max_mq, idx->stream));
   BVSS_TRY(from_device(idx, out_ids, oid, static_cast<size_t>(nq) * k * 8, dev));
   BVSS_TRY(from_device(idx, out_dist, odist, static_cast<size_t>(nq) * k * 4, dev));
   if (out_approx && c->approx) BVSS_TRY(from_device(idx, out_approx, c->approx, static_cast<size_t>(nq) * T * 4, dev));

@@ -275,6 +275,7 @@ struct TxSmem {
   uint32_t rowmin[256];   // min_v D^2 of each query row (kMaxMq)
   uint32_t colmin[32];    // min_q D^2 of each set row of the current block
   uint32_t prefix, need, wcount;
+  int nb, rows;           // SMALL: candidates and set rows of the current batch
   float hv;
   unsigned long long best;
 };
@@ -298,6 +299,12 @@ __device__ __forceinline__ void stage_rows(float* dst, int stride4, const float*
   tc::cp_async_commit();
 }
 
+// SMALL (host-chosen: every set and query set has <= 32 rows, d % 4 == 0): phase 2 packs the set rows of
+// the window candidates densely onto warp lanes (see the comment at the SMALL branch)
+constexpr int kSmRows = 1024;  // SMALL: set rows per batch (their column minima live in smem)
+constexpr int kSmRm = 1024;    // SMALL: (candidate, query row) row minima per batch
+
+template <bool SMALL>
 __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
     const float* __restrict__ approx, const int32_t* __restrict__ cand, const int32_t* __restrict__ count, int T, int k,
     const float* __restrict__ V, const int64_t* __restrict__ off, int64_t id_base, int d, int d4, int stride4, int RB, int RBV,
@@ -413,6 +420,174 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
   const int nw = static_cast<int>(S.wcount);
   if (tid == 0 && fixup_counter) atomicAdd(reinterpret_cast<unsigned long long*>(fixup_counter), nw);
   // ---- 2. exact H^2 of every window candidate
+  if constexpr (SMALL) {
+    // Set rows on lanes, packed: the window candidates' rows are concatenated (candidate order) and every
+    // warp job takes 32 consecutive rows x one group of <= 16 query rows, so a lane never idles on a short
+    // set (sizes 4..32 left ~45 % of the lanes of a one-candidate-per-warp mapping empty).  Lane = one set
+    // row streamed from global memory in 8-float4 chunks (register double buffer: the next chunk loads
+    // during this one's math); query rows resident in smem (broadcast reads); acc[i] = D^2(q_i, v) by fp32
+    // direct differences (FFMA2).  Row minima: a segmented min over the lanes of one candidate (shuffles),
+    // then one smem atomicMin per (candidate, query row) by the segment's first lane; column minima: one
+    // smem atomicMin per (lane, job).  Batches bound the smem minima (kSmRows rows, kSmRm row minima).
+    int* rs = reinterpret_cast<int*>(Qs + static_cast<int64_t>(32) * stride4 * 4);  // [kTxCache + 1] row starts
+    uint32_t* rowm = reinterpret_cast<uint32_t*>(rs + kTxCache + 1);                 // [kSmRm]
+    uint32_t* colm = rowm + kSmRm;                                                   // [kSmRows]
+    uint8_t* rc = reinterpret_cast<uint8_t*>(colm + kSmRows);                        // [kSmRows] row -> candidate
+    const float4* Q4 = reinterpret_cast<const float4*>(Qs);
+    stage_rows(Qs, stride4, Qv + q0 * d, mq, d, d4);
+    const int G = (mq + 15) >> 4;  // query-row groups of <= 16 rows (acc[16] per lane)
+    for (int xb = 0; xb < nw;) {
+      const int nc = min(kTxCache, nw - xb);
+      for (int t = tid; t < nc; t += blockDim.x) {
+        const int64_t cid = static_cast<int64_t>(cq[win[xb + t]]) - id_base;
+        const int64_t v0 = off[cid];
+        S.jv0[t] = v0;
+        S.jmi[t] = static_cast<int>(off[cid + 1] - v0);
+      }
+      __syncthreads();
+      if (warp == 0) {  // the batch: the longest prefix within both smem caps (a single candidate always fits)
+        int run = 0, nb = 0;
+        for (int t0 = 0; t0 < nc; t0 += 32) {
+          const int t = t0 + lane;
+          const int mi = t < nc ? S.jmi[t] : 0;
+          int incl = mi;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += u;
+          }
+          const int end = run + incl;
+          const bool fits = t < nc && end <= kSmRows && (t + 1) * mq <= kSmRm;
+          const int nf = __popc(__ballot_sync(0xffffffffu, fits));  // fits is a prefix of the lanes
+          if (lane < nf) rs[t] = end - mi;
+          nb = t0 + nf;
+          if (nf > 0) run = __shfl_sync(0xffffffffu, end, nf - 1);
+          if (nf < 32) break;
+        }
+        if (lane == 0) {
+          rs[nb] = run;
+          S.nb = nb;
+          S.rows = run;
+        }
+      }
+      __syncthreads();
+      const int nb = S.nb, rows = S.rows;
+      for (int t = tid; t < nb; t += blockDim.x)
+        for (int r = rs[t]; r < rs[t + 1]; ++r) rc[r] = static_cast<uint8_t>(t);
+      for (int t = tid; t < nb * mq; t += blockDim.x) rowm[t] = 0x7f800000u;
+      for (int t = tid; t < rows; t += blockDim.x) colm[t] = 0x7f800000u;
+      tc::cp_async_wait<0>();
+      __syncthreads();
+      const int njobs = ((rows + 31) >> 5) * G;
+      for (int job = warp; job < njobs; job += kTxThreads / 32) {
+        const int rb = job / G, g = job - rb * G;
+        const int i0 = g * mq / G, gn = (g + 1) * mq / G - i0;
+        const int r = rb * 32 + lane;
+        const bool valid = r < rows;
+        const int rr = valid ? r : rows - 1;  // idle lanes recompute the last row (results dropped)
+        const int x = rc[rr];
+        const float4* vrow = reinterpret_cast<const float4*>(V + (S.jv0[x] + (rr - rs[x])) * d);
+        const float4* Qg = Q4 + static_cast<int64_t>(i0) * stride4;
+        float2 acc[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] = make_float2(0.f, 0.f);
+        const float2 m1 = make_float2(-1.0f, -1.0f);
+        auto chunk = [&](const float4(&v)[8], int c0) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            if (i >= gn) break;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const float4 qv = Qg[i * stride4 + c0 + c];
+              const float2 t0 = __ffma2_rn(make_float2(v[c].x, v[c].y), m1, make_float2(qv.x, qv.y));
+              const float2 t1 = __ffma2_rn(make_float2(v[c].z, v[c].w), m1, make_float2(qv.z, qv.w));
+              acc[i] = __ffma2_rn(t0, t0, acc[i]);
+              acc[i] = __ffma2_rn(t1, t1, acc[i]);
+            }
+          }
+        };
+        float4 va[8], vb[8];
+        bool have_a = d4 >= 8;
+        if (have_a) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) va[c] = __ldg(vrow + c);
+        }
+        int c0 = 0;
+        for (; c0 + 16 <= d4; c0 += 16) {
+#pragma unroll
+          for (int c = 0; c < 8; ++c) vb[c] = __ldg(vrow + c0 + 8 + c);
+          chunk(va, c0);
+          have_a = c0 + 24 <= d4;
+          if (have_a) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) va[c] = __ldg(vrow + c0 + 16 + c);
+          }
+          chunk(vb, c0 + 8);
+        }
+        if (have_a) {
+          chunk(va, c0);
+          c0 += 8;
+        }
+        for (; c0 < d4; ++c0) {  // tail: d4 % 8 float4
+          const float4 v = __ldg(vrow + c0);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            if (i >= gn) break;
+            const float4 qv = Qg[i * stride4 + c0];
+            const float2 t0 = __ffma2_rn(make_float2(v.x, v.y), m1, make_float2(qv.x, qv.y));
+            const float2 t1 = __ffma2_rn(make_float2(v.z, v.w), m1, make_float2(qv.z, qv.w));
+            acc[i] = __ffma2_rn(t0, t0, acc[i]);
+            acc[i] = __ffma2_rn(t1, t1, acc[i]);
+          }
+        }
+        // segments: lanes of one candidate are consecutive; idle lanes get unique keys
+        const int key = valid ? x : -1 - lane;
+        unsigned same = 0u;
+#pragma unroll
+        for (int b = 0; b < 5; ++b) {
+          const int ko = __shfl_down_sync(0xffffffffu, key, 1 << b);
+          if (lane + (1 << b) < 32 && ko == key) same |= 1u << b;
+        }
+        const int kprev = __shfl_up_sync(0xffffffffu, key, 1);
+        const bool head = valid && (lane == 0 || kprev != key);
+        float cm = __int_as_float(0x7f800000);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          if (i >= gn) break;
+          float m = acc[i].x + acc[i].y;
+          cm = fminf(cm, m);
+#pragma unroll
+          for (int b = 0; b < 5; ++b) {
+            const float u = __shfl_down_sync(0xffffffffu, m, 1 << b);
+            if (same & (1u << b)) m = fminf(m, u);
+          }
+          if (head) atomicMin(&rowm[x * mq + i0 + i], __float_as_uint(m));
+        }
+        if (valid) atomicMin(&colm[r], __float_as_uint(cm));
+      }
+      __syncthreads();
+      for (int t = warp; t < nb; t += kTxThreads / 32) {  // H^2 = max(max_q min_v D^2, max_v min_q D^2) etc.
+        const int mi = rs[t + 1] - rs[t];
+        const float rm = lane < mq ? __uint_as_float(rowm[t * mq + lane]) : 0.0f;
+        float val;
+        if (metric == 1) {
+          float sq = lane < mq ? sqrtf(rm) : 0.0f;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+          val = sq / static_cast<float>(mq);  // MeanMin (a distance)
+        } else if (metric == 2) {
+          val = __uint_as_float(__reduce_min_sync(0xffffffffu, lane < mq ? __float_as_uint(rm) : 0x7f800000u));
+        } else {
+          const uint32_t hq = __reduce_max_sync(0xffffffffu, __float_as_uint(rm));
+          const uint32_t hv = __reduce_max_sync(0xffffffffu, lane < mi ? colm[rs[t] + lane] : 0u);
+          val = __uint_as_float(max(hq, hv));
+        }
+        if (lane == 0) ex[xb + t] = val;
+      }
+      __syncthreads();
+      xb += nb;
+    }
+  } else {
   const int nqb = (mq + RB - 1) / RB;
   const int rowsq0 = min(RB, mq);
   if (nqb == 1) stage_rows(Qs, stride4, Qv + q0 * d, rowsq0, d, d4);
@@ -427,61 +602,7 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
     S.jmi[x] = static_cast<int>(off[cid + 1] - v0);
   }
   __syncthreads();
-  // Warp path (every window candidate and the query have <= 32 rows, d % 4 == 0): one warp per candidate,
-  // lane j = set row j streamed from global memory in 32-float chunks, the query rows resident in shared
-  // memory; acc[i] = D^2(q_i, v_j) by fp32 direct differences (FFMA2); row minima by redux over the lanes,
-  // column minima per lane: no CTA-wide barrier per candidate (the CTA path below needs four per row block)
-  bool small = nqb == 1 && mq <= 32 && (d & 3) == 0 && nw <= kTxCache;
-  if (small)
-    for (int x = tid; x < nw; x += blockDim.x) small &= S.jmi[x] <= 32;
-  small = __syncthreads_and(small) != 0;
-  if (small) {
-    tc::cp_async_wait<0>();
-    __syncthreads();
-    const float4* Q4 = reinterpret_cast<const float4*>(Qs);
-    for (int x = warp; x < nw; x += kTxThreads / 32) {
-      const int64_t v0 = S.jv0[x];
-      const int mi = S.jmi[x];
-      const bool vj = lane < mi;
-      const float4* vrow = reinterpret_cast<const float4*>(V + (v0 + (vj ? lane : 0)) * d);
-      float2 acc[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) acc[i] = make_float2(0.f, 0.f);
-      const float2 m1 = make_float2(-1.0f, -1.0f);
-      for (int c0 = 0; c0 < d4; c0 += 8) {
-        float4 v[8];
-#pragma unroll
-        for (int c = 0; c < 8; ++c) v[c] = (c0 + c < d4) ? __ldg(vrow + c0 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          if (i >= mq) break;
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            if (c0 + c >= d4) break;
-            const float4 qv = Q4[i * stride4 + c0 + c];
-            const float2 t0 = __ffma2_rn(make_float2(v[c].x, v[c].y), m1, make_float2(qv.x, qv.y));
-            const float2 t1 = __ffma2_rn(make_float2(v[c].z, v[c].w), m1, make_float2(qv.z, qv.w));
-            acc[i] = __ffma2_rn(t0, t0, acc[i]);
-            acc[i] = __ffma2_rn(t1, t1, acc[i]);
-          }
-        }
-      }
-      float colmin = __int_as_float(0x7f800000), hq = 0.0f, sq = 0.0f, mn = __int_as_float(0x7f800000);
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        if (i >= mq) break;
-        const float a2 = acc[i].x + acc[i].y;
-        colmin = fminf(colmin, a2);
-        const float rm = __uint_as_float(__reduce_min_sync(0xffffffffu, vj ? __float_as_uint(a2) : 0x7f800000u));
-        hq = fmaxf(hq, rm);
-        sq += sqrtf(rm);
-        mn = fminf(mn, rm);
-      }
-      const float hv = __uint_as_float(__reduce_max_sync(0xffffffffu, vj ? __float_as_uint(colmin) : 0u));
-      if (lane == 0)
-        ex[x] = metric == 1 ? sq / static_cast<float>(mq) : (metric == 2 ? mn : fmaxf(hq, hv));
-    }
-  } else {
+  {
   // job sequence: (window entry w, set-row block vb)
   auto job_rows = [&](int w, int vb, const float** src, int* rows) {
     int64_t v0;
@@ -635,6 +756,7 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
     buf ^= 1;
   }
   }  // (CTA path)
+  }  // (!SMALL)
   __syncthreads();
   // ---- 3. the k smallest by (exact H^2, id)
   if (nw <= kTxCache) {  // one pass: every window entry's rank among the (distance, id) keys (unique ids)
@@ -711,11 +833,22 @@ int launch_topk_fixup(const float* approx, const int32_t* cand, const int32_t* c
                       const int64_t* off, int64_t id_base, int d, const float* Qv, const int64_t* qoff,
                       const float* qnorm, float vmax2, float c1, float c2, int exact_all, int64_t* out_ids,
                       float* out_dist, int nq, int64_t* fixup_counter, void* scratch /*[nq][T] x 8 B*/, int metric,
-                      const float* approx_err, cudaStream_t st) {
+                      const float* approx_err, int max_rows, int max_mq, cudaStream_t st) {
   if (nq <= 0) return BVSS_OK;
   if (k > T) BVSS_FAIL(BVSS_EINVAL, "k > T");
   const int d4 = (d + 3) / 4;
   const int stride4 = (d4 & 1) ? d4 + 2 : d4 + 1;  // odd stride in float4: conflict-free row-parallel reads
+  const size_t smem_small = static_cast<size_t>(32) * stride4 * 16 + (kTxCache + 1) * 4 + (kSmRm + kSmRows) * 4 + kSmRows;
+  if (scratch && (d & 3) == 0 && max_rows <= 32 && max_mq <= 32 && smem_small <= 110 * 1024) {
+    int32_t* win = static_cast<int32_t*>(scratch);
+    float* ex = reinterpret_cast<float*>(win + static_cast<int64_t>(nq) * T);
+    auto kfn = topk_exact_kernel<true>;
+    BVSS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_small)));
+    kfn<<<nq, kTxThreads, smem_small, st>>>(approx, cand, count, T, k, V, off, id_base, d, d4, stride4, 32, 0, Qv, qoff,
+                                            qnorm, vmax2, c1, c2, exact_all, win, ex, out_ids, out_dist, fixup_counter,
+                                            metric, approx_err);
+    return post_launch("topk_exact_kernel", st);
+  }
   int RB = 32, RBV = 16;  // query rows per block; set rows per (double-buffered) block
   while (RB > 4 && tx_smem(stride4, RB, RBV) > 110 * 1024) {  // two CTAs per SM
     if (RBV > 4) RBV >>= 1;
@@ -725,8 +858,9 @@ int launch_topk_fixup(const float* approx, const int32_t* cand, const int32_t* c
     const size_t smem = tx_smem(stride4, RB, RBV);
     int32_t* win = static_cast<int32_t*>(scratch);
     float* ex = reinterpret_cast<float*>(win + static_cast<int64_t>(nq) * T);
-    BVSS_CUDA(cudaFuncSetAttribute(topk_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    topk_exact_kernel<<<nq, kTxThreads, smem, st>>>(approx, cand, count, T, k, V, off, id_base, d, d4, stride4, RB, RBV, Qv,
+    auto kfn = topk_exact_kernel<false>;
+    BVSS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    kfn<<<nq, kTxThreads, smem, st>>>(approx, cand, count, T, k, V, off, id_base, d, d4, stride4, RB, RBV, Qv,
                                                     qoff, qnorm, vmax2, c1, c2, exact_all, win, ex, out_ids, out_dist,
                                                     fixup_counter, metric, approx_err);
     BVSS_TRY(post_launch("topk_exact_kernel", st));
