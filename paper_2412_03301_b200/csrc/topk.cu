@@ -11,6 +11,8 @@
 // top-k is always inside the window, so the result does not depend on the
 // tensor-core rounding.  With E = +inf (refine_terms = 0) the kernel is a plain
 // SIMT exact refine of every candidate (correctness anchor).
+#include <cstdlib>
+
 #include "tc.cuh"
 
 namespace bvss {
@@ -301,6 +303,9 @@ __device__ __forceinline__ void stage_rows(float* dst, int stride4, const float*
 
 // SMALL (host-chosen: every set and query set has <= 32 rows, d % 4 == 0): phase 2 packs the set rows of
 // the window candidates densely onto warp lanes (see the comment at the SMALL branch)
+__device__ int g_k6prof_on;                // debug (BVSS_K6_PROF): per-phase clock sums of the SMALL kernel
+__device__ unsigned long long g_k6prof[8];
+
 constexpr int kSmRows = 1024;  // SMALL: set rows per batch (their column minima live in smem)
 constexpr int kSmRm = 1024;    // SMALL: (candidate, query row) row minima per batch
 
@@ -331,6 +336,8 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
   int32_t* win = win_g + static_cast<int64_t>(q) * T;
   float* ex = ex_g + static_cast<int64_t>(q) * T;
   if (tid == 0) S.wcount = 0;
+  const bool prof = SMALL && g_k6prof_on;
+  long long pt0 = prof ? clock64() : 0, pt1 = 0, pt2 = 0, pt3 = 0;
   // ---- 1. window
   float W = __int_as_float(0x7f800000);
   if (!exact_all && kk > 0) {
@@ -420,22 +427,33 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
   const int nw = static_cast<int>(S.wcount);
   if (tid == 0 && fixup_counter) atomicAdd(reinterpret_cast<unsigned long long*>(fixup_counter), nw);
   // ---- 2. exact H^2 of every window candidate
+  if (prof) pt1 = clock64();
   if constexpr (SMALL) {
-    // Set rows on lanes, packed: the window candidates' rows are concatenated (candidate order) and every
-    // warp job takes 32 consecutive rows x one group of <= 16 query rows, so a lane never idles on a short
-    // set (sizes 4..32 left ~45 % of the lanes of a one-candidate-per-warp mapping empty).  Lane = one set
-    // row streamed from global memory in 8-float4 chunks (register double buffer: the next chunk loads
-    // during this one's math); query rows resident in smem (broadcast reads); acc[i] = D^2(q_i, v) by fp32
-    // direct differences (FFMA2).  Row minima: a segmented min over the lanes of one candidate (shuffles),
-    // then one smem atomicMin per (candidate, query row) by the segment's first lane; column minima: one
-    // smem atomicMin per (lane, job).  Batches bound the smem minima (kSmRows rows, kSmRm row minima).
-    int* rs = reinterpret_cast<int*>(Qs + static_cast<int64_t>(32) * stride4 * 4);  // [kTxCache + 1] row starts
-    uint32_t* rowm = reinterpret_cast<uint32_t*>(rs + kTxCache + 1);                 // [kSmRm]
-    uint32_t* colm = rowm + kSmRm;                                                   // [kSmRows]
-    uint8_t* rc = reinterpret_cast<uint8_t*>(colm + kSmRows);                        // [kSmRows] row -> candidate
+    // Set rows on lanes, packed, staged through shared memory.  The window candidates' rows are concatenated
+    // (candidate order) into blocks of kRB = 64 rows; lane l of a warp owns rows l and l + 32 of a block, so
+    // a short set never leaves a lane idle (sizes 4..32 left ~45 % of the lanes of a one-candidate-per-warp
+    // mapping empty).  The CTA is two warp groups of four warps; a group walks its blocks (wg, wg + 2, ...)
+    // in d-chunks of kCH float4: the group's 128 threads copy a chunk of all 64 rows with coalesced 16-byte
+    // cp.async (8 threads per 128-byte row piece) into a two-slot ring, the next chunk loading during this
+    // one's math, and each of the four warps takes a quarter of the query rows (<= 8, acc in registers).
+    // Staging matters: per-lane global loads of 32 different rows cost 32 L1 wavefronts per instruction and
+    // saturated the LSU data pipe (83 %); here a warp's copy instruction covers 4 rows (4 wavefronts).
+    // acc = D^2(q_i, v) by fp32 direct differences (FFMA2); the query rows are broadcast smem reads, each
+    // feeding 8 FFMA2 (two set rows).  Row minima: a segmented min over the lanes of one candidate
+    // (shuffles), then one smem atomicMin per (candidate, query row) by the segment's first lane; column
+    // minima: smem atomicMin per (row, warp).  Batches bound the smem minima (kSmRows rows, kSmRm minima).
+    constexpr int kRB = 64, kCH = 8, kRS = kCH + 1, kD = 2;
+    float4* ring = reinterpret_cast<float4*>(Qs + static_cast<int64_t>(33) * stride4 * 4);  // [2][kD][kRB][kRS]
+    int* rs = reinterpret_cast<int*>(ring + 2 * kD * kRB * kRS);                              // [kTxCache + 1]
+    uint32_t* rowm = reinterpret_cast<uint32_t*>(rs + kTxCache + 1);                         // [kSmRm]
+    uint32_t* colm = rowm + kSmRm;                                                           // [kSmRows]
+    uint8_t* rc = reinterpret_cast<uint8_t*>(colm + kSmRows);                                // row -> candidate
     const float4* Q4 = reinterpret_cast<const float4*>(Qs);
     stage_rows(Qs, stride4, Qv + q0 * d, mq, d, d4);
-    const int G = (mq + 15) >> 4;  // query-row groups of <= 16 rows (acc[16] per lane)
+    const int wg = warp >> 2, w4 = warp & 3, tg = tid & 127;
+    const int i0 = w4 * mq / 4, gn = (w4 + 1) * mq / 4 - i0;  // this warp's query rows (<= 8)
+    const int nch = (d4 + kCH - 1) / kCH;
+    const int crow = tg >> 3, ccol = tg & 7;  // copy role: rows crow + 16 j (j < 4), float4 column ccol
     for (int xb = 0; xb < nw;) {
       const int nc = min(kTxCache, nw - xb);
       for (int t = tid; t < nc; t += blockDim.x) {
@@ -478,93 +496,101 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
       for (int t = tid; t < rows; t += blockDim.x) colm[t] = 0x7f800000u;
       tc::cp_async_wait<0>();
       __syncthreads();
-      const int njobs = ((rows + 31) >> 5) * G;
-      for (int job = warp; job < njobs; job += kTxThreads / 32) {
-        const int rb = job / G, g = job - rb * G;
-        const int i0 = g * mq / G, gn = (g + 1) * mq / G - i0;
-        const int r = rb * 32 + lane;
-        const bool valid = r < rows;
-        const int rr = valid ? r : rows - 1;  // idle lanes recompute the last row (results dropped)
-        const int x = rc[rr];
-        const float4* vrow = reinterpret_cast<const float4*>(V + (S.jv0[x] + (rr - rs[x])) * d);
-        const float4* Qg = Q4 + static_cast<int64_t>(i0) * stride4;
-        float2 acc[16];
+      if (prof && xb == 0) pt2 = clock64();
+      const long long pj0 = prof ? clock64() : 0;
+      const int nrb = (rows + kRB - 1) / kRB;
+      const int nel = (nrb > wg ? (nrb - wg + 1) / 2 : 0) * nch;  // this group's (block, chunk) elements
+      const float4* src[4];
+      auto issue = [&](int e) {  // cp.async of element e into ring slot e % kD (one commit group per call)
+        if (e < nel) {
+          const int bi = e / nch, ch = e - bi * nch;
+          if (ch == 0) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i) acc[i] = make_float2(0.f, 0.f);
-        const float2 m1 = make_float2(-1.0f, -1.0f);
-        auto chunk = [&](const float4(&v)[8], int c0) {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            if (i >= gn) break;
-#pragma unroll
-            for (int c = 0; c < 8; ++c) {
-              const float4 qv = Qg[i * stride4 + c0 + c];
-              const float2 t0 = __ffma2_rn(make_float2(v[c].x, v[c].y), m1, make_float2(qv.x, qv.y));
-              const float2 t1 = __ffma2_rn(make_float2(v[c].z, v[c].w), m1, make_float2(qv.z, qv.w));
-              acc[i] = __ffma2_rn(t0, t0, acc[i]);
-              acc[i] = __ffma2_rn(t1, t1, acc[i]);
+            for (int j = 0; j < 4; ++j) {
+              const int rr = min((wg + 2 * bi) * kRB + crow + 16 * j, rows - 1);  // past the end: a copy of the last row
+              const int xx = rc[rr];
+              src[j] = reinterpret_cast<const float4*>(V + (S.jv0[xx] + (rr - rs[xx])) * d);
             }
           }
-        };
-        float4 va[8], vb[8];
-        bool have_a = d4 >= 8;
-        if (have_a) {
+          float4* dst = ring + static_cast<int64_t>((wg * kD + e % kD) * kRB) * kRS;
+          const int c = ch * kCH + ccol;
 #pragma unroll
-          for (int c = 0; c < 8; ++c) va[c] = __ldg(vrow + c);
+          for (int j = 0; j < 4; ++j)
+            tc::cp_async16(smem_u32(dst + (crow + 16 * j) * kRS + ccol), src[j] + (c < d4 ? c : 0), c < d4 ? 16u : 0u);
         }
-        int c0 = 0;
-        for (; c0 + 16 <= d4; c0 += 16) {
+        tc::cp_async_commit();
+      };
+      float2 a0[8], a1[8];
 #pragma unroll
-          for (int c = 0; c < 8; ++c) vb[c] = __ldg(vrow + c0 + 8 + c);
-          chunk(va, c0);
-          have_a = c0 + 24 <= d4;
-          if (have_a) {
+      for (int i = 0; i < 8; ++i) a0[i] = a1[i] = make_float2(0.f, 0.f);
+      const float2 m1 = make_float2(-1.0f, -1.0f);
+      issue(0);
+      for (int e = 0; e < nel; ++e) {
+        tc::cp_async_wait<0>();
+        if (wg == 0)  // element e landed; e - 1 consumed by the whole group
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+        else
+          asm volatile("bar.sync 2, 128;" ::: "memory");
+        issue(e + 1);
+        const int bi = e / nch, ch = e - bi * nch;
+        const float4* slot = ring + static_cast<int64_t>((wg * kD + e % kD) * kRB) * kRS;
+        const int cn = min(kCH, d4 - ch * kCH);
 #pragma unroll
-            for (int c = 0; c < 8; ++c) va[c] = __ldg(vrow + c0 + 16 + c);
-          }
-          chunk(vb, c0 + 8);
-        }
-        if (have_a) {
-          chunk(va, c0);
-          c0 += 8;
-        }
-        for (; c0 < d4; ++c0) {  // tail: d4 % 8 float4
-          const float4 v = __ldg(vrow + c0);
+        for (int c = 0; c < kCH; ++c) {
+          if (c >= cn) break;
+          const float4 va = slot[lane * kRS + c], vb = slot[(lane + 32) * kRS + c];
+          const float2 va0 = make_float2(va.x, va.y), va1 = make_float2(va.z, va.w);
+          const float2 vb0 = make_float2(vb.x, vb.y), vb1 = make_float2(vb.z, vb.w);
+          const float4* qc = Q4 + static_cast<int64_t>(i0) * stride4 + ch * kCH + c;
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
+          for (int i = 0; i < 8; ++i) {
             if (i >= gn) break;
-            const float4 qv = Qg[i * stride4 + c0];
-            const float2 t0 = __ffma2_rn(make_float2(v.x, v.y), m1, make_float2(qv.x, qv.y));
-            const float2 t1 = __ffma2_rn(make_float2(v.z, v.w), m1, make_float2(qv.z, qv.w));
-            acc[i] = __ffma2_rn(t0, t0, acc[i]);
-            acc[i] = __ffma2_rn(t1, t1, acc[i]);
+            const float4 q = qc[i * stride4];
+            const float2 q0 = make_float2(q.x, q.y), q1 = make_float2(q.z, q.w);
+            const float2 ta0 = __ffma2_rn(va0, m1, q0), ta1 = __ffma2_rn(va1, m1, q1);
+            const float2 tb0 = __ffma2_rn(vb0, m1, q0), tb1 = __ffma2_rn(vb1, m1, q1);
+            a0[i] = __ffma2_rn(ta0, ta0, a0[i]);
+            a1[i] = __ffma2_rn(tb0, tb0, a1[i]);
+            a0[i] = __ffma2_rn(ta1, ta1, a0[i]);
+            a1[i] = __ffma2_rn(tb1, tb1, a1[i]);
           }
         }
-        // segments: lanes of one candidate are consecutive; idle lanes get unique keys
-        const int key = valid ? x : -1 - lane;
-        unsigned same = 0u;
+        if (ch == nch - 1) {  // block done: row / column minima of its two 32-row halves
+          auto fold = [&](float2(&a)[8], int r) {
+            const bool valid = r < rows;
+            const int x = rc[valid ? r : rows - 1];
+            const int key = valid ? x : -1 - lane;  // idle lanes: unique keys
+            unsigned same = 0u;
 #pragma unroll
-        for (int b = 0; b < 5; ++b) {
-          const int ko = __shfl_down_sync(0xffffffffu, key, 1 << b);
-          if (lane + (1 << b) < 32 && ko == key) same |= 1u << b;
+            for (int b = 0; b < 5; ++b) {
+              const int ko = __shfl_down_sync(0xffffffffu, key, 1 << b);
+              if (lane + (1 << b) < 32 && ko == key) same |= 1u << b;
+            }
+            const int kprev = __shfl_up_sync(0xffffffffu, key, 1);
+            const bool head = valid && (lane == 0 || kprev != key);
+            float cm = __int_as_float(0x7f800000);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              if (i >= gn) break;
+              float m = a[i].x + a[i].y;
+              a[i] = make_float2(0.f, 0.f);
+              cm = fminf(cm, m);
+#pragma unroll
+              for (int b = 0; b < 5; ++b) {
+                const float u = __shfl_down_sync(0xffffffffu, m, 1 << b);
+                if (same & (1u << b)) m = fminf(m, u);
+              }
+              if (head) atomicMin(&rowm[x * mq + i0 + i], __float_as_uint(m));
+            }
+            if (valid && gn > 0) atomicMin(&colm[r], __float_as_uint(cm));
+          };
+          const int rbase = (wg + 2 * bi) * kRB;
+          fold(a0, rbase + lane);
+          fold(a1, rbase + 32 + lane);
         }
-        const int kprev = __shfl_up_sync(0xffffffffu, key, 1);
-        const bool head = valid && (lane == 0 || kprev != key);
-        float cm = __int_as_float(0x7f800000);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          if (i >= gn) break;
-          float m = acc[i].x + acc[i].y;
-          cm = fminf(cm, m);
-#pragma unroll
-          for (int b = 0; b < 5; ++b) {
-            const float u = __shfl_down_sync(0xffffffffu, m, 1 << b);
-            if (same & (1u << b)) m = fminf(m, u);
-          }
-          if (head) atomicMin(&rowm[x * mq + i0 + i], __float_as_uint(m));
-        }
-        if (valid) atomicMin(&colm[r], __float_as_uint(cm));
       }
+      tc::cp_async_wait<0>();
+      if (prof && lane == 0) atomicAdd(&g_k6prof[6], static_cast<unsigned long long>(clock64() - pj0));
       __syncthreads();
       for (int t = warp; t < nb; t += kTxThreads / 32) {  // H^2 = max(max_q min_v D^2, max_v min_q D^2) etc.
         const int mi = rs[t + 1] - rs[t];
@@ -758,6 +784,7 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
   }  // (CTA path)
   }  // (!SMALL)
   __syncthreads();
+  if (prof) pt3 = clock64();
   // ---- 3. the k smallest by (exact H^2, id)
   if (nw <= kTxCache) {  // one pass: every window entry's rank among the (distance, id) keys (unique ids)
     unsigned long long* keys = reinterpret_cast<unsigned long long*>(S.jv0);  // row ranges are done with
@@ -779,6 +806,15 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
     for (int r = nw + tid; r < k; r += blockDim.x) {
       oi[r] = -1;
       od[r] = __int_as_float(0x7f800000);
+    }
+    if (prof && tid == 0) {
+      const long long pt4 = clock64();
+      atomicAdd(&g_k6prof[0], static_cast<unsigned long long>(pt1 - pt0));
+      atomicAdd(&g_k6prof[1], static_cast<unsigned long long>(pt2 - pt1));
+      atomicAdd(&g_k6prof[2], static_cast<unsigned long long>(pt3 - pt2));
+      atomicAdd(&g_k6prof[3], static_cast<unsigned long long>(pt4 - pt3));
+      atomicAdd(&g_k6prof[4], 1ull);
+      atomicAdd(&g_k6prof[5], static_cast<unsigned long long>(nw));
     }
     return;
   }
@@ -838,15 +874,33 @@ int launch_topk_fixup(const float* approx, const int32_t* cand, const int32_t* c
   if (k > T) BVSS_FAIL(BVSS_EINVAL, "k > T");
   const int d4 = (d + 3) / 4;
   const int stride4 = (d4 & 1) ? d4 + 2 : d4 + 1;  // odd stride in float4: conflict-free row-parallel reads
-  const size_t smem_small = static_cast<size_t>(32) * stride4 * 16 + (kTxCache + 1) * 4 + (kSmRm + kSmRows) * 4 + kSmRows;
+  // SMALL: 33 query rows, the two groups' two-slot rings of 64 rows x 9 float4, row starts, minima, row map
+  const size_t smem_small = static_cast<size_t>(33) * stride4 * 16 + 2 * 2 * 64 * 9 * 16 + (kTxCache + 1) * 4 +
+                            (kSmRm + kSmRows) * 4 + kSmRows;
   if (scratch && (d & 3) == 0 && max_rows <= 32 && max_mq <= 32 && smem_small <= 110 * 1024) {
     int32_t* win = static_cast<int32_t*>(scratch);
     float* ex = reinterpret_cast<float*>(win + static_cast<int64_t>(nq) * T);
     auto kfn = topk_exact_kernel<true>;
     BVSS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_small)));
+    static const bool kprof = getenv("BVSS_K6_PROF") != nullptr;
+    if (kprof) {
+      const int one = 1;
+      unsigned long long z[8] = {};
+      BVSS_CUDA(cudaMemcpyToSymbolAsync(g_k6prof_on, &one, sizeof(int), 0, cudaMemcpyHostToDevice, st));
+      BVSS_CUDA(cudaMemcpyToSymbolAsync(g_k6prof, z, sizeof(z), 0, cudaMemcpyHostToDevice, st));
+    }
     kfn<<<nq, kTxThreads, smem_small, st>>>(approx, cand, count, T, k, V, off, id_base, d, d4, stride4, 32, 0, Qv, qoff,
                                             qnorm, vmax2, c1, c2, exact_all, win, ex, out_ids, out_dist, fixup_counter,
                                             metric, approx_err);
+    if (kprof) {
+      unsigned long long h[8];
+      BVSS_CUDA(cudaMemcpyFromSymbolAsync(h, g_k6prof, sizeof(h), 0, cudaMemcpyDeviceToHost, st));
+      BVSS_CUDA(cudaStreamSynchronize(st));
+      const double c = h[4] ? static_cast<double>(h[4]) : 1.0;
+      fprintf(stderr, "[k6prof] ctas=%llu nw/q=%.2f cycles/cta: window %.0f setup %.0f jobs %.0f final %.0f; "
+              "warp-job cycles/cta %.0f (of 8 x jobs phase)\n", h[4], h[5] / c, h[0] / c, h[1] / c, h[2] / c,
+              h[3] / c, h[6] / c);
+    }
     return post_launch("topk_exact_kernel", st);
   }
   int RB = 32, RBV = 16;  // query rows per block; set rows per (double-buffered) block
