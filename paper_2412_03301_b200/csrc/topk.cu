@@ -308,6 +308,34 @@ __device__ unsigned long long g_k6prof[8];
 
 constexpr int kSmRows = 1024;  // SMALL: set rows per batch (their column minima live in smem)
 constexpr int kSmRm = 1024;    // SMALL: (candidate, query row) row minima per batch
+__host__ __device__ constexpr int nch_pad(int d4) { return (d4 + 7) & ~7; }  // SMALL: d4 in whole 8-float4 chunks
+
+// SMALL phase 2, one full chunk (8 float4 of d) of a 64-row block: lane rows `lane` and `lane + 32` of the
+// ring slot (row stride 9 float4) against this warp's GN query rows; qc = the transposed query tile at
+// (first dim of the chunk, first query row of the warp): column-major [d4][32] float4, so the GN rows of a
+// dim sit at immediate offsets (broadcast reads).  a0 / a1: D^2 partial sums (even / odd dims in .x / .y).
+template <int GN>
+__device__ __forceinline__ void k6_chunk(const float4* __restrict__ slot, int lane, const float4* __restrict__ qc,
+                                         float2 (&a0)[8], float2 (&a1)[8]) {
+  const float2 m1 = make_float2(-1.0f, -1.0f);
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const float4 va = slot[lane * 9 + c], vb = slot[(lane + 32) * 9 + c];
+    const float2 va0 = make_float2(va.x, va.y), va1 = make_float2(va.z, va.w);
+    const float2 vb0 = make_float2(vb.x, vb.y), vb1 = make_float2(vb.z, vb.w);
+#pragma unroll
+    for (int i = 0; i < GN; ++i) {
+      const float4 q = qc[c * 32 + i];
+      const float2 q0 = make_float2(q.x, q.y), q1 = make_float2(q.z, q.w);
+      const float2 ta0 = __ffma2_rn(va0, m1, q0), ta1 = __ffma2_rn(va1, m1, q1);
+      const float2 tb0 = __ffma2_rn(vb0, m1, q0), tb1 = __ffma2_rn(vb1, m1, q1);
+      a0[i] = __ffma2_rn(ta0, ta0, a0[i]);
+      a1[i] = __ffma2_rn(tb0, tb0, a1[i]);
+      a0[i] = __ffma2_rn(ta1, ta1, a0[i]);
+      a1[i] = __ffma2_rn(tb1, tb1, a1[i]);
+    }
+  }
+}
 
 template <bool SMALL>
 __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
@@ -443,13 +471,18 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
     // (shuffles), then one smem atomicMin per (candidate, query row) by the segment's first lane; column
     // minima: smem atomicMin per (row, warp).  Batches bound the smem minima (kSmRows rows, kSmRm minima).
     constexpr int kRB = 64, kCH = 8, kRS = kCH + 1, kD = 2;
-    float4* ring = reinterpret_cast<float4*>(Qs + static_cast<int64_t>(33) * stride4 * 4);  // [2][kD][kRB][kRS]
+    const int d4p = nch_pad(d4);                                                    // d4 rounded up to kCH
+    float4* QT = reinterpret_cast<float4*>(Qs);                                      // [d4p][32] transposed
+    float4* ring = QT + static_cast<int64_t>(d4p) * 32;                              // [2][kD][kRB][kRS]
     int* rs = reinterpret_cast<int*>(ring + 2 * kD * kRB * kRS);                              // [kTxCache + 1]
     uint32_t* rowm = reinterpret_cast<uint32_t*>(rs + kTxCache + 1);                         // [kSmRm]
     uint32_t* colm = rowm + kSmRm;                                                           // [kSmRows]
     uint8_t* rc = reinterpret_cast<uint8_t*>(colm + kSmRows);                                // row -> candidate
-    const float4* Q4 = reinterpret_cast<const float4*>(Qs);
-    stage_rows(Qs, stride4, Qv + q0 * d, mq, d, d4);
+    for (int t = tid; t < mq * d4p; t += blockDim.x) {  // QT[c][r] = query row r, float4 c (zero past d)
+      const int r = t / d4p, c = t - r * d4p;
+      tc::cp_async16(smem_u32(QT + c * 32 + r), Qv + (q0 + r) * d + 4 * (c < d4 ? c : 0), c < d4 ? 16u : 0u);
+    }
+    tc::cp_async_commit();
     const int wg = warp >> 2, w4 = warp & 3, tg = tid & 127;
     const int i0 = w4 * mq / 4, gn = (w4 + 1) * mq / 4 - i0;  // this warp's query rows (<= 8)
     const int nch = (d4 + kCH - 1) / kCH;
@@ -512,7 +545,7 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
               src[j] = reinterpret_cast<const float4*>(V + (S.jv0[xx] + (rr - rs[xx])) * d);
             }
           }
-          float4* dst = ring + static_cast<int64_t>((wg * kD + e % kD) * kRB) * kRS;
+          float4* dst = ring + static_cast<int64_t>((wg * kD + (e & 1)) * kRB) * kRS;
           const int c = ch * kCH + ccol;
 #pragma unroll
           for (int j = 0; j < 4; ++j)
@@ -523,7 +556,6 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
       float2 a0[8], a1[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) a0[i] = a1[i] = make_float2(0.f, 0.f);
-      const float2 m1 = make_float2(-1.0f, -1.0f);
       issue(0);
       for (int e = 0; e < nel; ++e) {
         tc::cp_async_wait<0>();
@@ -533,27 +565,18 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
           asm volatile("bar.sync 2, 128;" ::: "memory");
         issue(e + 1);
         const int bi = e / nch, ch = e - bi * nch;
-        const float4* slot = ring + static_cast<int64_t>((wg * kD + e % kD) * kRB) * kRS;
-        const int cn = min(kCH, d4 - ch * kCH);
-#pragma unroll
-        for (int c = 0; c < kCH; ++c) {
-          if (c >= cn) break;
-          const float4 va = slot[lane * kRS + c], vb = slot[(lane + 32) * kRS + c];
-          const float2 va0 = make_float2(va.x, va.y), va1 = make_float2(va.z, va.w);
-          const float2 vb0 = make_float2(vb.x, vb.y), vb1 = make_float2(vb.z, vb.w);
-          const float4* qc = Q4 + static_cast<int64_t>(i0) * stride4 + ch * kCH + c;
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            if (i >= gn) break;
-            const float4 q = qc[i * stride4];
-            const float2 q0 = make_float2(q.x, q.y), q1 = make_float2(q.z, q.w);
-            const float2 ta0 = __ffma2_rn(va0, m1, q0), ta1 = __ffma2_rn(va1, m1, q1);
-            const float2 tb0 = __ffma2_rn(vb0, m1, q0), tb1 = __ffma2_rn(vb1, m1, q1);
-            a0[i] = __ffma2_rn(ta0, ta0, a0[i]);
-            a1[i] = __ffma2_rn(tb0, tb0, a1[i]);
-            a0[i] = __ffma2_rn(ta1, ta1, a0[i]);
-            a1[i] = __ffma2_rn(tb1, tb1, a1[i]);
-          }
+        const float4* slot = ring + static_cast<int64_t>((wg * kD + (e & 1)) * kRB) * kRS;
+        const float4* qc = QT + static_cast<int64_t>(ch * kCH) * 32 + i0;  // past d: zero query and set dims
+        switch (gn) {  // warp-uniform, fixed for the kernel: branch-free unrolled math
+          case 1: k6_chunk<1>(slot, lane, qc, a0, a1); break;
+          case 2: k6_chunk<2>(slot, lane, qc, a0, a1); break;
+          case 3: k6_chunk<3>(slot, lane, qc, a0, a1); break;
+          case 4: k6_chunk<4>(slot, lane, qc, a0, a1); break;
+          case 5: k6_chunk<5>(slot, lane, qc, a0, a1); break;
+          case 6: k6_chunk<6>(slot, lane, qc, a0, a1); break;
+          case 7: k6_chunk<7>(slot, lane, qc, a0, a1); break;
+          case 8: k6_chunk<8>(slot, lane, qc, a0, a1); break;
+          default: break;
         }
         if (ch == nch - 1) {  // block done: row / column minima of its two 32-row halves
           auto fold = [&](float2(&a)[8], int r) {
@@ -874,8 +897,8 @@ int launch_topk_fixup(const float* approx, const int32_t* cand, const int32_t* c
   if (k > T) BVSS_FAIL(BVSS_EINVAL, "k > T");
   const int d4 = (d + 3) / 4;
   const int stride4 = (d4 & 1) ? d4 + 2 : d4 + 1;  // odd stride in float4: conflict-free row-parallel reads
-  // SMALL: 33 query rows, the two groups' two-slot rings of 64 rows x 9 float4, row starts, minima, row map
-  const size_t smem_small = static_cast<size_t>(33) * stride4 * 16 + 2 * 2 * 64 * 9 * 16 + (kTxCache + 1) * 4 +
+  // SMALL: the transposed query tile (32 rows), the two groups' two-slot rings of 64 rows x 9 float4, row starts, minima, row map
+  const size_t smem_small = static_cast<size_t>(nch_pad(d4)) * 32 * 16 + 2 * 2 * 64 * 9 * 16 + (kTxCache + 1) * 4 +
                             (kSmRm + kSmRows) * 4 + kSmRows;
   if (scratch && (d & 3) == 0 && max_rows <= 32 && max_mq <= 32 && smem_small <= 110 * 1024) {
     int32_t* win = static_cast<int32_t*>(scratch);
