@@ -365,6 +365,15 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
   float* ex = ex_g + static_cast<int64_t>(q) * T;
   if (tid == 0) S.wcount = 0;
   const bool prof = SMALL && g_k6prof_on;
+  if (SMALL) {  // stage the transposed query tile QT[c][r] (row r, float4 c; zero past d) under phase 1
+    const int d4p = nch_pad(d4);
+    float4* QT = reinterpret_cast<float4*>(Qs);
+    for (int t = tid; t < mq * d4p; t += blockDim.x) {
+      const int r = t / d4p, c = t - r * d4p;
+      tc::cp_async16(smem_u32(QT + c * 32 + r), Qv + (q0 + r) * d + 4 * (c < d4 ? c : 0), c < d4 ? 16u : 0u);
+    }
+    tc::cp_async_commit();
+  }
   long long pt0 = prof ? clock64() : 0, pt1 = 0, pt2 = 0, pt3 = 0;
   // ---- 1. window
   float W = __int_as_float(0x7f800000);
@@ -478,13 +487,12 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
     uint32_t* rowm = reinterpret_cast<uint32_t*>(rs + kTxCache + 1);                         // [kSmRm]
     uint32_t* colm = rowm + kSmRm;                                                           // [kSmRows]
     uint8_t* rc = reinterpret_cast<uint8_t*>(colm + kSmRows);                                // row -> candidate
-    for (int t = tid; t < mq * d4p; t += blockDim.x) {  // QT[c][r] = query row r, float4 c (zero past d)
-      const int r = t / d4p, c = t - r * d4p;
-      tc::cp_async16(smem_u32(QT + c * 32 + r), Qv + (q0 + r) * d + 4 * (c < d4 ? c : 0), c < d4 ? 16u : 0u);
-    }
-    tc::cp_async_commit();
+    // (the transposed query tile was staged at kernel start, overlapping phase 1)
     const int wg = warp >> 2, w4 = warp & 3, tg = tid & 127;
-    const int i0 = w4 * mq / 4, gn = (w4 + 1) * mq / 4 - i0;  // this warp's query rows (<= 8)
+    // this warp's query rows: a quarter of them (<= 8) on the group's own blocks; an eighth on a shared last
+    // block (odd block count: both groups take it, each half of the query rows, so neither idles)
+    const int i0q = w4 * mq / 4, gnq = (w4 + 1) * mq / 4 - i0q;
+    const int i0e = (wg * 4 + w4) * mq / 8, gne = (wg * 4 + w4 + 1) * mq / 8 - i0e;
     const int nch = (d4 + kCH - 1) / kCH;
     const int crow = tg >> 3, ccol = tg & 7;  // copy role: rows crow + 16 j (j < 4), float4 column ccol
     for (int xb = 0; xb < nw;) {
@@ -532,7 +540,9 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
       if (prof && xb == 0) pt2 = clock64();
       const long long pj0 = prof ? clock64() : 0;
       const int nrb = (rows + kRB - 1) / kRB;
-      const int nel = (nrb > wg ? (nrb - wg + 1) / 2 : 0) * nch;  // this group's (block, chunk) elements
+      const int npair = nrb >> 1;                      // blocks 2b + wg (b < npair) are the group's own
+      const int nel = (npair + (nrb & 1)) * nch;       // (block, chunk) elements of this group
+      auto blk = [&](int bi) { return bi < npair ? 2 * bi + wg : nrb - 1; };
       const float4* src[4];
       auto issue = [&](int e) {  // cp.async of element e into ring slot e % kD (one commit group per call)
         if (e < nel) {
@@ -540,7 +550,7 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
           if (ch == 0) {
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              const int rr = min((wg + 2 * bi) * kRB + crow + 16 * j, rows - 1);  // past the end: a copy of the last row
+              const int rr = min(blk(bi) * kRB + crow + 16 * j, rows - 1);  // past the end: a copy of the last row
               const int xx = rc[rr];
               src[j] = reinterpret_cast<const float4*>(V + (S.jv0[xx] + (rr - rs[xx])) * d);
             }
@@ -565,9 +575,11 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
           asm volatile("bar.sync 2, 128;" ::: "memory");
         issue(e + 1);
         const int bi = e / nch, ch = e - bi * nch;
+        const bool shared_blk = bi >= npair;
+        const int i0 = shared_blk ? i0e : i0q, gn = shared_blk ? gne : gnq;
         const float4* slot = ring + static_cast<int64_t>((wg * kD + (e & 1)) * kRB) * kRS;
         const float4* qc = QT + static_cast<int64_t>(ch * kCH) * 32 + i0;  // past d: zero query and set dims
-        switch (gn) {  // warp-uniform, fixed for the kernel: branch-free unrolled math
+        switch (gn) {  // warp-uniform: branch-free unrolled math
           case 1: k6_chunk<1>(slot, lane, qc, a0, a1); break;
           case 2: k6_chunk<2>(slot, lane, qc, a0, a1); break;
           case 3: k6_chunk<3>(slot, lane, qc, a0, a1); break;
@@ -607,7 +619,7 @@ __global__ void __launch_bounds__(kTxThreads, 2) topk_exact_kernel(
             }
             if (valid && gn > 0) atomicMin(&colm[r], __float_as_uint(cm));
           };
-          const int rbase = (wg + 2 * bi) * kRB;
+          const int rbase = blk(bi) * kRB;
           fold(a0, rbase + lane);
           fold(a1, rbase + 32 + lane);
         }
