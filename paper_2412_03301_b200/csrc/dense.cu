@@ -306,9 +306,13 @@ __device__ __forceinline__ float set_colmin_max(const SetCols& c, int mvc, float
 
 __device__ __forceinline__ float vload_volatile(const float* p);
 
-// k-th smallest value of the union of a query's bound lists over nr ranges (from range r on) x kEpiSub warps:
-// any k distinct sets' upper bounds bound the exact k-th H^2 from above, so the union's k-th is a valid (and
-// much tighter) tau.  Warp-wide radix select on the (non-negative) float bits.
+// k-th smallest value of the union of a query's bound lists over nr <= R distinct ranges (from range r on) x
+// kEpiSub warps: any k distinct sets' upper bounds bound the exact k-th H^2 from above, so the union's k-th is
+// a valid (and much tighter) tau.  The lists are read while their owners may be inserting (a lane-parallel
+// shift): a torn read can show one value at two adjacent positions of a list, which would count one set twice
+// and make the k-th too small (an invalid tau: observed as a wrong top-k with R = 1).  So a value equal to its
+// predecessor in the same list counts as +inf (two sets with equal bounds then count once: conservative).
+// Warp-wide radix select on the (non-negative) float bits.
 __device__ float union_kth(const float* lq0 /* lists of (q, range 0) */, int R, int r, int nr, int k, int lane) {
   const int per_range = kEpiSub * k, total = nr * per_range;
   float v[8];
@@ -317,6 +321,15 @@ __device__ float union_kth(const float* lq0 /* lists of (q, range 0) */, int R, 
     const int x = lane + 32 * e;
     v[e] = __int_as_float(0x7f800000);
     if (x < total) v[e] = vload_volatile(lq0 + static_cast<int64_t>((r + x / per_range) % R) * per_range + x % per_range);
+  }
+  float last = __int_as_float(0x7f800000);  // lane 31's value of the previous row of 32
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int x = lane + 32 * e;
+    float prev = __shfl_up_sync(0xffffffffu, v[e], 1);
+    if (lane == 0) prev = last;
+    last = __shfl_sync(0xffffffffu, v[e], 31);
+    if (x < total && x % k != 0 && prev == v[e]) v[e] = __int_as_float(0x7f800000);
   }
   uint32_t prefix = 0;
   for (int bit = 30; bit >= 0; --bit) {  // largest x with count(< x) < k: the k-th smallest
@@ -332,7 +345,7 @@ __device__ float union_kth(const float* lq0 /* lists of (q, range 0) */, int R, 
 
 __device__ __forceinline__ float vload_volatile(const float* p) {
   float v;
-  asm volatile("ld.volatile.global.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  asm volatile("ld.relaxed.gpu.global.f32 %0, [%1];" : "=f"(v) : "l"(p));  // (gpu scope: L2-coherent)
   return v;
 }
 
@@ -549,8 +562,10 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
       for (int t = t0; t < t1; ++t, ++tile_ctr) {
         const uint32_t acc = tile_ctr & 1u;
         const int slot = tile_ctr % kInfoSlotsD;
-        tau = fminf(tau, other_k);
-        if (((tile_ctr + 8u * static_cast<uint32_t>(sub)) & 31u) == 0u) {  // every 32 tiles (staggered): the k-th of
+        // (developer BVSS_DENSE_DEBUG 8 .. 11 switch tau sources off: 8 none, 9 the own list, 10 + the other
+        // warps' lists at insertion, 11 + the union)
+        if (a.debug < 8) tau = fminf(tau, other_k);
+        if ((a.debug < 8 || a.debug == 11) && ((tile_ctr + 8u * static_cast<uint32_t>(sub)) & 31u) == 0u) {  // every 32 tiles (staggered): the k-th of
           unsigned pend = __ballot_sync(0xffffffffu, valid);               // the union of the query's lists
           while (pend) {
             const int ld = __ffs(pend) - 1;
@@ -625,14 +640,15 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
               const float* lqq = a.lists + (static_cast<int64_t>(q) * a.R + r) * kEpiSub * a.k;
               float* ownq = const_cast<float*>(lqq) + sub * a.k;
               const float old = lane < a.k ? ownq[lane] : INF;
-              const float oth = lane < kEpiSub - 1 ? vload_volatile(lqq + ((sub + 1 + lane) % kEpiSub) * a.k + a.k - 1)
+              const float oth = lane < kEpiSub - 1 && a.debug != 9 ? vload_volatile(lqq + ((sub + 1 + lane) % kEpiSub) * a.k + a.k - 1)
                                                    : INF;
               const int pos = __popc(__ballot_sync(0xffffffffu, lane < a.k && old <= ub));
               const float up = __shfl_up_sync(0xffffffffu, old, 1);
               const float nw = lane < pos ? old : (lane == pos ? ub : up);
               if (lane < a.k) ownq[lane] = nw;
               const float kth = __shfl_sync(0xffffffffu, nw, a.k - 1);
-              newtau = fminf(kth, __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(oth))));
+              // (min with tq: the warp's tau may be tighter than its lists, e.g. from the union)
+              newtau = fminf(tq, fminf(kth, __uint_as_float(__reduce_min_sync(0xffffffffu, __float_as_uint(oth)))));
             }
             if (lane == leader && h - Eq <= newtau) {
               const int slot = atomicAdd(a.cnt + q, 1);
@@ -642,7 +658,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
               }
               ++n_emit;
             }
-            if (inseg) {
+            if (inseg && a.debug != 8) {
               tau = newtau;
               thr = tau + E;
             }

@@ -912,7 +912,8 @@ int launch_topk_fixup(const float* approx, const int32_t* cand, const int32_t* c
   // SMALL: the transposed query tile (32 rows), the two groups' two-slot rings of 64 rows x 9 float4, row starts, minima, row map
   const size_t smem_small = static_cast<size_t>(nch_pad(d4)) * 32 * 16 + 2 * 2 * 64 * 9 * 16 + (kTxCache + 1) * 4 +
                             (kSmRm + kSmRows) * 4 + kSmRows;
-  if (scratch && (d & 3) == 0 && max_rows <= 32 && max_mq <= 32 && smem_small <= 110 * 1024) {
+  static const bool no_small = getenv("BVSS_K6_NOSMALL") != nullptr;  // developer switch: the CTA path only
+  if (!no_small && scratch && (d & 3) == 0 && max_rows <= 32 && max_mq <= 32 && smem_small <= 110 * 1024) {
     int32_t* win = static_cast<int32_t*>(scratch);
     float* ex = reinterpret_cast<float*>(win + static_cast<int64_t>(nq) * T);
     auto kfn = topk_exact_kernel<true>;
