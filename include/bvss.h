@@ -244,7 +244,9 @@ BVSS_API double bvss_refine_error_bound(const bvss_index* idx, double qnorm_max)
  * named *_dev are device pointers on the index's device.                     */
 typedef struct bvss_search_ctx bvss_search_ctx;
 
-/* Encode + sketch + scan one query batch; returns the number of radix rounds. */
+/* Encode + sketch + scan one query batch; returns the number of radix rounds.
+ * T is the GLOBAL candidate budget already clamped to the total number of
+ * sets (it may then be < k; the caller rejects an unclamped T < k).        */
 BVSS_API int bvss_dist_begin(bvss_index* idx, const float* queries, const int64_t* query_offsets, int64_t nq,
                     int32_t k, int32_t T, int64_t id_base, uint32_t flags, bvss_search_ctx** out,
                     int32_t* rounds);
@@ -263,6 +265,42 @@ BVSS_API int bvss_dist_finish(bvss_search_ctx* ctx, const int64_t* all_eq_dev, i
 BVSS_API int bvss_merge_topk(bvss_index* idx, const int64_t* ids_dev, const float* dist_dev, int32_t world,
                     int64_t nq, int32_t k, int64_t* out_ids_dev, float* out_dist_dev);
 BVSS_API void bvss_dist_end(bvss_search_ctx* ctx);
+
+/* -------------------------------- single-process multi-device index -- */
+/* SURVEY §8(b) "Multi-GPU" convention without torch.distributed: one process
+ * drives P shard indexes, shard i on CUDA device devices[i] (NULL: 0..P-1; an
+ * ordinal may repeat, several shards then share a device) over the contiguous,
+ * balanced set-id range [base_i, base_{i+1}) of the database.  Search runs the
+ * exact global-T protocol above (Alg 6 lines 10-23, P:795-814,
+ * with ONE global candidate budget T) with the collectives in-process: score
+ * histograms summed on shard 0's device and copied back (C1), tie counts
+ * all-gathered (C2), local top-k lists merged by K7 on shard 0 (C3), the bytes
+ * moved by cudaMemcpyPeer (NVLink / NVSwitch where peer access exists).  The
+ * encode + scan and refine phases of all shards run concurrently (one host
+ * thread per shard).  Results are identical to one index over the whole
+ * database, for any P and device assignment.                               */
+typedef struct bvss_group bvss_group;
+
+/* Build a group over n sets: n_devices = P in 1..64, or -1 = every visible
+ * device; P is reduced to n when n < P.  vectors / set_offsets are HOST arrays
+ * (BVSS_DEVICE_PTRS in p->flags is EINVAL); p->device is ignored (devices[]
+ * decides).  Each shard is built as by bvss_build_index (same params, same
+ * projection W), concurrently.  Errors: EINVAL as bvss_build_index plus a
+ * bad n_devices; a shard's failure frees the shards built so far and returns
+ * its status with the message prefixed "shard i:".                         */
+BVSS_API int bvss_group_build(const float* vectors, const int64_t* set_offsets, int64_t n, int32_t d,
+                              const bvss_params* p, int32_t n_devices, const int32_t* devices, bvss_group** out);
+/* Exact top-k of nq query sets (HOST arrays; flags may carry
+ * BVSS_VALIDATE_FINITE), out_ids [nq][k] int64 global set ids, out_dist
+ * [nq][k] fp32, as bvss_search.  P = 1 is bvss_search on the only shard. */
+BVSS_API int bvss_group_search(bvss_group* g, const float* queries, const int64_t* query_offsets, int64_t nq,
+                               int32_t k, int32_t T, int64_t* out_ids, float* out_dist, uint32_t flags);
+/* Number of shards (0 for NULL). */
+BVSS_API int32_t bvss_group_shards(const bvss_group* g);
+/* Shard i's index (owned by the group: do not free it) and its first global
+ * set id (for bvss_get_stats / bvss_get_info / exports).                   */
+BVSS_API int bvss_group_shard(const bvss_group* g, int32_t shard, bvss_index** out, int64_t* id_base);
+BVSS_API void bvss_free_group(bvss_group* g);
 
 #ifdef __cplusplus
 }

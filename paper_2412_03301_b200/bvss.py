@@ -29,7 +29,8 @@ EXPORTS = (
     "bvss_query_sketch", "bvss_filter", "bvss_refine", "bvss_bruteforce", "bvss_index_begin", "bvss_index_append",
     "bvss_index_finish", "bvss_refine_error_bound", "bvss_dist_begin",
     "bvss_dist_hist", "bvss_dist_resolve", "bvss_dist_tie_counts", "bvss_dist_finish", "bvss_merge_topk",
-    "bvss_dist_end",
+    "bvss_dist_end", "bvss_group_build", "bvss_group_search", "bvss_group_shards", "bvss_group_shard",
+    "bvss_free_group",
 )
 
 
@@ -103,6 +104,11 @@ def _load():
         "bvss_dist_finish": (C.c_int, [VP, P, I32, I32, P, P]),
         "bvss_merge_topk": (C.c_int, [VP, P, P, I32, I64, I32, P, P]),
         "bvss_dist_end": (None, [VP]),
+        "bvss_group_build": (C.c_int, [P, P, I64, I32, C.POINTER(Params), I32, P, C.POINTER(VP)]),
+        "bvss_group_search": (C.c_int, [VP, P, P, I64, I32, I32, P, P, U32]),
+        "bvss_group_shards": (I32, [VP]),
+        "bvss_group_shard": (C.c_int, [VP, I32, C.POINTER(VP), C.POINTER(I64)]),
+        "bvss_free_group": (None, [VP]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -349,3 +355,58 @@ class Index:
     @property
     def handle(self):
         return self._h
+
+
+class Group:
+    """A single-process multi-device index (bvss_group_*): the database sharded by contiguous set-id ranges
+    over `devices` (CUDA ordinals; one may repeat), searched by the exact global-T protocol with in-process
+    collectives.  Host arrays only."""
+
+    def __init__(self, vectors, offsets, *, devices, m, s, L, sketch="binary", seed=0, refine_terms=0,
+                 query_batch=0, select_mode=0, metric="hausdorff", score="default", gate_A=0, gate_M=1,
+                 filter="sketch"):
+        vectors = np.ascontiguousarray(vectors, dtype=np.float32)
+        offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+        n, d = int(offsets.shape[0]) - 1, int(vectors.shape[1])
+        devs = np.ascontiguousarray(devices, dtype=np.int32)
+        p = Params(m=m, s=s, L=L, sketch=SKETCH_BINARY if sketch == "binary" else SKETCH_COUNT_U8, seed=seed,
+                   projection=None, device=0, flags=0, query_batch=query_batch, refine_terms=refine_terms,
+                   select_mode=select_mode, metric=METRICS[metric], score=SCORES[score], gate_A=gate_A,
+                   gate_M=gate_M if gate_A else 0, filter=FILTERS[filter])
+        self._h = C.c_void_p()
+        _check(lib.bvss_group_build(C.c_void_p(vectors.ctypes.data), C.c_void_p(offsets.ctypes.data), n, d,
+                                    C.byref(p), int(devs.shape[0]), C.c_void_p(devs.ctypes.data),
+                                    C.byref(self._h)))
+        self.n, self.d = n, d
+
+    @property
+    def shards(self):
+        return lib.bvss_group_shards(self._h)
+
+    def shard_stats(self, i):
+        h, base = C.c_void_p(), C.c_int64()
+        _check(lib.bvss_group_shard(self._h, i, C.byref(h), C.byref(base)))
+        st = Stats()
+        _check(lib.bvss_get_stats(h, C.byref(st)))
+        return int(base.value), st.as_dict()
+
+    def search(self, queries, q_offsets, k, T):
+        queries = np.ascontiguousarray(queries, dtype=np.float32)
+        q_offsets = np.ascontiguousarray(q_offsets, dtype=np.int64)
+        nq = int(q_offsets.shape[0]) - 1
+        ids = np.empty((nq, k), np.int64)
+        dist = np.empty((nq, k), np.float32)
+        _check(lib.bvss_group_search(self._h, C.c_void_p(queries.ctypes.data), C.c_void_p(q_offsets.ctypes.data),
+                                     nq, k, T, C.c_void_p(ids.ctypes.data), C.c_void_p(dist.ctypes.data), 0))
+        return ids, dist
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.bvss_free_group(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

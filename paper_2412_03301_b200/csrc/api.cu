@@ -134,11 +134,11 @@ int launch_dense_norm_operand(const float* vn, int64_t nvec, float inv_s2, __hal
 int launch_dense_hausdorff(const __half* qd, int ntq, const __half* hd, int64_t nvec, int dpad, int ntiles,
                            const int32_t* tile_s0, const int32_t* tile_s1, const int64_t* off, const __half* va,
                            const __half* qa, const int32_t* lane_qid, const float* lane_qn, const float* qE,
-                           const float* tau0,
+                           float* tau0,
                            float kappa, float alpha, int k, int R, float* lists, int32_t* cnt, int32_t* ids,
                            float* vals, int cap,
                            const uint32_t* mask, int64_t mask_stride, int64_t id_base, unsigned long long* stat,
-                           int num_sms, cudaStream_t st);
+                           int dyn, int* unit_ctr, int num_sms, cudaStream_t st);
 
 // ------------------------------------------------------- small kernels --
 __global__ void fill_i32_kernel(int32_t* __restrict__ x, int64_t n, int32_t v) {
@@ -924,12 +924,25 @@ int dense_refine_topk(bvss_index* idx, bvss_search_ctx* c, const uint32_t* mask,
       }
   }
   const int ntiles = ntiles_use;
-  int R = static_cast<int>(ceil_div<int64_t>(2 * idx->num_sms, ntq));
-  if (R < 4) R = 4;
+  // work units = (query tile pair, database range).  Dynamic schedule (default): ranges of kDenseTPR tiles
+  // handed out range-major by a global counter (all pairs stream the same ranges at once: L2 reuse; tau of
+  // a unit starts from the query's lists of the ranges before it).  Static (BVSS_DENSE_DYN=0): at least two
+  // units per SM pair, pair-major.
+  int dyn = 1;
+  if (const char* e = getenv("BVSS_DENSE_DYN")) dyn = atoi(e) != 0;
+  int tpr = 512;
+  if (const char* e = getenv("BVSS_DENSE_TPR")) tpr = atoi(e) > 0 ? atoi(e) : tpr;  // developer switch
+  int R = dyn ? static_cast<int>(ceil_div<int64_t>(ntiles, tpr))
+              : static_cast<int>(ceil_div<int64_t>(2 * idx->num_sms, ntq));
+  if (!dyn && R < 4) R = 4;
   if (const char* e = getenv("BVSS_DENSE_R")) R = atoi(e) > 0 ? atoi(e) : R;  // developer switch: database ranges
   if (R > ntiles) R = ntiles < 1 ? 1 : ntiles;
-  const double spl = std::max(1.0, static_cast<double>(idx->n) / (static_cast<double>(R) * dense_epi_sub() * k));
-  const double lists_pq = static_cast<double>(R) * dense_epi_sub();  // bound lists per query
+  if (static_cast<int64_t>(ntq / 2) * R >= (int64_t(1) << 31)) R = static_cast<int>((int64_t(1) << 30) / (ntq / 2));
+  // (dyn: a unit's tau starts from the lists of the ranges run before it, so the emissions per query grow
+  // like those of a few ranges, not of R)
+  const int R_emit = dyn ? std::min(R, 8) : R;
+  const double spl = std::max(1.0, static_cast<double>(idx->n) / (static_cast<double>(R_emit) * dense_epi_sub() * k));
+  const double lists_pq = static_cast<double>(R_emit) * dense_epi_sub();  // bound lists per query
   int64_t cap = static_cast<int64_t>(lists_pq * k * (2.0 + std::log(spl)) * 2.0) + idx->dnhuge + 1024;
   if (const char* e = getenv("BVSS_DEBUG_DENSE_CAP")) cap = atoll(e);  // test switch: force overflows
   cap = (cap + 255) & ~int64_t(255);
@@ -973,6 +986,8 @@ int dense_refine_topk(bvss_index* idx, bvss_search_ctx* c, const uint32_t* mask,
   BVSS_TRY(c->alloc(static_cast<size_t>(nq) * cap * 4, reinterpret_cast<void**>(&ids)));
   BVSS_TRY(c->alloc(static_cast<size_t>(nq) * cap * 4, reinterpret_cast<void**>(&vals)));
   BVSS_TRY(c->alloc(2 * sizeof(unsigned long long), reinterpret_cast<void**>(&stat)));
+  int* unit_ctr;
+  BVSS_TRY(c->alloc(sizeof(int), reinterpret_cast<void**>(&unit_ctr)));
   BVSS_CUDA(cudaMemcpyAsync(d_rowmap, rowmap.data(), rows * 4, cudaMemcpyHostToDevice, idx->stream));
   BVSS_CUDA(cudaMemcpyAsync(d_rowq, rowq.data(), rows * 4, cudaMemcpyHostToDevice, idx->stream));
   BVSS_CUDA(cudaMemsetAsync(stat, 0, 2 * sizeof(unsigned long long), idx->stream));
@@ -992,7 +1007,7 @@ int dense_refine_topk(bvss_index* idx, bvss_search_ctx* c, const uint32_t* mask,
                                   idx->off, idx->va, qa, lane_qid, lane_qn, qE, tau0, -2.0f * sq * idx->dense_s, alpha,
                                   k, R,
                                   lists, cnt, ids, vals, static_cast<int>(cap), mask, mask_stride, c->id_base, stat,
-                                  idx->num_sms, idx->stream));
+                                  dyn, unit_ctr, idx->num_sms, idx->stream));
   cudaEventRecord(idx->ev[5], idx->stream);
   idx->stats.kernel_launches += 6;
   // overflow check
@@ -1846,7 +1861,10 @@ int bvss_dist_begin(bvss_index* idx, const float* queries, const int64_t* query_
                     int32_t T, int64_t id_base, uint32_t flags, bvss_search_ctx** out, int32_t* rounds) {
   if (!out || !rounds) BVSS_FAIL(BVSS_EINVAL, "null out");
   *out = nullptr;
-  BVSS_TRY(validate_search(idx, queries, query_offsets, nq, k, T));
+  // (T is the global budget already clamped to the total number of sets, so T < k is legal here when the
+  // whole database has fewer than k sets; the caller checks T >= k on its unclamped budget)
+  if (T < 1) BVSS_FAIL(BVSS_EINVAL, "T must be >= 1");
+  BVSS_TRY(validate_search(idx, queries, query_offsets, nq, k, T < k ? k : T));
   DeviceGuard g(idx->device);
   std::vector<int64_t> qo;
   BVSS_TRY(host_offsets(idx, query_offsets, nq, (flags & BVSS_DEVICE_PTRS) != 0, qo));

@@ -72,6 +72,10 @@ constexpr int kInfoWarp = 2 + kEpiWarpsD;
 constexpr int kDenseThreads = 32 * (kInfoWarp + 1);        // producer, MMA, epilogue, tile info
 constexpr int kInfoSlotsD = 4;
 constexpr int kDenseMaxStages = 8;
+constexpr int kUnitQ = 4;          // published unit ids in flight (dyn scheduling)
+// consumers of a published unit id: the peer's producer, the leader's MMA thread, both CTAs' info warps and
+// epilogue warps
+constexpr int kUnitConsumers = 1 + 1 + 2 + 2 * kEpiWarpsD;
 constexpr uint32_t kAChunkBytes = kDenseM * 128;  // one 64-element K chunk of the query tile (16 KB)
 // CTA pairs (cta_group::2): one tcgen05.mma M=256 N=240 per K step covers the two CTAs' query tiles (128
 // rows each, A in each CTA's shared memory) against one database tile whose rows are split between the
@@ -108,7 +112,11 @@ struct DenseArgs {
   const int32_t* lane_qid;      // [ntq*128] query of each packed row, -1 = padding
   const float* lane_qn;         // [ntq*128] squared norm of each packed row
   const float* qE;              // [nq] squared-distance error bound of each query
-  const float* tau0;            // [nq] initial tau (an upper bound on the k-th H^2; +inf if none)
+  float* tau0;                  // [nq] running tau of each query: an upper bound on its k-th H^2 (+inf if none),
+                                // lowered (atomicMin on the bits; every value is >= 0) by every warp whenever
+                                // it refreshes its own tau, read when a unit starts: a unit of range r starts
+                                // from the bound of every range run before it, not only from the union of the
+                                // last few ranges' lists
   float kappa;                  // -2 S_q S_db
   int k;
   float* lists;                 // [nq][R][kEpiSub][k] sorted upper bounds, +inf-initialised
@@ -123,6 +131,8 @@ struct DenseArgs {
   unsigned long long* prof;     // developer per-role cycle counters (env BVSS_DENSE_PROF) or null
   int debug;                    // developer switch BVSS_DENSE_DEBUG: 1 = epilogue skips its work, 2 = no MMAs,
                                 // 3 = no survivor work, 4 = no database loads and no epilogue (timing only)
+  int dyn;                      // 1: units handed out by a global counter in range-major order (see pair_unit)
+  int* unit_ctr;                // [1] next unit (dyn), zeroed before the launch
 };
 
 // per-tile metadata the info warp stages for the epilogue (shared memory): the database sets of the tile
@@ -141,6 +151,8 @@ struct DenseCtl {
   uint64_t empty[kDenseMaxStages];
   uint64_t a_full, a_empty;
   uint64_t tfull[2], tempty[2];
+  int unitq[kUnitQ];                                  // unit ids published by the leader's producer (dyn)
+  uint64_t unit_full[kUnitQ], unit_empty[kUnitQ];
   uint32_t tmem_base;
 };
 
@@ -191,6 +203,21 @@ __device__ __forceinline__ void expect_tx_remote(uint32_t cluster_addr, uint32_t
   asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_addr),
                "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void arrive_release_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {  // acquire at cluster scope
+  const uint32_t addr = smem_u32(bar);
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
 }
 // the pair's MMA (issued by the leader): D[both CTAs' TMEM] (+)= A[both CTAs' smem] * B[both halves]^T
 __device__ __forceinline__ void umma_pair(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
@@ -304,6 +331,88 @@ __device__ __forceinline__ float set_colmin_max(const SetCols& c, int mvc, float
   return B;
 }
 
+// Exact-width variant: a run of mvc (1..31) columns is read by the loads of its binary digits (x16, x8, x4,
+// x2, x1 at consecutive column offsets), so the epilogue reads exactly the set's columns from TMEM (the
+// 32 + 8 column form reads 40 columns for a set of 18 rows).  Branches are warp-uniform (one set per warp).
+struct SetColsX {
+  uint32_t a16[16], a8[8], a4[4], a2[2], a1[1];
+};
+__device__ __forceinline__ void tmem_ldx4(uint32_t t, uint32_t (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(t)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ldx2(uint32_t t, uint32_t (&r)[2]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(t) : "memory");
+}
+__device__ __forceinline__ void tmem_ldx1(uint32_t t, uint32_t (&r)[1]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r[0]) : "r"(t) : "memory");
+}
+__device__ __forceinline__ void load_set(uint32_t taddr, int mvc, SetColsX& c) {
+  if (mvc & 16) {
+    tc::tmem_ld16(taddr, c.a16);
+    taddr += 16;
+  }
+  if (mvc & 8) {
+    tmem_ld8(taddr, c.a8);
+    taddr += 8;
+  }
+  if (mvc & 4) {
+    tmem_ldx4(taddr, c.a4);
+    taddr += 4;
+  }
+  if (mvc & 2) {
+    tmem_ldx2(taddr, c.a2);
+    taddr += 2;
+  }
+  if (mvc & 1) tmem_ldx1(taddr, c.a1);
+  tc::tmem_ld_wait();
+}
+__device__ __forceinline__ float set_max(const SetColsX& c, int mvc) {
+  float m = __int_as_float(0xff800000);
+  if (mvc & 16) {
+#pragma unroll
+    for (int j = 0; j < 16; j += 2) m = fmax3(m, __uint_as_float(c.a16[j]), __uint_as_float(c.a16[j + 1]));
+  }
+  if (mvc & 8) {
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) m = fmax3(m, __uint_as_float(c.a8[j]), __uint_as_float(c.a8[j + 1]));
+  }
+  if (mvc & 4) m = fmax3(m, fmax3(__uint_as_float(c.a4[0]), __uint_as_float(c.a4[1]), __uint_as_float(c.a4[2])),
+                         __uint_as_float(c.a4[3]));
+  if (mvc & 2) m = fmax3(m, __uint_as_float(c.a2[0]), __uint_as_float(c.a2[1]));
+  if (mvc & 1) m = fmaxf(m, __uint_as_float(c.a1[0]));
+  return m;
+}
+__device__ __forceinline__ float set_colmin_max(const SetColsX& c, int mvc, float kappa, float qn, bool inseg) {
+  float B = 0.0f;
+  auto col = [&](uint32_t x) {
+    const float d2 = fmaxf(fmaf(kappa, __uint_as_float(x), qn), 0.0f);
+    B = fmaxf(B, __uint_as_float(__reduce_min_sync(0xffffffffu, inseg ? __float_as_uint(d2) : 0xffffffffu)));
+  };
+  if (mvc & 16) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) col(c.a16[j]);
+  }
+  if (mvc & 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) col(c.a8[j]);
+  }
+  if (mvc & 4) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) col(c.a4[j]);
+  }
+  if (mvc & 2) {
+    col(c.a2[0]);
+    col(c.a2[1]);
+  }
+  if (mvc & 1) col(c.a1[0]);
+  return B;
+}
+template <bool EXACT> struct ColsOf { using T = SetCols; static constexpr int CH = 32; };
+template <> struct ColsOf<true> { using T = SetColsX; static constexpr int CH = 31; };
+
 __device__ __forceinline__ float vload_volatile(const float* p);
 
 // k-th smallest value of the union of a query's bound lists over nr <= R distinct ranges (from range r on) x
@@ -313,14 +422,16 @@ __device__ __forceinline__ float vload_volatile(const float* p);
 // and make the k-th too small (an invalid tau: observed as a wrong top-k with R = 1).  So a value equal to its
 // predecessor in the same list counts as +inf (two sets with equal bounds then count once: conservative).
 // Warp-wide radix select on the (non-negative) float bits.
-__device__ float union_kth(const float* lq0 /* lists of (q, range 0) */, int R, int r, int nr, int k, int lane) {
+// (dir = +1: ranges r, r+1, ...; dir = -1: r, r-1, ... -- the ranges the range-major schedule has already run)
+__device__ float union_kth(const float* lq0 /* lists of (q, range 0) */, int R, int r, int nr, int k, int lane,
+                           int dir) {
   const int per_range = kEpiSub * k, total = nr * per_range;
   float v[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
     const int x = lane + 32 * e;
     v[e] = __int_as_float(0x7f800000);
-    if (x < total) v[e] = vload_volatile(lq0 + static_cast<int64_t>((r + x / per_range) % R) * per_range + x % per_range);
+    if (x < total) v[e] = vload_volatile(lq0 + static_cast<int64_t>((r + R + dir * (x / per_range)) % R) * per_range + x % per_range);
   }
   float last = __int_as_float(0x7f800000);  // lane 31's value of the previous row of 32
 #pragma unroll
@@ -349,6 +460,49 @@ __device__ __forceinline__ float vload_volatile(const float* p) {
   return v;
 }
 
+// The i-th work unit of this CTA pair (-1: none left).  Static (dyn = 0): u = pair + i * npairs, units
+// ordered (query tile pair, range) pair-major.  Dynamic (dyn = 1): the leader's producer takes the next unit
+// of a global counter when it starts a unit and publishes it to both CTAs (a kUnitQ-deep queue in shared
+// memory); units are ordered range-major, so all pairs work on the same one or two database ranges at any
+// moment and a range is read from HBM about once while every query tile pair streams it from L2 (pairs that
+// run faster simply take more units: no drift apart along the database).  Every consumer releases the slot
+// (pair_unit_release) once it has read it.
+__device__ __forceinline__ int pair_unit(const DenseArgs& a, DenseCtl& S, int i, int pair, int npairs, int units,
+                                         bool publisher) {
+  if (!a.dyn) {
+    const int u = pair + i * npairs;
+    return u < units ? u : -1;
+  }
+  const int slot = i % kUnitQ;
+  const uint32_t ph = static_cast<uint32_t>(i / kUnitQ) & 1u;
+  if (publisher) {
+    mbar_wait_cluster(&S.unit_empty[slot], ph ^ 1u);
+    int u = atomicAdd(a.unit_ctr, 1);
+    if (u >= units) u = -1;
+    *reinterpret_cast<volatile int*>(&S.unitq[slot]) = u;
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(map_to(&S.unitq[slot], 1)), "r"(u) : "memory");
+    arrive_release_cluster(map_to(&S.unit_full[slot], 0));
+    arrive_release_cluster(map_to(&S.unit_full[slot], 1));
+    return u;
+  }
+  mbar_wait_cluster(&S.unit_full[slot], ph);
+  return *reinterpret_cast<volatile int*>(&S.unitq[slot]);
+}
+__device__ __forceinline__ void pair_unit_release(const DenseArgs& a, DenseCtl& S, int i) {
+  if (a.dyn) arrive_release_cluster(map_to(&S.unit_empty[i % kUnitQ], 0));
+}
+// (query tile pair, database range) of unit u
+__device__ __forceinline__ void unit_coords(const DenseArgs& a, int u, int* qp, int* r) {
+  const int nqp = a.ntq / 2;
+  if (a.dyn) {
+    *r = u / nqp;
+    *qp = u - *r * nqp;
+  } else {
+    *qp = u / a.R;
+    *r = u - *qp * a.R;
+  }
+}
+
 __device__ __forceinline__ void range_tiles(int r, int R, int ntiles, int* t0, int* t1) {
   *t0 = static_cast<int>((static_cast<int64_t>(ntiles) * r) / R);
   *t1 = static_cast<int>((static_cast<int64_t>(ntiles) * (r + 1)) / R);
@@ -366,7 +520,10 @@ __device__ __forceinline__ void range_tiles(int r, int R, int ntiles, int* t0, i
     }                                                                       \
   } while (0)
 
+template <bool EXACT>
 __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const __grid_constant__ DenseArgs a) {
+  using Cols = typename ColsOf<EXACT>::T;
+  constexpr int CH = ColsOf<EXACT>::CH;  // columns per TMEM read of a set
   extern __shared__ __align__(1024) uint8_t dsm_raw[];
   __shared__ DenseCtl S;
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
@@ -385,6 +542,10 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&S.tfull[b], 1);
       tc::mbar_init(&S.tempty[b], 2 * kEpiWarpsD);  // (the leader's: both CTAs' epilogue warps arrive)
+    }
+    for (int b = 0; b < kUnitQ; ++b) {
+      tc::mbar_init(&S.unit_full[b], 1);
+      tc::mbar_init(&S.unit_empty[b], kUnitConsumers);
     }
     for (int b = 0; b < kInfoSlotsD; ++b) {
       tc::mbar_init(&S.info_full[b], 1);
@@ -417,8 +578,13 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
     // on the leader's barriers, armed (expect_tx of the pair's bytes) by the leader's producer
     if (lane == 0) {
       uint32_t st = 0, ph = 0, ua = 0;  // ring slot and its phase bit
-      for (int u = pair; u < units; u += npairs, ++ua) {
-        const int qt = 2 * (u / a.R) + static_cast<int>(crank), r = u % a.R;
+      for (int iu = 0;; ++iu, ++ua) {
+        const int u = pair_unit(a, S, iu, pair, npairs, units, leader);
+        if (!leader) pair_unit_release(a, S, iu);
+        if (u < 0) break;
+        int qp, r;
+        unit_coords(a, u, &qp, &r);
+        const int qt = 2 * qp + static_cast<int>(crank);
         tc::mbar_wait(&S.a_empty, (ua & 1u) ^ 1u);
         if (leader) expect_tx(&S.a_full, 2u * (static_cast<uint32_t>(a.KC) * kAChunkBytes + kAAugBytes));
         for (int kc = 0; kc < a.KC; ++kc) tma_2d_pair(a_s + kc * kAChunkBytes, &a.tmA, kc * 64, qt * kDenseM, a_full_l);
@@ -459,8 +625,12 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
       const uint64_t adesc0 = tc::sw128_desc(a_s), bdesc0 = tc::sw128_desc(ring_s);
       const uint64_t aadesc = sw32_desc(aa_s), badesc0 = sw32_desc(ring_s);
       const int KC = a.KC;
-      for (int u = pair; u < units; u += npairs, ++ua) {
-        const int r = u % a.R;
+      for (int iu = 0;; ++iu, ++ua) {
+        const int u = pair_unit(a, S, iu, pair, npairs, units, false);
+        pair_unit_release(a, S, iu);
+        if (u < 0) break;
+        int qp, r;
+        unit_coords(a, u, &qp, &r);
         tc::mbar_wait(&S.a_full, ua & 1u);
         tc::fence_after_sync();
         int t0, t1;
@@ -499,8 +669,13 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
   } else if (warp == kInfoWarp) {
     // =========================== tile info (sets, columns, norms) ===========================
     uint32_t tile_ctr = 0;
-    for (int u = pair; u < units; u += npairs) {
-      const int r = u % a.R;
+    for (int iu = 0;; ++iu) {
+      const int u = pair_unit(a, S, iu, pair, npairs, units, false);
+      __syncwarp();
+      if (lane == 0) pair_unit_release(a, S, iu);
+      if (u < 0) break;
+      int qp, r;
+      unit_coords(a, u, &qp, &r);
       int t0, t1;
       range_tiles(r, a.R, a.ntiles, &t0, &t1);
       for (int t = t0; t < t1; ++t, ++tile_ctr) {
@@ -546,8 +721,14 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
     uint32_t tile_ctr = 0;
     unsigned long long n_surv = 0, n_emit = 0;  // statistics, flushed once (a per-survivor global atomic on one
                                                 // address would serialise in L2)
-    for (int u = pair; u < units; u += npairs) {
-      const int qt = 2 * (u / a.R) + static_cast<int>(crank), r = u % a.R;
+    for (int iu = 0;; ++iu) {
+      const int u = pair_unit(a, S, iu, pair, npairs, units, false);
+      __syncwarp();
+      if (lane == 0) pair_unit_release(a, S, iu);
+      if (u < 0) break;
+      int qp, r;
+      unit_coords(a, u, &qp, &r);
+      const int qt = 2 * qp + static_cast<int>(crank);
       const int prow = qt * kDenseM + quarter * 32 + lane;
       const int qid = a.lane_qid[prow];
       const bool valid = qid >= 0;
@@ -555,7 +736,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
       const unsigned segmask = __match_any_sync(0xffffffffu, qid);
       const float E = valid ? a.qE[qid] : 0.0f;
       const float* lq = valid ? a.lists + (static_cast<int64_t>(qid) * a.R + r) * kEpiSub * a.k : nullptr;
-      float tau = valid ? a.tau0[qid] : INF;
+      float tau = valid ? vload_volatile(a.tau0 + qid) : INF;
       float other_k = INF;  // the other warps' k-th bounds, loaded one tile ahead (their latency stays hidden)
       int t0, t1;
       range_tiles(r, a.R, a.ntiles, &t0, &t1);
@@ -565,7 +746,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
         // (developer BVSS_DENSE_DEBUG 8 .. 11 switch tau sources off: 8 none, 9 the own list, 10 + the other
         // warps' lists at insertion, 11 + the union)
         if (a.debug < 8) tau = fminf(tau, other_k);
-        if ((a.debug < 8 || a.debug == 11) && ((tile_ctr + 8u * static_cast<uint32_t>(sub)) & 31u) == 0u) {  // every 32 tiles (staggered): the k-th of
+        // at the start of every unit and every 32 tiles (staggered): the k-th of
+        if ((a.debug < 8 || a.debug == 11) && (t == t0 || ((tile_ctr + 8u * static_cast<uint32_t>(sub)) & 31u) == 0u)) {
           unsigned pend = __ballot_sync(0xffffffffu, valid);               // the union of the query's lists
           while (pend) {
             const int ld = __ffs(pend) - 1;
@@ -573,8 +755,11 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
             pend &= ~sm;
             const int qq = __shfl_sync(0xffffffffu, qid, ld);
             const int nr = a.R < 8 ? a.R : 8;
-            const float uk = union_kth(a.lists + static_cast<int64_t>(qq) * a.R * kEpiSub * a.k, a.R, r, nr, a.k, lane);
-            if ((sm >> lane) & 1u) tau = fminf(tau, uk);
+            const float uk = union_kth(a.lists + static_cast<int64_t>(qq) * a.R * kEpiSub * a.k, a.R, r, nr, a.k, lane,
+                                       a.dyn ? -1 : 1);
+            const float tr = vload_volatile(a.tau0 + qq);
+            if ((sm >> lane) & 1u) tau = fminf(tau, fminf(uk, tr));
+            if (lane == ld && tau < tr) atomicMin(reinterpret_cast<int*>(a.tau0) + qq, __float_as_int(tau));
           }
         }
         if (valid) {
@@ -595,10 +780,10 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
           const int i = s0 + js;
           const int col0 = inf.col0[js];
           const int mv = inf.mv[js];
-          SetCols cols;  // (sets of <= 32 rows keep their columns in registers for the survivor's B)
+          Cols cols;  // (sets of <= CH rows keep their columns in registers for the survivor's B)
           float m = -INF;  // max_v acc (kappa < 0: the min over v of D^2)
-          for (int j0 = 0; j0 < mv; j0 += 32) {
-            const int mvc = min(32, mv - j0);
+          for (int j0 = 0; j0 < mv; j0 += CH) {
+            const int mvc = min(CH, mv - j0);
             load_set(tb + static_cast<uint32_t>(col0 + j0), mvc, cols);
             m = fmaxf(m, set_max(cols, mvc));
           }
@@ -619,13 +804,13 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
             const bool inseg = (smask >> lane) & 1u;
             const float A = __uint_as_float(__reduce_max_sync(0xffffffffu, inseg ? __float_as_uint(rq) : 0u));
             float B;
-            if (mv <= 32) {
+            if (mv <= CH) {
               B = set_colmin_max(cols, mv, a.kappa, qn, inseg);
             } else {
               B = 0.0f;
-              for (int j0 = 0; j0 < mv; j0 += 32) {
-                SetCols cb;
-                const int mvc = min(32, mv - j0);
+              for (int j0 = 0; j0 < mv; j0 += CH) {
+                Cols cb;
+                const int mvc = min(CH, mv - j0);
                 load_set(tb + static_cast<uint32_t>(col0 + j0), mvc, cb);
                 B = fmaxf(B, set_colmin_max(cb, mvc, a.kappa, qn, inseg));
               }
@@ -673,6 +858,9 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
           tc::mbar_arrive(&S.info_empty[slot]);
         }
       }
+      // the unit's final tau of each query segment -> the query's running tau
+      if (valid && lane == __ffs(segmask) - 1 && a.debug < 8)
+        atomicMin(reinterpret_cast<int*>(a.tau0) + qid, __float_as_int(tau));
     }
     unsigned int ne = static_cast<unsigned int>(n_emit);
     ne = __reduce_add_sync(0xffffffffu, ne);  // emissions were counted by the segment leaders
@@ -850,11 +1038,11 @@ int launch_dense_prep(const int64_t* qoff, const float* qnorm, int nq, float c1,
 int launch_dense_hausdorff(const __half* qd, int ntq, const __half* hd, int64_t nvec, int dpad, int ntiles,
                            const int32_t* tile_s0, const int32_t* tile_s1, const int64_t* off, const __half* va,
                            const __half* qa,
-                           const int32_t* lane_qid, const float* lane_qn, const float* qE, const float* tau0,
+                           const int32_t* lane_qid, const float* lane_qn, const float* qE, float* tau0,
                            float kappa, float alpha, int k, int R, float* lists, int32_t* cnt, int32_t* ids,
                            float* vals, int cap,
                            const uint32_t* mask, int64_t mask_stride, int64_t id_base, unsigned long long* stat,
-                           int num_sms, cudaStream_t st) {
+                           int dyn, int* unit_ctr, int num_sms, cudaStream_t st) {
   if (ntq <= 0 || ntiles <= 0) return BVSS_OK;
   if (dpad % 64 || dpad > dense_max_dpad()) BVSS_FAIL(BVSS_EUNSUPPORTED, "dense path needs dpad <= 512");
   DenseArgs a;
@@ -889,6 +1077,9 @@ int launch_dense_hausdorff(const __half* qd, int ntq, const __half* hd, int64_t 
   a.mask_stride = mask_stride;
   a.id_base = id_base;
   a.stat = stat;
+  a.dyn = dyn;
+  a.unit_ctr = unit_ctr;
+  if (dyn) BVSS_CUDA(cudaMemsetAsync(unit_ctr, 0, sizeof(int), st));
   {
     const char* e = getenv("BVSS_DENSE_DEBUG");
     a.debug = e ? atoi(e) : 0;
@@ -904,8 +1095,10 @@ int launch_dense_hausdorff(const __half* qd, int ntq, const __half* hd, int64_t 
   const int units = (ntq / 2) * R;
   int pairs = num_sms / 2;
   if (pairs > units) pairs = units;
-  BVSS_CUDA(cudaFuncSetAttribute(dense_hausdorff_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)));
+  int exact_ld = 1;
+  if (const char* e = getenv("BVSS_DENSE_LD")) exact_ld = atoi(e) != 0;  // developer switch: 0 = 32 + 8 columns
+  auto kern = exact_ld ? dense_hausdorff_kernel<true> : dense_hausdorff_kernel<false>;
+  BVSS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs));
   cfg.blockDim = dim3(kDenseThreads);
@@ -918,7 +1111,7 @@ int launch_dense_hausdorff(const __half* qd, int ntq, const __half* hd, int64_t 
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  BVSS_CUDA(cudaLaunchKernelEx(&cfg, dense_hausdorff_kernel, a));
+  BVSS_CUDA(cudaLaunchKernelEx(&cfg, kern, a));
   BVSS_TRY(post_launch("dense_hausdorff_kernel", st));
   if (a.prof) {  // developer instrumentation: per-CTA Mcycles per role and wait (epilogue: per warp)
     unsigned long long h[16];

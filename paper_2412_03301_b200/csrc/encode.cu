@@ -9,6 +9,8 @@
 // 32-step bisection on order-preserving uint32 keys (warp redux counts), ties
 // at the threshold go to the lowest row index (reading R4), and code word t is
 // a warp ballot, so the code is written without any shared-memory scatter.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace bvss {
@@ -138,6 +140,178 @@ __global__ void __launch_bounds__(256) flyhash_wta_kernel(
   }
 }
 
+// ---------------------------------------------------------------------------------------------------------
+// K1, lane-per-vector form (codes only).  A warp encodes 32 vectors at once, lane = vector: the tile is staged
+// dim-major in shared memory ([d][32] fp32, column = vector ^ (dim & 31), so both the transposing stores and
+// the gathers are conflict-free), W's row j is a warp-uniform list of s indices (a broadcast), and each gather
+// serves 32 vectors with one conflict-free wavefront (the warp-per-vector form's gathers at 32 random
+// addresses collide ~3.5-way and need a W-index load each).  The additions are the same left-to-right fp32
+// sums from +0.0f over the sorted S_j (reading R8), so the activations are bit-identical.
+// WTA per lane: rows come in increasing j; a row enters the lane's candidate buffer (shared memory, column =
+// lane) when its key beats the lane's threshold theta (strictly: a later row loses every tie, reading R4);
+// when a buffer nears its capacity it is compacted to the exact top L by (key desc, j asc) -- the L-th
+// largest key K by bisection on the key bits, every key > K and the first (lowest-j) entries equal to K --
+// and theta = K.  Dropped rows can never re-enter the top L, so the final compaction is exactly Def 7's WTA.
+constexpr int kLanesRB = 8;  // rows per block between buffer checks
+
+__device__ __forceinline__ int lanes_compact(uint32_t* kb, uint16_t* jb, int cnt, int L, int lane, uint32_t* theta) {
+  const int cmax = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(cnt));
+  uint32_t kmin = 0xffffffffu, kmax = 0u;
+  for (int e = 0; e < cmax; ++e)
+    if (e < cnt) {
+      const uint32_t k = kb[e * 32 + lane];
+      kmin = min(kmin, k);
+      kmax = max(kmax, k);
+    }
+  const bool act = cnt > L;
+  // bisection below the lane's common high bits of kmin / kmax; the loop bound is the warp's widest span
+  const uint32_t diff = act ? (kmin ^ kmax) : 0u;
+  const int hb = diff ? 31 - __clz(diff) : -1;
+  const int hbw = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(hb + 1))) - 1;
+  uint32_t prefix = hb >= 0 ? (kmin & ~((2u << hb) - 1u)) : kmin;  // (hb = 31: the mask is 0)
+  if (hb == 31) prefix = 0u;
+  for (int b = hbw; b >= 0; --b) {
+    const uint32_t cand = prefix | (1u << b);
+    int c = 0;
+    for (int e = 0; e < cmax; ++e) c += (e < cnt && kb[e * 32 + lane] >= cand) ? 1 : 0;
+    if (act && b <= hb && c >= L) prefix = cand;
+  }
+  if (!act) return cnt;
+  int gt = 0;
+  for (int e = 0; e < cmax; ++e) gt += (e < cnt && kb[e * 32 + lane] > prefix) ? 1 : 0;
+  int need = L - gt, w = 0;
+  for (int e = 0; e < cmax; ++e)
+    if (e < cnt) {
+      const uint32_t k = kb[e * 32 + lane];
+      bool keep = k > prefix;
+      if (!keep && k == prefix && need > 0) {
+        keep = true;
+        --need;
+      }
+      if (keep) {
+        const uint16_t j = jb[e * 32 + lane];
+        kb[w * 32 + lane] = k;
+        jb[w * 32 + lane] = j;
+        ++w;
+      }
+    }
+  *theta = prefix;
+  return w;
+}
+
+template <int SS>
+__global__ void __launch_bounds__(128) flyhash_lanes_kernel(const float* __restrict__ V, int64_t nvec, int d,
+                                                            const uint16_t* __restrict__ Wt /*[s][m]*/, int m, int L,
+                                                            int cap, uint32_t* __restrict__ codes) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  constexpr int S = SS;
+  uint16_t* sW = reinterpret_cast<uint16_t*>(smem);  // [m][S] (row-major: row j's indices are contiguous)
+  const size_t wbytes = (static_cast<size_t>(m) * S * 2 + 15) & ~size_t(15);
+  const int R = m >> 5;
+  const size_t per_warp = static_cast<size_t>(d) * 128 + static_cast<size_t>(cap) * 128 + static_cast<size_t>(cap) * 64 +
+                          static_cast<size_t>(R) * 128;
+  for (int i = threadIdx.x; i < S * m; i += blockDim.x) {
+    const int u = i / m, j = i - u * m;
+    sW[j * S + u] = Wt[i];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  uint8_t* wb = smem + wbytes + per_warp * warp;
+  float* sV = reinterpret_cast<float*>(wb);                                         // [d][32]
+  uint32_t* kb = reinterpret_cast<uint32_t*>(wb + static_cast<size_t>(d) * 128);     // [cap][32]
+  uint16_t* jb = reinterpret_cast<uint16_t*>(wb + static_cast<size_t>(d) * 128 + static_cast<size_t>(cap) * 128);
+  uint32_t* cw = reinterpret_cast<uint32_t*>(wb + static_cast<size_t>(d) * 128 + static_cast<size_t>(cap) * 192);  // [R][32]
+  const int64_t ntile = (nvec + 31) >> 5;
+  for (int64_t tile = static_cast<int64_t>(blockIdx.x) * nwarps + warp; tile < ntile;
+       tile += static_cast<int64_t>(gridDim.x) * nwarps) {
+    const int64_t v0 = tile << 5;
+    const int nv = nvec - v0 < 32 ? static_cast<int>(nvec - v0) : 32;
+    __syncwarp();
+#pragma unroll 4
+    for (int v = 0; v < 32; ++v) {  // dim-major staging (lane = dim within a 32-dim group)
+      const float* src = V + (v0 + v) * d;
+      for (int c = lane; c < d; c += 32) sV[c * 32 + (v ^ lane)] = v < nv ? src[c] : 0.0f;
+    }
+    for (int w = 0; w < R; ++w) cw[w * 32 + lane] = 0u;
+    __syncwarp();
+    uint32_t theta = 0u;  // every real key is > 0
+    int cnt = 0;
+    for (int j0 = 0; j0 < m; j0 += kLanesRB) {
+      uint32_t key[kLanesRB];
+#pragma unroll
+      for (int i = 0; i < kLanesRB; ++i) {
+        // row j's S indices by the widest aligned broadcast loads (S = 8: one 16-byte load)
+        uint16_t wr[S];
+        if constexpr (S % 8 == 0) {
+#pragma unroll
+          for (int q = 0; q < S / 8; ++q) *reinterpret_cast<uint4*>(wr + 8 * q) = reinterpret_cast<const uint4*>(sW + (j0 + i) * S)[q];
+        } else if constexpr (S % 4 == 0) {
+#pragma unroll
+          for (int q = 0; q < S / 4; ++q) *reinterpret_cast<uint2*>(wr + 4 * q) = reinterpret_cast<const uint2*>(sW + (j0 + i) * S)[q];
+        } else {
+#pragma unroll
+          for (int q = 0; q < S / 2; ++q) *reinterpret_cast<uint32_t*>(wr + 2 * q) = reinterpret_cast<const uint32_t*>(sW + (j0 + i) * S)[q];
+        }
+        float g[S];
+#pragma unroll
+        for (int u = 0; u < S; ++u) {
+          const int x = wr[u];
+          g[u] = sV[x * 32 + (lane ^ (x & 31))];
+        }
+        float acc = 0.0f;
+#pragma unroll
+        for (int u = 0; u < S; ++u) acc = __fadd_rn(acc, g[u]);
+        key[i] = float_order_key(acc);
+      }
+#pragma unroll
+      for (int i = 0; i < kLanesRB; ++i)
+        if (key[i] > theta) {
+          kb[cnt * 32 + lane] = key[i];
+          jb[cnt * 32 + lane] = static_cast<uint16_t>(j0 + i);
+          ++cnt;
+        }
+      if (__any_sync(0xffffffffu, cnt > cap - kLanesRB)) cnt = lanes_compact(kb, jb, cnt, L, lane, &theta);
+    }
+    cnt = lanes_compact(kb, jb, cnt, L, lane, &theta);  // exactly the top L
+    for (int e = 0; e < cnt; ++e) {  // (word w of vector `lane` lives at column lane ^ (w & 31))
+      const int j = jb[e * 32 + lane], w = j >> 5;
+      cw[w * 32 + (lane ^ (w & 31))] |= 1u << (j & 31);
+    }
+    __syncwarp();
+    for (int v = 0; v < nv; ++v)  // code of vector v: word w from lane w (coalesced rows, conflict-free reads)
+      for (int w = lane; w < R; w += 32) codes[(v0 + v) * R + w] = cw[w * 32 + (v ^ (w & 31))];
+  }
+}
+
+// shared memory of the lane-per-vector encoder per warp, and whether it applies (s compiled, cap fits)
+static size_t lanes_warp_bytes(int m, int d, int cap) {
+  return static_cast<size_t>(d) * 128 + static_cast<size_t>(cap) * 192 + static_cast<size_t>(m / 32) * 128;
+}
+
+int launch_encode_lanes(const float* V, int64_t nvec, int d, const uint16_t* Wt, int m, int s, int L,
+                        uint32_t* codes, int num_sms, cudaStream_t st, bool* done) {
+  *done = false;
+  if (const char* e = getenv("BVSS_ENC_LANES"))
+    if (atoi(e) == 0) return BVSS_OK;  // developer switch: the warp-per-vector kernel for codes too
+  if (nvec <= 0 || codes == nullptr || m > 65535 || (s != 8 && s != 6 && s != 12)) return BVSS_OK;
+  const int cap = ((L + kLanesRB + 24) + 7) & ~7;  // room for 3 blocks of appends past L between compactions
+  const size_t wbytes = (static_cast<size_t>(m) * s * 2 + 15) & ~size_t(15);
+  const size_t pw = lanes_warp_bytes(m, d, cap);
+  int warps = static_cast<int>((227 * 1024 - wbytes) / pw);
+  if (warps > 4) warps = 4;
+  if (warps < 2) return BVSS_OK;  // (large d / m / L: the warp-per-vector kernel)
+  const size_t smem = wbytes + pw * warps;
+  const int64_t ntile = (nvec + 31) / 32;
+  const int64_t want = ceil_div<int64_t>(ntile, warps);
+  const int grid = static_cast<int>(want < num_sms ? want : num_sms);
+  auto kfn = s == 8 ? flyhash_lanes_kernel<8> : s == 6 ? flyhash_lanes_kernel<6> : flyhash_lanes_kernel<12>;
+  BVSS_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  kfn<<<grid, 32 * warps, smem, st>>>(V, nvec, d, Wt, m, L, cap, codes);
+  BVSS_TRY(post_launch(__func__, st));
+  *done = true;
+  return BVSS_OK;
+}
+
 size_t encode_smem_bytes(int m, int s, int d) {
   return ((static_cast<size_t>(s) * m * 2 + 15) & ~size_t(15)) + static_cast<size_t>(8) * d * 4;
 }
@@ -146,6 +320,12 @@ int launch_encode(const float* V, int64_t nvec, int d, const uint16_t* Wt, int m
                   float* norms, __half* hs, __half* ls, float* scale, int dpad, int64_t rows, const int64_t* dst_row,
                   int kcs, int num_sms, cudaStream_t st) {
   if (nvec <= 0) return BVSS_OK;
+  bool lanes = false;  // codes by the lane-per-vector kernel; this one then writes only norms and the split
+  BVSS_TRY(launch_encode_lanes(V, nvec, d, Wt, m, s, L, codes, num_sms, st, &lanes));
+  if (lanes) {
+    codes = nullptr;
+    if (norms == nullptr && hs == nullptr) return BVSS_OK;
+  }
   const size_t smem = encode_smem_bytes(m, s, d);
   const int R = m / 32;
   const int64_t want = ceil_div<int64_t>(nvec, 8);

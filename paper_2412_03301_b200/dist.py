@@ -114,7 +114,9 @@ def sharded_search(ops, queries, q_offsets, k: int, T: int, n_total: int, group=
     the same merged top-k (ids int64 [nq][k], dist fp32 [nq][k])."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    T_eff = min(int(T), int(n_total))
+    if int(T) < int(k):
+        raise ValueError(f"T ({T}) < k ({k}) (reading R16)")
+    T_eff = min(int(T), int(n_total))  # (may be < k when the database has fewer than k sets: padded results)
     rounds = ops.begin(queries, q_offsets, k, T_eff)
     try:
         for r in range(rounds):

@@ -37,6 +37,12 @@ def test_no_cpu_fallback(libpath):
     with pytest.raises(bvss.BvssError) as e:
         bvss.Index(np.zeros((4, 8), np.float32), np.array([0, 4]), m=32, s=2, L=4)
     assert e.value.code in (bvss.EUNSUPPORTED, bvss.ECUDA)
+    with pytest.raises(bvss.BvssError) as e:  # the multi-device group too (every shard build fails loudly)
+        bvss.Group(np.zeros((4, 8), np.float32), np.array([0, 2, 4]), devices=[0, 0], m=32, s=2, L=4)
+    assert e.value.code in (bvss.EUNSUPPORTED, bvss.ECUDA)
+    with pytest.raises(bvss.BvssError) as e:
+        bvss.Group(np.zeros((4, 8), np.float32), np.array([0, 2, 4]), devices=[], m=32, s=2, L=4)
+    assert e.value.code == bvss.EINVAL
 
 
 @pytest.mark.parametrize("struct,pyname", [("bvss_params", "Params"), ("bvss_info", "Info"), ("bvss_stats", "Stats")])
