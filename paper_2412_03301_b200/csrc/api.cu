@@ -138,7 +138,7 @@ int launch_dense_hausdorff(const __half* qd, int ntq, const __half* hd, int64_t 
                            float kappa, float alpha, int k, int R, float* lists, int32_t* cnt, int32_t* ids,
                            float* vals, int cap,
                            const uint32_t* mask, int64_t mask_stride, int64_t id_base, unsigned long long* stat,
-                           int dyn, int* unit_ctr, int num_sms, cudaStream_t st);
+                           int dyn, int* unit_ctr, int* udone, int num_sms, cudaStream_t st);
 
 // ------------------------------------------------------- small kernels --
 __global__ void fill_i32_kernel(int32_t* __restrict__ x, int64_t n, int32_t v) {
@@ -930,7 +930,7 @@ int dense_refine_topk(bvss_index* idx, bvss_search_ctx* c, const uint32_t* mask,
   // units per SM pair, pair-major.
   int dyn = 1;
   if (const char* e = getenv("BVSS_DENSE_DYN")) dyn = atoi(e) != 0;
-  int tpr = 512;
+  int tpr = 1024;
   if (const char* e = getenv("BVSS_DENSE_TPR")) tpr = atoi(e) > 0 ? atoi(e) : tpr;  // developer switch
   int R = dyn ? static_cast<int>(ceil_div<int64_t>(ntiles, tpr))
               : static_cast<int>(ceil_div<int64_t>(2 * idx->num_sms, ntq));
@@ -944,8 +944,8 @@ int dense_refine_topk(bvss_index* idx, bvss_search_ctx* c, const uint32_t* mask,
   const double spl = std::max(1.0, static_cast<double>(idx->n) / (static_cast<double>(R_emit) * dense_epi_sub() * k));
   const double lists_pq = static_cast<double>(R_emit) * dense_epi_sub();  // bound lists per query
   int64_t cap = static_cast<int64_t>(lists_pq * k * (2.0 + std::log(spl)) * 2.0) + idx->dnhuge + 1024;
-  if (const char* e = getenv("BVSS_DEBUG_DENSE_CAP")) cap = atoll(e);  // test switch: force overflows
   cap = (cap + 255) & ~int64_t(255);
+  if (const char* e = getenv("BVSS_DEBUG_DENSE_CAP")) cap = atoll(e);  // test switch: force overflows (cap < k)
   // query max norm -> S_q
   unsigned int* vmax;
   BVSS_TRY(idx->ws.get("vmax", sizeof(unsigned int), reinterpret_cast<void**>(&vmax)));
@@ -988,6 +988,8 @@ int dense_refine_topk(bvss_index* idx, bvss_search_ctx* c, const uint32_t* mask,
   BVSS_TRY(c->alloc(2 * sizeof(unsigned long long), reinterpret_cast<void**>(&stat)));
   int* unit_ctr;
   BVSS_TRY(c->alloc(sizeof(int), reinterpret_cast<void**>(&unit_ctr)));
+  int* udone;
+  BVSS_TRY(c->alloc(static_cast<size_t>(ntq / 2) * R * sizeof(int), reinterpret_cast<void**>(&udone)));
   BVSS_CUDA(cudaMemcpyAsync(d_rowmap, rowmap.data(), rows * 4, cudaMemcpyHostToDevice, idx->stream));
   BVSS_CUDA(cudaMemcpyAsync(d_rowq, rowq.data(), rows * 4, cudaMemcpyHostToDevice, idx->stream));
   BVSS_CUDA(cudaMemsetAsync(stat, 0, 2 * sizeof(unsigned long long), idx->stream));
@@ -1007,7 +1009,7 @@ int dense_refine_topk(bvss_index* idx, bvss_search_ctx* c, const uint32_t* mask,
                                   idx->off, idx->va, qa, lane_qid, lane_qn, qE, tau0, -2.0f * sq * idx->dense_s, alpha,
                                   k, R,
                                   lists, cnt, ids, vals, static_cast<int>(cap), mask, mask_stride, c->id_base, stat,
-                                  dyn, unit_ctr, idx->num_sms, idx->stream));
+                                  dyn, unit_ctr, udone, idx->num_sms, idx->stream));
   cudaEventRecord(idx->ev[5], idx->stream);
   idx->stats.kernel_launches += 6;
   // overflow check

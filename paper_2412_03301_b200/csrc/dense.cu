@@ -133,6 +133,9 @@ struct DenseArgs {
                                 // 3 = no survivor work, 4 = no database loads and no epilogue (timing only)
   int dyn;                      // 1: units handed out by a global counter in range-major order (see pair_unit)
   int* unit_ctr;                // [1] next unit (dyn), zeroed before the launch
+  int* udone;                   // [nqp][R] (dyn): epilogue warps that finished unit (qp, r), zeroed before the
+                                // launch; a unit whose predecessor range is complete (2 kEpiWarpsD) inherits its
+                                // lists, so each warp's list holds its best k over every range run so far
 };
 
 // per-tile metadata the info warp stages for the epilogue (shared memory): the database sets of the tile
@@ -737,6 +740,26 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
       const float E = valid ? a.qE[qid] : 0.0f;
       const float* lq = valid ? a.lists + (static_cast<int64_t>(qid) * a.R + r) * kEpiSub * a.k : nullptr;
       float tau = valid ? vload_volatile(a.tau0 + qid) : INF;
+      // dyn: inherit this warp's list of the previous range when that unit is complete.  The three warps of
+      // a quarter see disjoint sets of the query, and an inherited list only ever continues in this range, so
+      // the union of the current range's three lists holds distinct sets: its k-th is a valid tau over every
+      // range run so far (the union never mixes ranges in dyn mode).
+      if (a.dyn && r > 0) {
+        int c;
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(c) : "l"(a.udone + static_cast<int64_t>(qp) * a.R + r - 1)
+                     : "memory");
+        if (c == 2 * kEpiWarpsD) {
+          unsigned pend = __ballot_sync(0xffffffffu, valid);
+          while (pend) {
+            const int ld = __ffs(pend) - 1;
+            pend &= ~__shfl_sync(0xffffffffu, segmask, ld);
+            const int qq = __shfl_sync(0xffffffffu, qid, ld);
+            float* dst = a.lists + ((static_cast<int64_t>(qq) * a.R + r) * kEpiSub + sub) * a.k;
+            if (lane < a.k) dst[lane] = vload_volatile(dst - kEpiSub * a.k + lane);
+          }
+          __syncwarp();
+        }
+      }
       float other_k = INF;  // the other warps' k-th bounds, loaded one tile ahead (their latency stays hidden)
       int t0, t1;
       range_tiles(r, a.R, a.ntiles, &t0, &t1);
@@ -754,7 +777,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
             const unsigned sm = __shfl_sync(0xffffffffu, segmask, ld);
             pend &= ~sm;
             const int qq = __shfl_sync(0xffffffffu, qid, ld);
-            const int nr = a.R < 8 ? a.R : 8;
+            const int nr = a.dyn ? 1 : (a.R < 8 ? a.R : 8);
             const float uk = union_kth(a.lists + static_cast<int64_t>(qq) * a.R * kEpiSub * a.k, a.R, r, nr, a.k, lane,
                                        a.dyn ? -1 : 1);
             const float tr = vload_volatile(a.tau0 + qq);
@@ -861,6 +884,13 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
       // the unit's final tau of each query segment -> the query's running tau
       if (valid && lane == __ffs(segmask) - 1 && a.debug < 8)
         atomicMin(reinterpret_cast<int*>(a.tau0) + qid, __float_as_int(tau));
+      if (a.dyn) {  // this warp's lists of the unit are final (release: the next range may inherit them)
+        __threadfence();
+        __syncwarp();
+        if (lane == 0)
+          asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.udone + static_cast<int64_t>(qp) * a.R + r)
+                       : "memory");
+      }
     }
     unsigned int ne = static_cast<unsigned int>(n_emit);
     ne = __reduce_add_sync(0xffffffffu, ne);  // emissions were counted by the segment leaders
@@ -1042,7 +1072,7 @@ int launch_dense_hausdorff(const __half* qd, int ntq, const __half* hd, int64_t 
                            float kappa, float alpha, int k, int R, float* lists, int32_t* cnt, int32_t* ids,
                            float* vals, int cap,
                            const uint32_t* mask, int64_t mask_stride, int64_t id_base, unsigned long long* stat,
-                           int dyn, int* unit_ctr, int num_sms, cudaStream_t st) {
+                           int dyn, int* unit_ctr, int* udone, int num_sms, cudaStream_t st) {
   if (ntq <= 0 || ntiles <= 0) return BVSS_OK;
   if (dpad % 64 || dpad > dense_max_dpad()) BVSS_FAIL(BVSS_EUNSUPPORTED, "dense path needs dpad <= 512");
   DenseArgs a;
@@ -1079,7 +1109,11 @@ int launch_dense_hausdorff(const __half* qd, int ntq, const __half* hd, int64_t 
   a.stat = stat;
   a.dyn = dyn;
   a.unit_ctr = unit_ctr;
-  if (dyn) BVSS_CUDA(cudaMemsetAsync(unit_ctr, 0, sizeof(int), st));
+  a.udone = udone;
+  if (dyn) {
+    BVSS_CUDA(cudaMemsetAsync(unit_ctr, 0, sizeof(int), st));
+    BVSS_CUDA(cudaMemsetAsync(udone, 0, static_cast<size_t>(ntq / 2) * R * sizeof(int), st));
+  }
   {
     const char* e = getenv("BVSS_DENSE_DEBUG");
     a.debug = e ? atoi(e) : 0;

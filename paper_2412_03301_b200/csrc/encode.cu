@@ -291,8 +291,11 @@ static size_t lanes_warp_bytes(int m, int d, int cap) {
 int launch_encode_lanes(const float* V, int64_t nvec, int d, const uint16_t* Wt, int m, int s, int L,
                         uint32_t* codes, int num_sms, cudaStream_t st, bool* done) {
   *done = false;
-  if (const char* e = getenv("BVSS_ENC_LANES"))
-    if (atoi(e) == 0) return BVSS_OK;  // developer switch: the warp-per-vector kernel for codes too
+  // opt-in (BVSS_ENC_LANES=1): measured slower than the warp-per-vector kernel on B200 (cfg3, 3.6M vectors:
+  // build 104 ms vs 37 ms; bit-identical codes): with 64 KB of shared memory per warp only 3 warps fit on an
+  // SM and the gather / compaction chains are latency-bound
+  const char* env = getenv("BVSS_ENC_LANES");
+  if (!env || atoi(env) == 0) return BVSS_OK;
   if (nvec <= 0 || codes == nullptr || m > 65535 || (s != 8 && s != 6 && s != 12)) return BVSS_OK;
   const int cap = ((L + kLanesRB + 24) + 7) & ~7;  // room for 3 blocks of appends past L between compactions
   const size_t wbytes = (static_cast<size_t>(m) * s * 2 + 15) & ~size_t(15);

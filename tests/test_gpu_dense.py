@@ -56,10 +56,18 @@ def test_dense_bruteforce_matches_oracle(name, ov, limit):
         check_topk(ids[qi], dist[qi], o_ids, o_d, lambda i: h[i])
 
 
-def test_dense_bruteforce_equals_query_major_refine():
+@pytest.mark.parametrize("sched", [{}, {"BVSS_DENSE_TPR": "3"}, {"BVSS_DENSE_TPR": "16"},
+                                   {"BVSS_DENSE_DYN": "0"}, {"BVSS_DENSE_DYN": "0", "BVSS_DENSE_R": "7"},
+                                   {"BVSS_DENSE_LD": "0"}])
+def test_dense_bruteforce_equals_query_major_refine(sched, monkeypatch):
     """Every query: the dense brute force and the query-major refine over all n candidates (bvss_refine) give
-    identical ids and distances (the same exact fp32 fix-up decides both)."""
+    identical ids and distances (the same exact fp32 fix-up decides both).  Under every schedule: the default
+    (dynamic range-major units; one range at this n), small ranges (many units per query tile pair: the
+    running tau and the list inheritance from the previous range are exercised), the static pair-major
+    schedule with its union over ranges, and the 32 + 8 column TMEM reads."""
     _need_gpu()
+    for k, v in sched.items():
+        monkeypatch.setenv(k, v)
     cfg = synth.get_config("cfg3", n=3000, nq=200)
     data = synth.to_numpy(synth.generate(cfg, device="cpu"))
     idx = _index(cfg, data)

@@ -1,5 +1,5 @@
-"""K1 encoder A/B (developer tool): the lane-per-vector kernel (default) vs the warp-per-vector kernel
-(BVSS_ENC_LANES=0) -- build time of the same index and identical codes (export_codes).  The library reads the
+"""K1 encoder A/B (developer tool): the lane-per-vector kernel (BVSS_ENC_LANES=1) vs the warp-per-vector
+kernel (default) -- build time of the same index and identical codes (export_codes).  The library reads the
 switch per call, so both run in one process."""
 import os, sys, time
 import numpy as np
