@@ -122,7 +122,7 @@ typedef struct bvss_index bvss_index;
 
 typedef struct {
   int64_t n, nvec;       /* sets and vectors in the index */
-  int32_t d, dpad;       /* dimension, and its padding to a multiple of 64 for the bf16 copies */
+  int32_t d, dpad;       /* dimension, and its padding to a multiple of 64 for the fp16 copies */
   uint32_t m, s, L, sketch;
   int32_t device;
   uint64_t device_bytes; /* device memory owned by the index (excluding search workspace) */
@@ -153,7 +153,7 @@ typedef struct {
 /* Build an index over n sets (Alg 1 + Alg 3 / Alg 5, P:323-343, P:665-682,
  * P:738-757): copies vectors to the device, generates W (or takes p->projection),
  * encodes every vector (FlyHash + WTA), folds per-set sketches, and prepares the
- * refine operands (bf16 hi/lo split, fp32 squared norms).
+ * refine operands (fp16 hi/lo split, fp32 squared norms).
  *   vectors     [set_offsets[n]][d] fp32
  *   set_offsets [n+1] int64
  * Errors: BVSS_EINVAL for bad sizes/offsets/params, BVSS_ENONFINITE (with

@@ -3,7 +3,7 @@
 // Owns the index (device buffers, stream, workspace), validates arguments,
 // generates the projection W (H2, reading R7), plans query sub-batches and
 // launches the kernels of the hot path:
-//   build : K1 encode (+K9 norms, bf16 split)  ->  K2 sketches
+//   build : K1 encode (+K9 norms, fp16 split)  ->  K2 sketches
 //   search: K1/K2 on the queries -> K3 scan -> K4 select -> K5 refine -> K6 top-k
 #include <algorithm>
 #include <chrono>
@@ -453,7 +453,7 @@ int host_offsets(bvss_index* idx, const int64_t* qoff_in, int64_t nq, bool dev_p
   return check_offsets(out.data(), nq, "query");
 }
 
-// ---- query preparation (a-4, Alg 6 lines 1-2): copy, encode (+norms, bf16 split), sketch.
+// ---- query preparation (a-4, Alg 6 lines 1-2): copy, encode (+norms, fp16 split), sketch.
 // `queries` points at row qoff_host[0] == 0 of this batch; qoff_host is validated.
 int prepare_queries(bvss_index* idx, bvss_search_ctx* c, const float* queries, const std::vector<int64_t>& qoff_host,
                     bool vec_dev, bool validate) {
@@ -930,7 +930,7 @@ int dense_refine_topk(bvss_index* idx, bvss_search_ctx* c, const uint32_t* mask,
   // units per SM pair, pair-major.
   int dyn = 1;
   if (const char* e = getenv("BVSS_DENSE_DYN")) dyn = atoi(e) != 0;
-  int tpr = 1024;
+  int tpr = 256;
   if (const char* e = getenv("BVSS_DENSE_TPR")) tpr = atoi(e) > 0 ? atoi(e) : tpr;  // developer switch
   int R = dyn ? static_cast<int>(ceil_div<int64_t>(ntiles, tpr))
               : static_cast<int>(ceil_div<int64_t>(2 * idx->num_sms, ntq));

@@ -8,14 +8,14 @@
 // moves T x (set rows) x d x 2 bytes per query.  This kernel instead streams the
 // database ONCE per 128-row query tile: the query tile is the stationary A
 // operand (M = 128 packed query rows, resident in shared memory), the database
-// rows stream through a TMA ring as the B operand (N = 240 rows per tile, K = d
+// rows stream through a TMA ring as the B operand (N = 256 rows per tile, K = d
 // in 64-element SW128 chunks), and tcgen05.mma accumulates the Gram tile in TMEM
-// (two 240-column accumulators, double-buffered against the epilogue).
+// (two 256-column accumulators, double-buffered against the epilogue).
 //
 // Layouts (built once per index / per batch):
 //   database  hd [nvec][dpad] fp16 = x / S_db, one global power-of-two scale
 //             S_db >= max|x| (row-major; tiles are runs of whole consecutive sets
-//             of <= 240 rows, any start row: TMA swizzles on the fly);
+//             of <= 256 rows, any start row: TMA swizzles on the fly);
 //   queries   qd [ntq*128][dpad] fp16 = x / S_q, query sets packed into 32-row
 //             warp bins (a set never straddles a warp), 4 bins per tile.
 // The squared norm of every database row rides in the MMA as one extra K = 16
@@ -61,10 +61,11 @@
 
 namespace bvss {
 
-// database rows per tile (MMA N): two 240-column accumulators leave 32 spare TMEM columns, so a 32-column
-// tcgen05.ld that starts at any set inside the second accumulator stays inside the 512-column allocation
-// (a load past it faults: tools/test_tmem_ld.cu); sets start at any column (unaligned loads are legal)
-constexpr int kDenseN = 240;
+// database rows per tile (MMA N): two 256-column accumulators fill the 512-column allocation; the epilogue's
+// exact-width reads never pass a set's last column (a load past column 511 faults: tools/test_tmem_ld.cu), and
+// sets start at any column (unaligned loads are legal).  A tcgen05.mma costs about the same for any N <= 256
+// (tools/microbench_umma.cu), so the widest tile does the most work per instruction.
+constexpr int kDenseN = 256;
 constexpr int kDenseM = 128;      // packed query rows per tile (MMA M)
 constexpr int kEpiSub = 3;                                  // epilogue warps per TMEM lane quarter
 constexpr int kEpiWarpsD = 4 * kEpiSub;
@@ -77,11 +78,11 @@ constexpr int kUnitQ = 4;          // published unit ids in flight (dyn scheduli
 // epilogue warps
 constexpr int kUnitConsumers = 1 + 1 + 2 + 2 * kEpiWarpsD;
 constexpr uint32_t kAChunkBytes = kDenseM * 128;  // one 64-element K chunk of the query tile (16 KB)
-// CTA pairs (cta_group::2): one tcgen05.mma M=256 N=240 per K step covers the two CTAs' query tiles (128
+// CTA pairs (cta_group::2): one tcgen05.mma M=256 N=256 per K step covers the two CTAs' query tiles (128
 // rows each, A in each CTA's shared memory) against one database tile whose rows are split between the
 // CTAs (120 each): every SM streams half of the tile, so the L2 -> SM traffic per flop halves
 constexpr int kHalfN = kDenseN / 2;
-constexpr uint32_t kBChunkBytes = kHalfN * 128;   // this CTA's half of one K chunk of a database tile (15 KB)
+constexpr uint32_t kBChunkBytes = kHalfN * 128;   // this CTA's half of one K chunk of a database tile (16 KB)
 constexpr uint32_t kAAugBytes = kDenseM * 32;     // the query tile's norm chunk (K = 16 halves = 32 B rows)
 constexpr uint32_t kBAugBytes = kHalfN * 32;      // this CTA's half of a database tile's norm chunk
 
@@ -126,6 +127,7 @@ struct DenseArgs {
   int cap;
   const uint32_t* mask;         // optional candidate bitmap, row q at mask + q * mask_stride (bit i = set i)
   int64_t mask_stride;          // words per query row (0: one row shared by every query)
+  int mask_last_word;           // last word of a row the kernel may read ((last set of the last tile) / 32)
   int64_t id_base;
   unsigned long long* stat;     // [2]: survivors, emitted (may be null)
   unsigned long long* prof;     // developer per-role cycle counters (env BVSS_DENSE_PROF) or null
@@ -264,79 +266,10 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
 }
 __device__ __forceinline__ float fmax3(float a, float b, float c) { return fmaxf(a, fmaxf(b, c)); }  // FMNMX3
 
-// The columns of a set of mvc (1..32) database rows starting at TMEM address taddr, for this lane's query row:
-// whole groups of 8 from one 32-column load (g) and the last 8 columns of the run (t, overlapping the groups:
-// max and max-of-min are idempotent); runs shorter than 8 are the first mvc columns of t.
-struct SetCols {
-  uint32_t g[32], t[8];
-};
-__device__ __forceinline__ void load_set(uint32_t taddr, int mvc, SetCols& c) {
-  if (mvc >= 8) {
-    tmem_ld32(taddr, c.g);
-    tmem_ld8(taddr + static_cast<uint32_t>(mvc - 8), c.t);
-  } else {
-    tmem_ld8(taddr, c.t);
-  }
-  tc::tmem_ld_wait();
-}
-// max over the run's columns (no per-column tests)
-__device__ __forceinline__ float set_max(const SetCols& c, int mvc) {
-  const float NINF = __int_as_float(0xff800000);
-  float m = NINF;
-  if (mvc >= 8) {
-#define BVSS_MAX8(R, o)                                                                        \
-  m = fmax3(m, __uint_as_float(R[o]), __uint_as_float(R[o + 1]));                            \
-  m = fmax3(m, __uint_as_float(R[o + 2]), __uint_as_float(R[o + 3]));                        \
-  m = fmax3(m, __uint_as_float(R[o + 4]), __uint_as_float(R[o + 5]));                        \
-  m = fmax3(m, __uint_as_float(R[o + 6]), __uint_as_float(R[o + 7]));
-    switch (mvc >> 3) {
-      case 4: BVSS_MAX8(c.g, 24) [[fallthrough]];
-      case 3: BVSS_MAX8(c.g, 16) [[fallthrough]];
-      case 2: BVSS_MAX8(c.g, 8) [[fallthrough]];
-      default: BVSS_MAX8(c.g, 0)
-    }
-    BVSS_MAX8(c.t, 0)
-#undef BVSS_MAX8
-  } else {
-    switch (mvc) {
-      case 7: m = fmaxf(m, __uint_as_float(c.t[6])); [[fallthrough]];
-      case 6: m = fmaxf(m, __uint_as_float(c.t[5])); [[fallthrough]];
-      case 5: m = fmaxf(m, __uint_as_float(c.t[4])); [[fallthrough]];
-      case 4: m = fmaxf(m, __uint_as_float(c.t[3])); [[fallthrough]];
-      case 3: m = fmaxf(m, __uint_as_float(c.t[2])); [[fallthrough]];
-      case 2: m = fmaxf(m, __uint_as_float(c.t[1])); [[fallthrough]];
-      default: m = fmaxf(m, __uint_as_float(c.t[0]));
-    }
-  }
-  return m;
-}
-// B part of a survivor: max over the run's columns of min over the segment's lanes of D^2 (the same registers)
-__device__ __forceinline__ float set_colmin_max(const SetCols& c, int mvc, float kappa, float qn, bool inseg) {
-  float B = 0.0f;
-  auto col = [&](uint32_t x) {
-    const float d2 = fmaxf(fmaf(kappa, __uint_as_float(x), qn), 0.0f);
-    B = fmaxf(B, __uint_as_float(__reduce_min_sync(0xffffffffu, inseg ? __float_as_uint(d2) : 0xffffffffu)));
-  };
-  if (mvc >= 8) {
-#pragma unroll
-    for (int j8 = 0; j8 < 32; j8 += 8) {
-      if (j8 + 8 > mvc) break;
-#pragma unroll
-      for (int j = j8; j < j8 + 8; ++j) col(c.g[j]);
-    }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) col(c.t[j]);
-  } else {
-#pragma unroll
-    for (int j = 0; j < 8; ++j)
-      if (j < mvc) col(c.t[j]);
-  }
-  return B;
-}
-
-// Exact-width variant: a run of mvc (1..31) columns is read by the loads of its binary digits (x16, x8, x4,
-// x2, x1 at consecutive column offsets), so the epilogue reads exactly the set's columns from TMEM (the
-// 32 + 8 column form reads 40 columns for a set of 18 rows).  Branches are warp-uniform (one set per warp).
+// The columns of a run of mvc (1..31) database rows starting at TMEM address taddr, for this lane's query row,
+// read by the loads of mvc's binary digits (x16, x8, x4, x2, x1 at consecutive column offsets): exactly the
+// set's columns (a 32 + 8 column form read 40 columns for a set of 18 rows and needed 32 spare TMEM columns
+// past the last accumulator).  Branches are warp-uniform (one set per warp).
 struct SetColsX {
   uint32_t a16[16], a8[8], a4[4], a2[2], a1[1];
 };
@@ -388,7 +321,10 @@ __device__ __forceinline__ float set_max(const SetColsX& c, int mvc) {
   if (mvc & 1) m = fmaxf(m, __uint_as_float(c.a1[0]));
   return m;
 }
-__device__ __forceinline__ float set_colmin_max(const SetColsX& c, int mvc, float kappa, float qn, bool inseg) {
+// (lim: the caller only needs B while B <= lim -- a survivor with B > tau + E can be neither inserted nor
+// emitted -- so the scan stops after the first group of columns that exceeds it; warp-uniform)
+__device__ __forceinline__ float set_colmin_max(const SetColsX& c, int mvc, float kappa, float qn, bool inseg,
+                                                float lim = 3.402823466e38f) {
   float B = 0.0f;
   auto col = [&](uint32_t x) {
     const float d2 = fmaxf(fmaf(kappa, __uint_as_float(x), qn), 0.0f);
@@ -396,11 +332,16 @@ __device__ __forceinline__ float set_colmin_max(const SetColsX& c, int mvc, floa
   };
   if (mvc & 16) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) col(c.a16[j]);
+    for (int j = 0; j < 8; ++j) col(c.a16[j]);
+    if (B > lim) return B;
+#pragma unroll
+    for (int j = 8; j < 16; ++j) col(c.a16[j]);
+    if (B > lim) return B;
   }
   if (mvc & 8) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) col(c.a8[j]);
+    if (B > lim) return B;
   }
   if (mvc & 4) {
 #pragma unroll
@@ -413,8 +354,6 @@ __device__ __forceinline__ float set_colmin_max(const SetColsX& c, int mvc, floa
   if (mvc & 1) col(c.a1[0]);
   return B;
 }
-template <bool EXACT> struct ColsOf { using T = SetCols; static constexpr int CH = 32; };
-template <> struct ColsOf<true> { using T = SetColsX; static constexpr int CH = 31; };
 
 __device__ __forceinline__ float vload_volatile(const float* p);
 
@@ -523,10 +462,9 @@ __device__ __forceinline__ void range_tiles(int r, int R, int ntiles, int* t0, i
     }                                                                       \
   } while (0)
 
-template <bool EXACT>
 __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const __grid_constant__ DenseArgs a) {
-  using Cols = typename ColsOf<EXACT>::T;
-  constexpr int CH = ColsOf<EXACT>::CH;  // columns per TMEM read of a set
+  using Cols = SetColsX;
+  constexpr int CH = 31;  // columns per TMEM read of a set
   extern __shared__ __align__(1024) uint8_t dsm_raw[];
   __shared__ DenseCtl S;
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(dsm_raw) + 1023) & ~uintptr_t(1023));
@@ -760,15 +698,40 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
           __syncwarp();
         }
       }
-      float other_k = INF;  // the other warps' k-th bounds, loaded one tile ahead (their latency stays hidden)
+      float other_k[kEpiSub - 1];  // the other warps' k-th bounds, loaded one tile ahead and used at the next
+                                   // tile (the load latency stays hidden behind this tile's work)
+#pragma unroll
+      for (int o = 0; o < kEpiSub - 1; ++o) other_k[o] = INF;
       int t0, t1;
       range_tiles(r, a.R, a.ntiles, &t0, &t1);
+      // candidate bitmap (top-T of the filter): this lane's query's bits of the tile's first two words, loaded
+      // one tile ahead; a set outside them (a tile of many tiny sets) reads its word directly
+      const uint32_t* mrow = (a.mask && valid) ? a.mask + static_cast<int64_t>(qid) * a.mask_stride : nullptr;
+      auto mask_load = [&](int tt, uint64_t* bits, int* w0) {
+        *bits = ~0ull;
+        *w0 = 0;
+        if (mrow && tt < t1) {
+          *w0 = __ldg(a.tile_s0 + tt) >> 5;
+          const uint32_t lo = __ldg(mrow + *w0);
+          const uint32_t hi = *w0 + 1 <= a.mask_last_word ? __ldg(mrow + *w0 + 1) : 0u;
+          *bits = static_cast<uint64_t>(lo) | (static_cast<uint64_t>(hi) << 32);
+        }
+      };
+      uint64_t mbits_nx;
+      int mw_nx;
+      mask_load(t0, &mbits_nx, &mw_nx);
       for (int t = t0; t < t1; ++t, ++tile_ctr) {
         const uint32_t acc = tile_ctr & 1u;
         const int slot = tile_ctr % kInfoSlotsD;
+        const uint64_t mbits = mbits_nx;
+        const int mw0 = mw_nx;
+        mask_load(t + 1, &mbits_nx, &mw_nx);
         // (developer BVSS_DENSE_DEBUG 8 .. 11 switch tau sources off: 8 none, 9 the own list, 10 + the other
         // warps' lists at insertion, 11 + the union)
-        if (a.debug < 8) tau = fminf(tau, other_k);
+        if (a.debug < 8) {
+#pragma unroll
+          for (int o = 0; o < kEpiSub - 1; ++o) tau = fminf(tau, other_k[o]);
+        }
         // at the start of every unit and every 32 tiles (staggered): the k-th of
         if ((a.debug < 8 || a.debug == 11) && (t == t0 || ((tile_ctr + 8u * static_cast<uint32_t>(sub)) & 31u) == 0u)) {
           unsigned pend = __ballot_sync(0xffffffffu, valid);               // the union of the query's lists
@@ -786,9 +749,8 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
           }
         }
         if (valid) {
-          other_k = INF;
 #pragma unroll
-          for (int o = 1; o < kEpiSub; ++o) other_k = fminf(other_k, vload_volatile(lq + ((sub + o) % kEpiSub) * a.k + a.k - 1));
+          for (int o = 1; o < kEpiSub; ++o) other_k[o - 1] = vload_volatile(lq + ((sub + o) % kEpiSub) * a.k + a.k - 1);
         }
         float thr = tau + E;
         DPROF(3, tc::mbar_wait_sleep(&S.info_full[slot], (tile_ctr / kInfoSlotsD) & 1u));
@@ -811,7 +773,12 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
             m = fmaxf(m, set_max(cols, mvc));
           }
           const float rq = fmaxf(fmaf(a.kappa, m, qn), 0.0f);
-          const unsigned pass = __ballot_sync(0xffffffffu, !valid || rq <= thr);
+          bool cand = true;  // set i is in this lane's query's candidate bitmap (always without a bitmap)
+          if (mrow) {
+            const int bi = i - 32 * mw0;
+            cand = bi < 64 ? ((mbits >> bi) & 1ull) != 0ull : ((__ldg(mrow + (i >> 5)) >> (i & 31)) & 1u) != 0u;
+          }
+          const unsigned pass = __ballot_sync(0xffffffffu, !valid || (rq <= thr && cand));
           unsigned sb = __ballot_sync(0xffffffffu, valid && (pass & segmask) == segmask);
           if (a.debug == 3) sb = 0u;  // developer: no survivor work (times the base epilogue)
           while (sb) {  // warp-uniform: one surviving query segment at a time
@@ -819,19 +786,19 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
             const unsigned smask = __shfl_sync(0xffffffffu, segmask, leader);
             sb &= ~smask;
             const int q = __shfl_sync(0xffffffffu, qid, leader);
-            if (a.mask) {  // candidate restriction (top-T of the filter): bit i of the query's row
-              const int64_t li = i;
-              const uint32_t w = __ldg(a.mask + static_cast<int64_t>(q) * a.mask_stride + (li >> 5));
-              if (((w >> (li & 31)) & 1u) == 0u) continue;
-            }
             const bool inseg = (smask >> lane) & 1u;
             const float A = __uint_as_float(__reduce_max_sync(0xffffffffu, inseg ? __float_as_uint(rq) : 0u));
+            const float Eq = __shfl_sync(0xffffffffu, E, leader);
+            const float tq = __shfl_sync(0xffffffffu, tau, leader);
+            // B is only needed while h = max(A, B) <= tq + Eq: above it the set is neither inserted (ub > tq)
+            // nor emitted (h - Eq > tq >= the tau after any insertion), so the column scan may stop early
+            const float lim = tq + Eq;
             float B;
             if (mv <= CH) {
-              B = set_colmin_max(cols, mv, a.kappa, qn, inseg);
+              B = set_colmin_max(cols, mv, a.kappa, qn, inseg, lim);
             } else {
               B = 0.0f;
-              for (int j0 = 0; j0 < mv; j0 += CH) {
+              for (int j0 = 0; j0 < mv && B <= lim; j0 += CH) {
                 Cols cb;
                 const int mvc = min(CH, mv - j0);
                 load_set(tb + static_cast<uint32_t>(col0 + j0), mvc, cb);
@@ -839,8 +806,6 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
               }
             }
             const float h = fmaxf(A, B);
-            const float Eq = __shfl_sync(0xffffffffu, E, leader);
-            const float tq = __shfl_sync(0xffffffffu, tau, leader);
             const float ub = h + Eq;
             float newtau = tq;
             ++n_surv;
@@ -973,7 +938,7 @@ __global__ void dense_fill_kernel(float* __restrict__ x, int64_t n, float v) {
     x[i] = v;
 }
 
-// sets the tiles cannot hold (> 240 rows): appended to every query's list with the K6 exact sentinel
+// sets the tiles cannot hold (> 256 rows): appended to every query's list with the K6 exact sentinel
 // (every one is recomputed exactly), honouring the candidate bitmap
 __global__ void dense_append_huge_kernel(const int32_t* __restrict__ huge, int nhuge, const uint32_t* __restrict__ mask,
                                          int64_t mask_stride, int nq, int64_t id_base, int32_t* __restrict__ cnt,
@@ -1105,6 +1070,12 @@ int launch_dense_hausdorff(const __half* qd, int ntq, const __half* hd, int64_t 
   a.cap = cap;
   a.mask = mask;
   a.mask_stride = mask_stride;
+  if (mask) {  // (tile_s1 is a device array: the last set of the last tile comes back once per launch)
+    int last = 0;
+    BVSS_CUDA(cudaMemcpyAsync(&last, tile_s1 + ntiles - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    BVSS_CUDA(cudaStreamSynchronize(st));
+    a.mask_last_word = (last - 1) >> 5;
+  }
   a.id_base = id_base;
   a.stat = stat;
   a.dyn = dyn;
@@ -1129,9 +1100,7 @@ int launch_dense_hausdorff(const __half* qd, int ntq, const __half* hd, int64_t 
   const int units = (ntq / 2) * R;
   int pairs = num_sms / 2;
   if (pairs > units) pairs = units;
-  int exact_ld = 1;
-  if (const char* e = getenv("BVSS_DENSE_LD")) exact_ld = atoi(e) != 0;  // developer switch: 0 = 32 + 8 columns
-  auto kern = exact_ld ? dense_hausdorff_kernel<true> : dense_hausdorff_kernel<false>;
+  auto kern = dense_hausdorff_kernel;
   BVSS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs));

@@ -22,13 +22,14 @@
 // every tile arrives by plain contiguous cp.async.bulk copies and no SM time is
 // spent on bit expansion.
 //
-// Queries are the STATIONARY operand: A = a tile of 128 query sketches (M = 128,
-// one TMEM lane per query), resident in shared memory while it fits (else
-// streamed with B).  B = kN database sets (N = 240 FP4 / 256 i8) streamed
-// through a stage ring, 128 bytes of K per stage (4 MMAs).  The (query tile,
-// database tile) pairs are split into equal contiguous ranges, one per
-// persistent CTA (query-tile-major, so a CTA reloads its query tile at most a
-// few times).
+// A = a tile of 128 query sketches (M = 128, one TMEM lane per query), B = kN
+// database sets (N = 240 FP4 / 256 i8), 128 bytes of K per stage (4 MMAs).  One
+// operand is STATIONARY in shared memory (scan_tc_mode): by default the database
+// tile (MODE_BRES: query tiles stream through the stage ring from L2), else the
+// query tile (MODE_ARES), else both stream (MODE_STREAM).  The (query tile,
+// database tile) pairs are ordered by the stationary operand and split into
+// equal contiguous ranges, one per persistent CTA, so a CTA reloads its
+// stationary tile at most a few times.
 //
 // Because a TMEM lane is a query, the epilogue thread owns one query: its mass
 // p_Q and threshold tau_Q live in registers and the per-value work is one FFMA

@@ -57,14 +57,13 @@ def test_dense_bruteforce_matches_oracle(name, ov, limit):
 
 
 @pytest.mark.parametrize("sched", [{}, {"BVSS_DENSE_TPR": "3"}, {"BVSS_DENSE_TPR": "16"},
-                                   {"BVSS_DENSE_DYN": "0"}, {"BVSS_DENSE_DYN": "0", "BVSS_DENSE_R": "7"},
-                                   {"BVSS_DENSE_LD": "0"}])
+                                   {"BVSS_DENSE_DYN": "0"}, {"BVSS_DENSE_DYN": "0", "BVSS_DENSE_R": "7"}])
 def test_dense_bruteforce_equals_query_major_refine(sched, monkeypatch):
     """Every query: the dense brute force and the query-major refine over all n candidates (bvss_refine) give
     identical ids and distances (the same exact fp32 fix-up decides both).  Under every schedule: the default
     (dynamic range-major units; one range at this n), small ranges (many units per query tile pair: the
     running tau and the list inheritance from the previous range are exercised), the static pair-major
-    schedule with its union over ranges, and the 32 + 8 column TMEM reads."""
+    schedule with its union over ranges."""
     _need_gpu()
     for k, v in sched.items():
         monkeypatch.setenv(k, v)
@@ -88,6 +87,21 @@ def test_dense_search_large_T_matches_oracle(T, monkeypatch):
     kernel and matches the oracle pipeline (filter to T, exact Hausdorff, top-k)."""
     _need_gpu()
     cfg = synth.get_config("cfg3", n=9000, nq=60, T=T)
+    _large_T_case(cfg, T)
+
+
+@pytest.mark.parametrize("tpr", ["1024", "2"])
+def test_dense_search_tiny_sets_bitmap(tpr, monkeypatch):
+    """cfg1's sets of 2-8 vectors put up to ~100 sets in one 240-row tile, so the kernel's two prefetched
+    bitmap words do not cover every set of a tile and the direct word reads run; 2-tile ranges (many units,
+    inheritance) as well as the default."""
+    _need_gpu()
+    monkeypatch.setenv("BVSS_DENSE_TPR", tpr)
+    cfg = synth.get_config("cfg1", n=2000, nq=30, T=700)
+    _large_T_case(cfg, 700)
+
+
+def _large_T_case(cfg, T):
     data = synth.to_numpy(synth.generate(cfg, device="cpu"))
     idx = _index(cfg, data, select_mode=1)
     ids, dist = idx.search(data["queries"], data["q_offsets"], cfg.k, T)
