@@ -59,6 +59,7 @@
 
 #include "tc.cuh"
 
+
 namespace bvss {
 
 // database rows per tile (MMA N): two 256-column accumulators fill the 512-column allocation; the epilogue's
@@ -759,13 +760,13 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
         tc::fence_after_sync();
         const int s0 = inf.s0, nsets = inf.nsets;
         const uint32_t tb = tmem + (static_cast<uint32_t>(quarter * 32) << 16) + acc * kDenseN;
-        for (int js = (a.debug == 1 || a.debug == 4) ? nsets : sub; js < nsets;) {
-          int nxt = 0;  // the next set of this warp (taken now: the shared-memory atomic's latency overlaps the set)
-          if (lane == 0) nxt = atomicAdd(const_cast<int*>(&inf.ctr[quarter]), 1);
+        // one set of the tile for this warp's lane quarter (its columns read into `cols`; a software-pipelined
+        // form that issued the next set's reads before this set's math needed a second column buffer and
+        // spilled ~1 KB per thread at the 128-register cap, so the reads stay synchronous)
+        auto do_set = [&](int js, Cols& cols) {
           const int i = s0 + js;
           const int col0 = inf.col0[js];
           const int mv = inf.mv[js];
-          Cols cols;  // (sets of <= CH rows keep their columns in registers for the survivor's B)
           float m = -INF;  // max_v acc (kappa < 0: the min over v of D^2)
           for (int j0 = 0; j0 < mv; j0 += CH) {
             const int mvc = min(CH, mv - j0);
@@ -836,6 +837,13 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
               thr = tau + E;
             }
           }
+        };
+        const int js0 = (a.debug == 1 || a.debug == 4) ? nsets : sub;
+        for (int js = js0; js < nsets;) {
+          int nxt = 0;  // the next set of this warp (taken now: the shared-memory atomic's latency overlaps the set)
+          if (lane == 0) nxt = atomicAdd(const_cast<int*>(&inf.ctr[quarter]), 1);
+          Cols cols;  // (sets of <= CH rows keep their columns in registers for the survivor's B)
+          do_set(js, cols);
           js = __shfl_sync(0xffffffffu, nxt, 0);
         }
         tc::fence_before_sync();
