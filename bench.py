@@ -439,6 +439,21 @@ def main_ours(args):
         roofs["refine_T2000"] = {"kernel": "refine_tc_kernel", "bound": "hbm", "achieved": round(ref_gbs, 1),
                                  "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": round(ref_gbs / peaks["hbm_gbs"], 4),
                                  "ms": round(ref_ms, 3), "bytes_per_step": int(s2["gather_bytes"])}
+    # the query encode stage of the step (K1 FlyHash + WTA with the K9 norms / fp16 split, then the K2 query
+    # sketches): bound by the shared-memory operand gathers, m*s per vector at 32 operands / clock / SM
+    # (DESIGN.md §5.1), at the median SM clock measured during the timed steps
+    nqvec = int(qo[-1])
+    enc_ms = stages["ms_encode"]
+    f_hz = (clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    enc_cap = nsm * 32.0 * f_hz / (cfg.m * cfg.s)
+    enc_vps = nqvec / (enc_ms * 1e-3) if enc_ms > 0 else 0.0
+    roofs["encode"] = {"kernel": "flyhash_wta_kernel + sketch (query batch)", "bound": "lds",
+                       "achieved": round(enc_vps / 1e6, 1), "peak": round(enc_cap / 1e6, 1), "unit": "Mvectors/s",
+                       "frac": round(enc_vps / enc_cap, 4) if enc_cap else None, "ms": round(enc_ms, 3),
+                       "input_GBps": round(nqvec * 4.0 * cfg.d / (enc_ms * 1e-3) / 1e9, 1) if enc_ms > 0 else None,
+                       "peak_src": f"{nsm} SMs x 32 smem operands / clk x {f_hz / 1e6:.0f} MHz (median under load) "
+                                   f"/ (m s = {cfg.m * cfg.s}) gathers per vector"}
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
