@@ -345,6 +345,15 @@ def main_ours(args):
     gt_ids = bruteforce(qv_sub, qo_sub)[0] if R > 0 else None
     torch.cuda.synchronize()
     t_gt = time.perf_counter() - t_gt
+    # K8 itself (BASELINE configs[4]'s tensor-pipe check: exact brute-force Hausdorff top-10 over the first 1M
+    # sets for 1000 queries), timed once more on the device: 2 x (query vectors) x (database vectors) x d
+    k8 = None
+    if R > 0 and world == 1:
+        k8_ms, _ = timed(lambda: bruteforce(qv_sub, qo_sub))
+        k8_flop = 2.0 * int(qo_sub[-1]) * nvec_shard * cfg.d
+        k8 = {"kernel": "dense_hausdorff_kernel + topk_exact_kernel (bvss_bruteforce, K8)", "bound": "tensor",
+              "queries": R, "sets": cfg.n, "ms": round(k8_ms, 2),
+              "achieved": round(k8_flop / (k8_ms * 1e-3) / 1e12, 1), "unit": "TFLOP/s"}
 
     # -------- T sweep (recall vs throughput), N = 1
     sweep, full_points = [], {}
@@ -454,6 +463,9 @@ def main_ours(args):
                        "input_GBps": round(nqvec * 4.0 * cfg.d / (enc_ms * 1e-3) / 1e9, 1) if enc_ms > 0 else None,
                        "peak_src": f"{nsm} SMs x 32 smem operands / clk x {f_hz / 1e6:.0f} MHz (median under load) "
                                    f"/ (m s = {cfg.m * cfg.s}) gathers per vector"}
+    if k8:
+        k8.update(peak=peaks["bf16_tflops_sustained"], frac=round(k8["achieved"] / peaks["bf16_tflops_sustained"], 4))
+        roofs["k8_bruteforce"] = k8
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):

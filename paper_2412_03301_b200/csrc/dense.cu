@@ -145,7 +145,6 @@ struct DenseArgs {
 // (first set id, count, column and size of each)
 struct DenseInfo {
   int s0, nsets, pad0, pad1;
-  int ctr[4];  // next set of each TMEM lane quarter (dynamic split among the quarter's epilogue warps)
   int16_t col0[kDenseN];
   int16_t mv[kDenseN];
 };
@@ -650,7 +649,6 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
           inf.s0 = s0;
           inf.nsets = s1 - s0;
         }
-        if (lane < 4) inf.ctr[lane] = kEpiSub;  // sets 0 .. kEpiSub-1 go to the warps statically
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&S.info_full[slot]);
       }
@@ -839,12 +837,11 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
           }
         };
         const int js0 = (a.debug == 1 || a.debug == 4) ? nsets : sub;
-        for (int js = js0; js < nsets;) {
-          int nxt = 0;  // the next set of this warp (taken now: the shared-memory atomic's latency overlaps the set)
-          if (lane == 0) nxt = atomicAdd(const_cast<int*>(&inf.ctr[quarter]), 1);
+        // the quarter's warps take the tile's sets in turn (static: a shared-memory work counter per set cost
+        // more than the imbalance it removed, 2795 vs 2730 ms per bench step, profiles/r02/s3/ab_static_split.log)
+        for (int js = js0; js < nsets; js += kEpiSub) {
           Cols cols;  // (sets of <= CH rows keep their columns in registers for the survivor's B)
           do_set(js, cols);
-          js = __shfl_sync(0xffffffffu, nxt, 0);
         }
         tc::fence_before_sync();
         __syncwarp();
