@@ -20,7 +20,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, cfg_kw, out_dir):
+def _worker(rank, world, port, cfg_kw, out_dir, backend="gloo"):
     import torch
     import torch.distributed as dist
     from gen import synth
@@ -28,7 +28,9 @@ def _worker(rank, world, port, cfg_kw, out_dir):
     from paper_2412_03301_b200 import dist as D
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    if backend == "nccl":
+        torch.cuda.set_device(0)
+    dist.init_process_group(backend, rank=rank, world_size=world)
     try:
         torch.cuda.set_device(0)
         cfg = synth.get_config(**cfg_kw)
@@ -99,3 +101,27 @@ def test_sharded_search_matches_oracle(tmp_path):
         Q = h["queries"][h["q_offsets"][qi]:h["q_offsets"][qi + 1]]
         r_ids, r_d = oi.search(Q, cfg.k, cfg.T)
         check_topk(ids[qi], dd[qi], r_ids, r_d, lambda i: O.hausdorff(Q, V[off[i]:off[i + 1]]))
+
+
+@pytest.mark.parametrize("cfg_kw", [dict(name="cfg3", n=6001, nq=9, T=300), dict(name="cfg3", n=5003, nq=7, T=4000)])
+def test_sharded_search_over_nccl_one_rank(tmp_path, cfg_kw):
+    """The collectives on CUDA tensors through NCCL (dist._host_collectives is false for nccl): one rank, the
+    only NCCL world one GPU allows (NCCL rejects two ranks on one device).  C1 all-reduce, C2/C3 all-gathers run
+    as NCCL kernels on the device buffers; the result must equal the single-index search exactly, both at a
+    small T (sorted top-T) and at T close to n (bitmap + dense refine in bvss_dist_finish)."""
+    import torch.multiprocessing as mp
+    from gen import synth
+    from paper_2412_03301_b200 import bvss as B
+    if B.device_count() < 1:
+        pytest.fail("no sm_100 device visible to libbvss")
+    port = _free_port()
+    mp.start_processes(_worker, args=(1, port, cfg_kw, str(tmp_path), "nccl"), nprocs=1, join=True,
+                       start_method="spawn")
+    cfg = synth.get_config(**cfg_kw)
+    g = synth.generate(cfg, device="cuda")
+    idx = B.Index(g["vectors"], g["offsets"], m=cfg.m, s=cfg.s, L=cfg.L, sketch=cfg.sketch, seed=cfg.seed,
+                  select_mode=1)
+    ref_ids, ref_d = idx.search(g["queries"], g["q_offsets"], cfg.k, cfg.T)
+    idx.close()
+    np.testing.assert_array_equal(np.load(tmp_path / "ids0.npy"), ref_ids.cpu().numpy())
+    np.testing.assert_array_equal(np.load(tmp_path / "dist0.npy"), ref_d.cpu().numpy())
