@@ -134,6 +134,12 @@ struct DenseArgs {
   unsigned long long* prof;     // developer per-role cycle counters (env BVSS_DENSE_PROF) or null
   int debug;                    // developer switch BVSS_DENSE_DEBUG: 1 = epilogue skips its work, 2 = no MMAs,
                                 // 3 = no survivor work, 4 = no database loads and no epilogue (timing only)
+  uint32_t refresh_mask;        // union refresh every refresh_mask + 1 tiles (a power of two; default 32) ...
+  uint32_t refresh_stagger;     // ... at tile_ctr + stagger * sub (default 8; developer env BVSS_DENSE_REFRESH=p,s)
+  int l2pf_ahead, l2pf_mod;     // producer L2 prefetch of tile t + ahead by the pairs with pair % mod == t % mod
+                                // (0: off; developer env BVSS_DENSE_L2PF=ahead,mod)
+  int ukth_fast;                // union k-th by lane ranks when the union has <= 32 values, 2: with the loads of
+                                // up to 4 query segments issued together (env BVSS_DENSE_UKTH=0 / 1 / 2, default 2)
   int dyn;                      // 1: units handed out by a global counter in range-major order (see pair_unit)
   int* unit_ctr;                // [1] next unit (dyn), zeroed before the launch
   int* udone;                   // [nqp][R] (dyn): epilogue warps that finished unit (qp, r), zeroed before the
@@ -166,6 +172,13 @@ __device__ __forceinline__ void tma_2d(uint32_t dst, const CUtensorMap* map, int
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
       : "memory");
+}
+// L2 prefetch of one tensor box (no shared memory, no barrier): pulls a database tile into L2 ahead of the
+// pairs that will load it
+__device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
 }
 // the same TMA with the pair's completion barrier in the leader CTA (cta_group::2: the bytes of both CTAs'
 // loads complete on the leader's barrier, whose MMA thread consumes both halves)
@@ -365,9 +378,31 @@ __device__ __forceinline__ float vload_volatile(const float* p);
 // predecessor in the same list counts as +inf (two sets with equal bounds then count once: conservative).
 // Warp-wide radix select on the (non-negative) float bits.
 // (dir = +1: ranges r, r+1, ...; dir = -1: r, r-1, ... -- the ranges the range-major schedule has already run)
+// The k-th smallest (with multiplicity) of one value per lane (lanes past the union hold +inf), after the
+// dedup rule of union_kth (a value equal to its predecessor in the same sorted list of k is a torn read of a
+// list being shifted and counts once): each lane's rank by 32 independent shuffles.
+__device__ __forceinline__ float ukth_rank(float x, int k, int lane) {
+  const float prev = __shfl_up_sync(0xffffffffu, x, 1);
+  if (lane % k != 0 && prev == x) x = __int_as_float(0x7f800000);
+  int rank = 0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const float y = __shfl_sync(0xffffffffu, x, j);
+    rank += (y < x || (y == x && j < lane)) ? 1 : 0;
+  }
+  const unsigned at = __ballot_sync(0xffffffffu, rank == k - 1);
+  return __shfl_sync(0xffffffffu, x, __ffs(at) - 1);
+}
+
 __device__ float union_kth(const float* lq0 /* lists of (q, range 0) */, int R, int r, int nr, int k, int lane,
-                           int dir) {
+                           int dir, bool fast) {
   const int per_range = kEpiSub * k, total = nr * per_range;
+  if (fast && total <= 32) {  // one value per lane: the k-th smallest by rank (32 independent shuffles instead
+                              // of 31 dependent warp reductions; same value, ties counted with multiplicity)
+    float x = __int_as_float(0x7f800000);
+    if (lane < total) x = vload_volatile(lq0 + static_cast<int64_t>((r + R + dir * (lane / per_range)) % R) * per_range + lane % per_range);
+    return ukth_rank(x, k, lane);
+  }
   float v[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
@@ -534,6 +569,11 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
         range_tiles(r, a.R, a.ntiles, &t0, &t1);
         for (int t = t0; t < t1; ++t) {
           const int row0 = static_cast<int>(a.off[a.tile_s0[t]]) + static_cast<int>(crank) * kHalfN;
+          if (a.l2pf_ahead > 0 && t + a.l2pf_ahead < t1 && (t % a.l2pf_mod) == (pair % a.l2pf_mod)) {
+            const int prow = static_cast<int>(a.off[a.tile_s0[t + a.l2pf_ahead]]) + static_cast<int>(crank) * kHalfN;
+            for (int kc = 0; kc < a.KC; ++kc) tma_prefetch_l2(&a.tmB, kc * 64, prow);
+            tma_prefetch_l2(&a.tmBa, 0, prow);
+          }
           for (int kc = 0; kc <= a.KC; ++kc) {  // kc == KC: the norm chunk
             DPROF(0, tc::mbar_wait_sleep(&S.empty[st], ph ^ 1u));
             const uint32_t fb = full_l0 + st * 8u;
@@ -732,17 +772,50 @@ __global__ void __launch_bounds__(kDenseThreads, 1) dense_hausdorff_kernel(const
           for (int o = 0; o < kEpiSub - 1; ++o) tau = fminf(tau, other_k[o]);
         }
         // at the start of every unit and every 32 tiles (staggered): the k-th of
-        if ((a.debug < 8 || a.debug == 11) && (t == t0 || ((tile_ctr + 8u * static_cast<uint32_t>(sub)) & 31u) == 0u)) {
+        if ((a.debug < 8 || a.debug == 11) &&
+            (t == t0 || ((tile_ctr + a.refresh_stagger * static_cast<uint32_t>(sub)) & a.refresh_mask) == 0u)) {
           unsigned pend = __ballot_sync(0xffffffffu, valid);               // the union of the query's lists
+          if (a.ukth_fast == 2 && a.dyn && kEpiSub * a.k <= 32) {
+            // the loads of the first kPre query segments (their union values and running tau) are all issued
+            // before any is used: one global round trip per refresh instead of two per segment
+            constexpr int kPre = 4;
+            float pv[kPre], pt[kPre];
+            unsigned p = pend;
+#pragma unroll
+            for (int s2 = 0; s2 < kPre; ++s2) {
+              pv[s2] = INF;
+              pt[s2] = INF;
+              if (p) {
+                const int ld = __ffs(p) - 1;
+                p &= ~__shfl_sync(0xffffffffu, segmask, ld);
+                const int qq = __shfl_sync(0xffffffffu, qid, ld);
+                pt[s2] = vload_volatile(a.tau0 + qq);
+                if (lane < kEpiSub * a.k) pv[s2] = vload_volatile(a.lists + (static_cast<int64_t>(qq) * a.R + r) * kEpiSub * a.k + lane);
+              }
+            }
+#pragma unroll
+            for (int s2 = 0; s2 < kPre; ++s2) {
+              if (pend) {
+                const int ld = __ffs(pend) - 1;
+                const unsigned sm = __shfl_sync(0xffffffffu, segmask, ld);
+                pend &= ~sm;
+                const int qq = __shfl_sync(0xffffffffu, qid, ld);
+                const float uk = ukth_rank(pv[s2], a.k, lane);
+                const float tr = pt[s2];
+                if ((sm >> lane) & 1u) tau = fminf(tau, fminf(uk, tr));
+                if (lane == ld && tau < tr) atomicMin(reinterpret_cast<int*>(a.tau0) + qq, __float_as_int(tau));
+              }
+            }
+          }
           while (pend) {
             const int ld = __ffs(pend) - 1;
             const unsigned sm = __shfl_sync(0xffffffffu, segmask, ld);
             pend &= ~sm;
             const int qq = __shfl_sync(0xffffffffu, qid, ld);
             const int nr = a.dyn ? 1 : (a.R < 8 ? a.R : 8);
+            const float tr = vload_volatile(a.tau0 + qq);  // (issued before the list loads: both in flight at once)
             const float uk = union_kth(a.lists + static_cast<int64_t>(qq) * a.R * kEpiSub * a.k, a.R, r, nr, a.k, lane,
-                                       a.dyn ? -1 : 1);
-            const float tr = vload_volatile(a.tau0 + qq);
+                                       a.dyn ? -1 : 1, a.ukth_fast != 0);
             if ((sm >> lane) & 1u) tau = fminf(tau, fminf(uk, tr));
             if (lane == ld && tau < tr) atomicMin(reinterpret_cast<int*>(a.tau0) + qq, __float_as_int(tau));
           }
@@ -1093,6 +1166,17 @@ int launch_dense_hausdorff(const __half* qd, int ntq, const __half* hd, int64_t 
   {
     const char* e = getenv("BVSS_DENSE_DEBUG");
     a.debug = e ? atoi(e) : 0;
+    int per = 32, stag = 8;
+    if (const char* f = getenv("BVSS_DENSE_REFRESH")) sscanf(f, "%d,%d", &per, &stag);
+    if (per < 1 || (per & (per - 1))) BVSS_FAIL(BVSS_EINVAL, "BVSS_DENSE_REFRESH: the period must be a power of two");
+    a.refresh_mask = static_cast<uint32_t>(per - 1);
+    a.refresh_stagger = static_cast<uint32_t>(stag);
+    const char* g = getenv("BVSS_DENSE_UKTH");
+    a.ukth_fast = g ? atoi(g) : 2;
+    a.l2pf_ahead = 0;
+    a.l2pf_mod = 1;
+    if (const char* f = getenv("BVSS_DENSE_L2PF")) sscanf(f, "%d,%d", &a.l2pf_ahead, &a.l2pf_mod);
+    if (a.l2pf_mod < 1) a.l2pf_mod = 1;
   }
   static unsigned long long* prof = nullptr;
   a.prof = nullptr;
