@@ -1399,7 +1399,7 @@ int bvss_index_begin(int64_t n_total, int64_t nvec_total, int32_t d, const bvss_
   int num_sms = 0;
   BVSS_TRY(check_device(p->device, &num_sms));
   DeviceGuard g(p->device);
-  std::unique_ptr<bvss_index> idx(new bvss_index());
+  IndexGuard idx{new bvss_index(), nullptr};  // a failed allocation below releases the stream too
   idx->pending = true;
   idx->device = p->device;
   idx->num_sms = num_sms;
